@@ -165,10 +165,11 @@ const char* regot_b200_status_name(regot_status s);       /* reference exception
 const char* regot_b200_version(void);
 
 /* Row-sharded multi-GPU (north_star item 5).  One process per GPU; rank r owns a
- * contiguous block of rows.  `unique_id` is the 128-byte ncclUniqueId made by
+ * contiguous block of rows.  `unique_ids` is 256 bytes -- two ncclUniqueIds (one
+ * communicator per CUDA stream of the solver) made by
  * regot_b200_comm_unique_id() on rank 0 and broadcast by the host program. */
-regot_status regot_b200_comm_unique_id(void* out128);
-regot_status regot_b200_comm_init(regot_ctx* ctx, int rank, int world, const void* unique_id128);
+regot_status regot_b200_comm_unique_id(void* out256);
+regot_status regot_b200_comm_init(regot_ctx* ctx, int rank, int world, const void* unique_ids256);
 
 /* ---- problem upload: ProblemInstance (problem.h:20-28) ---------------------- */
 /* Full problem on one GPU.  M is n x m with leading dimension ld (elements). */

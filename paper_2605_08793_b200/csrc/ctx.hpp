@@ -1,0 +1,200 @@
+// ctx.hpp -- host-side context of the device solver: device buffers, streams,
+// error plumbing.  Internal to the library (the public surface is
+// include/regot_b200.h).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/regot_b200.h"
+
+struct ncclComm;
+
+namespace rg {
+
+// Error carrying a regot_status; thrown inside the library, converted to a
+// status code + message at the C boundary.
+struct Error : std::runtime_error {
+    regot_status code;
+    Error(regot_status c, const std::string& w) : std::runtime_error(w), code(c) {}
+};
+[[noreturn]] inline void raise(regot_status c, const std::string& w) { throw Error(c, w); }
+
+#define RG_CUDA(expr)                                                                                         \
+    do {                                                                                                      \
+        cudaError_t e__ = (expr);                                                                             \
+        if (e__ != cudaSuccess)                                                                               \
+            ::rg::raise(REGOT_E_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e__) + " (" + __FILE__ + \
+                                          ":" + std::to_string(__LINE__) + ")");                              \
+    } while (0)
+
+// RAII device buffer of T (grow-only)
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { release(); }
+    void release()
+    {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    void ensure(size_t count)
+    {
+        if (count <= n && p) return;
+        release();
+        cudaError_t e = cudaMalloc((void**)&p, sizeof(T) * (count ? count : 1));
+        if (e != cudaSuccess) {
+            p = nullptr;
+            cudaGetLastError();
+            raise(REGOT_E_NOMEM, std::string("cudaMalloc of ") + std::to_string(sizeof(T) * count) +
+                                     " bytes failed: " + cudaGetErrorString(e));
+        }
+        n = count;
+    }
+};
+
+// Geometry of the panel sweep shared by the fused-gradient and LSE kernels:
+// M is cut into tiles of tile_rows x tile_cols, ordered column-panel-major
+// (tile id = panel * n_row_tiles + row_tile); CTA b owns the contiguous tile
+// range [total*b/grid, total*(b+1)/grid).  A "segment" is the part of one
+// CTA's range inside one panel; column partials are produced per segment and
+// reduced per panel in segment order (deterministic, no atomics).
+struct SweepPlan {
+    int tile_rows = 0, tile_cols = 0;
+    int n_row_tiles = 0, n_panels = 0;
+    long total_tiles = 0;
+    int grid = 0;
+    int n_segments = 0;
+    DevBuf<int> d_cta_seg0;      // grid + 1: first segment id of each CTA
+    DevBuf<int> d_panel_seg0;    // n_panels + 1: first segment id of each panel
+};
+
+// Scalars produced by every gradient pass.
+struct GradScalars {
+    double f, marginal_error, duality_gap, grad_sqnorm, total_mass, g_dot_d;
+    double row_abs, col_abs;  // the two halves of the marginal error
+};
+
+// Per-stream scratch of one sweep (gradient or LSE) so the main stream and the
+// Sinkhorn side stream can run concurrently.
+struct SweepWS {
+    DevBuf<double> rowpart;   // n_panels x nloc            (gradient row partials / LSE row sums)
+    DevBuf<double> rowpart2;  // n_panels x nloc            (LSE row maxima)
+    DevBuf<double> colpart;   // n_segments x tile_cols     (column partial sums)
+    DevBuf<double> colpart2;  // n_segments x tile_cols     (LSE column maxima)
+    DevBuf<double> pack;      // m + 16: column sums + row-side scalars (the allreduce payload)
+    DevBuf<double> pack2;     // LSE: second payload
+    DevBuf<double> partials;  // per-CTA scalar partials of the finalize kernels
+    DevBuf<unsigned int> ticket;
+    DevBuf<GradScalars> d_scal;
+    GradScalars* h_scal = nullptr;  // pinned
+    ~SweepWS()
+    {
+        if (h_scal) cudaFreeHost(h_scal);
+    }
+};
+
+// Problem resident on the device (one row block).
+struct DeviceProblem {
+    int64_t n = 0, m = 0;             // global sizes
+    int64_t row_begin = 0, nloc = 0;  // this rank's row block
+    int64_t ld = 0;                   // row pitch of M in elements
+    double eta = 0.0;
+    const double* M = nullptr;  // row-major nloc x ld
+    const double* a = nullptr;  // nloc entries (this block)
+    const double* b = nullptr;  // m entries
+    DevBuf<double> M_own, a_own, b_own;
+    CUtensorMap tmap;  // 2-D map over M for the sweep kernels
+    bool loaded = false;
+};
+
+// A dual-space vector on the device: alpha block (nloc, row-sharded) + beta
+// block (m, replicated).  Free vectors use beta[0..m-2]; beta[m-1] is kept 0.
+struct DVec {
+    DevBuf<double> a, b;
+    void ensure(int64_t nloc, int64_t m)
+    {
+        a.ensure((size_t)nloc);
+        b.ensure((size_t)m);
+    }
+};
+
+// Outputs of a gradient pass on the device.
+struct GradOut {
+    DVec g;          // grad: g.a = row_sums - a, g.b[j] = col_sums[j] - b[j] (all m; free part is j < m-1)
+    DVec sums;       // sums.a = row_sums, sums.b = col_sums
+    GradScalars sc;  // host copy, valid after the stream is synchronised
+    void ensure(int64_t nloc, int64_t m)
+    {
+        g.ensure(nloc, m);
+        sums.ensure(nloc, m);
+    }
+};
+
+}  // namespace rg
+
+struct regot_ctx {
+    int device = 0;
+    int sm_count = 148;
+    cudaStream_t stream = nullptr;  // main stream
+    cudaStream_t side = nullptr;    // Sinkhorn candidate chain (splr.h:373-378)
+    cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_fork = nullptr, ev_join = nullptr;
+    std::string err;
+    int64_t launches = 0;
+
+    // multi-GPU
+    int rank = 0, world = 1;
+    ncclComm* comm = nullptr;       // main-stream collectives
+    ncclComm* comm_side = nullptr;  // side-stream collectives (own communicator: no cross-stream ordering hazards)
+
+    rg::DeviceProblem prob;
+    rg::SweepPlan plan;
+    rg::SweepWS ws_main, ws_side;
+    rg::DevBuf<double> exp_table;  // kExpN doubles: 2^(j/N), high word biased (common.cuh)
+
+    // staging for API calls that take host vectors
+    rg::DVec api_x, api_y, api_d;
+    rg::GradOut api_grad;
+
+    void* solver_ws = nullptr;  // opaque solver workspace (solver.cu)
+};
+
+namespace rg {
+
+void ctx_require_problem(const regot_ctx* ctx);
+void make_sweep_plan(regot_ctx* ctx);
+void ensure_sweep_ws(regot_ctx* ctx, SweepWS& ws);
+
+// ---- kernel launchers (k1_gradient.cu) ----------------------------------------
+// Enqueue one fused-gradient pass at (alpha, beta) on `st`.  dir_a/dir_b
+// (nullable) give a direction d for phi'(gamma) = grad . d.  Column sums and
+// the row-side scalars are allreduced over `comm` when world > 1.  On return
+// everything is enqueued; out.sc is valid after sync_scalars().
+void launch_gradient(regot_ctx* ctx, cudaStream_t st, SweepWS& ws, ncclComm* comm, const double* alpha,
+                     const double* beta, const double* dir_a, const double* dir_b, GradOut& out);
+// Wait for the pass enqueued on `st` and copy its scalars into out.sc.
+void sync_scalars(regot_ctx* ctx, cudaStream_t st, SweepWS& ws, GradOut& out);
+// Only the main sweep kernel, for timing (regot_b200_time_kernel).
+void launch_gradient_sweep_only(regot_ctx* ctx, cudaStream_t st, SweepWS& ws, const double* alpha, const double* beta);
+// Dense plan T (row-major nloc x m) for tests/diagnostics.
+void launch_plan(regot_ctx* ctx, cudaStream_t st, const double* alpha, const double* beta, double* T_rowmajor);
+
+// host <-> device helpers (ctx.cu)
+void upload_dual(regot_ctx* ctx, const double* alpha_host, const double* beta_host, DVec& x, bool check_gauge,
+                 const char* who);
+void allreduce_sum(regot_ctx* ctx, ncclComm* comm, double* buf, size_t count, cudaStream_t st);
+void allreduce_max(regot_ctx* ctx, ncclComm* comm, double* buf, size_t count, cudaStream_t st);
+
+}  // namespace rg

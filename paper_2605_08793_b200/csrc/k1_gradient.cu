@@ -1,0 +1,445 @@
+// k1_gradient.cu -- K1: the fused dual-gradient pass.
+//
+// Replaces regot::fused_gradient (dual.h:106-164) and, through its epilogue,
+// marginal_error (dual.h:219-222), duality_gap (dual.h:225-229) and the
+// phi'(gamma) = grad . d of the line search (splr.h:204-213).
+//
+// One coalesced pass over the row-major cost block: T_ij = exp(clamp((alpha_i +
+// beta_j - M_ij) / eta)) is formed in registers from TMA-staged tiles and
+// reduced to row sums, column sums and the objective.  No float atomics
+// anywhere: every reduction has a fixed order, so results are bitwise
+// reproducible for a fixed grid.
+//
+// Algorithmic bytes per launch: 8*nloc*m (M read once) + 16*(nloc+m).
+#include "ctx.hpp"
+#include "sweep.cuh"
+
+#include <algorithm>
+#include <cmath>
+
+namespace rg {
+
+struct GradParams {
+    SweepGeom g;
+    const double* alpha;  // nloc
+    const double* beta;   // m
+    double inv_eta;
+    const double* exp_table;
+    double* rowpart;  // n_panels x nloc
+    double* colpart;  // n_segments x kTC
+};
+
+// One row of one tile for one lane: 8 plan entries from the staged costs.
+// Returns the lane's partial row sum; column accumulators are updated in place.
+template <bool kRagged>
+__device__ __forceinline__ double gradient_row(const double2* __restrict__ trow, int lane, double ai,
+                                               const double (&bj)[kEPL], double (&colacc)[kEPL], unsigned cmask,
+                                               double inv_eta, uint32_t tbl_lane)
+{
+    double2 mv[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) mv[q] = trow[q * 32 + lane];
+    double t[kEPL];
+    unsigned amax = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        // same association as the reference: (alpha_i + beta_j) - M_ij, then scale (dual.h:64)
+        t[2 * q] = ((ai + bj[2 * q]) - mv[q].x) * inv_eta;
+        t[2 * q + 1] = ((ai + bj[2 * q + 1]) - mv[q].y) * inv_eta;
+        amax = max(amax, max(abs_hi(t[2 * q]), abs_hi(t[2 * q + 1])));
+    }
+    if (amax >= kHi700) {  // rare: some |t| >= 700 -> reference clamp (dual.h:65-69)
+#pragma unroll
+        for (int k = 0; k < kEPL; ++k) t[k] = clamp700(t[k]);
+    }
+    double T[kEPL];
+#pragma unroll
+    for (int k = 0; k < kEPL; ++k) {
+        T[k] = exp_tbl(t[k], tbl_lane);
+        if (kRagged) T[k] = (cmask >> k) & 1u ? T[k] : 0.0;
+        colacc[k] += T[k];
+    }
+    return ((T[0] + T[1]) + (T[2] + T[3])) + ((T[4] + T[5]) + (T[6] + T[7]));
+}
+
+__global__ void __launch_bounds__(kSweepThreads, 1)
+k_gradient_sweep(const __grid_constant__ CUtensorMap tmap, const GradParams p)
+{
+    extern __shared__ __align__(128) unsigned char smem[];
+    const SweepSmem sm = sweep_prologue(smem, &tmap, p.exp_table);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+
+    if (warp == kTR) {
+        sweep_producer(&tmap, p.g, sm.tiles, sm.full, sm.empty);
+        return;
+    }
+
+    // ---- consumer warp `warp` owns row `warp` of every tile ----
+    long t0, t1;
+    sweep_range(p.g, t0, t1);
+    if (t0 >= t1) return;
+    const uint32_t tbl_lane = smem_u32(sm.table) + (uint32_t)(lane & 15) * 8u;
+    double* stage = sm.scratch + warp * kTC;  // this warp's 2 KB: row staging, then column exchange
+    const double2* tile_row = reinterpret_cast<const double2*>(sm.tiles + warp * kTC);
+    const double inv_eta = p.inv_eta;
+    const int nloc = p.g.nloc, m = p.g.m, nrt = p.g.n_row_tiles;
+    int seg = p.g.cta_seg0[blockIdx.x];
+    int s = 0;
+    uint32_t ph = 0;
+
+    long left = t1 - t0;                       // tiles still to process
+    int panel = (int)(t0 / nrt);
+    int rt = (int)(t0 - (long)panel * nrt);    // row tile inside the panel
+    // alpha of the next row is fetched one tile ahead so its latency hides behind the current row
+    double ai_next = (rt * kTR + warp < nloc) ? __ldg(p.alpha + rt * kTR + warp) : 0.0;
+
+    while (left > 0) {
+        // ---- one segment: the rest of panel `panel` (or of the range) ----
+        const int seg_tiles = (int)min((long)(nrt - rt), left);
+        const int col0 = panel * kTC;
+        double bj[kEPL], colacc[kEPL];
+        unsigned cmask = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int c = col0 + 64 * q + 2 * lane + e;
+                const bool ok = c < m;
+                bj[2 * q + e] = ok ? __ldg(p.beta + c) : 0.0;
+                cmask |= (ok ? 1u : 0u) << (2 * q + e);
+                colacc[2 * q + e] = 0.0;
+            }
+        }
+        const bool ragged = (col0 + kTC > m);
+
+        int done = 0;
+        while (done < seg_tiles) {
+            // up to kRowGroup consecutive row tiles, then one transposing flush
+            const int cnt = min(kRowGroup, seg_tiles - done);
+            const int rt0 = rt;
+            for (int k = 0; k < cnt; ++k) {
+                const int row = rt * kTR + warp;
+                const double ai = ai_next;
+                {   // prefetch alpha for the tile after this one (next panel starts again at row tile 0)
+                    int nrow = row + kTR;
+                    if (rt + 1 == nrt) nrow = warp;
+                    ai_next = (nrow < nloc && left > 1) ? __ldg(p.alpha + nrow) : 0.0;
+                }
+                mbar_wait(&sm.full[s], ph);
+                double rs = 0.0;
+                if (row < nloc) {
+                    const double2* trow = tile_row + (size_t)s * (kTileElems / 2);
+                    rs = ragged ? gradient_row<true>(trow, lane, ai, bj, colacc, cmask, inv_eta, tbl_lane)
+                                : gradient_row<false>(trow, lane, ai, bj, colacc, cmask, inv_eta, tbl_lane);
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&sm.empty[s]);
+                if (++s == kStages) {
+                    s = 0;
+                    ph ^= 1u;
+                }
+                stage[k * 32 + lane] = rs;
+                ++rt;
+                --left;
+            }
+            done += cnt;
+            // flush: lane L sums 8 of the 32 lane-partials of staged row L/4
+            __syncwarp();
+            {
+                const int k = lane >> 2, part = lane & 3;
+                const double* src = stage + k * 32 + part * 8;
+                double v = ((src[0] + src[1]) + (src[2] + src[3])) + ((src[4] + src[5]) + (src[6] + src[7]));
+                v += shfl_xor_d(v, 1);
+                v += shfl_xor_d(v, 2);
+                const int row = (rt0 + k) * kTR + warp;
+                if (part == 0 && k < cnt && row < nloc) p.rowpart[(size_t)panel * nloc + row] = v;
+            }
+            __syncwarp();
+        }
+
+        // column partials of this segment: exchange through shared memory,
+        // summed over the kTR warps in warp order
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            reinterpret_cast<double2*>(stage)[q * 32 + lane] = make_double2(colacc[2 * q], colacc[2 * q + 1]);
+        bar_sync(1, kConsumerThreads);
+        if (threadIdx.x < kTC) {
+            double v = 0.0;
+#pragma unroll
+            for (int w = 0; w < kTR; ++w) v += sm.scratch[w * kTC + threadIdx.x];
+            p.colpart[(size_t)seg * kTC + threadIdx.x] = v;
+        }
+        bar_sync(1, kConsumerThreads);
+        ++seg;
+        if (rt == nrt) {
+            rt = 0;
+            ++panel;
+        }
+    }
+}
+
+// ---- epilogue 1: reduce partials, row-side scalars ---------------------------------
+// pack[0..m)   = local column sums
+// pack[m + k]  = row-side scalars: 0 sum(r) 1 alpha.a 2 sum|r-a| 3 alpha.(r-a) 4 |r-a|^2 5 (r-a).d_alpha
+constexpr int kNScal = 8;
+constexpr int kFinThreads = 256;
+
+struct Fin1Params {
+    int nloc, m, n_panels;
+    const double* rowpart;
+    const double* colpart;
+    const int* panel_seg0;
+    const double* alpha;
+    const double* a;
+    const double* dir_a;  // nullable
+    double* row_sums;
+    double* g_alpha;
+    double* pack;
+    double* partials;  // gridDim.x * kNScal
+    unsigned int* ticket;
+};
+
+__device__ __forceinline__ bool last_block_done(unsigned int* ticket)
+{
+    __shared__ bool is_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned int prev = atomicAdd(ticket, 1u);
+        is_last = (prev == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (is_last) __threadfence();
+    return is_last;
+}
+
+// sum of per-block partials in block order; valid in every lane of warp 0
+__device__ __forceinline__ double ordered_partial_sum(const double* partials, int k, int nblocks, int lane)
+{
+    double s = 0.0;
+    for (int b = lane; b < nblocks; b += 32) s += partials[(size_t)b * kNScal + k];
+    return warp_sum(s);
+}
+
+__global__ void __launch_bounds__(kFinThreads) k_gradient_fin1(const Fin1Params p)
+{
+    __shared__ double scratch[kNScal * (kFinThreads / 32)];
+    double acc[6] = {0, 0, 0, 0, 0, 0};
+    const int stride = gridDim.x * blockDim.x;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < p.nloc; i += stride) {
+        double r = 0.0;
+        for (int P = 0; P < p.n_panels; ++P) r += p.rowpart[(size_t)P * p.nloc + i];
+        const double al = p.alpha[i], ai = p.a[i];
+        const double ga = r - ai;
+        p.row_sums[i] = r;
+        p.g_alpha[i] = ga;
+        acc[0] += r;
+        acc[1] += al * ai;
+        acc[2] += fabs(ga);
+        acc[3] += al * ga;
+        acc[4] += ga * ga;
+        if (p.dir_a) acc[5] += ga * p.dir_a[i];
+    }
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < p.m; j += stride) {
+        const int P = j / kTC, off = j - P * kTC;
+        double c = 0.0;
+        for (int sg = p.panel_seg0[P]; sg < p.panel_seg0[P + 1]; ++sg) c += p.colpart[(size_t)sg * kTC + off];
+        p.pack[j] = c;
+    }
+    block_sum<6>(acc, scratch);
+    if (threadIdx.x == 0)
+        for (int k = 0; k < 6; ++k) p.partials[(size_t)blockIdx.x * kNScal + k] = acc[k];
+    if (last_block_done(p.ticket)) {
+        if (threadIdx.x < 32) {
+            for (int k = 0; k < 6; ++k) {
+                const double v = ordered_partial_sum(p.partials, k, gridDim.x, threadIdx.x);
+                if (threadIdx.x == 0) p.pack[p.m + k] = v;
+            }
+            if (threadIdx.x == 0) *p.ticket = 0u;
+        }
+    }
+}
+
+// ---- epilogue 2 (after the allreduce of pack): column-side scalars, objective -------
+struct Fin2Params {
+    int m;
+    double eta;
+    const double* pack;  // m column sums + row-side scalars (global after allreduce)
+    const double* beta;
+    const double* b;
+    const double* dir_b;  // nullable
+    double* col_sums;
+    double* g_beta;
+    double* partials;
+    unsigned int* ticket;
+    GradScalars* out;
+};
+
+__global__ void __launch_bounds__(kFinThreads) k_gradient_fin2(const Fin2Params p)
+{
+    __shared__ double scratch[kNScal * (kFinThreads / 32)];
+    // 0 beta.b (free part) 1 sum|c-b| (all m) 2 beta.(c-b) 3 |c-b|^2 (free part) 4 (c-b).d_beta (free part)
+    double acc[5] = {0, 0, 0, 0, 0};
+    const int stride = gridDim.x * blockDim.x;
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < p.m; j += stride) {
+        const double c = p.pack[j], bj = p.b[j], be = p.beta[j];
+        const double gb = c - bj;
+        p.col_sums[j] = c;
+        p.g_beta[j] = gb;
+        acc[1] += fabs(gb);
+        acc[2] += be * gb;
+        if (j < p.m - 1) {
+            acc[0] += be * bj;
+            acc[3] += gb * gb;
+            if (p.dir_b) acc[4] += gb * p.dir_b[j];
+        }
+    }
+    block_sum<5>(acc, scratch);
+    if (threadIdx.x == 0)
+        for (int k = 0; k < 5; ++k) p.partials[(size_t)blockIdx.x * kNScal + k] = acc[k];
+    if (last_block_done(p.ticket)) {
+        if (threadIdx.x < 32) {
+            double c[5];
+            for (int k = 0; k < 5; ++k) c[k] = ordered_partial_sum(p.partials, k, gridDim.x, threadIdx.x);
+            if (threadIdx.x == 0) {
+                const double* S = p.pack + p.m;
+                GradScalars o;
+                o.total_mass = S[0];
+                o.f = p.eta * S[0] - S[1] - c[0];  // dual.h:157-158
+                o.row_abs = S[2];
+                o.col_abs = c[1];
+                o.marginal_error = S[2] + c[1];  // dual.h:219-222
+                o.duality_gap = S[3] + c[2];     // dual.h:225-229
+                o.grad_sqnorm = S[4] + c[3];
+                o.g_dot_d = S[5] + c[4];
+                *p.out = o;
+                *p.ticket = 0u;
+            }
+        }
+    }
+}
+
+// ---- dense plan (tests / diagnostics; dual.h:83-94) ---------------------------------
+__global__ void k_plan(int nloc, int m, long ld, const double* __restrict__ M, const double* __restrict__ alpha,
+                       const double* __restrict__ beta, double inv_eta, const double* __restrict__ exp_table,
+                       double* __restrict__ T)
+{
+    __shared__ double tbl[kExpN * kExpCopies];
+    exp_table_fill(tbl, exp_table, threadIdx.x, blockDim.x);
+    __syncthreads();
+    const uint32_t tbl_lane = smem_u32(tbl) + (uint32_t)(threadIdx.x & 15) * 8u;
+    const long total = (long)nloc * m;
+    for (long q = (long)blockIdx.x * blockDim.x + threadIdx.x; q < total; q += (long)gridDim.x * blockDim.x) {
+        const int i = (int)(q / m), j = (int)(q % m);
+        const double t = ((alpha[i] + beta[j]) - M[(size_t)i * ld + j]) * inv_eta;
+        T[q] = exp_tbl(clamp700(t), tbl_lane);
+    }
+}
+
+// ---- host side ------------------------------------------------------------------------
+static int fin_grid(const regot_ctx* ctx, long work)
+{
+    long g = (work + kFinThreads - 1) / kFinThreads;
+    return (int)std::max<long>(1, std::min<long>(g, 2L * ctx->sm_count));
+}
+
+static GradParams make_params(regot_ctx* ctx, SweepWS& ws, const double* alpha, const double* beta)
+{
+    GradParams p;
+    p.g.nloc = (int)ctx->prob.nloc;
+    p.g.m = (int)ctx->prob.m;
+    p.g.n_row_tiles = ctx->plan.n_row_tiles;
+    p.g.n_panels = ctx->plan.n_panels;
+    p.g.total_tiles = ctx->plan.total_tiles;
+    p.g.cta_seg0 = ctx->plan.d_cta_seg0.p;
+    // M larger than ~half of L2 streams through with evict-first; small problems stay L2 resident
+    p.g.evict_first = ((double)ctx->prob.nloc * (double)ctx->prob.ld * 8.0 > 48e6) ? 1 : 0;
+    p.alpha = alpha;
+    p.beta = beta;
+    p.inv_eta = 1.0 / ctx->prob.eta;
+    p.exp_table = ctx->exp_table.p;
+    p.rowpart = ws.rowpart.p;
+    p.colpart = ws.colpart.p;
+    return p;
+}
+
+void launch_gradient_sweep_only(regot_ctx* ctx, cudaStream_t st, SweepWS& ws, const double* alpha, const double* beta)
+{
+    static bool attr_set = false;
+    if (!attr_set) {
+        RG_CUDA(cudaFuncSetAttribute(k_gradient_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, kSweepSmem));
+        attr_set = true;
+    }
+    const GradParams p = make_params(ctx, ws, alpha, beta);
+    k_gradient_sweep<<<ctx->plan.grid, kSweepThreads, kSweepSmem, st>>>(ctx->prob.tmap, p);
+    RG_CUDA(cudaGetLastError());
+    ++ctx->launches;
+}
+
+void launch_gradient(regot_ctx* ctx, cudaStream_t st, SweepWS& ws, ncclComm* comm, const double* alpha,
+                     const double* beta, const double* dir_a, const double* dir_b, GradOut& out)
+{
+    const DeviceProblem& pr = ctx->prob;
+    out.ensure(pr.nloc, pr.m);
+    launch_gradient_sweep_only(ctx, st, ws, alpha, beta);
+
+    const int g1 = fin_grid(ctx, std::max<long>(pr.nloc, pr.m));
+    Fin1Params f1;
+    f1.nloc = (int)pr.nloc;
+    f1.m = (int)pr.m;
+    f1.n_panels = ctx->plan.n_panels;
+    f1.rowpart = ws.rowpart.p;
+    f1.colpart = ws.colpart.p;
+    f1.panel_seg0 = ctx->plan.d_panel_seg0.p;
+    f1.alpha = alpha;
+    f1.a = pr.a;
+    f1.dir_a = dir_a;
+    f1.row_sums = out.sums.a.p;
+    f1.g_alpha = out.g.a.p;
+    f1.pack = ws.pack.p;
+    f1.partials = ws.partials.p;
+    f1.ticket = ws.ticket.p;
+    k_gradient_fin1<<<g1, kFinThreads, 0, st>>>(f1);
+    RG_CUDA(cudaGetLastError());
+    ++ctx->launches;
+
+    if (ctx->world > 1) allreduce_sum(ctx, comm, ws.pack.p, (size_t)pr.m + kNScal, st);
+
+    const int g2 = fin_grid(ctx, pr.m);
+    Fin2Params f2;
+    f2.m = (int)pr.m;
+    f2.eta = pr.eta;
+    f2.pack = ws.pack.p;
+    f2.beta = beta;
+    f2.b = pr.b;
+    f2.dir_b = dir_b;
+    f2.col_sums = out.sums.b.p;
+    f2.g_beta = out.g.b.p;
+    f2.partials = ws.partials.p;
+    f2.ticket = ws.ticket.p + 1;
+    f2.out = ws.d_scal.p;
+    k_gradient_fin2<<<g2, kFinThreads, 0, st>>>(f2);
+    RG_CUDA(cudaGetLastError());
+    ++ctx->launches;
+    RG_CUDA(cudaMemcpyAsync(ws.h_scal, ws.d_scal.p, sizeof(GradScalars), cudaMemcpyDeviceToHost, st));
+}
+
+void sync_scalars(regot_ctx* ctx, cudaStream_t st, SweepWS& ws, GradOut& out)
+{
+    (void)ctx;
+    RG_CUDA(cudaStreamSynchronize(st));
+    out.sc = *ws.h_scal;
+}
+
+void launch_plan(regot_ctx* ctx, cudaStream_t st, const double* alpha, const double* beta, double* T_rowmajor)
+{
+    const DeviceProblem& pr = ctx->prob;
+    const long total = (long)pr.nloc * pr.m;
+    const int grid = (int)std::max<long>(1, std::min<long>((total + 255) / 256, 8L * ctx->sm_count));
+    k_plan<<<grid, 256, 0, st>>>((int)pr.nloc, (int)pr.m, (long)pr.ld, pr.M, alpha, beta, 1.0 / pr.eta,
+                                 ctx->exp_table.p, T_rowmajor);
+    RG_CUDA(cudaGetLastError());
+    ++ctx->launches;
+}
+
+}  // namespace rg

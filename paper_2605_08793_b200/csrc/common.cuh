@@ -133,6 +133,24 @@ __device__ __forceinline__ double exp_tbl(double t, uint32_t tbl_lane)
     return __fma_rn(s, q, s);
 }
 
+// same function with the (non-replicated) table read through the read-only
+// global path; for low-volume kernels that do not stage the table in smem
+__device__ __forceinline__ double exp_tbl_g(double t, const double* __restrict__ tbl)
+{
+    const double kd = __fma_rn(t, ExpConst::inv_ln2_n, ExpConst::shift);
+    const int ki = __double2loint(kd);
+    const double kf = kd - ExpConst::shift;
+    double r = __fma_rn(kf, -ExpConst::ln2_n_hi, t);
+    r = __fma_rn(kf, -ExpConst::ln2_n_lo, r);
+    double s = __ldg(tbl + ((unsigned)ki & (kExpN - 1)));
+    s = __hiloint2double(__double2hiint(s) + (int)((unsigned)ki << (20 - kExpShift)), __double2loint(s));
+    const double r2 = r * r;
+    double p = __fma_rn(r, ExpConst::c3, ExpConst::c2);
+    p = __fma_rn(r2, ExpConst::c4, p);
+    const double q = __fma_rn(r2, p, r);
+    return __fma_rn(s, q, s);
+}
+
 // |t| >= 700 (or NaN) test on the high word; amax accumulates max |hi|
 __device__ __forceinline__ unsigned abs_hi(double t) { return (unsigned)__double2hiint(t) & 0x7fffffffu; }
 constexpr unsigned kHi700 = 0x4085E000u;

@@ -100,6 +100,13 @@ void allreduce_max(regot_ctx* ctx, ncclComm* comm, double* buf, size_t count, cu
     nccl_check(nccl().AllReduce(buf, buf, count, ncclDouble, ncclMax, comm, st), "ncclAllReduce(max)");
 }
 
+void allreduce_sum_u64(regot_ctx* ctx, ncclComm* comm, unsigned long long* buf, size_t count, cudaStream_t st)
+{
+    if (ctx->world == 1) return;
+    if (!comm) raise(REGOT_E_NCCL, "allreduce: communicator not initialised (regot_b200_comm_init)");
+    nccl_check(nccl().AllReduce(buf, buf, count, ncclUint64, ncclSum, comm, st), "ncclAllReduce(u64)");
+}
+
 // ---- context ---------------------------------------------------------------------------
 void ctx_require_problem(const regot_ctx* ctx)
 {
@@ -239,7 +246,7 @@ void ensure_sweep_ws(regot_ctx* ctx, SweepWS& ws)
     ws.colpart.ensure((size_t)pl.n_segments * kTC);
     ws.colpart2.ensure((size_t)pl.n_segments * kTC);
     ws.pack.ensure((size_t)pr.m + 16);
-    ws.pack2.ensure((size_t)pr.m + 16);
+    ws.pack2.ensure(2 * (size_t)pr.m + 32);
     ws.partials.ensure((size_t)(2 * ctx->sm_count + 8) * 8);
     if (!ws.ticket.p) {
         ws.ticket.ensure(8);

@@ -11,6 +11,7 @@
 #include <cstdlib>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/regot_b200.h"
@@ -49,6 +50,11 @@ struct DevBuf {
         if (p) cudaFree(p);
         p = nullptr;
         n = 0;
+    }
+    void swap(DevBuf& o)
+    {
+        std::swap(p, o.p);
+        std::swap(n, o.n);
     }
     void ensure(size_t count)
     {
@@ -129,6 +135,11 @@ struct DVec {
         a.ensure((size_t)nloc);
         b.ensure((size_t)m);
     }
+    void swap(DVec& o)
+    {
+        a.swap(o.a);
+        b.swap(o.b);
+    }
 };
 
 // Outputs of a gradient pass on the device.
@@ -140,6 +151,12 @@ struct GradOut {
     {
         g.ensure(nloc, m);
         sums.ensure(nloc, m);
+    }
+    void swap(GradOut& o)
+    {
+        g.swap(o.g);
+        sums.swap(o.sums);
+        std::swap(sc, o.sc);
     }
 };
 
@@ -190,6 +207,15 @@ void sync_scalars(regot_ctx* ctx, cudaStream_t st, SweepWS& ws, GradOut& out);
 void launch_gradient_sweep_only(regot_ctx* ctx, cudaStream_t st, SweepWS& ws, const double* alpha, const double* beta);
 // Dense plan T (row-major nloc x m) for tests/diagnostics.
 void launch_plan(regot_ctx* ctx, cudaStream_t st, const double* alpha, const double* beta, double* T_rowmajor);
+
+// ---- Sinkhorn launchers (k7_lse.cu) ----------------------------------------------
+void launch_row_lse_sweep_only(regot_ctx* ctx, cudaStream_t st, SweepWS& ws, const double* beta);
+void launch_col_lse_sweep_only(regot_ctx* ctx, cudaStream_t st, SweepWS& ws, const double* alpha);
+void launch_optimal_alpha(regot_ctx* ctx, cudaStream_t st, SweepWS& ws, const double* beta, double* alpha_out);
+void launch_optimal_beta(regot_ctx* ctx, cudaStream_t st, SweepWS& ws, ncclComm* comm, double* alpha_io,
+                         double* beta_out, int gauge);
+void launch_sinkhorn_step(regot_ctx* ctx, cudaStream_t st, SweepWS& ws, ncclComm* comm, double* alpha_io,
+                          double* beta_io);
 
 // host <-> device helpers (ctx.cu)
 void upload_dual(regot_ctx* ctx, const double* alpha_host, const double* beta_host, DVec& x, bool check_gauge,

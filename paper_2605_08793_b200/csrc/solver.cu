@@ -1,0 +1,507 @@
+// solver.cu -- host-side drivers over the device kernels.
+//
+// run_sinkhorn (sinkhorn.h:123-171) and run_splr / splr_step (splr.h:348-534)
+// keep the reference's control flow decision for decision: refresh schedule,
+// tau rule and escalation, low-rank guards, Woodbury fallbacks, Wolfe line
+// search, hybrid selection rule, trace cadence and error classes.  Only scalars
+// cross the PCIe bus inside the loops; every vector stays in HBM.
+#include "solver.hpp"
+#include "capi_util.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+
+namespace rg {
+
+SolverWS& solver_ws(regot_ctx* ctx)
+{
+    if (!ctx->solver_ws) ctx->solver_ws = new SolverWS();
+    return *static_cast<SolverWS*>(ctx->solver_ws);
+}
+void solver_ws_free(regot_ctx* ctx)
+{
+    delete static_cast<SolverWS*>(ctx->solver_ws);
+    ctx->solver_ws = nullptr;
+}
+
+namespace {
+
+struct Timer {
+    regot_ctx* ctx;
+    explicit Timer(regot_ctx* c) : ctx(c) { cudaEventRecord(ctx->ev_a, ctx->stream); }
+    double stop()
+    {
+        float ms = 0.f;
+        cudaEventRecord(ctx->ev_b, ctx->stream);
+        cudaEventSynchronize(ctx->ev_b);
+        cudaEventElapsedTime(&ms, ctx->ev_a, ctx->ev_b);
+        return ms;
+    }
+};
+
+void gradient_sync(regot_ctx* ctx, cudaStream_t st, SweepWS& ws, ncclComm* comm, const DVec& x, const DVec* dir,
+                   GradOut& out, SolveOut* stats)
+{
+    launch_gradient(ctx, st, ws, comm, x.a.p, x.b.p, dir ? dir->a.p : nullptr, dir ? dir->b.p : nullptr, out);
+    sync_scalars(ctx, st, ws, out);
+    if (stats) ++stats->gradient_passes;
+}
+
+// copy the dual point back: this rank's rows of alpha (allgathered by summing a
+// zero-padded vector when sharded), all of beta
+void download_point(regot_ctx* ctx, const DVec& x, SolveOut& out)
+{
+    const DeviceProblem& pr = ctx->prob;
+    out.alpha.assign((size_t)pr.n, 0.0);
+    out.beta.assign((size_t)pr.m, 0.0);
+    if (ctx->world > 1) {
+        DevBuf<double> full;
+        full.ensure((size_t)pr.n);
+        RG_CUDA(cudaMemsetAsync(full.p, 0, sizeof(double) * (size_t)pr.n, ctx->stream));
+        RG_CUDA(cudaMemcpyAsync(full.p + pr.row_begin, x.a.p, sizeof(double) * (size_t)pr.nloc, cudaMemcpyDeviceToDevice,
+                                ctx->stream));
+        allreduce_sum(ctx, ctx->comm, full.p, (size_t)pr.n, ctx->stream);
+        RG_CUDA(cudaMemcpyAsync(out.alpha.data(), full.p, sizeof(double) * (size_t)pr.n, cudaMemcpyDeviceToHost, ctx->stream));
+        RG_CUDA(cudaStreamSynchronize(ctx->stream));
+    } else {
+        RG_CUDA(cudaMemcpyAsync(out.alpha.data(), x.a.p, sizeof(double) * (size_t)pr.nloc, cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    RG_CUDA(cudaMemcpyAsync(out.beta.data(), x.b.p, sizeof(double) * (size_t)pr.m, cudaMemcpyDeviceToHost, ctx->stream));
+    RG_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+void append_row(SolveOut& out, long iter, double wall_ms, const GradScalars& sc)
+{
+    // trace.h:26-36 ordering invariants
+    if (!out.trace.empty()) {
+        if (iter <= out.trace.back().iter) raise(REGOT_E_VALIDATION, "SolverTrace: iter must be strictly increasing");
+        if (wall_ms < out.trace.back().wall_ms) raise(REGOT_E_VALIDATION, "SolverTrace: wall_ms must be nondecreasing");
+    }
+    out.trace.push_back({iter, wall_ms, sc.f, sc.marginal_error, sc.duality_gap});
+}
+
+}  // namespace
+
+// ---- run_sinkhorn (sinkhorn.h:123-171) ------------------------------------------------------
+void solve_sinkhorn(regot_ctx* ctx, const double* alpha0, const double* beta0, const regot_sinkhorn_config& cfg,
+                    SolveOut& out)
+{
+    validate_sinkhorn_config(cfg);
+    ctx_require_problem(ctx);
+    SolverWS& W = solver_ws(ctx);
+    const int64_t launches0 = ctx->launches;
+    upload_dual(ctx, alpha0, beta0, W.x, true, "run_sinkhorn");
+    WallClock clk;
+    Timer tm(ctx);
+    cudaStream_t st = ctx->stream;
+
+    gradient_sync(ctx, st, ctx->ws_main, ctx->comm, W.x, nullptr, W.cur, &out);
+    append_row(out, 0, clk.ms(), W.cur.sc);
+    long it = 0;
+    bool fresh = true;
+    while (it < cfg.max_iter) {
+        if (cfg.tol > 0.0 && W.cur.sc.marginal_error <= cfg.tol) break;
+        launch_sinkhorn_step(ctx, st, ctx->ws_main, ctx->comm, W.x.a.p, W.x.b.p);
+        out.lse_passes += 2;
+        ++it;
+        fresh = false;
+        const bool rec = (it % cfg.record_every == 0) || it == cfg.max_iter;
+        if (cfg.tol > 0.0 || rec) {
+            gradient_sync(ctx, st, ctx->ws_main, ctx->comm, W.x, nullptr, W.cur, &out);
+            fresh = true;
+            if (rec) append_row(out, it, clk.ms(), W.cur.sc);
+        }
+    }
+    if (!fresh) gradient_sync(ctx, st, ctx->ws_main, ctx->comm, W.x, nullptr, W.cur, &out);
+    if (out.trace.back().iter != it) append_row(out, it, clk.ms(), W.cur.sc);
+    out.device_ms = tm.stop();
+    download_point(ctx, W.x, out);
+    out.kernel_launches = ctx->launches - launches0;
+}
+
+// ---- SPLR pieces ---------------------------------------------------------------------------------
+namespace {
+
+struct LowRankDev {
+    bool active = false;
+    double xi = 0.0, zeta = 0.0;  // u = W.ydiff, v = W.v
+};
+
+double dot1(regot_ctx* ctx, SolverWS& W, const DVec& a, const DVec& b)
+{
+    const DVec* xs[1] = {&a};
+    const DVec* ys[1] = {&b};
+    double r = 0.0;
+    vec_dots(ctx, ctx->stream, ctx->comm, W.dots, 1, xs, ys, &r);
+    return r;
+}
+
+// build_low_rank (splr.h:102-122): s- and y- are differences of the free vectors of
+// the last two accepted iterates
+LowRankDev build_low_rank(regot_ctx* ctx, SolverWS& W, bool has_prev)
+{
+    LowRankDev R;
+    if (!has_prev) return R;
+    cudaStream_t st = ctx->stream;
+    vec_sub(ctx, st, W.x, W.x_prev, W.sdiff);
+    vec_sub(ctx, st, W.cur.g, W.g_prev, W.ydiff);
+    W.v.ensure(ctx->prob.nloc, ctx->prob.m);
+    sparse_matvec(ctx, st, ctx->comm, W.A, 1, W.sdiff.a.p, W.sdiff.b.p, W.v.a.p, W.v.b.p, 0, 0);
+    const DVec* xs[5] = {&W.ydiff, &W.ydiff, &W.v, &W.v, &W.sdiff};
+    const DVec* ys[5] = {&W.sdiff, &W.ydiff, &W.sdiff, &W.v, &W.sdiff};
+    double r[5];
+    vec_dots(ctx, st, ctx->comm, W.dots, 5, xs, ys, r);
+    const double ys_ = r[0], yy = r[1], vs = r[2], vv = r[3], ss = r[4];
+    if (!(ys_ > 1e-6 * yy)) return R;
+    if (std::fabs(vs) <= 1e-12 * std::sqrt(vv) * std::sqrt(ss)) return R;
+    R.active = true;
+    R.xi = 1.0 / ys_;
+    R.zeta = -1.0 / vs;
+    return R;
+}
+
+// compute_direction (splr.h:128-167) with A^{-1} applied by batched PCG.
+// Returns false on PCG breakdown (the caller escalates tau like a failed
+// factorization, splr.h:400-407).  g_dot_d receives g . d.
+bool compute_direction(regot_ctx* ctx, SolverWS& W, const regot_sparse& A, const DVec& g, double g_sqnorm,
+                       const LowRankDev& R, const DVec& u, const DVec& v, double rtol, int max_iter, DVec& d,
+                       double& g_dot_d, int& cg_iters)
+{
+    cudaStream_t st = ctx->stream;
+    cg_iters = 0;
+    if (g_sqnorm == 0.0) {  // splr.h:131-132
+        vec_zero(ctx, st, d);
+        g_dot_d = 0.0;
+        return true;
+    }
+    const DVec* rhs[3] = {&g, &u, &v};
+    DVec* sol[3] = {&W.ag, &W.au, &W.av};
+    const int nrhs = R.active ? 3 : 1;
+    const int it = sparse_pcg(ctx, st, ctx->comm, W.sparse, A, nrhs, rhs, sol, rtol, max_iter);
+    if (it < 0) return false;
+    cg_iters = it;
+    bool woodbury = false;
+    if (R.active) {
+        const DVec* xs[5] = {&u, &u, &v, &u, &v};
+        const DVec* ys[5] = {&W.au, &W.av, &W.av, &W.ag, &W.ag};
+        double r[5];
+        vec_dots(ctx, st, ctx->comm, W.dots, 5, xs, ys, r);
+        const double k11 = 1.0 / R.xi + r[0], k12 = r[1], k22 = 1.0 / R.zeta + r[2];
+        const double det = k11 * k22 - k12 * k12;
+        const double sc = std::max({std::fabs(k11), std::fabs(k12), std::fabs(k22)});
+        if (std::fabs(det) > 1e-14 * sc * sc && sc > 0.0) {
+            const double t1 = r[3], t2 = r[4];
+            const double z1 = (k22 * t1 - k12 * t2) / det;
+            const double z2 = (-k12 * t1 + k11 * t2) / det;
+            vec_lincomb(ctx, st, -1.0, W.ag, z1, &W.au, z2, &W.av, d);  // d = -(ag - au z1 - av z2)
+            woodbury = true;
+        }
+    }
+    if (!woodbury) vec_lincomb(ctx, st, -1.0, W.ag, 0.0, nullptr, 0.0, nullptr, d);
+    g_dot_d = dot1(ctx, W, g, d);
+    if (g_dot_d < 0.0) return true;
+    if (woodbury) {
+        vec_lincomb(ctx, st, -1.0, W.ag, 0.0, nullptr, 0.0, nullptr, d);
+        g_dot_d = dot1(ctx, W, g, d);
+        if (g_dot_d < 0.0) return true;
+    }
+    raise(REGOT_E_DIRECTION, "compute_direction: no descent direction");
+}
+
+struct LsOut {
+    double gamma = 0.0, g0_dot_d = 0.0, gnew_dot_d = 0.0;
+    bool curvature_ok = false;
+    int evals = 0;
+    int slot = -1;  // trial slot holding x_new / gr_new
+};
+
+// line_search (splr.h:185-290).  Trial points and their gradients live in three
+// rotating device slots; only (f, phi') come back to the host per evaluation.
+struct LineSearch {
+    regot_ctx* ctx;
+    SolverWS& W;
+    SolveOut& stats;
+    DVec tx[3];
+    GradOut tg[3];
+    bool used[3] = {false, false, false};
+
+    int grab()
+    {
+        for (int s = 0; s < 3; ++s)
+            if (!used[s]) {
+                used[s] = true;
+                return s;
+            }
+        raise(REGOT_E_CUDA, "line_search: out of trial slots (internal error)");
+    }
+
+    LsOut run(const DVec& x0, const DVec& d, double f0, double dphi0, const regot_splr_config& cfg)
+    {
+        if (!(dphi0 < 0.0)) raise(REGOT_E_VALIDATION, "line_search: g'd must be negative");
+        const double c1 = cfg.c1, c2 = cfg.c2;
+        int evals = 0, best = -1;
+        double best_f = 0.0, best_gamma = 0.0, best_dphi = 0.0;
+        struct Trial {
+            double gamma, f, dphi;
+            int slot;
+        };
+        auto probe = [&](double gamma) {
+            Trial e;
+            e.gamma = gamma;
+            e.slot = grab();
+            vec_axpy(ctx, ctx->stream, gamma, x0, d, tx[e.slot]);
+            gradient_sync(ctx, ctx->stream, ctx->ws_main, ctx->comm, tx[e.slot], &d, tg[e.slot], &stats);
+            e.f = tg[e.slot].sc.f;
+            e.dphi = tg[e.slot].sc.g_dot_d;
+            ++evals;
+            return e;
+        };
+        auto armijo = [&](const Trial& e) { return std::isfinite(e.f) && e.f <= f0 + c1 * e.gamma * dphi0; };
+        auto drop = [&](const Trial& e) { used[e.slot] = false; };
+        auto remember = [&](const Trial& e) {
+            if (best < 0 || e.f < best_f) {
+                if (best >= 0) used[best] = false;
+                best = e.slot;
+                best_f = e.f;
+                best_gamma = e.gamma;
+                best_dphi = e.dphi;
+            } else {
+                drop(e);
+            }
+        };
+        auto accept = [&](const Trial& e) {
+            LsOut r;
+            r.gamma = e.gamma;
+            r.g0_dot_d = dphi0;
+            r.gnew_dot_d = e.dphi;
+            r.curvature_ok = true;
+            r.evals = evals;
+            r.slot = e.slot;
+            return r;
+        };
+        auto fallback = [&]() {
+            if (best < 0)
+                raise(REGOT_E_LINE_SEARCH,
+                      "line_search: no sufficient-decrease point in " + std::to_string(evals) + " trials");
+            LsOut r;
+            r.gamma = best_gamma;
+            r.g0_dot_d = dphi0;
+            r.gnew_dot_d = best_dphi;
+            r.curvature_ok = false;
+            r.evals = evals;
+            r.slot = best;
+            return r;
+        };
+        auto zoom = [&](double lo, double f_lo, double hi) {
+            while (evals < cfg.max_ls_trials) {
+                const double mid = 0.5 * (lo + hi);
+                if (mid == lo || mid == hi) break;
+                Trial e = probe(mid);
+                if (!armijo(e) || e.f >= f_lo) {
+                    hi = mid;
+                    drop(e);
+                    continue;
+                }
+                if (e.dphi >= c2 * dphi0) return accept(e);
+                const double dphi = e.dphi, ef = e.f;
+                remember(e);
+                if (dphi * (hi - lo) >= 0.0) hi = lo;
+                lo = mid;
+                f_lo = ef;
+            }
+            return fallback();
+        };
+        double g_prev = 0.0, f_prev = f0, gamma = 1.0;
+        while (evals < cfg.max_ls_trials) {
+            Trial e = probe(gamma);
+            if (!armijo(e) || (g_prev > 0.0 && e.f >= f_prev)) {
+                drop(e);
+                return zoom(g_prev, f_prev, gamma);
+            }
+            if (e.dphi >= c2 * dphi0) return accept(e);
+            const double ef = e.f;
+            remember(e);
+            g_prev = gamma;
+            f_prev = ef;
+            gamma *= 2.0;
+        }
+        return fallback();
+    }
+};
+
+}  // namespace
+
+// entry used by regot_b200_compute_direction (tests exercise the direction alone)
+bool compute_direction_api(regot_ctx* ctx, const regot_sparse& A, const DVec& g, double g_sqnorm, bool active, double xi,
+                           double zeta, const DVec& u, const DVec& v, double rtol, int max_iter, DVec& d, int& cg_iters)
+{
+    LowRankDev R;
+    R.active = active;
+    R.xi = xi;
+    R.zeta = zeta;
+    double gd = 0.0;
+    return compute_direction(ctx, solver_ws(ctx), A, g, g_sqnorm, R, u, v, rtol, max_iter, d, gd, cg_iters);
+}
+
+// ---- run_splr (splr.h:487-534) -----------------------------------------------------------------
+void solve_splr(regot_ctx* ctx, const double* alpha0, const double* beta0, const regot_splr_config& cfg, SolveOut& out)
+{
+    validate_splr_config(cfg);
+    ctx_require_problem(ctx);
+    const DeviceProblem& pr = ctx->prob;
+    SolverWS& W = solver_ws(ctx);
+    const int64_t launches0 = ctx->launches;
+    cudaStream_t st = ctx->stream;
+    upload_dual(ctx, alpha0, beta0, W.x, true, "run_splr");
+    WallClock clk;
+    Timer tm(ctx);
+
+    const double cg_rtol = cfg.cg_rtol > 0.0 ? cfg.cg_rtol : 1e-10;
+    const long dim = (long)pr.n + pr.m - 1;
+    const int cg_max = cfg.cg_max_iter > 0 ? cfg.cg_max_iter : (int)std::min<long>(20 * dim, 200000);
+
+    // splr_init (splr.h:326-334)
+    gradient_sync(ctx, st, ctx->ws_main, ctx->comm, W.x, nullptr, W.cur, &out);
+    bool has_prev = false;
+    long iter = 0;
+    append_row(out, 0, clk.ms(), W.cur.sc);
+    LineSearch ls_engine{ctx, W, out};
+
+    while (iter < cfg.max_iter) {
+        if (W.cur.sc.marginal_error <= cfg.tol) break;
+        regot_step_record rec;
+        std::memset(&rec, 0, sizeof(rec));
+        rec.f_cand_sinkhorn = std::numeric_limits<double>::quiet_NaN();
+        try {
+            // ---------------- splr_step (splr.h:348-478) ----------------
+            const long k = iter;
+            const bool refresh = (k % cfg.S == 0);
+            double tau = std::min(cfg.tau_max, std::sqrt(W.cur.sc.grad_sqnorm));  // splr.h:353
+            bool have_s = false;
+
+            if (refresh) {
+                // plan + select_topk + assemble (splr.h:361-364); T is never materialised
+                topk_build_pattern(ctx, st, W.sparse, kFromDual, W.x.a.p, W.x.b.p,
+                                   regot_b200_topk_budget(pr.n, pr.m, cfg.density), W.A);
+                out.gradient_passes += 3;  // three sweeps over M
+                sparse_fill_values(ctx, st, W.A, W.x.a.p, W.x.b.p, tau, W.cur.sums.a.p, W.cur.sums.b.p);
+                if (cfg.J > 0) {
+                    // candidate chain from the same snapshot (splr.h:366-372); on the side
+                    // stream when cfg.overlap is set (splr.h:373-378)
+                    cudaStream_t cs = cfg.overlap ? ctx->side : st;
+                    SweepWS& cws = cfg.overlap ? ctx->ws_side : ctx->ws_main;
+                    ncclComm* ccomm = cfg.overlap ? ctx->comm_side : ctx->comm;
+                    if (cfg.overlap) {
+                        RG_CUDA(cudaEventRecord(ctx->ev_fork, st));
+                        RG_CUDA(cudaStreamWaitEvent(cs, ctx->ev_fork, 0));
+                    }
+                    W.xs.ensure(pr.nloc, pr.m);
+                    RG_CUDA(cudaMemcpyAsync(W.xs.a.p, W.x.a.p, sizeof(double) * (size_t)pr.nloc, cudaMemcpyDeviceToDevice, cs));
+                    RG_CUDA(cudaMemcpyAsync(W.xs.b.p, W.x.b.p, sizeof(double) * (size_t)pr.m, cudaMemcpyDeviceToDevice, cs));
+                    for (long j = 0; j < cfg.J; ++j) launch_sinkhorn_step(ctx, cs, cws, ccomm, W.xs.a.p, W.xs.b.p);
+                    out.lse_passes += 2 * cfg.J;
+                    launch_gradient(ctx, cs, cws, ccomm, W.xs.a.p, W.xs.b.p, nullptr, nullptr, W.cand);
+                    ++out.gradient_passes;
+                    if (!cfg.overlap) sync_scalars(ctx, cs, cws, W.cand);
+                    have_s = true;
+                }
+            } else {
+                sparse_fill_values(ctx, st, W.A, W.x.a.p, W.x.b.p, tau, W.cur.sums.a.p, W.cur.sums.b.p);  // update_values
+            }
+
+            // direction; PCG breakdown plays the role of NotPositiveDefiniteError (splr.h:391-408)
+            int retries = 0, cg_iters = 0;
+            double g_dot_d = 0.0;
+            LowRankDev R;
+            for (;;) {
+                R = build_low_rank(ctx, W, has_prev);
+                if (compute_direction(ctx, W, W.A, W.cur.g, W.cur.sc.grad_sqnorm, R, W.ydiff, W.v, cg_rtol, cg_max, W.d,
+                                      g_dot_d, cg_iters))
+                    break;
+                if (retries >= 8) raise(REGOT_E_NOT_POSITIVE_DEFINITE, "pcg: matrix is not positive definite");
+                tau = (tau > 0.0) ? 2.0 * tau : 1e-8;
+                sparse_fill_values(ctx, st, W.A, W.x.a.p, W.x.b.p, tau, W.cur.sums.a.p, W.cur.sums.b.p);
+                ++retries;
+            }
+
+            // Wolfe line search on the fused gradient (splr.h:414-436)
+            LsOut ls;
+            bool ls_failed = false;
+            for (bool& u : ls_engine.used) u = false;
+            try {
+                ls = ls_engine.run(W.x, W.d, W.cur.sc.f, g_dot_d, cfg);
+            } catch (const Error& e) {
+                if (e.code != REGOT_E_LINE_SEARCH) throw;
+                ls_failed = true;
+                ls.gamma = 0.0;
+                ls.g0_dot_d = g_dot_d;
+                ls.gnew_dot_d = g_dot_d;
+                ls.curvature_ok = false;
+                ls.evals = (int)cfg.max_ls_trials;
+                ls.slot = -1;
+            }
+            const double f_qn = ls_failed ? W.cur.sc.f : ls_engine.tg[ls.slot].sc.f;
+
+            if (have_s && cfg.overlap) {
+                // join the side stream, then read its scalars
+                sync_scalars(ctx, ctx->side, ctx->ws_side, W.cand);
+            }
+            // hybrid selection, ties to the Sinkhorn candidate (splr.h:442-443)
+            const bool pick_s = have_s && std::isfinite(W.cand.sc.f) && (ls_failed || W.cand.sc.f <= f_qn);
+
+            rec.iter = k;
+            rec.refresh = refresh;
+            rec.sinkhorn_selected = pick_s;
+            rec.f_before = W.cur.sc.f;
+            rec.f_cand_qn = f_qn;
+            rec.f_cand_sinkhorn = have_s ? W.cand.sc.f : std::numeric_limits<double>::quiet_NaN();
+            rec.gamma = ls.gamma;
+            rec.g_dot_d = ls.g0_dot_d;
+            rec.gnew_dot_d = ls.gnew_dot_d;
+            rec.curvature_ok = ls.curvature_ok;
+            rec.ls_failed = ls_failed;
+            rec.lowrank_active = R.active;
+            rec.tau = tau;
+            rec.factor_retries = retries;
+            rec.ls_evals = ls.evals;
+            rec.cg_iters = cg_iters;
+
+            // rotate (x_prev, g_prev) <- (x, g) (splr.h:463-476)
+            W.x_prev.swap(W.x);
+            W.g_prev.swap(W.cur.g);
+            has_prev = true;
+            if (pick_s) {
+                W.x.swap(W.xs);
+                W.cur.swap(W.cand);
+            } else if (ls_failed) {
+                // zero step: x and its sums stay, only the gradient buffer was rotated away
+                vec_copy(ctx, st, W.x_prev, W.x);
+                vec_copy(ctx, st, W.g_prev, W.cur.g);
+            } else {
+                W.x.swap(ls_engine.tx[ls.slot]);
+                W.cur.swap(ls_engine.tg[ls.slot]);
+            }
+            rec.f_after = W.cur.sc.f;
+            iter = k + 1;
+        } catch (const Error& e) {
+            if (e.code == REGOT_E_CUDA || e.code == REGOT_E_NCCL || e.code == REGOT_E_NOMEM) throw;
+            // StepError (splr.h:315-324, 520-525): partial trace, no point
+            cudaStreamSynchronize(ctx->side);
+            out.status = REGOT_E_STEP;
+            out.message = "run_splr: step " + std::to_string(iter) + " failed: " + e.what();
+            out.device_ms = tm.stop();
+            out.kernel_launches = ctx->launches - launches0;
+            return;
+        }
+        out.steps.push_back(rec);
+        if (iter % cfg.record_every == 0 || iter == cfg.max_iter) append_row(out, iter, clk.ms(), W.cur.sc);
+    }
+    if (out.trace.back().iter != iter) append_row(out, iter, clk.ms(), W.cur.sc);
+    out.device_ms = tm.stop();
+    download_point(ctx, W.x, out);
+    out.kernel_launches = ctx->launches - launches0;
+}
+
+}  // namespace rg

@@ -1,0 +1,51 @@
+// solver.hpp -- host-side drivers (solver.cu) and their device workspace.
+#pragma once
+
+#include "ctx.hpp"
+#include "sparse.hpp"
+#include "vecops.hpp"
+
+#include <chrono>
+#include <vector>
+
+namespace rg {
+
+struct WallClock {
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    double ms() const
+    {
+        return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    }
+};
+
+// Host-side result before it is flattened into regot_result.
+struct SolveOut {
+    regot_status status = REGOT_OK;
+    std::string message;
+    std::vector<regot_trace_row> trace;
+    std::vector<regot_step_record> steps;
+    std::vector<double> alpha, beta;  // global n / m (this rank's rows filled when sharded)
+    double device_ms = 0.0;
+    int64_t gradient_passes = 0, lse_passes = 0, kernel_launches = 0;
+};
+
+// Everything the solvers keep on the device between calls.
+struct SolverWS {
+    DVec x, x_prev, g_prev, xs, d, trial, sdiff, ydiff, v, ag, au, av, tmp;
+    GradOut cur, cand, trial_g[2];
+    DotScratch dots;
+    SparseWS sparse;
+    regot_sparse A;  // H_Omega + tau I at the frozen pattern (SplrState::A)
+};
+
+SolverWS& solver_ws(regot_ctx* ctx);
+
+void solve_sinkhorn(regot_ctx* ctx, const double* alpha0, const double* beta0, const regot_sinkhorn_config& cfg,
+                    SolveOut& out);
+void solve_splr(regot_ctx* ctx, const double* alpha0, const double* beta0, const regot_splr_config& cfg, SolveOut& out);
+
+// compute_direction alone (regot_b200_compute_direction); false on PCG breakdown
+bool compute_direction_api(regot_ctx* ctx, const regot_sparse& A, const DVec& g, double g_sqnorm, bool active, double xi,
+                           double zeta, const DVec& u, const DVec& v, double rtol, int max_iter, DVec& d, int& cg_iters);
+
+}  // namespace rg

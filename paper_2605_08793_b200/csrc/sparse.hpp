@@ -1,0 +1,84 @@
+// sparse.hpp -- device representation of A = H_Omega + tau I (sparsity.h:97-195)
+// and the scratch of the top-k selection.
+//
+// A = [ diag(dA)   B      ]    B = T_Omega / eta, nloc x (m-1), stored twice:
+//     [ B'         diag(dB) ]   CSR (row-major == the reference's lexicographic
+//                               coordinate order) for B v, CSC for B' v.
+// The reference's CSC-of-both-triangles layout (sparsity.h:249-289) is produced
+// on export only.
+#pragma once
+
+#include "ctx.hpp"
+
+struct regot_sparse {
+    regot_ctx* ctx = nullptr;
+    int64_t n = 0, m = 0, nloc = 0, row_begin = 0;
+    int64_t nnz = 0;  // |Omega| restricted to this rank's rows
+    double tau = 0.0;
+    // CSR of B over local rows; `row` is the local row of each entry
+    rg::DevBuf<int> rowptr, col, row;
+    rg::DevBuf<double> val, mval;  // values and the gathered costs M_ij (so value refreshes never touch M)
+    // CSC of B (columns 0..m-2), rows ascending inside a column
+    rg::DevBuf<int> cscptr, cscrow, slot;  // slot[t] = CSC position of CSR entry t
+    rg::DevBuf<double> cscval;
+    rg::DevBuf<double> dA, dB;  // diagonal: row_sums/eta + tau, col_sums/eta + tau
+    // rows / columns too long for one warp (always includes row 0 and column 0 of Omega*)
+    rg::DevBuf<int> long_rows, long_cols;
+    int n_long_rows = 0, n_long_cols = 0;
+};
+
+namespace rg {
+
+struct SparseWS {
+    // top-k selection scratch
+    DevBuf<unsigned long long> hist;  // 4096 coarse bins | 8192 refine bins
+    DevBuf<int> cnt, pre, rowtot, candptr;
+    DevBuf<unsigned long long> cand_key;
+    DevBuf<int> cand_col, cand_row, keep, tie, scan_a, scan_b;
+    DevBuf<double> cand_m;
+    DevBuf<unsigned char> cub_tmp;
+    DevBuf<int> sort_k0, sort_k1, sort_v0, sort_v1;
+    unsigned long long* h_hist = nullptr;  // pinned
+    int* h_small = nullptr;                // pinned
+    // PCG scratch
+    DevBuf<double> cg;  // vectors
+    DevBuf<double> cg_scal;
+    DevBuf<double> cg_partials;
+    DevBuf<unsigned int> cg_ticket;
+    double* h_cg = nullptr;  // pinned
+    ~SparseWS()
+    {
+        if (h_hist) cudaFreeHost(h_hist);
+        if (h_small) cudaFreeHost(h_small);
+        if (h_cg) cudaFreeHost(h_cg);
+    }
+};
+
+// Source of plan entries for the selection sweeps.
+enum TopkSource { kFromDual = 0, kFromDenseT = 1 };
+
+// k2_topk.cu -- select_topk (sparsity.h:44-91) + the structural half of assemble
+// (sparsity.h:226-289) on the device.  In kFromDual mode T is formed on the fly
+// from (alpha, beta) and the resident cost matrix; in kFromDenseT mode the
+// "cost matrix" resident in ctx IS the dense plan (the parity entry point).
+// Fills S's structure arrays (rowptr/col/row/mval, CSC, slot, long rows).
+void topk_build_pattern(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, TopkSource src, const double* alpha,
+                        const double* beta, int64_t k, regot_sparse& S);
+// assemble at a caller-given pattern (host coords, sorted unique, global rows)
+void pattern_from_coords(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, const int32_t* coords, int64_t ncoords,
+                         regot_sparse& S);
+// builds CSC + slot map + long row/col lists from rowptr/col/row (called by both of the above)
+void finish_structure(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, regot_sparse& S);
+
+// k4_sparse.cu -- fill_transport_values (sparsity.h:202-220): K3
+void sparse_fill_values(regot_ctx* ctx, cudaStream_t st, regot_sparse& S, const double* alpha, const double* beta,
+                        double tau, const double* row_sums, const double* col_sums);
+// y = A v on free vectors (K4); nrhs systems stored back to back with strides
+void sparse_matvec(regot_ctx* ctx, cudaStream_t st, ncclComm* comm, const regot_sparse& S, int nrhs, const double* va,
+                   const double* vb, double* ya, double* yb, int64_t stride_a, int64_t stride_b);
+// Jacobi-PCG (K5): solves A x_k = rhs_k for k < nrhs simultaneously.  Returns
+// iterations, or -1 on breakdown (p'Ap <= 0: "not positive definite").
+int sparse_pcg(regot_ctx* ctx, cudaStream_t st, ncclComm* comm, SparseWS& ws, const regot_sparse& S, int nrhs,
+               const DVec* const* rhs, DVec* const* sol, double rtol, int max_iter);
+
+}  // namespace rg

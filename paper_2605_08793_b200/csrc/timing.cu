@@ -9,11 +9,15 @@ void time_kernel_once(regot_ctx* ctx, int which)
     case 0:
         launch_gradient_sweep_only(ctx, ctx->stream, ctx->ws_main, ctx->api_x.a.p, ctx->api_x.b.p);
         break;
+    case 1:
+        launch_row_lse_sweep_only(ctx, ctx->stream, ctx->ws_main, ctx->api_x.b.p);
+        break;
+    case 2:
+        launch_col_lse_sweep_only(ctx, ctx->stream, ctx->ws_main, ctx->api_x.a.p);
+        break;
     default:
         raise(REGOT_E_VALIDATION, "time_kernel: unknown kernel id");
     }
 }
-
-void solver_ws_free(regot_ctx*) {}
 
 }  // namespace rg

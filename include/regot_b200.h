@@ -77,7 +77,7 @@ typedef struct regot_splr_config {
     int32_t tile_cols; /* default 32 */
     /* --- extensions --- */
     int32_t cg_max_iter; /* PCG iteration cap per solve; <=0 -> 20 * dim */
-    double cg_rtol;      /* PCG relative preconditioned-residual tolerance; <=0 -> 1e-10 */
+    double cg_rtol;      /* PCG relative preconditioned-residual tolerance; <=0 -> 1e-6 */
 } regot_splr_config;
 
 /* SinkhornConfig (sinkhorn.h:16-31). */
@@ -268,6 +268,12 @@ void regot_b200_result_free(regot_result* r);
  * which: 0 fused gradient (K1), 1 row LSE (K7), 2 column LSE (K8). */
 regot_status regot_b200_time_kernel(regot_ctx* ctx, int which, const double* alpha, const double* beta,
                                     int iters, float* ms_out);
+/* Per-kernel device timing inside solves: when enabled every sweep / SpMV launch
+ * is bracketed by CUDA events on its stream.  kind: 0 fused gradient (K1),
+ * 1 row LSE (K7), 2 column LSE (K8), 3 top-k sweeps (K2), 4 SpMV (K4).
+ * set_profiling() also clears the recorded events. */
+regot_status regot_b200_set_profiling(regot_ctx* ctx, int enabled);
+regot_status regot_b200_get_profile(regot_ctx* ctx, int kind, int64_t* launches, double* total_ms);
 /* Kernels of this library launched on this context since creation. */
 int64_t regot_b200_launch_count(const regot_ctx* ctx);
 

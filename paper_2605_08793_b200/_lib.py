@@ -169,6 +169,8 @@ PROTOTYPES = {
     "regot_b200_result_free": (None, [C.POINTER(ResultC)]),
     "regot_b200_time_kernel": (C.c_int, [_vp, C.c_int, _vp, _vp, C.c_int, c_float_p]),
     "regot_b200_launch_count": (C.c_int64, [_vp]),
+    "regot_b200_set_profiling": (C.c_int, [_vp, C.c_int]),
+    "regot_b200_get_profile": (C.c_int, [_vp, C.c_int, c_int64_p, c_double_p]),
 }
 
 _lib = None

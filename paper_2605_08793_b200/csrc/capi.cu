@@ -73,6 +73,37 @@ const char* regot_b200_last_error(const regot_ctx* ctx) { return ctx ? ctx->err.
 
 int64_t regot_b200_launch_count(const regot_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
+regot_status regot_b200_set_profiling(regot_ctx* ctx, int enabled)
+{
+    return guard(ctx, [&] {
+        RG_CUDA(cudaDeviceSynchronize());
+        for (auto& e : ctx->prof_events) {
+            cudaEventDestroy(e.a);
+            cudaEventDestroy(e.b);
+        }
+        ctx->prof_events.clear();
+        ctx->profiling = enabled != 0;
+    });
+}
+
+regot_status regot_b200_get_profile(regot_ctx* ctx, int kind, int64_t* launches, double* total_ms)
+{
+    return guard(ctx, [&] {
+        RG_CUDA(cudaDeviceSynchronize());
+        int64_t n = 0;
+        double tot = 0.0;
+        for (const auto& e : ctx->prof_events) {
+            if (e.kind != kind) continue;
+            float ms = 0.f;
+            RG_CUDA(cudaEventElapsedTime(&ms, e.a, e.b));
+            tot += ms;
+            ++n;
+        }
+        if (launches) *launches = n;
+        if (total_ms) *total_ms = tot;
+    });
+}
+
 regot_status regot_b200_comm_unique_id(void* out256)
 {
     try {

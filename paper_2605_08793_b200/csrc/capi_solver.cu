@@ -380,7 +380,7 @@ regot_status regot_b200_compute_direction(regot_ctx* ctx, const regot_sparse* A,
         double gg = 0.0;
         vec_dots(ctx, ctx->stream, ctx->comm, W.dots, 1, gx, gx, &gg);
         int its = 0;
-        const double rtol = cg_rtol > 0.0 ? cg_rtol : 1e-10;
+        const double rtol = cg_rtol > 0.0 ? cg_rtol : kDefaultCgRtol;
         const long dim = (long)pr.n + pr.m - 1;
         const int maxit = cg_max_iter > 0 ? cg_max_iter : (int)std::min<long>(20 * dim, 200000);
         if (!compute_direction_api(ctx, *A, ctx->api_x, gg, active, xi, zeta, ctx->api_y, ctx->api_d, rtol, maxit, W.d, its))

@@ -131,6 +131,7 @@ regot_ctx* ctx_create(int device)
     try {
         ctx->device = device;
         ctx->sm_count = prop.multiProcessorCount;
+        if (const char* e = std::getenv("REGOT_B200_MULTIKERNEL_PCG")) ctx->force_multikernel_pcg = e[0] == '1';
         RG_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
         RG_CUDA(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
         RG_CUDA(cudaEventCreate(&ctx->ev_a));

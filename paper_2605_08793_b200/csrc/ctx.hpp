@@ -186,11 +186,44 @@ struct regot_ctx {
     rg::GradOut api_grad;
 
     void* solver_ws = nullptr;  // opaque solver workspace (solver.cu)
+
+    // tests: run the sharded (multi-kernel + NCCL) PCG path on one GPU (REGOT_B200_MULTIKERNEL_PCG=1)
+    bool force_multikernel_pcg = false;
+
+    // optional per-kernel timing (regot_b200_set_profiling): event pairs around the sweep kernels
+    bool profiling = false;
+    struct ProfEvent {
+        int kind;
+        cudaEvent_t a, b;
+    };
+    std::vector<ProfEvent> prof_events;
 };
 
 namespace rg {
 
 void ctx_require_problem(const regot_ctx* ctx);
+// kind: 0 gradient sweep (K1), 1 row LSE (K7), 2 column LSE (K8), 3 top-k sweeps (K2), 4 spmv (K4),
+// 5 persistent PCG solve (K5)
+struct ProfScope {
+    regot_ctx* ctx;
+    cudaStream_t st;
+    int idx = -1;
+    ProfScope(regot_ctx* c, cudaStream_t s, int kind) : ctx(c), st(s)
+    {
+        if (!ctx->profiling) return;
+        regot_ctx::ProfEvent e;
+        e.kind = kind;
+        cudaEventCreate(&e.a);
+        cudaEventCreate(&e.b);
+        cudaEventRecord(e.a, st);
+        ctx->prof_events.push_back(e);
+        idx = (int)ctx->prof_events.size() - 1;
+    }
+    ~ProfScope()
+    {
+        if (idx >= 0) cudaEventRecord(ctx->prof_events[(size_t)idx].b, st);
+    }
+};
 void make_sweep_plan(regot_ctx* ctx);
 void ensure_sweep_ws(regot_ctx* ctx, SweepWS& ws);
 

@@ -371,6 +371,7 @@ void launch_gradient_sweep_only(regot_ctx* ctx, cudaStream_t st, SweepWS& ws, co
         attr_set = true;
     }
     const GradParams p = make_params(ctx, ws, alpha, beta);
+    ProfScope prof(ctx, st, 0);
     k_gradient_sweep<<<ctx->plan.grid, kSweepThreads, kSweepSmem, st>>>(ctx->prob.tmap, p);
     RG_CUDA(cudaGetLastError());
     ++ctx->launches;

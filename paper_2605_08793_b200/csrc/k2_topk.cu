@@ -325,6 +325,7 @@ template <int kPass, int kSrc>
 static void launch_sweep(regot_ctx* ctx, cudaStream_t st, const TopkParams& p)
 {
     RG_CUDA(cudaFuncSetAttribute(k_topk_sweep<kPass, kSrc>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSweepSmem));
+    ProfScope prof(ctx, st, 3);
     k_topk_sweep<kPass, kSrc><<<ctx->plan.grid, kSweepThreads, kSweepSmem, st>>>(ctx->prob.tmap, p);
     RG_CUDA(cudaGetLastError());
     ++ctx->launches;
@@ -575,23 +576,57 @@ void finish_structure(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, regot_spars
         RG_CUDA(cudaGetLastError());
         ctx->launches += 4;
     }
-    // long rows / columns (always row 0 and column 0 of Omega*): one CTA each in the mat-vec
+    // Lines (rows of B, columns of B) longer than kLongLine entries -- always row 0 and column 0 of
+    // Omega* at scale -- are cut into chunks of kChunkLen entries that different warps process; the
+    // last warp to finish a line sums its chunk partials in chunk order (deterministic).
     std::vector<int> rp((size_t)nloc + 1), cp((size_t)std::max(mm1, 0) + 1);
     RG_CUDA(cudaMemcpyAsync(rp.data(), S.rowptr.p, sizeof(int) * rp.size(), cudaMemcpyDeviceToHost, st));
     RG_CUDA(cudaMemcpyAsync(cp.data(), S.cscptr.p, sizeof(int) * cp.size(), cudaMemcpyDeviceToHost, st));
     RG_CUDA(cudaStreamSynchronize(st));
-    constexpr int kLong = 1024;
-    std::vector<int> lr, lc;
-    for (int i = 0; i < nloc; ++i)
-        if (rp[(size_t)i + 1] - rp[(size_t)i] > kLong) lr.push_back(i);
-    for (int j = 0; j < mm1; ++j)
-        if (cp[(size_t)j + 1] - cp[(size_t)j] > kLong) lc.push_back(j);
-    S.n_long_rows = (int)lr.size();
-    S.n_long_cols = (int)lc.size();
-    S.long_rows.ensure(lr.size() + 1);
-    S.long_cols.ensure(lc.size() + 1);
-    if (!lr.empty()) RG_CUDA(cudaMemcpy(S.long_rows.p, lr.data(), sizeof(int) * lr.size(), cudaMemcpyHostToDevice));
-    if (!lc.empty()) RG_CUDA(cudaMemcpy(S.long_cols.p, lc.data(), sizeof(int) * lc.size(), cudaMemcpyHostToDevice));
+    std::vector<int> chunk;      // 4 ints per chunk: line, beg, end, long-line slot
+    std::vector<int> longline;   // 2 ints per long line: first chunk, chunk count
+    auto cut = [&](int line, int beg, int end) {
+        if (end - beg <= kLongLine) return;
+        const int slot = (int)longline.size() / 2;
+        longline.push_back((int)chunk.size() / 4);
+        int cnt = 0;
+        for (int b0 = beg; b0 < end; b0 += kChunkLen, ++cnt) {
+            chunk.push_back(line);
+            chunk.push_back(b0);
+            chunk.push_back(std::min(end, b0 + kChunkLen));
+            chunk.push_back(slot);
+        }
+        longline.push_back(cnt);
+    };
+    std::vector<int> ls, lm;  // short / medium lines
+    auto bin = [&](int line, int len) {
+        if (len <= kShortLine) ls.push_back(line);
+        else if (len <= kLongLine) lm.push_back(line);
+    };
+    for (int i = 0; i < nloc; ++i) {
+        cut(i, rp[(size_t)i], rp[(size_t)i + 1]);
+        bin(i, rp[(size_t)i + 1] - rp[(size_t)i]);
+    }
+    for (int j = 0; j < mm1; ++j) {
+        cut(nloc + j, cp[(size_t)j], cp[(size_t)j + 1]);
+        bin(nloc + j, cp[(size_t)j + 1] - cp[(size_t)j]);
+    }
+    S.n_lines_s = (int)ls.size();
+    S.n_lines_m = (int)lm.size();
+    S.lines_s.ensure(ls.size() + 1);
+    S.lines_m.ensure(lm.size() + 1);
+    if (!ls.empty()) RG_CUDA(cudaMemcpy(S.lines_s.p, ls.data(), sizeof(int) * ls.size(), cudaMemcpyHostToDevice));
+    if (!lm.empty()) RG_CUDA(cudaMemcpy(S.lines_m.p, lm.data(), sizeof(int) * lm.size(), cudaMemcpyHostToDevice));
+    S.n_chunks = (int)chunk.size() / 4;
+    S.n_long = (int)longline.size() / 2;
+    S.chunks.ensure(chunk.size() + 4);
+    S.longlines.ensure(longline.size() + 2);
+    S.chunk_part.ensure((size_t)S.n_chunks * 3 + 3);
+    S.chunk_cnt.ensure((size_t)S.n_long + 1);
+    RG_CUDA(cudaMemset(S.chunk_cnt.p, 0, sizeof(unsigned int) * ((size_t)S.n_long + 1)));
+    if (!chunk.empty()) RG_CUDA(cudaMemcpy(S.chunks.p, chunk.data(), sizeof(int) * chunk.size(), cudaMemcpyHostToDevice));
+    if (!longline.empty())
+        RG_CUDA(cudaMemcpy(S.longlines.p, longline.data(), sizeof(int) * longline.size(), cudaMemcpyHostToDevice));
 }
 
 }  // namespace rg

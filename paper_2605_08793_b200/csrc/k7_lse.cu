@@ -382,6 +382,7 @@ void launch_row_lse_sweep_only(regot_ctx* ctx, cudaStream_t st, SweepWS& ws, con
         attr_set = true;
     }
     const LseParams p = make_lse_params(ctx, beta, ws.rowpart.p, ws.rowpart2.p);
+    ProfScope prof(ctx, st, 1);
     k_row_lse_sweep<<<ctx->plan.grid, kSweepThreads, kSweepSmem, st>>>(ctx->prob.tmap, p);
     RG_CUDA(cudaGetLastError());
     ++ctx->launches;
@@ -395,6 +396,7 @@ void launch_col_lse_sweep_only(regot_ctx* ctx, cudaStream_t st, SweepWS& ws, con
         attr_set = true;
     }
     const LseParams p = make_lse_params(ctx, alpha, ws.colpart.p, ws.colpart2.p);
+    ProfScope prof(ctx, st, 2);
     k_col_lse_sweep<<<ctx->plan.grid, kSweepThreads, kSweepSmem, st>>>(ctx->prob.tmap, p);
     RG_CUDA(cudaGetLastError());
     ++ctx->launches;

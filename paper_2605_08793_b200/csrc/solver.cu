@@ -358,7 +358,7 @@ void solve_splr(regot_ctx* ctx, const double* alpha0, const double* beta0, const
     WallClock clk;
     Timer tm(ctx);
 
-    const double cg_rtol = cfg.cg_rtol > 0.0 ? cfg.cg_rtol : 1e-10;
+    const double cg_rtol = cfg.cg_rtol > 0.0 ? cfg.cg_rtol : kDefaultCgRtol;
     const long dim = (long)pr.n + pr.m - 1;
     const int cg_max = cfg.cg_max_iter > 0 ? cfg.cg_max_iter : (int)std::min<long>(20 * dim, 200000);
 

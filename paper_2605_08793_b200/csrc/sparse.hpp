@@ -22,10 +22,24 @@ struct regot_sparse {
     rg::DevBuf<int> cscptr, cscrow, slot;  // slot[t] = CSC position of CSR entry t
     rg::DevBuf<double> cscval;
     rg::DevBuf<double> dA, dB;  // diagonal: row_sums/eta + tau, col_sums/eta + tau
-    // rows / columns too long for one warp (always includes row 0 and column 0 of Omega*)
-    rg::DevBuf<int> long_rows, long_cols;
-    int n_long_rows = 0, n_long_cols = 0;
+    // lines (rows / columns of B) too long for one warp -- always row 0 and column 0 of
+    // Omega* at scale -- cut into chunks: chunks = {line, beg, end, slot} x n_chunks,
+    // longlines = {first chunk, count} x n_long; chunk_part / chunk_cnt are mat-vec scratch
+    rg::DevBuf<int> chunks, longlines;
+    mutable rg::DevBuf<double> chunk_part;
+    mutable rg::DevBuf<unsigned int> chunk_cnt;
+    int n_chunks = 0, n_long = 0;
+    // the other lines, binned by length so the mat-vec can give each line a fitting number of
+    // lanes: short (<= kShortLine entries, 8 lanes) and medium (<= kLongLine, one warp)
+    rg::DevBuf<int> lines_s, lines_m;
+    int n_lines_s = 0, n_lines_m = 0;
 };
+
+namespace rg {
+constexpr int kShortLine = 64;  // <= this: 8 lanes per line, four lines per warp
+constexpr int kLongLine = 512;  // > this: chunked across warps
+constexpr int kChunkLen = 256;
+}  // namespace rg
 
 namespace rg {
 

@@ -586,6 +586,15 @@ class Solver:
         return d, int(its.value)
 
     # -- measurement ----------------------------------------------------------------------
+    def set_profiling(self, enabled: bool) -> None:
+        self._check(self._lib.regot_b200_set_profiling(self._h, int(enabled)))
+
+    def get_profile(self, kind: int) -> Tuple[int, float]:
+        """(launches, total device ms) of kernel class `kind` since set_profiling(True)."""
+        n, ms = C.c_int64(0), C.c_double(0.0)
+        self._check(self._lib.regot_b200_get_profile(self._h, kind, C.byref(n), C.byref(ms)))
+        return int(n.value), float(ms.value)
+
     def time_kernel(self, which: int, x: DualPoint, iters: int) -> np.ndarray:
         al, be = self._dual(x, "time_kernel")
         ms = np.zeros(iters, dtype=np.float32)

@@ -1,5 +1,6 @@
 #!/bin/bash
-# GPU trip: parity tests, K1 timing.  Output under gpurun_out/.
-mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -15 | tee gpurun_out/pytest_gpu.txt
-timeout 300 python scripts/time_gradient.py 10000 10000 20 2>&1 | tee gpurun_out/time_gradient.txt
+for dbg in 6 7; do
+  echo "=== PCG_DBG=$dbg"; REGOT_B200_PCG_DBG=$dbg MAXIT=3 timeout 300 python scripts/solve_config.py B 2>&1 | grep -E "pcg " | tail -1
+done
+timeout 600 python scripts/solve_config.py B 0 1e-6 2>&1 | grep -E "rep|pcg" 
+timeout 600 python scripts/solve_config.py B 0 1e-6 2>&1 | grep -E "rep|pcg" 

@@ -77,7 +77,7 @@ typedef struct regot_splr_config {
     int32_t tile_cols; /* default 32 */
     /* --- extensions --- */
     int32_t cg_max_iter; /* PCG iteration cap per solve; <=0 -> 20 * dim */
-    double cg_rtol;      /* PCG relative preconditioned-residual tolerance; <=0 -> 1e-6 */
+    double cg_rtol;      /* PCG relative preconditioned-residual tolerance; <=0 -> 1e-10 */
 } regot_splr_config;
 
 /* SinkhornConfig (sinkhorn.h:16-31). */

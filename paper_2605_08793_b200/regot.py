@@ -427,6 +427,18 @@ class Solver:
         self.n, self.m, self.row_begin, self.row_count = p.n, p.m, begin, count
         self._problem_key = (id(p), p.eta, begin, count)
 
+    def set_problem_block(self, p: ProblemInstance, M_block: np.ndarray, row_begin: int, row_count: int) -> None:
+        """Upload rows [row_begin, row_begin + row_count) given as a C-contiguous (row_count x m) array
+        (e.g. a view of pinned memory); p supplies n, m, the global marginals and eta (p.M is not read)."""
+        if M_block.shape != (row_count, p.m) or not M_block.flags.c_contiguous or M_block.dtype != np.float64:
+            raise ValidationError("problem: cost matrix shape mismatch")
+        a = _vec(p.a, p.n, "problem: marginal")
+        b = _vec(p.b, p.m, "problem: marginal")
+        self._check(self._lib.regot_b200_set_problem_rows(
+            self._h, p.n, p.m, row_begin, row_count, _ptr(M_block), LAYOUT_ROWMAJOR, p.m, _ptr(a), _ptr(b), p.eta))
+        self.n, self.m, self.row_begin, self.row_count = p.n, p.m, row_begin, row_count
+        self._problem_key = None
+
     def set_problem_device(self, n: int, m: int, M_ptr: int, ld: int, a_ptr: int, b_ptr: int, eta: float,
                            rows: Optional[Tuple[int, int]] = None) -> None:
         """Borrow a row-major block already resident in HBM (raw device pointers)."""

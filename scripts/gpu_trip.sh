@@ -1,6 +1,6 @@
 #!/bin/bash
-for dbg in 6 7; do
-  echo "=== PCG_DBG=$dbg"; REGOT_B200_PCG_DBG=$dbg MAXIT=3 timeout 300 python scripts/solve_config.py B 2>&1 | grep -E "pcg " | tail -1
-done
-timeout 600 python scripts/solve_config.py B 0 1e-6 2>&1 | grep -E "rep|pcg" 
-timeout 600 python scripts/solve_config.py B 0 1e-6 2>&1 | grep -E "rep|pcg" 
+mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -3
+timeout 900 python -m pytest tests -m gpu -q 2>&1 | tail -5 | tee gpurun_out/pytest_gpu.txt
+timeout 900 python bench.py --gpus 1 --steps 5 --warmup 3 2>&1 | tail -3 | tee gpurun_out/bench.txt
+timeout 900 python bench.py --impl reference --gpus 1 --steps 2 --warmup 1 2>&1 | tail -2 | tee gpurun_out/bench_ref.txt

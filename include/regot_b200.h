@@ -262,6 +262,14 @@ void regot_b200_splr_config_hash(const regot_splr_config* cfg, char out17[17]); 
 void regot_b200_sinkhorn_config_hash(const regot_sinkhorn_config* cfg, char out17[17]); /* sinkhorn.h:33-39 */
 void regot_b200_result_free(regot_result* r);
 
+/* ---- host-side logic of the row-sharded path (pure functions, no device needed) ---- */
+/* Row block of rank `rank` of `world`: [n*rank/world, n*(rank+1)/world). */
+void regot_b200_host_row_block(int64_t n, int rank, int world, int64_t* row_begin, int64_t* row_count);
+/* Threshold search of the distributed top-k: given the (allreduced) histogram of an
+ * order-preserving key digit, the largest bucket b with count(buckets >= b) >= need, and the count
+ * strictly above it.  bucket = -1 when the histogram holds fewer than `need` entries. */
+void regot_b200_host_pick_bucket(const uint64_t* hist, int nbins, int64_t need, int* bucket, int64_t* above);
+
 /* ---- measurement hooks (bench.py; not part of the reference surface) --------- */
 /* Runs `iters` back-to-back launches of one hot kernel on the context's stream
  * at the given dual point and returns the CUDA-event time of each launch (ms).

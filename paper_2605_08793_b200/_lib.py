@@ -167,6 +167,8 @@ PROTOTYPES = {
     "regot_b200_splr_config_hash": (None, [C.POINTER(SplrConfigC), C.c_char_p]),
     "regot_b200_sinkhorn_config_hash": (None, [C.POINTER(SinkhornConfigC), C.c_char_p]),
     "regot_b200_result_free": (None, [C.POINTER(ResultC)]),
+    "regot_b200_host_row_block": (None, [C.c_int64, C.c_int, C.c_int, c_int64_p, c_int64_p]),
+    "regot_b200_host_pick_bucket": (None, [C.POINTER(C.c_uint64), C.c_int, C.c_int64, C.POINTER(C.c_int), c_int64_p]),
     "regot_b200_time_kernel": (C.c_int, [_vp, C.c_int, _vp, _vp, C.c_int, c_float_p]),
     "regot_b200_launch_count": (C.c_int64, [_vp]),
     "regot_b200_set_profiling": (C.c_int, [_vp, C.c_int]),

@@ -310,6 +310,26 @@ void regot_b200_result_free(regot_result* r)
     r->n_trace = r->n_steps = 0;
 }
 
+void regot_b200_host_row_block(int64_t n, int rank, int world, int64_t* row_begin, int64_t* row_count)
+{
+    const int64_t r0 = n * rank / world, r1 = n * (rank + 1) / world;
+    *row_begin = r0;
+    *row_count = r1 - r0;
+}
+
+void regot_b200_host_pick_bucket(const uint64_t* hist, int nbins, int64_t need, int* bucket, int64_t* above)
+{
+    // largest bucket b with count(buckets >= b) >= need; above = count(buckets > b)
+    int64_t acc = 0;
+    int b = nbins - 1;
+    for (; b >= 0; --b) {
+        if (acc + (int64_t)hist[b] >= need) break;
+        acc += (int64_t)hist[b];
+    }
+    *bucket = b;
+    *above = b >= 0 ? acc : 0;
+}
+
 int64_t regot_b200_topk_budget(int64_t n, int64_t m, double density)
 {
     // splr.h:336-340

@@ -383,12 +383,9 @@ void topk_build_pattern(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, TopkSourc
         p.hist = ws.hist.p;
         launch_sweep_src<kPassHist>(ctx, st, src, p);
         fetch_hist(ctx, st, ws, kCoarseBins);
-        long long above = 0;
-        int b = kCoarseBins - 1;
-        for (; b >= 0; --b) {
-            if (above + (long long)ws.h_hist[b] >= take) break;
-            above += (long long)ws.h_hist[b];
-        }
+        int b = -1;
+        int64_t above = 0;
+        regot_b200_host_pick_bucket((const uint64_t*)ws.h_hist, kCoarseBins, take, &b, &above);
         if (b < 0) raise(REGOT_E_CUDA, "select_topk: histogram does not cover the block (internal error)");
         bstar = (unsigned)b;
         need = take - above;
@@ -436,12 +433,9 @@ void topk_build_pattern(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, TopkSourc
             RG_CUDA(cudaGetLastError());
             ++ctx->launches;
             fetch_hist(ctx, st, ws, kFineBins);
-            int d = kFineBins - 1;
-            long long above = 0;
-            for (; d >= 0; --d) {
-                if (above + (long long)ws.h_hist[d] >= rem) break;
-                above += (long long)ws.h_hist[d];
-            }
+            int d = -1;
+            int64_t above = 0;
+            regot_b200_host_pick_bucket((const uint64_t*)ws.h_hist, kFineBins, rem, &d, &above);
             if (d < 0) raise(REGOT_E_CUDA, "select_topk: radix refinement lost the threshold (internal error)");
             rem -= above;
             fixed_mask |= (unsigned long long)(kFineBins - 1) << shift;

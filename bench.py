@@ -103,7 +103,7 @@ def cpu_sample(oracle, prob, reps: int = 1):
     return t_grad, t_sink
 
 
-def reference_pass_structure(oracle):
+def reference_pass_structure(oracle, port):
     """Gradient passes / Sinkhorn steps of one reference solve, counted by running the reference
     algorithm (oracle restatement, sparse-Cholesky direction) to 1e-8 on the same generator at
     n = m = 1024 (32 x 32 grids)."""
@@ -111,7 +111,7 @@ def reference_pass_structure(oracle):
     import ctypes as C
     from paper_2605_08793_b200 import _lib
 
-    small = oracle.gen_problem("image", 1024, 1024, ETA, d=32)
+    small = port.gen_problem("image", 1024, 1024, ETA, d=32)  # config-B generator (not in the reference)
     cfg = SplrConfigC()
     _lib.load().regot_b200_splr_config_default(C.byref(cfg))
     t0 = time.perf_counter()
@@ -130,10 +130,14 @@ def run_reference(args, rank: int):
         return
     from tests import oracle_lib
 
-    oracle = oracle_lib.load()
+    # the reference's own code (oracle/_ref: its headers compiled over the Eigen stand-in) when it was
+    # built, else the restatement (bitwise identical to it, tests/test_ref_vs_oracle_cpu.py)
+    port = oracle_lib.load()
+    oracle = oracle_lib.load_ref() or port
+    kind = "reference" if oracle is not port else "port"
     t0 = time.time()
-    prob = oracle.gen_problem("image", SIDE * SIDE, SIDE * SIDE, ETA, d=SIDE)
-    structure = reference_pass_structure(oracle)
+    prob = port.gen_problem("image", SIDE * SIDE, SIDE * SIDE, ETA, d=SIDE)
+    structure = reference_pass_structure(oracle, port)
     for _ in range(max(args.warmup, 0) and 1):
         cpu_sample(oracle, prob)
     samples = [cpu_sample(oracle, prob) for _ in range(args.steps)]
@@ -149,8 +153,10 @@ def run_reference(args, rank: int):
         "impl": "reference", "metric": "time_to_marginal_err_1e-8", "value": value, "unit": "s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * value,
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "arm": "CPU oracle restatement of the reference (oracle/liboracle.so)"},
-        "cpu_baseline": {"value": value, "unit": "s", "cores": 1, "kind": "port", "sample": sample},
+        "config": {"workload": WORKLOAD,
+                   "arm": ("the reference's own headers compiled over oracle/eigen_shim (oracle/_ref/libregot_ref.so)"
+                           if kind == "reference" else "CPU restatement of the reference (oracle/liboracle.so)")},
+        "cpu_baseline": {"value": value, "unit": "s", "cores": 1, "kind": kind, "sample": sample},
         "e2e": {"value": value, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "fused_gradient_cpu_GBps": 8.0 * prob["n"] * prob["m"] / t_grad * 1e-9,
         "wall_s": time.time() - t0,
@@ -284,11 +290,13 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     if world == 1 and not args.no_cpu:
         from tests import oracle_lib
 
-        oracle = oracle_lib.load()
+        port = oracle_lib.load()
+        oracle = oracle_lib.load_ref() or port
+        cpu_kind = "reference" if oracle is not port else "port"
         oprob = dict(n=n, m=m, M=np.asfortranarray(p.M), a=p.a, b=p.b, eta=p.eta)
         t_grad, t_sink = cpu_sample(oracle, oprob)
         est = prof.stats.gradient_passes * t_grad + (prof.stats.lse_passes / 2) * t_sink
-        cpu = {"value": est, "unit": "s", "cores": 1, "kind": "port",
+        cpu = {"value": est, "unit": "s", "cores": 1, "kind": cpu_kind,
                "sample": (f"1 fused_gradient pass ({t_grad:.3f} s, {8e-9 * n * m / t_grad:.2f} GB/s) + 1 sinkhorn_step "
                           f"({t_sink:.3f} s) of the CPU oracle on the full config-B matrix, extrapolated to the "
                           f"{prof.stats.gradient_passes} gradient-equivalent passes + {prof.stats.lse_passes // 2} Sinkhorn "

@@ -31,7 +31,8 @@ class Oracle:
         lib.rgo_last_error.restype = C.c_char_p
         lib.rgo_topk_budget.restype = C.c_long
         lib.rgo_time_gradient.restype = C.c_double
-        lib.rgo_rng_uniform_nth.restype = C.c_double
+        if hasattr(lib, "rgo_rng_uniform_nth"):
+            lib.rgo_rng_uniform_nth.restype = C.c_double
 
     def _ck(self, st):
         if st != 0:
@@ -186,3 +187,16 @@ def load() -> Oracle:
             build()
         _oracle = Oracle(C.CDLL(LIB))
     return _oracle
+
+
+REF_LIB = os.path.join(ORACLE_DIR, "_ref", "libregot_ref.so")
+_ref = None
+
+
+def load_ref():
+    """The reference's OWN code (its headers compiled over oracle/eigen_shim into oracle/_ref), or
+    None where it has not been built (it is built only where /root/reference is mounted)."""
+    global _ref
+    if _ref is None and os.path.exists(REF_LIB):
+        _ref = Oracle(C.CDLL(REF_LIB))
+    return _ref

@@ -11,6 +11,7 @@
 #include "regot/sparsity.h"
 #include "regot/sparse_chol.h"
 #include "regot/splr.h"
+#include "regot/bench.h"
 
 #include "../include/regot_b200.h"
 
@@ -374,6 +375,38 @@ double rgo_time_gradient(long n, long m, const double* M, const double* a, const
     for (int r = 0; r < reps; ++r) sink += fused_gradient(x, p).f;
     const double s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() / reps;
     return sink == 12345.678 ? -s : s;
+}
+
+// ---- data formats either side of the path (problem.h:218-280, bench.h:243-256): used once, here, to
+// write the golden ROTB / CSV fixtures under tests/golden with the reference's own writers ----
+int rgo_save_problem(const char* path, long n, long m, const double* M, const double* a, const double* b, double eta)
+{
+    return guarded([&] { save_problem(view(n, m, M, a, b, eta), path); });
+}
+
+// M (column-major like every matrix on this surface), a, b may be NULL to query the dimensions first
+int rgo_load_problem(const char* path, long* n, long* m, double* eta, double* M, double* a, double* b)
+{
+    return guarded([&] {
+        const ProblemInstance p = load_problem(path);
+        *n = (long)p.n;
+        *m = (long)p.m;
+        *eta = p.eta;
+        if (M) std::memcpy(M, p.M.data(), sizeof(double) * (size_t)(p.n * p.m));
+        if (a) put(a, p.a);
+        if (b) put(b, p.b);
+    });
+}
+
+int rgo_emit_trace_csv(const char* path, long nrows, const regot_trace_row* rows)
+{
+    return guarded([&] {
+        SolverTrace t;
+        t.algo = "splr";
+        for (long r = 0; r < nrows; ++r)
+            t.rows.push_back(TraceRow{(long)rows[r].iter, rows[r].wall_ms, rows[r].f, rows[r].marginal_error, rows[r].duality_gap});
+        emit_csv(t, path);
+    });
 }
 
 }  // extern "C"

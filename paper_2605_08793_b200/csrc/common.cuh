@@ -5,6 +5,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <string.h>
 
 namespace rg {
 
@@ -45,6 +46,30 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity)
 {
     while (!mbar_try_wait(bar, parity)) {
     }
+}
+// the same on a precomputed shared-window address (keeps generic->shared conversions out of hot loops)
+__device__ __forceinline__ void mbar_wait_s(uint32_t bar, uint32_t parity)
+{
+    uint32_t ok;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(bar), "r"(parity)
+            : "memory");
+    } while (!ok);
+}
+__device__ __forceinline__ void mbar_arrive_s(uint32_t bar)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ double2 lds_f64x2(uint32_t addr)
+{
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+    return v;
 }
 
 // ---- TMA: 2-D tiled bulk tensor load, completion on an mbarrier -------------
@@ -151,6 +176,95 @@ __device__ __forceinline__ double exp_tbl_g(double t, const double* __restrict__
     return __fma_rn(s, q, s);
 }
 
+// ---- the same exponential in the scaled domain (the sweep kernels' fast path) ---------
+// T = exp(d / eta) straight from d = (alpha_i + beta_j) - M_ij:  with cN = N / (eta ln2),
+// k = rint(d cN) comes out of one fused multiply-add against the shift constant and the
+// reduced argument rw = d cN - k (|rw| <= 1/2, in units of ln2/N) out of a second one with a
+// single rounding, so no Cody-Waite split is needed; exp(rw ln2/N) - 1 is the same degree-4
+// Taylor polynomial with the powers of ln2/N folded into its coefficients.  9 fp64
+// instructions from d to T (the t-domain form above needs 10 from t, 11 from d).  Valid for
+// |d / eta| < 700; callers test that on the high word of d (ExpScale::dl_hi) and fall back to
+// the clamped t-domain form, so every plan entry has ONE definition (plan_entry_dev) no
+// matter which kernel evaluates it.
+struct ExpScale {
+    double cN;       // N / (eta ln2)
+    double inv_eta;  // 1 / eta (slow path, same as the t-domain form)
+    unsigned dl_hi;  // high word of a double slightly below 700 eta: abs_hi(d) < dl_hi  =>  |d / eta| < 700
+};
+inline ExpScale make_exp_scale(double eta)
+{
+    ExpScale E;
+    E.cN = (double)((long double)kExpN / ((long double)eta * 0.693147180559945309417232121458176568L));
+    E.inv_eta = 1.0 / eta;
+    const double lim = 700.0 * eta * (1.0 - 1e-9);
+    unsigned long long bits;
+    memcpy(&bits, &lim, sizeof(bits));
+    E.dl_hi = (unsigned)(bits >> 32);  // truncation of the low word only lowers the bound
+    return E;
+}
+struct ExpPoly {
+    static constexpr double a1 = 0x1.62e42fefa39efp-9;   // (ln2/N)
+    static constexpr double a2 = 0x1.ebfbdff82c58fp-19;  // (ln2/N)^2 / 2
+    static constexpr double a3 = 0x1.c6b08d704a0c0p-29;  // (ln2/N)^3 / 6
+    static constexpr double a4 = 0x1.3b2ab6fba4e77p-39;  // (ln2/N)^4 / 24
+};
+
+// shared address of table entry (ki mod N) of this lane's copy: LOP3 + LEA
+__device__ __forceinline__ uint32_t exp_tbl_addr(int ki, uint32_t tbl_lane)
+{
+    uint32_t a;
+    asm("{\n\t.reg .u32 j;\n\tand.b32 j, %1, 255;\n\tmad.lo.u32 %0, j, 128, %2;\n\t}" : "=r"(a) : "r"(ki), "r"(tbl_lane));
+    return a;
+}
+__device__ __forceinline__ double lds_f64(uint32_t addr)
+{
+    double s;
+    asm("ld.shared.f64 %0, [%1];" : "=d"(s) : "r"(addr));
+    return s;
+}
+// 2^(k/N) from the table word and k: exponent inserted with one integer multiply-add
+__device__ __forceinline__ double exp_scale_pow2(double s, int ki)
+{
+    return __hiloint2double(__double2hiint(s) + (int)((unsigned)ki << (20 - kExpShift)), __double2loint(s));
+}
+
+__device__ __forceinline__ double exp_scaled(double d, double cN, uint32_t tbl_lane)
+{
+    const double kd = __fma_rn(d, cN, ExpConst::shift);
+    const int ki = __double2loint(kd);
+    const double rw = __fma_rn(d, cN, ExpConst::shift - kd);  // shift - kd == -k exactly
+    const double s = exp_scale_pow2(lds_f64(exp_tbl_addr(ki, tbl_lane)), ki);
+    double p = __fma_rn(rw, ExpPoly::a4, ExpPoly::a3);
+    p = __fma_rn(rw, p, ExpPoly::a2);
+    p = __fma_rn(rw, p, ExpPoly::a1);
+    return __fma_rn(s, rw * p, s);
+}
+
+// NE independent entries, written stage by stage so the NE dependency chains interleave
+template <int NE>
+__device__ __forceinline__ void exp_scaled_vec(const double (&d)[NE], double cN, uint32_t tbl_lane, double (&T)[NE])
+{
+    double kd[NE], rw[NE], s[NE], p[NE];
+#pragma unroll
+    for (int k = 0; k < NE; ++k) kd[k] = __fma_rn(d[k], cN, ExpConst::shift);
+#pragma unroll
+    for (int k = 0; k < NE; ++k) {
+        s[k] = lds_f64(exp_tbl_addr(__double2loint(kd[k]), tbl_lane));
+        rw[k] = __fma_rn(d[k], cN, ExpConst::shift - kd[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < NE; ++k) p[k] = __fma_rn(rw[k], ExpPoly::a4, ExpPoly::a3);
+#pragma unroll
+    for (int k = 0; k < NE; ++k) p[k] = __fma_rn(rw[k], p[k], ExpPoly::a2);
+#pragma unroll
+    for (int k = 0; k < NE; ++k) p[k] = __fma_rn(rw[k], p[k], ExpPoly::a1);
+#pragma unroll
+    for (int k = 0; k < NE; ++k) {
+        s[k] = exp_scale_pow2(s[k], __double2loint(kd[k]));
+        T[k] = __fma_rn(s[k], rw[k] * p[k], s[k]);
+    }
+}
+
 // |t| >= 700 (or NaN) test on the high word; amax accumulates max |hi|
 __device__ __forceinline__ unsigned abs_hi(double t) { return (unsigned)__double2hiint(t) & 0x7fffffffu; }
 constexpr unsigned kHi700 = 0x4085E000u;
@@ -164,6 +278,70 @@ __device__ __forceinline__ double clamp700(double t)
         t = __hiloint2double((hi & 0x80000000) | (int)kHi700, 0);
     }
     return t;
+}
+
+// plan_entry (dual.h:62-70) on the device, from d = (alpha_i + beta_j) - M_ij: the ONE definition
+// every kernel uses (gradient sweep, top-k sweeps, value refresh, dense plan), so a plan entry has
+// the same bits wherever it is evaluated:
+//     |d / eta| >= 700  ->  exp(+-700) exactly (the reference's clamp, as correctly rounded constants)
+//     otherwise         ->  exp_scaled(d)
+// The cheap filter abs_hi(d) < dl_hi proves |d / eta| < 700; only entries (or 8-entry groups) that
+// fail it pay for t = d / eta and the saturation selects.
+constexpr double kExp700 = 0x1.d945df4f8ec8ep+1009;    // exp(700)
+constexpr double kExpM700 = 0x1.14f2b0fb9307fp-1010;   // exp(-700)
+
+__device__ __forceinline__ bool saturates(double d, double inv_eta, double& sat_value)
+{
+    const double t = d * inv_eta;
+    const int hi = __double2hiint(t);
+    sat_value = hi < 0 ? kExpM700 : kExp700;
+    return ((unsigned)hi & 0x7fffffffu) >= kHi700;  // |t| >= 700 (low word of 700.0 is zero), inf or NaN
+}
+__device__ __forceinline__ double plan_entry_dev(double d, const ExpScale& E, uint32_t tbl_lane)
+{
+    double c;
+    if (abs_hi(d) >= E.dl_hi && saturates(d, E.inv_eta, c)) return c;
+    return exp_scaled(d, E.cN, tbl_lane);
+}
+// NE entries of one lane: the whole group skips the saturation test when the filter clears it
+template <int NE>
+__device__ __forceinline__ void plan_entries_dev(const double (&d)[NE], const ExpScale& E, uint32_t tbl_lane,
+                                                 double (&T)[NE])
+{
+    unsigned amax = 0;
+#pragma unroll
+    for (int k = 0; k < NE; ++k) amax = max(amax, abs_hi(d[k]));
+    // warp-uniform choice (all 32 lanes call this together): one lane with a saturating entry sends
+    // the whole warp down the second branch instead of serialising both; per-entry results do not
+    // depend on the branch taken
+    if (!__any_sync(0xffffffffu, amax >= E.dl_hi)) {
+        exp_scaled_vec<NE>(d, E.cN, tbl_lane, T);
+    } else {
+        double dc[NE], c[NE];
+        bool sat[NE];
+#pragma unroll
+        for (int k = 0; k < NE; ++k) {
+            sat[k] = saturates(d[k], E.inv_eta, c[k]);
+            dc[k] = sat[k] ? 0.0 : d[k];
+        }
+        exp_scaled_vec<NE>(dc, E.cN, tbl_lane, T);
+#pragma unroll
+        for (int k = 0; k < NE; ++k) T[k] = sat[k] ? c[k] : T[k];
+    }
+}
+// the same with the (non-replicated) table read through the read-only global path
+__device__ __forceinline__ double plan_entry_dev_g(double d, const ExpScale& E, const double* __restrict__ tbl)
+{
+    double c;
+    if (abs_hi(d) >= E.dl_hi && saturates(d, E.inv_eta, c)) return c;
+    const double kd = __fma_rn(d, E.cN, ExpConst::shift);
+    const int ki = __double2loint(kd);
+    const double rw = __fma_rn(d, E.cN, ExpConst::shift - kd);
+    const double s = exp_scale_pow2(__ldg(tbl + ((unsigned)ki & (kExpN - 1))), ki);
+    double p = __fma_rn(rw, ExpPoly::a4, ExpPoly::a3);
+    p = __fma_rn(rw, p, ExpPoly::a2);
+    p = __fma_rn(rw, p, ExpPoly::a1);
+    return __fma_rn(s, rw * p, s);
 }
 
 // ---- warp reductions ---------------------------------------------------------

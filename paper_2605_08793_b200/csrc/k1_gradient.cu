@@ -23,43 +23,71 @@ struct GradParams {
     SweepGeom g;
     const double* alpha;  // nloc
     const double* beta;   // m
-    double inv_eta;
+    ExpScale E;
     const double* exp_table;
     double* rowpart;  // n_panels x nloc
     double* colpart;  // n_segments x kTC
 };
 
-// One row of one tile for one lane: 8 plan entries from the staged costs.
+// One row of one tile for one lane: 8 plan entries from the lane's 8 staged costs.
 // Returns the lane's partial row sum; column accumulators are updated in place.
 template <bool kRagged>
-__device__ __forceinline__ double gradient_row(const double2* __restrict__ trow, int lane, double ai,
-                                               const double (&bj)[kEPL], double (&colacc)[kEPL], unsigned cmask,
-                                               double inv_eta, uint32_t tbl_lane)
+__device__ __forceinline__ double gradient_row(const double (&mv)[kEPL], double ai, const double (&bj)[kEPL],
+                                               double (&colacc)[kEPL], unsigned cmask, const ExpScale& E,
+                                               uint32_t tbl_lane)
 {
-    double2 mv[4];
+    double d[kEPL], T[kEPL];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) mv[q] = trow[q * 32 + lane];
-    double t[kEPL];
-    unsigned amax = 0;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        // same association as the reference: (alpha_i + beta_j) - M_ij, then scale (dual.h:64)
-        t[2 * q] = ((ai + bj[2 * q]) - mv[q].x) * inv_eta;
-        t[2 * q + 1] = ((ai + bj[2 * q + 1]) - mv[q].y) * inv_eta;
-        amax = max(amax, max(abs_hi(t[2 * q]), abs_hi(t[2 * q + 1])));
-    }
-    if (amax >= kHi700) {  // rare: some |t| >= 700 -> reference clamp (dual.h:65-69)
-#pragma unroll
-        for (int k = 0; k < kEPL; ++k) t[k] = clamp700(t[k]);
-    }
-    double T[kEPL];
+    for (int k = 0; k < kEPL; ++k) d[k] = (ai + bj[k]) - mv[k];  // same association as dual.h:64
+    plan_entries_dev<kEPL>(d, E, tbl_lane, T);
 #pragma unroll
     for (int k = 0; k < kEPL; ++k) {
-        T[k] = exp_tbl(t[k], tbl_lane);
         if (kRagged) T[k] = (cmask >> k) & 1u ? T[k] : 0.0;
         colacc[k] += T[k];
     }
     return ((T[0] + T[1]) + (T[2] + T[3])) + ((T[4] + T[5]) + (T[6] + T[7]));
+}
+
+// The rows of one segment (the part of this CTA's tile range inside one column panel) for one
+// consumer warp: `row` is the warp's row in the segment's first tile.  Row partials are staged per
+// lane and flushed every kRowGroup tiles with one transposing sum.
+template <bool kRagged>
+__device__ __forceinline__ void gradient_segment(RingCursor& ring, int lane, int row, int seg_tiles, int nloc,
+                                                 const double* __restrict__ alpha, const double (&bj)[kEPL],
+                                                 double (&colacc)[kEPL], unsigned cmask, const ExpScale& E,
+                                                 uint32_t tbl_lane, double* stage, double* rowdst)
+{
+    // alpha of the next row is fetched one tile ahead so its latency hides behind the current row
+    // (index clamped: the value is unused when the row does not exist)
+    double ai_next = __ldg(alpha + min(row, nloc - 1));
+    for (int done = 0; done < seg_tiles; done += kRowGroup) {
+        const int cnt = min(kRowGroup, seg_tiles - done);
+        const int row0 = row;
+        for (int k = 0; k < cnt; ++k) {
+            const double ai = ai_next;
+            ai_next = __ldg(alpha + min(row + kTR, nloc - 1));
+            double mv[kEPL];
+            ring.wait();
+            ring.load_row(mv);
+            ring.release(lane);  // the costs are in registers: the slot refills while we compute
+            double rs = 0.0;
+            if (row < nloc) rs = gradient_row<kRagged>(mv, ai, bj, colacc, cmask, E, tbl_lane);
+            stage[k * 32 + lane] = rs;
+            row += kTR;
+        }
+        // flush: lane L sums 8 of the 32 lane-partials of staged row L/4
+        __syncwarp();
+        {
+            const int k = lane >> 2, part = lane & 3;
+            const double* src = stage + k * 32 + part * 8;
+            double v = ((src[0] + src[1]) + (src[2] + src[3])) + ((src[4] + src[5]) + (src[6] + src[7]));
+            v += shfl_xor_d(v, 1);
+            v += shfl_xor_d(v, 2);
+            const int r = row0 + k * kTR;
+            if (part == 0 && k < cnt && r < nloc) rowdst[r] = v;
+        }
+        __syncwarp();
+    }
 }
 
 __global__ void __launch_bounds__(kSweepThreads, 1)
@@ -80,22 +108,19 @@ k_gradient_sweep(const __grid_constant__ CUtensorMap tmap, const GradParams p)
     if (t0 >= t1) return;
     const uint32_t tbl_lane = smem_u32(sm.table) + (uint32_t)(lane & 15) * 8u;
     double* stage = sm.scratch + warp * kTC;  // this warp's 2 KB: row staging, then column exchange
-    const double2* tile_row = reinterpret_cast<const double2*>(sm.tiles + warp * kTC);
-    const double inv_eta = p.inv_eta;
+    const ExpScale E = p.E;
     const int nloc = p.g.nloc, m = p.g.m, nrt = p.g.n_row_tiles;
     int seg = p.g.cta_seg0[blockIdx.x];
-    int s = 0;
-    uint32_t ph = 0;
+    RingCursor ring;
+    ring.init(sm, warp, lane);
 
-    long left = t1 - t0;                       // tiles still to process
+    int left = (int)(t1 - t0);                 // tiles still to process
     int panel = (int)(t0 / nrt);
     int rt = (int)(t0 - (long)panel * nrt);    // row tile inside the panel
-    // alpha of the next row is fetched one tile ahead so its latency hides behind the current row
-    double ai_next = (rt * kTR + warp < nloc) ? __ldg(p.alpha + rt * kTR + warp) : 0.0;
 
     while (left > 0) {
         // ---- one segment: the rest of panel `panel` (or of the range) ----
-        const int seg_tiles = (int)min((long)(nrt - rt), left);
+        const int seg_tiles = min(nrt - rt, left);
         const int col0 = panel * kTC;
         double bj[kEPL], colacc[kEPL];
         unsigned cmask = 0;
@@ -110,52 +135,15 @@ k_gradient_sweep(const __grid_constant__ CUtensorMap tmap, const GradParams p)
                 colacc[2 * q + e] = 0.0;
             }
         }
-        const bool ragged = (col0 + kTC > m);
-
-        int done = 0;
-        while (done < seg_tiles) {
-            // up to kRowGroup consecutive row tiles, then one transposing flush
-            const int cnt = min(kRowGroup, seg_tiles - done);
-            const int rt0 = rt;
-            for (int k = 0; k < cnt; ++k) {
-                const int row = rt * kTR + warp;
-                const double ai = ai_next;
-                {   // prefetch alpha for the tile after this one (next panel starts again at row tile 0)
-                    int nrow = row + kTR;
-                    if (rt + 1 == nrt) nrow = warp;
-                    ai_next = (nrow < nloc && left > 1) ? __ldg(p.alpha + nrow) : 0.0;
-                }
-                mbar_wait(&sm.full[s], ph);
-                double rs = 0.0;
-                if (row < nloc) {
-                    const double2* trow = tile_row + (size_t)s * (kTileElems / 2);
-                    rs = ragged ? gradient_row<true>(trow, lane, ai, bj, colacc, cmask, inv_eta, tbl_lane)
-                                : gradient_row<false>(trow, lane, ai, bj, colacc, cmask, inv_eta, tbl_lane);
-                }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&sm.empty[s]);
-                if (++s == kStages) {
-                    s = 0;
-                    ph ^= 1u;
-                }
-                stage[k * 32 + lane] = rs;
-                ++rt;
-                --left;
-            }
-            done += cnt;
-            // flush: lane L sums 8 of the 32 lane-partials of staged row L/4
-            __syncwarp();
-            {
-                const int k = lane >> 2, part = lane & 3;
-                const double* src = stage + k * 32 + part * 8;
-                double v = ((src[0] + src[1]) + (src[2] + src[3])) + ((src[4] + src[5]) + (src[6] + src[7]));
-                v += shfl_xor_d(v, 1);
-                v += shfl_xor_d(v, 2);
-                const int row = (rt0 + k) * kTR + warp;
-                if (part == 0 && k < cnt && row < nloc) p.rowpart[(size_t)panel * nloc + row] = v;
-            }
-            __syncwarp();
-        }
+        double* const rowdst = p.rowpart + (size_t)panel * nloc;
+        if (col0 + kTC > m)
+            gradient_segment<true>(ring, lane, rt * kTR + warp, seg_tiles, nloc, p.alpha, bj, colacc, cmask, E, tbl_lane,
+                                   stage, rowdst);
+        else
+            gradient_segment<false>(ring, lane, rt * kTR + warp, seg_tiles, nloc, p.alpha, bj, colacc, cmask, E, tbl_lane,
+                                    stage, rowdst);
+        left -= seg_tiles;
+        rt += seg_tiles;
 
         // column partials of this segment: exchange through shared memory,
         // summed over the kTR warps in warp order
@@ -321,7 +309,7 @@ __global__ void __launch_bounds__(kFinThreads) k_gradient_fin2(const Fin2Params 
 
 // ---- dense plan (tests / diagnostics; dual.h:83-94) ---------------------------------
 __global__ void k_plan(int nloc, int m, long ld, const double* __restrict__ M, const double* __restrict__ alpha,
-                       const double* __restrict__ beta, double inv_eta, const double* __restrict__ exp_table,
+                       const double* __restrict__ beta, const ExpScale E, const double* __restrict__ exp_table,
                        double* __restrict__ T)
 {
     __shared__ double tbl[kExpN * kExpCopies];
@@ -331,8 +319,7 @@ __global__ void k_plan(int nloc, int m, long ld, const double* __restrict__ M, c
     const long total = (long)nloc * m;
     for (long q = (long)blockIdx.x * blockDim.x + threadIdx.x; q < total; q += (long)gridDim.x * blockDim.x) {
         const int i = (int)(q / m), j = (int)(q % m);
-        const double t = ((alpha[i] + beta[j]) - M[(size_t)i * ld + j]) * inv_eta;
-        T[q] = exp_tbl(clamp700(t), tbl_lane);
+        T[q] = plan_entry_dev((alpha[i] + beta[j]) - M[(size_t)i * ld + j], E, tbl_lane);
     }
 }
 
@@ -356,7 +343,7 @@ static GradParams make_params(regot_ctx* ctx, SweepWS& ws, const double* alpha, 
     p.g.evict_first = ((double)ctx->prob.nloc * (double)ctx->prob.ld * 8.0 > 48e6) ? 1 : 0;
     p.alpha = alpha;
     p.beta = beta;
-    p.inv_eta = 1.0 / ctx->prob.eta;
+    p.E = make_exp_scale(ctx->prob.eta);
     p.exp_table = ctx->exp_table.p;
     p.rowpart = ws.rowpart.p;
     p.colpart = ws.colpart.p;
@@ -437,8 +424,8 @@ void launch_plan(regot_ctx* ctx, cudaStream_t st, const double* alpha, const dou
     const DeviceProblem& pr = ctx->prob;
     const long total = (long)pr.nloc * pr.m;
     const int grid = (int)std::max<long>(1, std::min<long>((total + 255) / 256, 8L * ctx->sm_count));
-    k_plan<<<grid, 256, 0, st>>>((int)pr.nloc, (int)pr.m, (long)pr.ld, pr.M, alpha, beta, 1.0 / pr.eta,
-                                 ctx->exp_table.p, T_rowmajor);
+    k_plan<<<grid, 256, 0, st>>>((int)pr.nloc, (int)pr.m, (long)pr.ld, pr.M, alpha, beta,
+                                 make_exp_scale(pr.eta), ctx->exp_table.p, T_rowmajor);
     RG_CUDA(cudaGetLastError());
     ++ctx->launches;
 }

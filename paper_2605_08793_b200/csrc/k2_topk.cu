@@ -42,7 +42,7 @@ struct TopkParams {
     SweepGeom g;
     const double* alpha;
     const double* beta;
-    double inv_eta;
+    ExpScale E;
     const double* exp_table;
     int row_begin;  // global index of local row 0 (Omega* first row lives on rank 0)
     int mm1;        // m - 1: the last column is never a candidate
@@ -77,7 +77,7 @@ k_topk_sweep(const __grid_constant__ CUtensorMap tmap, const TopkParams p)
     sweep_range(p.g, t0, t1);
     const uint32_t tbl_lane = smem_u32(sm.table) + (uint32_t)(lane & 15) * 8u;
     const double2* tile_row = reinterpret_cast<const double2*>(sm.tiles + warp * kTC);
-    const double inv_eta = p.inv_eta;
+    const ExpScale E = p.E;
     const int nloc = p.g.nloc, nrt = p.g.n_row_tiles, mm1 = p.mm1;
     int s = 0;
     uint32_t ph = 0;
@@ -117,9 +117,10 @@ k_topk_sweep(const __grid_constant__ CUtensorMap tmap, const TopkParams p)
                 }
                 if (kSrc == kFromDual) {
                     const double ai = __ldg(p.alpha + row);
+                    double d[kEPL];
 #pragma unroll
-                    for (int k = 0; k < kEPL; ++k)  // identical arithmetic to K1 / k_plan
-                        T[k] = exp_tbl(clamp700(((ai + bj[k]) - cost[k]) * inv_eta), tbl_lane);
+                    for (int k = 0; k < kEPL; ++k) d[k] = (ai + bj[k]) - cost[k];
+                    plan_entries_dev<kEPL>(d, E, tbl_lane, T);  // identical arithmetic to K1 / k_plan
                 } else {
 #pragma unroll
                     for (int k = 0; k < kEPL; ++k) T[k] = cost[k];
@@ -369,7 +370,7 @@ void topk_build_pattern(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, TopkSourc
     p.g.evict_first = ((double)pr.nloc * (double)pr.ld * 8.0 > 48e6) ? 1 : 0;
     p.alpha = alpha;
     p.beta = beta;
-    p.inv_eta = 1.0 / pr.eta;
+    p.E = make_exp_scale(pr.eta);
     p.exp_table = ctx->exp_table.p;
     p.row_begin = (int)pr.row_begin;
     p.mm1 = mm1;

@@ -19,7 +19,7 @@
 namespace rg {
 
 // ---- K3 -----------------------------------------------------------------------------------
-__global__ void k_fill_values(int nnz, int nloc, int mm1, double eta, double tau, const int* __restrict__ row,
+__global__ void k_fill_values(int nnz, int nloc, int mm1, double eta, const ExpScale E, double tau, const int* __restrict__ row,
                               const int* __restrict__ col, const int* __restrict__ slot,
                               const double* __restrict__ mval, const double* __restrict__ alpha,
                               const double* __restrict__ beta, const double* __restrict__ row_sums,
@@ -27,12 +27,10 @@ __global__ void k_fill_values(int nnz, int nloc, int mm1, double eta, double tau
                               double* __restrict__ val, double* __restrict__ cscval, double* __restrict__ dA,
                               double* __restrict__ dB)
 {
-    const double inv_eta = 1.0 / eta;
     const int stride = gridDim.x * blockDim.x;
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nnz; t += stride) {
         // plan_entry(...) / eta (sparsity.h:216): same T arithmetic as K1, true division by eta
-        const double tt = ((alpha[row[t]] + beta[col[t]]) - mval[t]) * inv_eta;
-        const double v = __ddiv_rn(exp_tbl_g(clamp700(tt), exp_table), eta);
+        const double v = __ddiv_rn(plan_entry_dev_g((alpha[row[t]] + beta[col[t]]) - mval[t], E, exp_table), eta);
         val[t] = v;
         cscval[slot[t]] = v;
     }
@@ -50,7 +48,7 @@ void sparse_fill_values(regot_ctx* ctx, cudaStream_t st, regot_sparse& S, const 
     S.tau = tau;
     const long work = std::max<long>(S.nnz, std::max<long>(S.nloc, S.m));
     const int grid = (int)std::max<long>(1, std::min<long>((work + 255) / 256, 8L * ctx->sm_count));
-    k_fill_values<<<grid, 256, 0, st>>>((int)S.nnz, (int)S.nloc, (int)S.m - 1, ctx->prob.eta, tau, S.row.p, S.col.p,
+    k_fill_values<<<grid, 256, 0, st>>>((int)S.nnz, (int)S.nloc, (int)S.m - 1, ctx->prob.eta, make_exp_scale(ctx->prob.eta), tau, S.row.p, S.col.p,
                                         S.slot.p, S.mval.p, alpha, beta, row_sums, col_sums, ctx->exp_table.p, S.val.p,
                                         S.cscval.p, S.dA.p, S.dB.p);
     RG_CUDA(cudaGetLastError());

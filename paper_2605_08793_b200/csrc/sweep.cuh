@@ -103,4 +103,54 @@ __device__ __forceinline__ SweepSmem sweep_prologue(unsigned char* smem, const C
     return s;
 }
 
+// Consumer-side view of the ring, all in 32-bit shared-window addresses so the per-tile
+// bookkeeping is a handful of integer instructions (no generic->shared conversions in the loop).
+struct RingCursor {
+    uint32_t full0, empty0;  // &full[0], &empty[0]
+    uint32_t row0;           // this warp's row of stage 0, this lane's first double2
+    uint32_t full, empty, row;  // the same for the current stage
+    int s;
+    uint32_t ph;
+    __device__ __forceinline__ void init(const SweepSmem& sm, int warp, int lane)
+    {
+        full0 = smem_u32(sm.full);
+        empty0 = smem_u32(sm.empty);
+        row0 = smem_u32(sm.tiles) + (uint32_t)warp * (kTC * 8) + (uint32_t)lane * 16u;
+        full = full0;
+        empty = empty0;
+        row = row0;
+        s = 0;
+        ph = 0;
+    }
+    // block until the current stage has landed
+    __device__ __forceinline__ void wait() const { mbar_wait_s(full, ph); }
+    // this lane's 8 entries of its warp's row: columns 2 lane + 64 q + {0, 1}
+    __device__ __forceinline__ void load_row(double (&mv)[kEPL]) const
+    {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const double2 v = lds_f64x2(row + (uint32_t)q * 512u);
+            mv[2 * q] = v.x;
+            mv[2 * q + 1] = v.y;
+        }
+    }
+    // hand the stage back to the producer and step to the next one
+    __device__ __forceinline__ void release(int lane)
+    {
+        __syncwarp();
+        if (lane == 0) mbar_arrive_s(empty);
+        if (++s == kStages) {
+            s = 0;
+            ph ^= 1u;
+            full = full0;
+            empty = empty0;
+            row = row0;
+        } else {
+            full += 8u;
+            empty += 8u;
+            row += (uint32_t)kTileBytes;
+        }
+    }
+};
+
 }  // namespace rg

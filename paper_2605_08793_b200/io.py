@@ -1,0 +1,301 @@
+"""Data formats either side of the hot path: the ROTB problem container,
+the trace / report CSV, the generator selector and the fixed-checkpoint benchmark protocol.
+
+Host-side mirror of proj/include/regot/problem.h:218-324 and bench.h:22-35, 62-279, 289-339 -- same
+names, argument meaning, file bytes and error classes, so a `.rotb` problem or a `%.17g` CSV written by
+the reference is read here (and vice versa) bit for bit.  Solves run on the GPU through `regot.Solver`.
+"""
+from __future__ import annotations
+
+import math
+import struct
+import time
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence, Union
+
+import numpy as np
+
+from . import problems
+from .regot import (DualPoint, FormatError, IoError, ProblemInstance, RegotError, SinkhornConfig, SolverTrace,
+                    SplrConfig, TraceRow, TruncationError, ValidationError, default_solver, splr_config_hash)
+
+ROTB_MAGIC = b"ROTB"
+ROTB_VERSION = 1
+_MAX_DIM = 1 << 24
+
+
+# ---- ROTB (problem.h:218-280) ---------------------------------------------------------------------------------
+def save_problem(p: ProblemInstance, path: str) -> None:
+    """magic "ROTB", version byte 1, little-endian u64 n, u64 m, f64 eta, a[n], b[m], M row-major."""
+    try:
+        with open(path, "wb") as f:
+            f.write(ROTB_MAGIC + bytes([ROTB_VERSION]))
+            f.write(struct.pack("<QQd", p.n, p.m, p.eta))
+            f.write(np.ascontiguousarray(p.a, dtype="<f8").tobytes())
+            f.write(np.ascontiguousarray(p.b, dtype="<f8").tobytes())
+            f.write(np.ascontiguousarray(p.M, dtype="<f8").tobytes())  # C order == row-major
+    except OSError as e:
+        raise IoError(f"save_problem: cannot open {path}") from e
+
+
+def load_problem(path: str) -> ProblemInstance:
+    try:
+        f = open(path, "rb")
+    except OSError as e:
+        raise IoError(f"load_problem: cannot open {path}") from e
+    with f:
+        head = f.read(4)
+        if len(head) < 4:
+            raise TruncationError("load_problem: truncated header")
+        if head != ROTB_MAGIC:
+            raise FormatError("load_problem: bad magic")
+        ver = f.read(1)
+        if len(ver) < 1:
+            raise TruncationError("load_problem: truncated header")
+        if ver[0] != ROTB_VERSION:
+            raise FormatError("load_problem: unsupported version")
+
+        def take(nbytes: int) -> bytes:
+            buf = f.read(nbytes)
+            if len(buf) < nbytes:
+                raise TruncationError("load_problem: truncated payload")
+            return buf
+
+        n, m = struct.unpack("<QQ", take(16))
+        if n == 0 or m == 0 or n > _MAX_DIM or m > _MAX_DIM:
+            raise FormatError("load_problem: implausible dimensions")
+        (eta,) = struct.unpack("<d", take(8))
+        a = np.frombuffer(take(8 * n), dtype="<f8").astype(np.float64)
+        b = np.frombuffer(take(8 * m), dtype="<f8").astype(np.float64)
+        M = np.frombuffer(take(8 * n * m), dtype="<f8").astype(np.float64).reshape(n, m)
+    p = ProblemInstance(int(n), int(m), M, a, b, float(eta))
+    problems.validate_problem(p)
+    return p
+
+
+# ---- generator selector (problem.h:283-324) ---------------------------------------------------------------------
+@dataclass
+class GeneratorSpec:
+    kind: str = "synth2"  # synth1-iid | synth1-diff | synth2 | file   (+ image | gmm | uniform: BASELINE configs B, D, E)
+    n: int = 64
+    m: int = 64
+    d: int = 2
+    seed: int = 0
+    path: str = ""
+
+
+def make_problem(spec: GeneratorSpec, eta: float) -> ProblemInstance:
+    if spec.kind == "file":
+        p = load_problem(spec.path)
+        if eta > 0.0:
+            p.eta = eta
+        problems.validate_problem(p)
+        return p
+    return problems.make_problem(spec.kind, spec.n, spec.m, eta, spec.d, spec.seed)  # raises on unknown kinds
+
+
+def describe(spec: GeneratorSpec) -> str:
+    if spec.kind == "file":
+        return f"file:{spec.path}"
+    s = f"{spec.kind} {spec.n}x{spec.m}"
+    if spec.kind != "synth2":
+        s += f" d={spec.d} seed={spec.seed}"
+    return s
+
+
+# ---- CSV (bench.h:22-35, 243-279, 289-339) ------------------------------------------------------------------------
+CSV_HEADER = "iter,wall_ms,f,marginal_error,duality_gap"
+
+
+def fmt_g17(v: float) -> str:
+    """printf("%.17g"): enough digits for a bit-exact strtod round trip."""
+    return "%.17g" % v
+
+
+def median(v: Sequence[float]) -> float:
+    s = sorted(v)
+    n = len(s)
+    if n == 0:
+        return math.nan
+    return s[n // 2] if n % 2 == 1 else 0.5 * (s[n // 2 - 1] + s[n // 2])
+
+
+@dataclass
+class RepeatSample:
+    wall_ms: float = 0.0
+    f: float = 0.0
+    marginal_error: float = 0.0
+    duality_gap: float = 0.0
+
+
+@dataclass
+class CheckpointStat:
+    iter: int = 0
+    failed: bool = False
+    wall_ms: float = 0.0
+    f: float = 0.0
+    marginal_error: float = 0.0
+    duality_gap: float = 0.0
+    samples: List[RepeatSample] = field(default_factory=list)
+
+
+@dataclass
+class AlgoReport:
+    algo: str = ""
+    config_hash: str = ""
+    rows: List[CheckpointStat] = field(default_factory=list)
+
+
+@dataclass
+class BenchReport:
+    problem: str = ""
+    eta: float = 0.0
+    algos: List[AlgoReport] = field(default_factory=list)
+
+
+def _row(r) -> str:
+    return f"{r.iter},{fmt_g17(r.wall_ms)},{fmt_g17(r.f)},{fmt_g17(r.marginal_error)},{fmt_g17(r.duality_gap)}\n"
+
+
+def emit_csv(obj: Union[SolverTrace, BenchReport], path: str) -> None:
+    """Trace CSV (one row per record) or report CSV ("# algo=..." comment per algorithm)."""
+    try:
+        with open(path, "w", newline="") as f:
+            f.write(CSV_HEADER + "\n")
+            if isinstance(obj, BenchReport):
+                for ar in obj.algos:
+                    f.write(f"# algo={ar.algo} problem={obj.problem} eta={fmt_g17(obj.eta)} config={ar.config_hash}\n")
+                    for r in ar.rows:
+                        f.write(_row(r))
+            else:
+                for r in obj.rows:
+                    f.write(_row(r))
+    except OSError as e:
+        raise IoError(f"emit_csv: cannot open {path}") from e
+
+
+@dataclass
+class PlotSeries:
+    algo: str
+    rows: List[TraceRow] = field(default_factory=list)
+
+
+def parse_report_csv(path: str) -> List[PlotSeries]:
+    try:
+        with open(path, "r") as f:
+            lines = f.read().split("\n")
+    except OSError as e:
+        raise IoError(f"parse_report_csv: cannot open {path}") from e
+    if lines and lines[-1] == "":
+        lines.pop()
+    if not lines:
+        raise FormatError("parse_report_csv: empty file")
+    if lines[0].strip(" \t\r\n") != CSV_HEADER:
+        raise FormatError("parse_report_csv: unexpected header")
+    series: List[PlotSeries] = []
+    for line in lines[1:]:
+        t = line.strip(" \t\r\n")
+        if not t:
+            continue
+        if t[0] == "#":
+            pos = t.find("algo=")
+            if pos >= 0:
+                end = t.find(" ", pos)
+                if end < 0:
+                    end = len(t)
+                series.append(PlotSeries(t[pos + 5:end]))
+            continue
+        parts = [q.strip(" \t\r\n") for q in t.split(",")]
+        if len(parts) != 5:
+            raise FormatError(f"parse_report_csv: malformed row '{t}'")
+        if not series:
+            series.append(PlotSeries("trace"))
+        try:
+            it = int(parts[0])
+        except ValueError as e:
+            raise FormatError(f"parse_report_csv: bad iteration field '{parts[0]}'") from e
+
+        def num(s: str) -> float:  # strtod semantics: unparsable -> 0
+            try:
+                return float(s)
+            except ValueError:
+                return 0.0
+
+        series[-1].rows.append(TraceRow(it, num(parts[1]), num(parts[2]), num(parts[3]), num(parts[4])))
+    return series
+
+
+# ---- benchmark protocol (bench.h:75-240) --------------------------------------------------------------------------
+@dataclass
+class BenchSpec:
+    gen: GeneratorSpec = field(default_factory=GeneratorSpec)
+    eta: float = 0.001
+    algos: List[str] = field(default_factory=lambda: ["sinkhorn", "splr"])
+    splr: SplrConfig = field(default_factory=SplrConfig)
+    checkpoints: List[int] = field(default_factory=lambda: [10, 20, 50, 100])
+    repeats: int = 10
+    warmup: int = 1
+
+    def validate(self) -> None:
+        if self.repeats < 1:
+            raise ValidationError("BenchSpec: repeats must be >= 1")
+        if self.warmup < 0:
+            raise ValidationError("BenchSpec: warmup must be >= 0")
+        if not self.checkpoints:
+            raise ValidationError("BenchSpec: need at least one checkpoint")
+        for i, c in enumerate(self.checkpoints):
+            if c < 1:
+                raise ValidationError("BenchSpec: checkpoints must be >= 1")
+            if i > 0 and c <= self.checkpoints[i - 1]:
+                raise ValidationError("BenchSpec: checkpoints must be strictly increasing")
+        if not self.algos:
+            raise ValidationError("BenchSpec: need at least one algorithm")
+        for a in self.algos:
+            if a not in ("sinkhorn", "splr"):
+                raise ValidationError(f"BenchSpec: unknown algorithm '{a}'")
+            if a == "splr":
+                self.splr.validate()
+
+
+def bench_solve(algo: str, p: ProblemInstance, splr_cfg: SplrConfig, iters: int, solver=None) -> DualPoint:
+    """One run for exactly `iters` iterations (tolerance zero); bench.h:148-164."""
+    s = solver or default_solver()
+    s.ensure_problem(p)
+    if algo == "sinkhorn":
+        return s.run_sinkhorn(DualPoint.zeros(p.n, p.m), SinkhornConfig(max_iter=iters, record_every=iters, tol=0.0)).x
+    c = SplrConfig(**{**splr_cfg.__dict__})
+    c.max_iter, c.record_every, c.tol = iters, iters, 0.0
+    return s.run_splr(DualPoint.zeros(p.n, p.m), c).x
+
+
+def run_benchmark(spec: BenchSpec, solver=None) -> BenchReport:
+    """Per algorithm and checkpoint: `warmup` discarded runs, `repeats` timed runs of exactly that many
+    iterations from x0 = 0, medians; a solver failure marks the cell failed (NaN) and the run goes on."""
+    spec.validate()
+    p = make_problem(spec.gen, spec.eta)
+    s = solver or default_solver()
+    s.ensure_problem(p)
+    report = BenchReport(describe(spec.gen), p.eta)
+    for algo in spec.algos:
+        ar = AlgoReport(algo, splr_config_hash(spec.splr) if algo == "splr" else "sinkhorn")
+        for cp in spec.checkpoints:
+            stat = CheckpointStat(iter=cp)
+            try:
+                for _ in range(spec.warmup):
+                    bench_solve(algo, p, spec.splr, cp, s)
+                for _ in range(spec.repeats):
+                    t0 = time.perf_counter()
+                    x = bench_solve(algo, p, spec.splr, cp, s)
+                    wall = 1e3 * (time.perf_counter() - t0)
+                    g = s.fused_gradient(x)
+                    stat.samples.append(RepeatSample(wall, g.f, g.marginal_error, g.duality_gap))
+                stat.wall_ms = median([q.wall_ms for q in stat.samples])
+                stat.f = median([q.f for q in stat.samples])
+                stat.marginal_error = median([q.marginal_error for q in stat.samples])
+                stat.duality_gap = median([q.duality_gap for q in stat.samples])
+            except RegotError:
+                stat.failed = True
+                stat.wall_ms = stat.f = stat.marginal_error = stat.duality_gap = math.nan
+            ar.rows.append(stat)
+        report.algos.append(ar)
+    return report

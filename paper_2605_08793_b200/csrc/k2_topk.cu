@@ -622,6 +622,7 @@ void finish_structure(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, regot_spars
     if (!chunk.empty()) RG_CUDA(cudaMemcpy(S.chunks.p, chunk.data(), sizeof(int) * chunk.size(), cudaMemcpyHostToDevice));
     if (!longline.empty())
         RG_CUDA(cudaMemcpy(S.longlines.p, longline.data(), sizeof(int) * longline.size(), cudaMemcpyHostToDevice));
+    if (ctx->world == 1) build_pcg_schedule(ctx, S, rp, cp);
 }
 
 }  // namespace rg

@@ -489,7 +489,7 @@ static int pcg_multikernel(regot_ctx* ctx, cudaStream_t st, ncclComm* comm, Spar
         ws.cg_ticket.ensure(1);
         RG_CUDA(cudaMemsetAsync(ws.cg_ticket.p, 0, sizeof(unsigned int), st));
     }
-    if (!ws.h_cg) RG_CUDA(cudaMallocHost((void**)&ws.h_cg, sizeof(double) * (kScalCount + 8 + 4 * kMaxRhs)));
+    if (!ws.h_cg) RG_CUDA(cudaMallocHost((void**)&ws.h_cg, sizeof(double) * 4096));
     RG_CUDA(cudaMemsetAsync(ws.cg_scal.p, 0, sizeof(double) * (kScalCount + 2 * kMaxRhs), st));
 
     CgVecs v;
@@ -754,7 +754,7 @@ static int pcg_persistent(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, const r
     const int grid = blocks_per_sm * ctx->sm_count;
     ws.cg_partials.ensure((size_t)2 * (grid + S.n_long) * 2 * kMaxRhs + 8);
     ws.cg_scal.ensure(kScalCount + 2 * kMaxRhs);
-    if (!ws.h_cg) RG_CUDA(cudaMallocHost((void**)&ws.h_cg, sizeof(double) * (kScalCount + 8 + 4 * kMaxRhs)));
+    if (!ws.h_cg) RG_CUDA(cudaMallocHost((void**)&ws.h_cg, sizeof(double) * 4096));
 
     PcgParams P;
     P.A = mat_view(ctx, S);
@@ -812,7 +812,11 @@ int sparse_pcg(regot_ctx* ctx, cudaStream_t st, ncclComm* comm, SparseWS& ws, co
                const DVec* const* rhs, DVec* const* sol, double rtol, int max_iter)
 {
     if (nrhs < 1 || nrhs > kMaxRhs) raise(REGOT_E_VALIDATION, "pcg: bad number of right-hand sides");
-    if (ctx->world == 1 && !ctx->force_multikernel_pcg) return pcg_persistent(ctx, st, ws, S, nrhs, rhs, sol, rtol, max_iter);
+    if (ctx->world == 1 && !ctx->force_multikernel_pcg) {
+        static const bool full_system = std::getenv("REGOT_B200_PCG_FULL") != nullptr;  // A/B experiments only
+        if (full_system) return pcg_persistent(ctx, st, ws, S, nrhs, rhs, sol, rtol, max_iter);
+        return pcg_schur_persistent(ctx, st, ws, S, nrhs, rhs, sol, rtol, max_iter);
+    }
     return pcg_multikernel(ctx, st, comm, ws, S, nrhs, rhs, sol, rtol, max_iter);
 }
 

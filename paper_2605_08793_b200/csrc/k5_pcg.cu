@@ -1,0 +1,867 @@
+// k5_pcg.cu -- K5 on one GPU: the whole direction solve in ONE persistent kernel, on the Schur
+// complement of the alpha block.
+//
+// Replaces numeric_factorize + solve (sparse_chol.h:330-427) inside compute_direction
+// (splr.h:128-167).  A = [D1 B; B' D2] (D1, D2 diagonal, B = T_Omega / eta) is SPD, so
+//     S x_b = r_b - B' D1^-1 r_a,   S = D2 - B' D1^-1 B,   x_a = D1^-1 (r_a - B x_b)
+// and Jacobi-preconditioned CG on S takes half the iterations of block-Jacobi CG on A (the matrix
+// is 2-cyclic) on vectors of length m-1 only.  Two right-hand sides (g and u of the Woodbury
+// identity, splr.h:134-140; A^-1 v needs no solve, see solver.cu) are carried through every pass,
+// interleaved 2 doubles per index so one gather serves both.
+//
+// Single-reduction CG (Chronopoulos-Gear): z = D2^-1 r, w = S z, gamma = r'z, delta = z'w;
+//   beta = gamma / gamma_old, alpha = gamma / (delta - beta gamma / alpha_old),
+//   p = z + beta p, s = w + beta s, x += alpha p, r -= alpha s.
+// One iteration = row phase (t = D1^-1 B z) | barrier | column phase (w = D2 z - B' t, delta
+// partials) | grid reduction | vector update (gamma partials) | grid reduction.
+//
+// What bounds a phase is the number of L2 requests an SM can issue (a scattered gather is one
+// request per entry, about 0.5 requests / clk / SM measured), not bytes.  So, per phase:
+//   * if the gathered vector fits in shared memory (16 B x length), every CTA copies it there with
+//     coalesced loads at the start of the phase and gathers from shared memory; the matrix streams
+//     from global memory, coalesced;
+//   * otherwise the warps keep THEIR part of the matrix in a shared-memory log (below) and only the
+//     gathers go to L2.
+// Work schedule (built on the host per pattern, sparse.hpp PcgSchedule): rows and columns of B are
+// cut into warp-sized items -- 4 short lines (8 lanes each), one medium line, or one 256-entry
+// chunk of a long line -- dealt to the grid's warps longest-first.  The assignment is static over
+// the CG iterations, so in log mode every warp copies its items' (index, value) pairs and diagonals
+// into a private shared-memory log once per solve and replays it each iteration; items that do not
+// fit are read from global memory.  Every sum has a fixed order (lane-sequential partials,
+// butterfly, chunk order, CTA order): results are bitwise reproducible.  No float atomics.
+#include "common.cuh"
+#include "ctx.hpp"
+#include "sparse.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+namespace rg {
+
+constexpr int kSchurThreads = 512;
+constexpr int kSchurWarps = kSchurThreads / 32;
+static_assert(kSchurWarps == kPcgWarpsPerCta, "schedule and kernel disagree on warps per CTA");
+constexpr int kLogRowBytes = 32 * 12;  // 32 doubles + 32 ints
+constexpr int kSchurScratchBytes = (4 * kSchurWarps + 8) * 8;
+
+enum { kRowMain = 0, kRowFinal = 1, kColInit = 2, kColMain = 3 };
+
+struct SchurParams {
+    int nloc, mfree, nrhs, max_iter, n_long, nw, fixed_iters;
+    int vec_smem_r, vec_smem_c;  // phase gathers from a shared-memory copy of the vector
+    int vec_bytes, log_rows;     // shared-memory carve-up: vector buffer, then log_rows rows per warp
+    double tol2;
+    const int* col;  // CSR of B
+    const double* val;
+    const int* cscrow;  // CSC of B
+    const double* cscval;
+    const double* dA;
+    const double* dB;
+    const int* items;  // kPcgItemInts per item
+    const int* wptr;   // 2 x (nw + 1)
+    const int* wres;   // 2 x nw: leading items of each warp that live in the shared-memory log
+    double* chunk_part;  // n_chunks x 2
+    unsigned int* chunk_cnt;
+    double* longdot;  // n_long x 2
+    const double* rhs_a[2];
+    const double* rhs_b[2];
+    double* sol_a[2];
+    double* sol_b[2];
+    double *ta, *zb, *wb, *pb, *sb, *rb, *xb;  // interleaved x2
+    double* blockpart;                         // gridDim.x x 4
+    unsigned int* barrier;
+    double* out;  // iters[2], -, breakdown flag, then timing
+};
+
+__device__ __forceinline__ double2 ldcg_x2(const double* p) { return __ldcg(reinterpret_cast<const double2*>(p)); }
+
+// ~2400 clk among 148 CTAs on B200 (tools/barrier_bench.cu); cooperative_groups' grid.sync costs the same
+__device__ __forceinline__ void grid_barrier(unsigned int* ctr, unsigned int& target)
+{
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        target += gridDim.x;
+        __threadfence();
+        atomicAdd(ctr, 1u);
+        unsigned int v;
+        do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+        } while (v < target);
+    }
+    __syncthreads();
+}
+
+// sum of 4 per-thread values over the grid, in CTA order (+ the long lines' dot contributions added
+// to components [2 long_range, 2 long_range + 2)); result in every thread.  Contains a grid barrier.
+__device__ __noinline__ void grid_sum4(const SchurParams& P, double (&v)[4], double* scratch, double* bcast,
+                                       unsigned int& target, int long_range)
+{
+    block_sum<4>(v, scratch);
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) P.blockpart[(size_t)blockIdx.x * 4 + k] = v[k];
+    }
+    grid_barrier(P.barrier, target);
+    if (threadIdx.x < 32 * 4) {
+        const int k = threadIdx.x >> 5, l = threadIdx.x & 31;
+        double s = 0.0;
+        for (int b = l; b < (int)gridDim.x; b += 32) s += __ldcg(P.blockpart + (size_t)b * 4 + k);
+        if (k / 2 == long_range)
+            for (int q = l; q < P.n_long; q += 32) s += __ldcg(P.longdot + (size_t)q * 2 + (k % 2));
+        s = warp_sum(s);
+        if (l == 0) bcast[k] = s;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] = bcast[k];
+    __syncthreads();
+}
+
+// This warp's log, as 32-bit shared-window addresses
+struct WarpLog {
+    uint32_t val0, idx0;  // lane 0's slot of row 0: row r of lane l at val0 + 256 r + 8 l / idx0 + 128 r + 4 l
+    uint32_t vec;         // the shared copy of the gathered vector (x2)
+};
+__device__ __forceinline__ int lds_i32(uint32_t addr)
+{
+    int v;
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ double lds_f64v(uint32_t addr)
+{
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ void sts_i32(uint32_t addr, int v) { asm volatile("st.shared.b32 [%0], %1;" ::"r"(addr), "r"(v) : "memory"); }
+__device__ __forceinline__ void sts_f64(uint32_t addr, double v) { asm volatile("st.shared.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory"); }
+__device__ __forceinline__ void sts_f64x2(uint32_t addr, double2 v)
+{
+    asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(addr), "d"(v.x), "d"(v.y) : "memory");
+}
+
+// Copy the leading `n_res` items of one phase into the warp's log, starting at log row `row`.
+// Row layout of an item: header {idx: line ids at lanes 0/8/16/24, meta (kind, nE, chunk, slot,
+// first, cnt) at lanes 1..6; val: the diagonal entry at the group leaders' lanes}, then nE rows of
+// (byte offset of the gathered x2 entry, value), lane-major.  Padding entries are (0, 0.0).
+__device__ __noinline__ int fill_log(const SchurParams& P, const bool rows, const WarpLog& L, int i0, int n_res, int row,
+                                    int lane)
+{
+    const int* __restrict__ src_idx = rows ? P.col : P.cscrow;
+    const double* __restrict__ src_val = rows ? P.val : P.cscval;
+    const double* __restrict__ diagv = rows ? P.dA : P.dB;
+    for (int q = i0; q < i0 + n_res; ++q) {
+        const int* d = P.items + (size_t)q * kPcgItemInts;
+        const int kind = __ldg(d), nE = __ldg(d + 1);
+        const int sub = kind == 0 ? lane >> 3 : 0, gl = kind == 0 ? lane & 7 : lane, stride = kind == 0 ? 8 : 32;
+        const int line = __ldg(d + 8 + sub), beg = __ldg(d + 12 + sub), len = __ldg(d + 16 + sub);
+        int h = (gl == 0) ? line : -1;
+        if (lane >= 1 && lane <= 6) h = __ldg(d + lane - 1);
+        double hv = 0.0;
+        if (gl == 0 && line >= 0) hv = __ldg(diagv + line);
+        sts_i32(L.idx0 + 128u * row + 4u * lane, h);
+        sts_f64(L.val0 + 256u * row + 8u * lane, hv);
+#pragma unroll 4
+        for (int e = 0; e < nE; ++e) {
+            const int t = gl + stride * e;
+            const bool ok = t < len;
+            const int c = ok ? __ldg(src_idx + beg + t) : 0;
+            const double v = ok ? __ldg(src_val + beg + t) : 0.0;
+            sts_i32(L.idx0 + 128u * (row + 1 + e) + 4u * lane, c * 16);
+            sts_f64(L.val0 + 256u * (row + 1 + e) + 8u * lane, v);
+        }
+        row += nE + 1;
+    }
+    return row;
+}
+
+// Transposing reduction of (a0, a1) over groups of 8 lanes (full == false) or the warp: on return
+// even lanes hold the group sum of a0, odd lanes that of a1.  3 / 5 shuffles; fixed order.
+__device__ __forceinline__ double reduce2(double a0, double a1, int lane, bool full)
+{
+    const bool odd = lane & 1;
+    double c = (odd ? a1 : a0) + shfl_xor_d(odd ? a0 : a1, 1);
+    c += shfl_xor_d(c, 2);
+    c += shfl_xor_d(c, 4);
+    if (full) {
+        c += shfl_xor_d(c, 8);
+        c += shfl_xor_d(c, 16);
+    }
+    return c;
+}
+
+// gathered x2 entry at byte offset `off`: from the shared copy or through L2
+template <bool kVecSmem>
+__device__ __forceinline__ double2 gather2(const char* gxb, uint32_t vec, unsigned off)
+{
+    if (kVecSmem) {
+        double2 v;
+        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(vec + off));
+        return v;
+    }
+    return __ldcg(reinterpret_cast<const double2*>(gxb + off));
+}
+
+// One mat-vec phase over this warp's items.  kRows: lines are rows of B, gx is a beta-space vector
+// (x2); else lines are columns of B, gx is the alpha-space vector ta (x2).  `dot` accumulates this
+// lane's component (lane & 1) of gamma (kColInit) or delta (kColMain) over the lines this warp
+// finished.
+template <bool kRows, bool kVecSmem>
+__device__ __forceinline__ void run_phase(const SchurParams& P, int mode, const double* gx, const WarpLog& L, int i0,
+                                          int i1, int n_res, int row, int lane, double& dot)
+{
+    const int* __restrict__ src_idx = kRows ? P.col : P.cscrow;
+    const double* __restrict__ src_val = kRows ? P.val : P.cscval;
+    const double* __restrict__ diagv = kRows ? P.dA : P.dB;
+    const char* gxb = reinterpret_cast<const char*>(gx);
+    const int kk = lane & 1;
+    for (int q = i0; q < i1; ++q) {
+        const bool resident = (q - i0) < n_res;
+        int kind, nE, chunk = 0, slot = 0, first = 0, cnt = 0, line;
+        double diag;
+        double a0 = 0.0, a1 = 0.0;
+        if (resident) {
+            const uint32_t h = L.idx0 + 128u * row;
+            kind = lds_i32(h + 4);
+            nE = lds_i32(h + 8);
+            if (kind == 2) {
+                chunk = lds_i32(h + 12);
+                slot = lds_i32(h + 16);
+                first = lds_i32(h + 20);
+                cnt = lds_i32(h + 24);
+            }
+            const uint32_t lead = kind == 0 ? (uint32_t)(lane & 24) : 0u;  // the group leader's lane
+            line = lds_i32(h + 4u * lead);
+            diag = lds_f64v(L.val0 + 256u * row + 8u * lead);
+            uint32_t ai = L.idx0 + 128u * (row + 1) + 4u * lane, av = L.val0 + 256u * (row + 1) + 8u * lane;
+            int e = 0;
+            for (; e + 8 <= nE; e += 8) {
+                int id[8];
+                double v[8];
+                double2 g[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    id[u] = lds_i32(ai + 128u * u);
+                    v[u] = lds_f64v(av + 256u * u);
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) g[u] = gather2<kVecSmem>(gxb, L.vec, (unsigned)id[u]);
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    a0 += v[u] * g[u].x;
+                    a1 += v[u] * g[u].y;
+                }
+                ai += 8 * 128u;
+                av += 8 * 256u;
+            }
+            for (; e + 2 <= nE; e += 2) {
+                int id[2];
+                double v[2];
+                double2 g[2];
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    id[u] = lds_i32(ai + 128u * u);
+                    v[u] = lds_f64v(av + 256u * u);
+                }
+#pragma unroll
+                for (int u = 0; u < 2; ++u) g[u] = gather2<kVecSmem>(gxb, L.vec, (unsigned)id[u]);
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    a0 += v[u] * g[u].x;
+                    a1 += v[u] * g[u].y;
+                }
+                ai += 2 * 128u;
+                av += 2 * 256u;
+            }
+            if (e < nE) {
+                const int id = lds_i32(ai);
+                const double v = lds_f64v(av);
+                const double2 g = gather2<kVecSmem>(gxb, L.vec, (unsigned)id);
+                a0 += v * g.x;
+                a1 += v * g.y;
+            }
+            row += nE + 1;
+        } else {
+            // matrix from global memory (coalesced): descriptor, then indices and values
+            const int* d = P.items + (size_t)q * kPcgItemInts;
+            const int4 m0 = __ldg(reinterpret_cast<const int4*>(d));
+            kind = m0.x;
+            nE = m0.y;
+            chunk = m0.z;
+            slot = m0.w;
+            if (kind == 2) {
+                first = __ldg(d + 4);
+                cnt = __ldg(d + 5);
+            }
+            const int sub = kind == 0 ? lane >> 3 : 0, gl = kind == 0 ? lane & 7 : lane, stride = kind == 0 ? 8 : 32;
+            line = __ldg(d + 8 + sub);
+            const int beg = __ldg(d + 12 + sub), len = __ldg(d + 16 + sub);
+            diag = line >= 0 ? __ldg(diagv + line) : 1.0;
+            for (int e0 = 0; e0 < nE; e0 += 8) {
+                int c[8];
+                double v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int t = gl + stride * (e0 + u);
+                    const bool ok = t < len;
+                    c[u] = ok ? __ldg(src_idx + beg + t) : 0;
+                    v[u] = ok ? __ldg(src_val + beg + t) : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const double2 g = gather2<kVecSmem>(gxb, L.vec, (unsigned)c[u] * 16u);
+                    a0 += v[u] * g.x;
+                    a1 += v[u] * g.y;
+                }
+            }
+        }
+        double sum = reduce2(a0, a1, lane, kind != 0);
+        // lanes 0 and 1 of a group finish components 0 and 1 of the group's line
+        bool finish = line >= 0 && (lane & (kind == 0 ? 6 : 30)) == 0;
+        bool is_long = false;
+        if (kind == 2) {
+            // chunk of a long line: publish the partial; the last chunk to arrive sums them in chunk order
+            if (finish) P.chunk_part[(size_t)chunk * 2 + kk] = sum;
+            __threadfence();
+            unsigned int prev = 0;
+            if (lane == 0) prev = atomicAdd(&P.chunk_cnt[slot], 1u);
+            prev = __shfl_sync(0xffffffffu, prev, 0);
+            if ((int)prev == cnt - 1) {
+                __threadfence();
+                double s0 = 0.0, s1 = 0.0;
+                for (int c = lane; c < cnt; c += 32) {
+                    s0 += __ldcg(P.chunk_part + (size_t)(first + c) * 2);
+                    s1 += __ldcg(P.chunk_part + (size_t)(first + c) * 2 + 1);
+                }
+                s0 = warp_sum(s0);
+                s1 = warp_sum(s1);
+                sum = kk ? s1 : s0;
+                if (lane == 0) P.chunk_cnt[slot] = 0u;
+                is_long = true;
+            } else {
+                finish = false;
+            }
+        }
+        if (finish) {
+            const size_t o = (size_t)line * 2 + kk;
+            if (kRows) {
+                if (mode == kRowMain) {
+                    P.ta[o] = sum / diag;
+                } else if (kk < P.nrhs) {
+                    const double* ra = kk ? P.rhs_a[1] : P.rhs_a[0];
+                    double* xa = kk ? P.sol_a[1] : P.sol_a[0];
+                    xa[line] = (ra[line] - sum) / diag;
+                }
+            } else {
+                double dk;
+                if (mode == kColInit) {
+                    const double* rb = kk ? P.rhs_b[1] : P.rhs_b[0];
+                    const double c = (kk < P.nrhs ? rb[line] : 0.0) - sum;  // Schur right-hand side
+                    const double z = c / diag;
+                    P.rb[o] = c;
+                    P.zb[o] = z;
+                    P.xb[o] = 0.0;
+                    P.pb[o] = 0.0;
+                    P.sb[o] = 0.0;
+                    dk = c * z;
+                } else {
+                    const double z = __ldcg(P.zb + o);
+                    const double w = diag * z - sum;
+                    P.wb[o] = w;
+                    dk = z * w;
+                }
+                // which warp finishes a long line varies from run to run: its dot product goes to a fixed
+                // slot of the ordered grid reduction instead of this lane's partial
+                if (is_long) P.longdot[(size_t)slot * 2 + kk] = dk;
+                else dot += dk;
+            }
+        }
+    }
+}
+
+// all threads of the CTA: shared copy of an x2 vector of `count` entries (after a grid barrier)
+__device__ __forceinline__ void stage_vector(uint32_t vec, const double* gx, int count)
+{
+    for (int i = threadIdx.x; i < count; i += kSchurThreads * 4) {
+        double2 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int j = i + u * kSchurThreads;
+            v[u] = j < count ? ldcg_x2(gx + (size_t)j * 2) : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int j = i + u * kSchurThreads;
+            if (j < count) sts_f64x2(vec + 16u * (uint32_t)j, v[u]);
+        }
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(kSchurThreads, 1) k_pcg_schur(const __grid_constant__ SchurParams P)
+{
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    WarpLog L;
+    L.vec = smem_u32(smem);
+    L.val0 = L.vec + (uint32_t)P.vec_bytes + (uint32_t)warp * ((uint32_t)P.log_rows * 256u);
+    L.idx0 = L.vec + (uint32_t)P.vec_bytes + (uint32_t)kSchurWarps * ((uint32_t)P.log_rows * 256u) +
+             (uint32_t)warp * ((uint32_t)P.log_rows * 128u);
+    double* scratch = reinterpret_cast<double*>(smem + P.vec_bytes + (size_t)kSchurWarps * P.log_rows * kLogRowBytes);
+    double* bcast = scratch + 4 * kSchurWarps;
+
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x, nthr = gridDim.x * blockDim.x;
+    // the schedule deals items CTA-first so the heaviest ones land on different SMs
+    const int gw = warp * gridDim.x + blockIdx.x;
+    const int nloc = P.nloc, mfree = P.mfree, nrhs = P.nrhs;
+    unsigned int bar_target = 0;
+#ifdef REGOT_PCG_TIMING  // per-section cycle counts per CTA (experiments only; costs registers)
+    long long tsec[8] = {0, 0, 0, 0, 0, 0, 0, 0}, tprev = clock64();
+#define RG_TICK(i)                         \
+    {                                      \
+        const long long now__ = clock64(); \
+        tsec[i] += now__ - tprev;          \
+        tprev = now__;                     \
+    }
+#else
+#define RG_TICK(i)
+#endif
+
+    const int r0 = P.wptr[gw], r1 = P.wptr[gw + 1], rres = P.wres[gw];
+    const int c0 = P.wptr[P.nw + 1 + gw], c1 = P.wptr[P.nw + 1 + gw + 1], cres = P.wres[P.nw + gw];
+    const int col_row0 = fill_log(P, true, L, r0, rres, 0, lane);
+    fill_log(P, false, L, c0, cres, col_row0, lane);
+    __syncwarp();
+
+    // ---- t = D1^-1 r_a; gamma0 = r' D^-1 r of the FULL system (the meaning of rtol is unchanged) ----
+    double red[4] = {0.0, 0.0, 0.0, 0.0};  // [0..1] gamma partials, [2..3] second quantity
+    for (int i = tid; i < nloc; i += nthr) {
+        const double d = P.dA[i];
+        double t[2];
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const double r = (k < nrhs) ? P.rhs_a[k][i] : 0.0;
+            t[k] = r / d;
+            red[2 + k] += r * t[k];
+        }
+        *reinterpret_cast<double2*>(P.ta + (size_t)i * 2) = make_double2(t[0], t[1]);
+    }
+    for (int j = tid; j < mfree; j += nthr) {
+        const double d = P.dB[j];
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const double r = (k < nrhs) ? P.rhs_b[k][j] : 0.0;
+            red[2 + k] += r * (r / d);
+        }
+    }
+
+    double gamma[2] = {0.0, 0.0}, gamma0[2] = {0.0, 0.0};
+    double gamma_old[2] = {1.0, 1.0}, alpha_old[2] = {1.0, 1.0};
+    bool done[2] = {false, false};
+    int iters[2] = {0, 0};
+    bool broke = false;
+    // One loop body serves the set-up pass (no row phase, column phase forms the Schur right-hand side),
+    // the CG iterations, and the final back-substitution, so each phase is instantiated once.
+    int row_mode = -1, col_mode = kColInit, it = 0;
+    for (;;) {
+        if (row_mode >= 0) {
+            // kRowMain: t = D1^-1 B z;  kRowFinal: x_a = D1^-1 (r_a - B x_b)
+            double none = 0.0;
+            const double* gx = row_mode == kRowMain ? P.zb : P.xb;
+            if (P.vec_smem_r) {
+                stage_vector(L.vec, gx, mfree);
+                run_phase<true, true>(P, row_mode, gx, L, r0, r1, 0, 0, lane, none);
+            } else {
+                run_phase<true, false>(P, row_mode, gx, L, r0, r1, rres, 0, lane, none);
+            }
+            if (row_mode == kRowFinal) break;
+        }
+        RG_TICK(1)
+        grid_barrier(P.barrier, bar_target);
+        RG_TICK(2)
+        // kColInit: c = r_b - B' t, r = c, z = D2^-1 c, x = p = s = 0, gamma = r'z
+        // kColMain: w = D2 z - B' t, delta = z'w
+        {
+            double dot = 0.0;
+            if (P.vec_smem_c) {
+                stage_vector(L.vec, P.ta, nloc);
+                run_phase<false, true>(P, col_mode, P.ta, L, c0, c1, 0, 0, lane, dot);
+            } else {
+                run_phase<false, false>(P, col_mode, P.ta, L, c0, c1, cres, col_row0, lane, dot);
+            }
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                const double dk = ((lane & 1) == k) ? dot : 0.0;
+                if (col_mode == kColInit) red[k] = dk;
+                else {
+                    red[k] = 0.0;
+                    red[2 + k] = dk;
+                }
+            }
+        }
+        RG_TICK(3)
+        grid_sum4(P, red, scratch, bcast, bar_target, col_mode == kColInit ? 0 : 1);
+        RG_TICK(4)
+        if (col_mode == kColInit) {
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                gamma[k] = red[k];
+                gamma0[k] = red[2 + k];
+                done[k] = (k >= nrhs) || gamma0[k] == 0.0 || !(gamma[k] > P.tol2 * gamma0[k]);
+                if (P.fixed_iters > 0 && k < nrhs) done[k] = false;
+            }
+            col_mode = kColMain;
+        } else {
+            double al[2], be[2];
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                al[k] = be[k] = 0.0;
+                if (done[k]) continue;
+                const double delta = red[2 + k];
+                be[k] = (it == 0) ? 0.0 : gamma[k] / gamma_old[k];
+                const double denom = delta - be[k] * gamma[k] / alpha_old[k];  // = p'Sp
+                if (!(denom > 0.0) && P.fixed_iters == 0) broke = true;        // not positive definite (or NaN)
+                al[k] = gamma[k] / denom;
+                gamma_old[k] = gamma[k];
+                alpha_old[k] = al[k];
+                ++iters[k];
+            }
+            ++it;
+            if (!broke) {
+                // p = z + beta p, s = w + beta s, x += alpha p, r -= alpha s, z = D2^-1 r, gamma = r'z
+#pragma unroll
+                for (int k = 0; k < 4; ++k) red[k] = 0.0;
+                for (int j = tid; j < mfree; j += nthr) {
+                    const size_t o = (size_t)j * 2;
+                    const double2 z2 = ldcg_x2(P.zb + o), p2 = ldcg_x2(P.pb + o), w2 = ldcg_x2(P.wb + o);
+                    const double2 s2 = ldcg_x2(P.sb + o), x2 = ldcg_x2(P.xb + o), r2 = ldcg_x2(P.rb + o);
+                    const double dj = __ldg(P.dB + j);
+                    const double zv[2] = {z2.x, z2.y}, pv[2] = {p2.x, p2.y}, wv[2] = {w2.x, w2.y};
+                    const double sv[2] = {s2.x, s2.y}, xv[2] = {x2.x, x2.y}, rv[2] = {r2.x, r2.y};
+                    double pn[2], sn[2], xn[2], rn[2], zn[2];
+#pragma unroll
+                    for (int k = 0; k < 2; ++k) {
+                        pn[k] = zv[k] + be[k] * pv[k];
+                        sn[k] = wv[k] + be[k] * sv[k];
+                        xn[k] = xv[k] + al[k] * pn[k];
+                        rn[k] = rv[k] - al[k] * sn[k];
+                        zn[k] = rn[k] / dj;
+                        if (done[k]) {  // a finished system is frozen
+                            pn[k] = pv[k];
+                            sn[k] = sv[k];
+                            xn[k] = xv[k];
+                            rn[k] = rv[k];
+                            zn[k] = zv[k];
+                        } else {
+                            red[k] += rn[k] * zn[k];
+                        }
+                    }
+                    *reinterpret_cast<double2*>(P.pb + o) = make_double2(pn[0], pn[1]);
+                    *reinterpret_cast<double2*>(P.sb + o) = make_double2(sn[0], sn[1]);
+                    *reinterpret_cast<double2*>(P.xb + o) = make_double2(xn[0], xn[1]);
+                    *reinterpret_cast<double2*>(P.rb + o) = make_double2(rn[0], rn[1]);
+                    *reinterpret_cast<double2*>(P.zb + o) = make_double2(zn[0], zn[1]);
+                }
+                // gamma is needed by every CTA before the next decision; z by the next row phase
+                RG_TICK(5)
+                grid_sum4(P, red, scratch, bcast, bar_target, -1);
+                RG_TICK(6)
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    if (done[k]) continue;
+                    gamma[k] = red[k];
+                    if (!(gamma[k] > P.tol2 * gamma0[k]) && P.fixed_iters == 0) done[k] = true;
+                }
+            }
+        }
+        bool all_done = done[0] && done[1];
+        if (P.fixed_iters > 0) all_done = it >= P.fixed_iters;
+        row_mode = (all_done || broke || it >= P.max_iter) ? kRowFinal : kRowMain;
+    }
+    // planar outputs
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        if (k >= nrhs) break;
+        for (int j = tid; j < mfree; j += nthr) P.sol_b[k][j] = __ldcg(P.xb + (size_t)j * 2 + k);
+        if (tid == 0) P.sol_b[k][mfree] = 0.0;
+    }
+    RG_TICK(7)
+    if (tid == 0) {
+#pragma unroll
+        for (int k = 0; k < 2; ++k) P.out[k] = (double)iters[k];
+        P.out[3] = broke ? 1.0 : 0.0;
+    }
+#ifdef REGOT_PCG_TIMING
+    if (threadIdx.x == 0)
+        for (int k = 0; k < 8; ++k) P.out[4 + (size_t)blockIdx.x * 8 + k] = (double)tsec[k];
+#endif
+#undef RG_TICK
+}
+
+// ---- host: the work schedule ------------------------------------------------------------------
+namespace {
+struct HostItem {
+    int kind = 0, nE = 0, chunk = 0, slot = 0, first = 0, cnt = 0;
+    int line[4] = {-1, -1, -1, -1}, beg[4] = {0, 0, 0, 0}, len[4] = {0, 0, 0, 0};
+};
+}  // namespace
+
+void build_pcg_schedule(regot_ctx* ctx, regot_sparse& S, const std::vector<int>& rp, const std::vector<int>& cp)
+{
+    PcgSchedule& Q = S.pcg;
+    const int nloc = (int)S.nloc, mm1 = std::max((int)S.m - 1, 0);
+    const int grid = ctx->sm_count, nw = grid * kPcgWarpsPerCta;
+    Q.nw = nw;
+    // shared-memory plan (see the header comment): a phase whose gathered vector fits next to the
+    // reduction scratch gathers from a shared copy; the other phase(s) get the rest as matrix log
+    const int budget = kPcgSmemBudget - kSchurScratchBytes;
+    const long need_r = 16L * std::max(mm1, 1), need_c = 16L * std::max(nloc, 1);  // row phase gathers beta-space
+    Q.vec_smem_r = need_r <= kPcgVecSmemMax;
+    Q.vec_smem_c = need_c <= kPcgVecSmemMax;
+    Q.vec_bytes = (int)std::max(Q.vec_smem_r ? need_r : 0L, Q.vec_smem_c ? need_c : 0L);
+    Q.vec_bytes = (Q.vec_bytes + 127) / 128 * 128;
+    Q.log_rows = (Q.vec_smem_r && Q.vec_smem_c) ? 0 : (budget - Q.vec_bytes) / (kPcgWarpsPerCta * kLogRowBytes);
+    const int phase_logs[2] = {Q.vec_smem_r ? 0 : 1, Q.vec_smem_c ? 0 : 1};
+    int n_long = 0, n_chunks = 0;
+    std::vector<int> h_items, h_wptr((size_t)2 * (nw + 1), 0), h_wres((size_t)2 * nw, 0);
+    std::vector<int> used_rows((size_t)nw, 0);
+    long resident_entries = 0, global_entries = 0;
+
+    for (int phase = 0; phase < 2; ++phase) {
+        const std::vector<int>& ptr = phase == 0 ? rp : cp;
+        const int nlines = phase == 0 ? nloc : mm1;
+        std::vector<HostItem> items;
+        // short lines, bucketed by length (descending) so a quad holds lines of similar length
+        std::vector<std::vector<int>> bucket((size_t)kShortLine + 1);
+        for (int l = 0; l < nlines; ++l) {
+            const int beg = ptr[(size_t)l], len = ptr[(size_t)l + 1] - beg;
+            if (len > kLongLine) {
+                const int slot = n_long++, first = n_chunks;
+                const int cnt = (len + kChunkLen - 1) / kChunkLen;
+                for (int c = 0; c < cnt; ++c) {
+                    HostItem it;
+                    it.kind = 2;
+                    it.line[0] = l;
+                    it.beg[0] = beg + c * kChunkLen;
+                    it.len[0] = std::min(kChunkLen, len - c * kChunkLen);
+                    it.nE = (it.len[0] + 31) / 32;
+                    it.chunk = n_chunks++;
+                    it.slot = slot;
+                    it.first = first;
+                    it.cnt = cnt;
+                    items.push_back(it);
+                }
+            } else if (len > kShortLine) {
+                HostItem it;
+                it.kind = 1;
+                it.line[0] = l;
+                it.beg[0] = beg;
+                it.len[0] = len;
+                it.nE = (len + 31) / 32;
+                items.push_back(it);
+            } else {
+                bucket[(size_t)len].push_back(l);
+            }
+        }
+        {
+            HostItem it;
+            int fill = 0;
+            auto flush = [&]() {
+                if (!fill) return;
+                int mx = 0;
+                for (int s = 0; s < fill; ++s) mx = std::max(mx, it.len[s]);
+                it.kind = 0;
+                it.nE = (mx + 7) / 8;
+                items.push_back(it);
+                it = HostItem();
+                fill = 0;
+            };
+            for (int len = kShortLine; len >= 0; --len)
+                for (int l : bucket[(size_t)len]) {
+                    it.line[fill] = l;
+                    it.beg[fill] = ptr[(size_t)l];
+                    it.len[fill] = len;
+                    if (++fill == 4) flush();
+                }
+            flush();
+        }
+        // longest first (stable), dealt over the warps in a snake so the loads stay level
+        std::vector<int> order(items.size());
+        for (size_t q = 0; q < order.size(); ++q) order[q] = (int)q;
+        std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return items[(size_t)x].nE > items[(size_t)y].nE; });
+        std::vector<std::vector<int>> mine((size_t)nw);
+        for (size_t q = 0; q < order.size(); ++q) {
+            const size_t round = q / (size_t)nw, pos = q % (size_t)nw;
+            const size_t w = (round & 1) ? (size_t)nw - 1 - pos : pos;
+            mine[w].push_back(order[q]);
+        }
+        const int base = (int)(h_items.size() / kPcgItemInts);
+        int cursor = base;
+        for (int w = 0; w < nw; ++w) {
+            h_wptr[(size_t)phase * (nw + 1) + w] = cursor;
+            bool open = true;
+            int nres = 0;
+            for (int q : mine[(size_t)w]) {
+                const HostItem& it = items[(size_t)q];
+                long entries = 0;
+                for (int s = 0; s < 4; ++s) entries += it.len[s];
+                if (open && phase_logs[phase] && used_rows[(size_t)w] + it.nE + 1 <= Q.log_rows) {
+                    used_rows[(size_t)w] += it.nE + 1;
+                    ++nres;
+                    resident_entries += entries;
+                } else {
+                    open = false;
+                    global_entries += entries;
+                }
+                const int rec[kPcgItemInts] = {it.kind, it.nE, it.chunk, it.slot, it.first, it.cnt, 0, 0,
+                                               it.line[0], it.line[1], it.line[2], it.line[3],
+                                               it.beg[0], it.beg[1], it.beg[2], it.beg[3],
+                                               it.len[0], it.len[1], it.len[2], it.len[3], 0, 0, 0, 0};
+                h_items.insert(h_items.end(), rec, rec + kPcgItemInts);
+                ++cursor;
+            }
+            h_wres[(size_t)phase * nw + w] = nres;
+        }
+        h_wptr[(size_t)phase * (nw + 1) + nw] = cursor;
+    }
+    Q.n_long = n_long;
+    Q.n_chunks = n_chunks;
+    Q.resident_entries = resident_entries;
+    Q.global_entries = global_entries;
+    Q.items.ensure(h_items.size() + kPcgItemInts);
+    Q.wptr.ensure(h_wptr.size());
+    Q.wres.ensure(h_wres.size());
+    Q.chunk_part.ensure((size_t)n_chunks * 2 + 2);
+    Q.chunk_cnt.ensure((size_t)n_long + 1);
+    Q.longdot.ensure((size_t)n_long * 2 + 2);
+    if (!h_items.empty())
+        RG_CUDA(cudaMemcpy(Q.items.p, h_items.data(), sizeof(int) * h_items.size(), cudaMemcpyHostToDevice));
+    RG_CUDA(cudaMemcpy(Q.wptr.p, h_wptr.data(), sizeof(int) * h_wptr.size(), cudaMemcpyHostToDevice));
+    RG_CUDA(cudaMemcpy(Q.wres.p, h_wres.data(), sizeof(int) * h_wres.size(), cudaMemcpyHostToDevice));
+    RG_CUDA(cudaMemset(Q.chunk_cnt.p, 0, sizeof(unsigned int) * ((size_t)n_long + 1)));
+    RG_CUDA(cudaMemset(Q.longdot.p, 0, sizeof(double) * ((size_t)n_long * 2 + 2)));
+}
+
+// ---- host: launch --------------------------------------------------------------------------------
+// one launch solves up to 2 systems
+static int pcg_schur_launch(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, const regot_sparse& S, int nrhs,
+                            const DVec* const* rhs, DVec* const* sol, double rtol, int max_iter)
+{
+    const PcgSchedule& Q = S.pcg;
+    const int nloc = (int)S.nloc, mfree = std::max((int)S.m - 1, 0);
+    const int grid = ctx->sm_count;
+    if (Q.nw != grid * kPcgWarpsPerCta) raise(REGOT_E_CUDA, "pcg: schedule was built for a different grid (internal error)");
+    const int smem = Q.vec_bytes + kPcgWarpsPerCta * Q.log_rows * kLogRowBytes + kSchurScratchBytes;
+    static bool attr_set = false;
+    if (!attr_set) {
+        RG_CUDA(cudaFuncSetAttribute(k_pcg_schur, cudaFuncAttributeMaxDynamicSharedMemorySize, kPcgSmemBudget));
+        int per_sm = 0;
+        RG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pcg_schur, kSchurThreads, kPcgSmemBudget));
+        if (per_sm < 1) raise(REGOT_E_CUDA, "pcg: persistent kernel does not fit on an SM");
+        attr_set = true;
+    }
+    if (smem > kPcgSmemBudget) raise(REGOT_E_CUDA, "pcg: shared-memory plan exceeds the budget (internal error)");
+    const size_t va = (size_t)std::max(nloc, 1) * 2, vb = (size_t)std::max(mfree, 1) * 2;
+    ws.cg.ensure(va + 6 * vb + 16);
+    ws.cg_partials.ensure((size_t)grid * 4 + 8);
+    ws.cg_scal.ensure(16 + (size_t)grid * 8);
+    ws.cg_barrier.ensure(4);
+    if (!ws.h_cg) RG_CUDA(cudaMallocHost((void**)&ws.h_cg, sizeof(double) * 4096));
+
+    SchurParams P;
+    std::memset(&P, 0, sizeof(P));
+    P.nloc = nloc;
+    P.mfree = mfree;
+    P.nrhs = nrhs;
+    P.max_iter = max_iter;
+    P.n_long = Q.n_long;
+    P.nw = Q.nw;
+    P.fixed_iters = 0;
+    if (const char* e = std::getenv("REGOT_B200_PCG_FIXED_ITERS")) P.fixed_iters = std::atoi(e);
+    P.vec_smem_r = Q.vec_smem_r;
+    P.vec_smem_c = Q.vec_smem_c;
+    P.vec_bytes = Q.vec_bytes;
+    P.log_rows = Q.log_rows;
+#ifdef REGOT_PCG_TIMING
+    const bool timing = true;
+#else
+    const bool timing = false;
+#endif
+    P.tol2 = rtol * rtol;
+    P.col = S.col.p;
+    P.val = S.val.p;
+    P.cscrow = S.cscrow.p;
+    P.cscval = S.cscval.p;
+    P.dA = S.dA.p;
+    P.dB = S.dB.p;
+    P.items = Q.items.p;
+    P.wptr = Q.wptr.p;
+    P.wres = Q.wres.p;
+    P.chunk_part = Q.chunk_part.p;
+    P.chunk_cnt = Q.chunk_cnt.p;
+    P.longdot = Q.longdot.p;
+    for (int k = 0; k < 2; ++k) {
+        const int kk = k < nrhs ? k : 0;
+        P.rhs_a[k] = rhs[kk]->a.p;
+        P.rhs_b[k] = rhs[kk]->b.p;
+        sol[kk]->ensure(S.nloc, S.m);
+        P.sol_a[k] = sol[kk]->a.p;
+        P.sol_b[k] = sol[kk]->b.p;
+    }
+    double* base = ws.cg.p;
+    P.ta = base;
+    P.zb = base + va;
+    P.wb = P.zb + vb;
+    P.pb = P.wb + vb;
+    P.sb = P.pb + vb;
+    P.rb = P.sb + vb;
+    P.xb = P.rb + vb;
+    P.blockpart = ws.cg_partials.p;
+    P.barrier = ws.cg_barrier.p;
+    P.out = ws.cg_scal.p;
+    RG_CUDA(cudaMemsetAsync(P.barrier, 0, sizeof(unsigned int), st));
+    void* args[] = {&P};
+    {
+        ProfScope prof(ctx, st, 5);
+        RG_CUDA(cudaLaunchCooperativeKernel((const void*)k_pcg_schur, dim3(grid), dim3(kSchurThreads), args, (size_t)smem, st));
+    }
+    ++ctx->launches;
+    RG_CUDA(cudaMemcpyAsync(ws.h_cg, ws.cg_scal.p, sizeof(double) * (timing ? 4 + (size_t)grid * 8 : 4), cudaMemcpyDeviceToHost, st));
+    RG_CUDA(cudaStreamSynchronize(st));
+    if (timing) {
+        const char* nm[8] = {"init", "row", "bar1", "col", "reduce_delta", "update", "reduce_gamma", "final"};
+        std::fprintf(stderr, "pcg_schur kcycles min/avg/max over CTAs:");
+        for (int k = 0; k < 8; ++k) {
+            double mn = 1e300, mx = 0.0, sum = 0.0;
+            for (int b = 0; b < grid; ++b) {
+                const double v = ws.h_cg[4 + (size_t)b * 8 + k];
+                mn = std::min(mn, v);
+                mx = std::max(mx, v);
+                sum += v;
+            }
+            std::fprintf(stderr, " %s %.0f/%.0f/%.0f", nm[k], mn * 1e-3, sum / grid * 1e-3, mx * 1e-3);
+        }
+        std::fprintf(stderr, " | iters %.0f resident %ld global %ld entries, %d long lines, vec_smem %d/%d log rows %d\n", ws.h_cg[0],
+                     Q.resident_entries, Q.global_entries, Q.n_long, Q.vec_smem_r, Q.vec_smem_c, Q.log_rows);
+    }
+    if (ws.h_cg[3] != 0.0) return -1;
+    int it = 0;
+    for (int k = 0; k < nrhs; ++k) it = std::max(it, (int)ws.h_cg[k]);
+    return it;
+}
+
+int pcg_schur_persistent(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, const regot_sparse& S, int nrhs,
+                         const DVec* const* rhs, DVec* const* sol, double rtol, int max_iter)
+{
+    int it = 0;
+    for (int k0 = 0; k0 < nrhs; k0 += 2) {
+        const int r = pcg_schur_launch(ctx, st, ws, S, std::min(2, nrhs - k0), rhs + k0, sol + k0, rtol, max_iter);
+        if (r < 0) return -1;
+        it = std::max(it, r);
+    }
+    return it;
+}
+
+}  // namespace rg

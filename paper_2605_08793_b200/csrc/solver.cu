@@ -167,7 +167,7 @@ LowRankDev build_low_rank(regot_ctx* ctx, SolverWS& W, bool has_prev)
 // factorization, splr.h:400-407).  g_dot_d receives g . d.
 bool compute_direction(regot_ctx* ctx, SolverWS& W, const regot_sparse& A, const DVec& g, double g_sqnorm,
                        const LowRankDev& R, const DVec& u, const DVec& v, double rtol, int max_iter, DVec& d,
-                       double& g_dot_d, int& cg_iters)
+                       double& g_dot_d, int& cg_iters, const DVec* av_known = nullptr)
 {
     cudaStream_t st = ctx->stream;
     cg_iters = 0;
@@ -178,14 +178,18 @@ bool compute_direction(regot_ctx* ctx, SolverWS& W, const regot_sparse& A, const
     }
     const DVec* rhs[3] = {&g, &u, &v};
     DVec* sol[3] = {&W.ag, &W.au, &W.av};
-    const int nrhs = R.active ? 3 : 1;
+    // Inside the solver v = A s^- (build_low_rank) for the SAME matrix the solves use, so A^-1 v is
+    // s^- itself: the reference's third solve (splr.h:136) reproduces it to rounding, and it is passed
+    // in as av_known.  Only the stand-alone entry point (arbitrary v) solves three systems.
+    const DVec& av = av_known ? *av_known : W.av;
+    const int nrhs = R.active ? (av_known ? 2 : 3) : 1;
     const int it = sparse_pcg(ctx, st, ctx->comm, W.sparse, A, nrhs, rhs, sol, rtol, max_iter);
     if (it < 0) return false;
     cg_iters = it;
     bool woodbury = false;
     if (R.active) {
         const DVec* xs[5] = {&u, &u, &v, &u, &v};
-        const DVec* ys[5] = {&W.au, &W.av, &W.av, &W.ag, &W.ag};
+        const DVec* ys[5] = {&W.au, &av, &av, &W.ag, &W.ag};
         double r[5];
         vec_dots(ctx, st, ctx->comm, W.dots, 5, xs, ys, r);
         const double k11 = 1.0 / R.xi + r[0], k12 = r[1], k22 = 1.0 / R.zeta + r[2];
@@ -195,7 +199,7 @@ bool compute_direction(regot_ctx* ctx, SolverWS& W, const regot_sparse& A, const
             const double t1 = r[3], t2 = r[4];
             const double z1 = (k22 * t1 - k12 * t2) / det;
             const double z2 = (-k12 * t1 + k11 * t2) / det;
-            vec_lincomb(ctx, st, -1.0, W.ag, z1, &W.au, z2, &W.av, d);  // d = -(ag - au z1 - av z2)
+            vec_lincomb(ctx, st, -1.0, W.ag, z1, &W.au, z2, &av, d);  // d = -(ag - au z1 - av z2)
             woodbury = true;
         }
     }
@@ -418,7 +422,7 @@ void solve_splr(regot_ctx* ctx, const double* alpha0, const double* beta0, const
             for (;;) {
                 R = build_low_rank(ctx, W, has_prev);
                 if (compute_direction(ctx, W, W.A, W.cur.g, W.cur.sc.grad_sqnorm, R, W.ydiff, W.v, cg_rtol, cg_max, W.d,
-                                      g_dot_d, cg_iters))
+                                      g_dot_d, cg_iters, &W.sdiff))
                     break;
                 if (retries >= 8) raise(REGOT_E_NOT_POSITIVE_DEFINITE, "pcg: matrix is not positive definite");
                 tau = (tau > 0.0) ? 2.0 * tau : 1e-8;

@@ -10,6 +10,28 @@
 
 #include "ctx.hpp"
 
+namespace rg {
+// Work schedule of the persistent Schur-complement PCG kernel (k5_pcg.cu), built on the host per
+// pattern: rows and columns of B cut into warp-sized items (4 short lines / 1 medium line / 1 chunk
+// of a long line), dealt to the grid's warps longest-first.  items: kPcgItemInts ints each
+// {kind, nE, chunk, slot, first, cnt, -, -, line[4], beg[4], len[4], -...}; wptr: per phase
+// (rows, columns) nw + 1 offsets into items; wres: per phase and warp, how many of the warp's
+// leading items fit its shared-memory log.
+constexpr int kPcgWarpsPerCta = 16;
+constexpr int kPcgItemInts = 24;
+constexpr int kPcgSmemBudget = 227 * 1024;     // dynamic shared memory of the persistent kernel
+constexpr int kPcgVecSmemMax = 168 * 1024;     // largest gathered vector (16 B / entry) staged in shared memory
+struct PcgSchedule {
+    DevBuf<int> items, wptr, wres;
+    mutable DevBuf<double> chunk_part, longdot;
+    mutable DevBuf<unsigned int> chunk_cnt;
+    int nw = 0, n_long = 0, n_chunks = 0;
+    int vec_smem_r = 0, vec_smem_c = 0;  // row / column phase gathers from a shared-memory copy of the vector
+    int vec_bytes = 0, log_rows = 0;     // shared-memory carve-up (vector buffer, log rows per warp)
+    long resident_entries = 0, global_entries = 0;
+};
+}  // namespace rg
+
 struct regot_sparse {
     regot_ctx* ctx = nullptr;
     int64_t n = 0, m = 0, nloc = 0, row_begin = 0;
@@ -33,6 +55,7 @@ struct regot_sparse {
     // lanes: short (<= kShortLine entries, 8 lanes) and medium (<= kLongLine, one warp)
     rg::DevBuf<int> lines_s, lines_m;
     int n_lines_s = 0, n_lines_m = 0;
+    rg::PcgSchedule pcg;  // single-GPU direction solve (k5_pcg.cu)
 };
 
 namespace rg {
@@ -59,6 +82,7 @@ struct SparseWS {
     DevBuf<double> cg_scal;
     DevBuf<double> cg_partials;
     DevBuf<unsigned int> cg_ticket;
+    DevBuf<unsigned int> cg_barrier;
     double* h_cg = nullptr;  // pinned
     ~SparseWS()
     {
@@ -92,6 +116,11 @@ void sparse_matvec(regot_ctx* ctx, cudaStream_t st, ncclComm* comm, const regot_
                    const double* vb, double* ya, double* yb, int64_t stride_a, int64_t stride_b);
 // Jacobi-PCG (K5): solves A x_k = rhs_k for k < nrhs simultaneously.  Returns
 // iterations, or -1 on breakdown (p'Ap <= 0: "not positive definite").
+// k5_pcg.cu -- the single-GPU path of sparse_pcg: Schur-complement PCG in one persistent kernel
+void build_pcg_schedule(regot_ctx* ctx, regot_sparse& S, const std::vector<int>& rowptr_host,
+                        const std::vector<int>& cscptr_host);
+int pcg_schur_persistent(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, const regot_sparse& S, int nrhs,
+                         const DVec* const* rhs, DVec* const* sol, double rtol, int max_iter);
 int sparse_pcg(regot_ctx* ctx, cudaStream_t st, ncclComm* comm, SparseWS& ws, const regot_sparse& S, int nrhs,
                const DVec* const* rhs, DVec* const* sol, double rtol, int max_iter);
 

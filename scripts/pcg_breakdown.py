@@ -1,9 +1,9 @@
-"""Where a PCG iteration's time goes (config B pattern): runs the persistent kernel for a fixed 1000
-iterations with parts switched off (REGOT_B200_PCG_DBG bits: 1 skip mat-vec, 2 skip vector update,
-4 fixed iteration count).  Usage: python scripts/pcg_breakdown.py [nrhs=3]"""
+"""Time of the direction solve (config B pattern after 20 Sinkhorn steps): the persistent Schur-complement
+PCG kernel to convergence and for a fixed 1000 iterations (REGOT_B200_PCG_FIXED_ITERS), and the former
+full-system kernel (REGOT_B200_PCG_FULL=1 in the environment) for comparison.
+Usage: python scripts/pcg_breakdown.py [nrhs=3]"""
 import os
 import sys
-import time
 
 import numpy as np
 
@@ -24,8 +24,9 @@ rng = np.random.default_rng(0)
 dim = p.n + p.m - 1
 u = rng.normal(size=dim) if nrhs == 3 else None
 v = rng.normal(size=dim) if nrhs == 3 else None
-for dbg in (0, 4, 5, 6, 7):
-    os.environ["REGOT_B200_PCG_DBG"] = str(dbg)
+for fixed in (0, 1000):
+    if fixed:
+        os.environ["REGOT_B200_PCG_FIXED_ITERS"] = str(fixed)
     best = 1e9
     for rep in range(3):
         s.set_profiling(True)
@@ -36,5 +37,5 @@ for dbg in (0, 4, 5, 6, 7):
         n, ms = s.get_profile(5)
         s.set_profiling(False)
         best = min(best, ms / max(n, 1))
-    iters = its if dbg == 0 else 1000
-    print(f"dbg={dbg} nrhs={nrhs}: kernel {best:.3f} ms, {iters} iterations -> {1e3 * best / max(iters, 1):.2f} us/iteration", flush=True)
+    iters = fixed if fixed else its
+    print(f"fixed={fixed} nrhs={nrhs}: kernel {best:.3f} ms, {iters} iterations -> {1e3 * best / max(iters, 1):.2f} us/iteration", flush=True)

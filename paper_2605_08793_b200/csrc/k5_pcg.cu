@@ -43,14 +43,16 @@ constexpr int kSchurThreads = 512;
 constexpr int kSchurWarps = kSchurThreads / 32;
 static_assert(kSchurWarps == kPcgWarpsPerCta, "schedule and kernel disagree on warps per CTA");
 constexpr int kLogRowBytes = 32 * 12;  // 32 doubles + 32 ints
-constexpr int kSchurScratchBytes = (4 * kSchurWarps + 8) * 8;
+constexpr int kMaxGrid = 160;     // CTAs whose partials are staged in shared memory by grid_sum4
+constexpr int kLongStage = 256;   // long lines whose dot contributions are staged likewise
+constexpr int kSchurScratchBytes = (4 * kSchurWarps + 8 + 4 * kMaxGrid + 2 * kLongStage) * 8;
 
 enum { kRowMain = 0, kRowFinal = 1, kColInit = 2, kColMain = 3 };
 
 struct SchurParams {
     int nloc, mfree, nrhs, max_iter, n_long, nw, fixed_iters;
     int vec_smem_r, vec_smem_c;  // phase gathers from a shared-memory copy of the vector
-    int vec_bytes, log_rows;     // shared-memory carve-up: vector buffer, then log_rows rows per warp
+    int vec_bytes, desc_cap, log_rows;  // shared-memory carve-up: vector buffer, desc_cap descriptors and log_rows log rows per warp
     double tol2;
     const int* col;  // CSR of B
     const double* val;
@@ -94,21 +96,32 @@ __device__ __forceinline__ void grid_barrier(unsigned int* ctr, unsigned int& ta
 
 // sum of 4 per-thread values over the grid, in CTA order (+ the long lines' dot contributions added
 // to components [2 long_range, 2 long_range + 2)); result in every thread.  Contains a grid barrier.
+// All partials are fetched with ONE round of independent loads into shared memory and summed there.
 __device__ __noinline__ void grid_sum4(const SchurParams& P, double (&v)[4], double* scratch, double* bcast,
                                        unsigned int& target, int long_range)
 {
+    double* stage = bcast + 8;
+    double* stage_long = stage + 4 * kMaxGrid;
     block_sum<4>(v, scratch);
     if (threadIdx.x == 0) {
 #pragma unroll
         for (int k = 0; k < 4; ++k) P.blockpart[(size_t)blockIdx.x * 4 + k] = v[k];
     }
     grid_barrier(P.barrier, target);
+    const int nvals = (int)gridDim.x * 4, nlong = long_range >= 0 ? min(P.n_long, kLongStage) * 2 : 0;
+    for (int i = threadIdx.x; i < nvals + nlong; i += kSchurThreads) {
+        if (i < nvals) stage[i] = __ldcg(P.blockpart + i);
+        else stage_long[i - nvals] = __ldcg(P.longdot + (i - nvals));
+    }
+    __syncthreads();
     if (threadIdx.x < 32 * 4) {
         const int k = threadIdx.x >> 5, l = threadIdx.x & 31;
         double s = 0.0;
-        for (int b = l; b < (int)gridDim.x; b += 32) s += __ldcg(P.blockpart + (size_t)b * 4 + k);
-        if (k / 2 == long_range)
-            for (int q = l; q < P.n_long; q += 32) s += __ldcg(P.longdot + (size_t)q * 2 + (k % 2));
+        for (int b = l; b < (int)gridDim.x; b += 32) s += stage[b * 4 + k];
+        if (k / 2 == long_range) {
+            for (int q = l; q < P.n_long; q += 32)
+                s += q < kLongStage ? stage_long[q * 2 + (k % 2)] : __ldcg(P.longdot + (size_t)q * 2 + (k % 2));
+        }
         s = warp_sum(s);
         if (l == 0) bcast[k] = s;
     }
@@ -122,6 +135,7 @@ __device__ __noinline__ void grid_sum4(const SchurParams& P, double (&v)[4], dou
 struct WarpLog {
     uint32_t val0, idx0;  // lane 0's slot of row 0: row r of lane l at val0 + 256 r + 8 l / idx0 + 128 r + 4 l
     uint32_t vec;         // the shared copy of the gathered vector (x2)
+    uint32_t desc;        // this warp's cached item descriptors (kPcgItemInts ints each)
 };
 __device__ __forceinline__ int lds_i32(uint32_t addr)
 {
@@ -204,25 +218,68 @@ __device__ __forceinline__ double2 gather2(const char* gxb, uint32_t vec, unsign
     return __ldcg(reinterpret_cast<const double2*>(gxb + off));
 }
 
+// Head of one item as every lane needs it, and the first 8 (index, value) pairs of the lane
+struct ItemHead {
+    int kind, nE, chunk, slot, first, cnt, line, beg, len;
+    double diag;
+};
+
+// descriptor from the warp's shared-memory cache (slot >= 0) or from global memory
+__device__ __forceinline__ ItemHead load_head(const SchurParams& P, const double* __restrict__ diagv, uint32_t cached,
+                                              bool is_cached, int q, int lane)
+{
+    ItemHead h;
+    if (is_cached) {
+        h.kind = lds_i32(cached);
+        h.nE = lds_i32(cached + 4);
+        h.chunk = lds_i32(cached + 8);
+        h.slot = lds_i32(cached + 12);
+        h.first = lds_i32(cached + 16);
+        h.cnt = lds_i32(cached + 20);
+        const uint32_t sub = h.kind == 0 ? (uint32_t)(lane >> 3) : 0u;
+        h.line = lds_i32(cached + 32 + 4 * sub);
+        h.beg = lds_i32(cached + 48 + 4 * sub);
+        h.len = lds_i32(cached + 64 + 4 * sub);
+    } else {
+        const int* d = P.items + (size_t)q * kPcgItemInts;
+        const int4 m0 = __ldg(reinterpret_cast<const int4*>(d));
+        h.kind = m0.x;
+        h.nE = m0.y;
+        h.chunk = m0.z;
+        h.slot = m0.w;
+        h.first = __ldg(d + 4);
+        h.cnt = __ldg(d + 5);
+        const int sub = h.kind == 0 ? lane >> 3 : 0;
+        h.line = __ldg(d + 8 + sub);
+        h.beg = __ldg(d + 12 + sub);
+        h.len = __ldg(d + 16 + sub);
+    }
+    h.diag = h.line >= 0 ? __ldg(diagv + h.line) : 1.0;
+    return h;
+}
 // One mat-vec phase over this warp's items.  kRows: lines are rows of B, gx is a beta-space vector
 // (x2); else lines are columns of B, gx is the alpha-space vector ta (x2).  `dot` accumulates this
 // lane's component (lane & 1) of gamma (kColInit) or delta (kColMain) over the lines this warp
-// finished.
+// finished.  Items [i0, i0 + n_res) replay the shared-memory log; the others stream the matrix from
+// global memory, the next item's descriptor and first entries prefetched while the current one is
+// reduced (descriptors of the first n_desc streamed items are cached in shared memory at `desc`).
 template <bool kRows, bool kVecSmem>
 __device__ __forceinline__ void run_phase(const SchurParams& P, int mode, const double* gx, const WarpLog& L, int i0,
-                                          int i1, int n_res, int row, int lane, double& dot)
+                                          int i1, int n_res, int row, uint32_t desc, int n_desc, int lane, double& dot)
 {
     const int* __restrict__ src_idx = kRows ? P.col : P.cscrow;
     const double* __restrict__ src_val = kRows ? P.val : P.cscval;
     const double* __restrict__ diagv = kRows ? P.dA : P.dB;
     const char* gxb = reinterpret_cast<const char*>(gx);
     const int kk = lane & 1;
+    // a phase that gathers from shared memory has no log (the vector took its place)
+    const int s0 = kVecSmem ? i0 : i0 + n_res;  // first streamed item
     for (int q = i0; q < i1; ++q) {
-        const bool resident = (q - i0) < n_res;
+        const bool resident = !kVecSmem && q < s0;
         int kind, nE, chunk = 0, slot = 0, first = 0, cnt = 0, line;
         double diag;
         double a0 = 0.0, a1 = 0.0;
-        if (resident) {
+        if (!kVecSmem && resident) {
             const uint32_t h = L.idx0 + 128u * row;
             kind = lds_i32(h + 4);
             nE = lds_i32(h + 8);
@@ -284,30 +341,27 @@ __device__ __forceinline__ void run_phase(const SchurParams& P, int mode, const 
             }
             row += nE + 1;
         } else {
-            // matrix from global memory (coalesced): descriptor, then indices and values
-            const int* d = P.items + (size_t)q * kPcgItemInts;
-            const int4 m0 = __ldg(reinterpret_cast<const int4*>(d));
-            kind = m0.x;
-            nE = m0.y;
-            chunk = m0.z;
-            slot = m0.w;
-            if (kind == 2) {
-                first = __ldg(d + 4);
-                cnt = __ldg(d + 5);
-            }
-            const int sub = kind == 0 ? lane >> 3 : 0, gl = kind == 0 ? lane & 7 : lane, stride = kind == 0 ? 8 : 32;
-            line = __ldg(d + 8 + sub);
-            const int beg = __ldg(d + 12 + sub), len = __ldg(d + 16 + sub);
-            diag = line >= 0 ? __ldg(diagv + line) : 1.0;
+            // matrix from global memory, coalesced, 8 entries per lane in flight
+            const int qs = q - s0;
+            const ItemHead h = load_head(P, diagv, desc + (uint32_t)qs * (kPcgItemInts * 4), qs < n_desc, q, lane);
+            kind = h.kind;
+            nE = h.nE;
+            chunk = h.chunk;
+            slot = h.slot;
+            first = h.first;
+            cnt = h.cnt;
+            line = h.line;
+            diag = h.diag;
+            const int gl = kind == 0 ? lane & 7 : lane, stride = kind == 0 ? 8 : 32;
             for (int e0 = 0; e0 < nE; e0 += 8) {
                 int c[8];
                 double v[8];
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
                     const int t = gl + stride * (e0 + u);
-                    const bool ok = t < len;
-                    c[u] = ok ? __ldg(src_idx + beg + t) : 0;
-                    v[u] = ok ? __ldg(src_val + beg + t) : 0.0;
+                    const bool ok = (e0 + u) < nE && t < h.len;
+                    c[u] = ok ? __ldg(src_idx + h.beg + t) : 0;
+                    v[u] = ok ? __ldg(src_val + h.beg + t) : 0.0;
                 }
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
@@ -330,14 +384,14 @@ __device__ __forceinline__ void run_phase(const SchurParams& P, int mode, const 
             prev = __shfl_sync(0xffffffffu, prev, 0);
             if ((int)prev == cnt - 1) {
                 __threadfence();
-                double s0 = 0.0, s1 = 0.0;
+                double s0_ = 0.0, s1_ = 0.0;
                 for (int c = lane; c < cnt; c += 32) {
-                    s0 += __ldcg(P.chunk_part + (size_t)(first + c) * 2);
-                    s1 += __ldcg(P.chunk_part + (size_t)(first + c) * 2 + 1);
+                    s0_ += __ldcg(P.chunk_part + (size_t)(first + c) * 2);
+                    s1_ += __ldcg(P.chunk_part + (size_t)(first + c) * 2 + 1);
                 }
-                s0 = warp_sum(s0);
-                s1 = warp_sum(s1);
-                sum = kk ? s1 : s0;
+                s0_ = warp_sum(s0_);
+                s1_ = warp_sum(s1_);
+                sum = kk ? s1_ : s0_;
                 if (lane == 0) P.chunk_cnt[slot] = 0u;
                 is_long = true;
             } else {
@@ -384,15 +438,15 @@ __device__ __forceinline__ void run_phase(const SchurParams& P, int mode, const 
 // all threads of the CTA: shared copy of an x2 vector of `count` entries (after a grid barrier)
 __device__ __forceinline__ void stage_vector(uint32_t vec, const double* gx, int count)
 {
-    for (int i = threadIdx.x; i < count; i += kSchurThreads * 4) {
-        double2 v[4];
+    for (int i = threadIdx.x; i < count; i += kSchurThreads * 10) {
+        double2 v[10];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < 10; ++u) {
             const int j = i + u * kSchurThreads;
             v[u] = j < count ? ldcg_x2(gx + (size_t)j * 2) : make_double2(0.0, 0.0);
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < 10; ++u) {
             const int j = i + u * kSchurThreads;
             if (j < count) sts_f64x2(vec + 16u * (uint32_t)j, v[u]);
         }
@@ -406,10 +460,13 @@ __global__ void __launch_bounds__(kSchurThreads, 1) k_pcg_schur(const __grid_con
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     WarpLog L;
     L.vec = smem_u32(smem);
-    L.val0 = L.vec + (uint32_t)P.vec_bytes + (uint32_t)warp * ((uint32_t)P.log_rows * 256u);
-    L.idx0 = L.vec + (uint32_t)P.vec_bytes + (uint32_t)kSchurWarps * ((uint32_t)P.log_rows * 256u) +
-             (uint32_t)warp * ((uint32_t)P.log_rows * 128u);
-    double* scratch = reinterpret_cast<double*>(smem + P.vec_bytes + (size_t)kSchurWarps * P.log_rows * kLogRowBytes);
+    const uint32_t desc_bytes = (uint32_t)P.desc_cap * (kPcgItemInts * 4);
+    L.desc = L.vec + (uint32_t)P.vec_bytes + (uint32_t)warp * desc_bytes;
+    const uint32_t log0 = L.vec + (uint32_t)P.vec_bytes + (uint32_t)kSchurWarps * desc_bytes;
+    L.val0 = log0 + (uint32_t)warp * ((uint32_t)P.log_rows * 256u);
+    L.idx0 = log0 + (uint32_t)kSchurWarps * ((uint32_t)P.log_rows * 256u) + (uint32_t)warp * ((uint32_t)P.log_rows * 128u);
+    double* scratch = reinterpret_cast<double*>(smem + P.vec_bytes + (size_t)kSchurWarps * desc_bytes +
+                                                (size_t)kSchurWarps * P.log_rows * kLogRowBytes);
     double* bcast = scratch + 4 * kSchurWarps;
 
     const int tid = blockIdx.x * blockDim.x + threadIdx.x, nthr = gridDim.x * blockDim.x;
@@ -433,6 +490,13 @@ __global__ void __launch_bounds__(kSchurThreads, 1) k_pcg_schur(const __grid_con
     const int c0 = P.wptr[P.nw + 1 + gw], c1 = P.wptr[P.nw + 1 + gw + 1], cres = P.wres[P.nw + gw];
     const int col_row0 = fill_log(P, true, L, r0, rres, 0, lane);
     fill_log(P, false, L, c0, cres, col_row0, lane);
+    // descriptors of the streamed items (those not in the log), rows first
+    const int nd_r = min(r1 - r0 - rres, P.desc_cap), nd_c = min(c1 - c0 - cres, P.desc_cap - nd_r);
+    for (int q = 0; q < nd_r + nd_c; ++q) {
+        const int item = q < nd_r ? r0 + rres + q : c0 + cres + (q - nd_r);
+        if (lane < kPcgItemInts) sts_i32(L.desc + (uint32_t)q * (kPcgItemInts * 4) + 4u * lane, __ldg(P.items + (size_t)item * kPcgItemInts + lane));
+    }
+    const uint32_t desc_r = L.desc, desc_c = L.desc + (uint32_t)nd_r * (kPcgItemInts * 4);
     __syncwarp();
 
     // ---- t = D1^-1 r_a; gamma0 = r' D^-1 r of the FULL system (the meaning of rtol is unchanged) ----
@@ -472,9 +536,9 @@ __global__ void __launch_bounds__(kSchurThreads, 1) k_pcg_schur(const __grid_con
             const double* gx = row_mode == kRowMain ? P.zb : P.xb;
             if (P.vec_smem_r) {
                 stage_vector(L.vec, gx, mfree);
-                run_phase<true, true>(P, row_mode, gx, L, r0, r1, 0, 0, lane, none);
+                run_phase<true, true>(P, row_mode, gx, L, r0, r1, 0, 0, desc_r, nd_r, lane, none);
             } else {
-                run_phase<true, false>(P, row_mode, gx, L, r0, r1, rres, 0, lane, none);
+                run_phase<true, false>(P, row_mode, gx, L, r0, r1, rres, 0, desc_r, nd_r, lane, none);
             }
             if (row_mode == kRowFinal) break;
         }
@@ -487,9 +551,9 @@ __global__ void __launch_bounds__(kSchurThreads, 1) k_pcg_schur(const __grid_con
             double dot = 0.0;
             if (P.vec_smem_c) {
                 stage_vector(L.vec, P.ta, nloc);
-                run_phase<false, true>(P, col_mode, P.ta, L, c0, c1, 0, 0, lane, dot);
+                run_phase<false, true>(P, col_mode, P.ta, L, c0, c1, 0, 0, desc_c, nd_c, lane, dot);
             } else {
-                run_phase<false, false>(P, col_mode, P.ta, L, c0, c1, cres, col_row0, lane, dot);
+                run_phase<false, false>(P, col_mode, P.ta, L, c0, c1, cres, col_row0, desc_c, nd_c, lane, dot);
             }
 #pragma unroll
             for (int k = 0; k < 2; ++k) {
@@ -622,7 +686,9 @@ void build_pcg_schedule(regot_ctx* ctx, regot_sparse& S, const std::vector<int>&
     Q.vec_smem_c = need_c <= kPcgVecSmemMax;
     Q.vec_bytes = (int)std::max(Q.vec_smem_r ? need_r : 0L, Q.vec_smem_c ? need_c : 0L);
     Q.vec_bytes = (Q.vec_bytes + 127) / 128 * 128;
-    Q.log_rows = (Q.vec_smem_r && Q.vec_smem_c) ? 0 : (budget - Q.vec_bytes) / (kPcgWarpsPerCta * kLogRowBytes);
+    Q.desc_cap = std::min(40, (budget - Q.vec_bytes) / (kPcgWarpsPerCta * kPcgItemInts * 4) / 2);
+    const int left = budget - Q.vec_bytes - kPcgWarpsPerCta * Q.desc_cap * kPcgItemInts * 4;
+    Q.log_rows = (Q.vec_smem_r && Q.vec_smem_c) ? 0 : left / (kPcgWarpsPerCta * kLogRowBytes);
     const int phase_logs[2] = {Q.vec_smem_r ? 0 : 1, Q.vec_smem_c ? 0 : 1};
     int n_long = 0, n_chunks = 0;
     std::vector<int> h_items, h_wptr((size_t)2 * (nw + 1), 0), h_wres((size_t)2 * nw, 0);
@@ -752,8 +818,9 @@ static int pcg_schur_launch(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, const
     const PcgSchedule& Q = S.pcg;
     const int nloc = (int)S.nloc, mfree = std::max((int)S.m - 1, 0);
     const int grid = ctx->sm_count;
-    if (Q.nw != grid * kPcgWarpsPerCta) raise(REGOT_E_CUDA, "pcg: schedule was built for a different grid (internal error)");
-    const int smem = Q.vec_bytes + kPcgWarpsPerCta * Q.log_rows * kLogRowBytes + kSchurScratchBytes;
+    if (Q.nw != grid * kPcgWarpsPerCta || grid > kMaxGrid)
+        raise(REGOT_E_CUDA, "pcg: schedule was built for a different grid (internal error)");
+    const int smem = Q.vec_bytes + kPcgWarpsPerCta * (Q.desc_cap * kPcgItemInts * 4 + Q.log_rows * kLogRowBytes) + kSchurScratchBytes;
     static bool attr_set = false;
     if (!attr_set) {
         RG_CUDA(cudaFuncSetAttribute(k_pcg_schur, cudaFuncAttributeMaxDynamicSharedMemorySize, kPcgSmemBudget));
@@ -784,6 +851,7 @@ static int pcg_schur_launch(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, const
     P.vec_smem_c = Q.vec_smem_c;
     P.vec_bytes = Q.vec_bytes;
     P.log_rows = Q.log_rows;
+    P.desc_cap = Q.desc_cap;
 #ifdef REGOT_PCG_TIMING
     const bool timing = true;
 #else

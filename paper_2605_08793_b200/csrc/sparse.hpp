@@ -27,7 +27,7 @@ struct PcgSchedule {
     mutable DevBuf<unsigned int> chunk_cnt;
     int nw = 0, n_long = 0, n_chunks = 0;
     int vec_smem_r = 0, vec_smem_c = 0;  // row / column phase gathers from a shared-memory copy of the vector
-    int vec_bytes = 0, log_rows = 0;     // shared-memory carve-up (vector buffer, log rows per warp)
+    int vec_bytes = 0, desc_cap = 0, log_rows = 0;  // shared-memory carve-up (vector buffer; descriptors, log rows per warp)
     long resident_entries = 0, global_entries = 0;
 };
 }  // namespace rg

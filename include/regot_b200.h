@@ -187,6 +187,22 @@ regot_status regot_b200_set_problem_rows(regot_ctx* ctx, int64_t n, int64_t m, i
 regot_status regot_b200_set_problem_device(regot_ctx* ctx, int64_t n, int64_t m, int64_t row_begin,
                                            int64_t row_count, const double* M_device, int64_t ld,
                                            const double* a_device, const double* b_device, double eta);
+/* Point-cloud problem: squared-Euclidean cost of X (n x d, row-major) and Y (m x d) divided by its
+ * maximum -- what gen_synthetic1 builds (problem.h:124-132) and normalize_cost (problem.h:53-61)
+ * scales -- formed ON THE DEVICE with the same arithmetic (coordinates accumulated in order, multiply
+ * and add rounded separately, true division), so the cost equals the host generator's bit for bit.
+ * on_the_fly == 0 materialises the row block in HBM (no 8 n m bytes over PCIe); on_the_fly != 0 never
+ * stores it: every pass over the cost recomputes its tiles in shared memory (BASELINE config E).  Both
+ * modes give bitwise identical results.  The row-block variant serves sharded contexts (X holds all
+ * n rows; the maximum is taken over all ranks). */
+regot_status regot_b200_set_pointcloud(regot_ctx* ctx, int64_t n, int64_t m, int32_t d, const double* X,
+                                       const double* Y, const double* a, const double* b, double eta,
+                                       int32_t on_the_fly);
+regot_status regot_b200_set_pointcloud_rows(regot_ctx* ctx, int64_t n, int64_t m, int64_t row_begin,
+                                            int64_t row_count, int32_t d, const double* X, const double* Y,
+                                            const double* a, const double* b, double eta, int32_t on_the_fly);
+/* The resident (or on-the-fly) cost block of this context, row-major row_count x m, to host memory. */
+regot_status regot_b200_get_cost(regot_ctx* ctx, double* M_rowmajor);
 /* validate_problem (problem.h:30-50) on the uploaded instance. */
 regot_status regot_b200_validate_problem(regot_ctx* ctx);
 /* eta override, like `regot solve --eta` (tools/regot.cpp:121-122). */

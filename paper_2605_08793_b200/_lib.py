@@ -135,6 +135,13 @@ PROTOTYPES = {
         C.c_int,
         [_vp, C.c_int64, C.c_int64, C.c_int64, C.c_int64, _vp, C.c_int64, _vp, _vp, C.c_double],
     ),
+    "regot_b200_set_pointcloud": (
+        C.c_int, [_vp, C.c_int64, C.c_int64, C.c_int32, _vp, _vp, _vp, _vp, C.c_double, C.c_int32]),
+    "regot_b200_set_pointcloud_rows": (
+        C.c_int,
+        [_vp, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int32, _vp, _vp, _vp, _vp, C.c_double, C.c_int32],
+    ),
+    "regot_b200_get_cost": (C.c_int, [_vp, _vp]),
     "regot_b200_validate_problem": (C.c_int, [_vp]),
     "regot_b200_set_eta": (C.c_int, [_vp, C.c_double]),
     "regot_b200_fused_gradient": (C.c_int, [_vp, _vp, _vp, C.POINTER(GradientInfoC), _vp, _vp, _vp]),

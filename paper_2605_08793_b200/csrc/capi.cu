@@ -18,6 +18,9 @@ void set_problem_host(regot_ctx* ctx, int64_t n, int64_t m, int64_t row_begin, i
 void set_problem_device(regot_ctx* ctx, int64_t n, int64_t m, int64_t row_begin, int64_t row_count,
                         const double* M_dev, int64_t ld, const double* a_dev, const double* b_dev, double eta);
 void validate_problem_device(regot_ctx* ctx);
+void set_pointcloud(regot_ctx* ctx, int64_t n, int64_t m, int64_t row_begin, int64_t row_count, int d, const double* X,
+                    const double* Y, const double* a, const double* b, double eta, bool on_the_fly);
+void get_cost_host(regot_ctx* ctx, double* out);
 std::string g_create_error;
 }  // namespace rg
 
@@ -145,6 +148,31 @@ regot_status regot_b200_set_problem_device(regot_ctx* ctx, int64_t n, int64_t m,
                                            const double* a_device, const double* b_device, double eta)
 {
     return guard(ctx, [&] { set_problem_device(ctx, n, m, row_begin, row_count, M_device, ld, a_device, b_device, eta); });
+}
+
+regot_status regot_b200_set_pointcloud(regot_ctx* ctx, int64_t n, int64_t m, int32_t d, const double* X, const double* Y,
+                                       const double* a, const double* b, double eta, int32_t on_the_fly)
+{
+    return guard(ctx, [&] {
+        if (ctx->world != 1) raise(REGOT_E_VALIDATION, "set_pointcloud: use set_pointcloud_rows on a sharded context");
+        set_pointcloud(ctx, n, m, 0, n, d, X, Y, a, b, eta, on_the_fly != 0);
+    });
+}
+
+regot_status regot_b200_set_pointcloud_rows(regot_ctx* ctx, int64_t n, int64_t m, int64_t row_begin, int64_t row_count,
+                                            int32_t d, const double* X, const double* Y, const double* a,
+                                            const double* b, double eta, int32_t on_the_fly)
+{
+    return guard(ctx, [&] { set_pointcloud(ctx, n, m, row_begin, row_count, d, X, Y, a, b, eta, on_the_fly != 0); });
+}
+
+regot_status regot_b200_get_cost(regot_ctx* ctx, double* M_rowmajor)
+{
+    return guard(ctx, [&] {
+        ctx_require_problem(ctx);
+        if (!M_rowmajor) raise(REGOT_E_VALIDATION, "get_cost: null output");
+        get_cost_host(ctx, M_rowmajor);
+    });
 }
 
 regot_status regot_b200_validate_problem(regot_ctx* ctx)

@@ -277,7 +277,8 @@ __global__ void k_transpose(int rows, int cols, const double* __restrict__ in, l
 
 static void finish_problem(regot_ctx* ctx)
 {
-    build_tensor_map(ctx);
+    if (ctx->prob.on_the_fly) std::memset(&ctx->prob.tmap, 0, sizeof(ctx->prob.tmap));  // the sweeps compute their tiles
+    else build_tensor_map(ctx);
     ctx->prob.loaded = true;
     make_sweep_plan(ctx);
     ensure_sweep_ws(ctx, ctx->ws_main);
@@ -307,6 +308,8 @@ void set_problem_host(regot_ctx* ctx, int64_t n, int64_t m, int64_t row_begin, i
     RG_CUDA(cudaSetDevice(ctx->device));
     DeviceProblem& pr = ctx->prob;
     pr.loaded = false;
+    pr.on_the_fly = false;
+    pr.cloud_d = 0;
     pr.n = n;
     pr.m = m;
     pr.row_begin = row_begin;
@@ -351,6 +354,8 @@ void set_problem_device(regot_ctx* ctx, int64_t n, int64_t m, int64_t row_begin,
     RG_CUDA(cudaSetDevice(ctx->device));
     DeviceProblem& pr = ctx->prob;
     pr.loaded = false;
+    pr.on_the_fly = false;
+    pr.cloud_d = 0;
     pr.n = n;
     pr.m = m;
     pr.row_begin = row_begin;
@@ -361,6 +366,139 @@ void set_problem_device(regot_ctx* ctx, int64_t n, int64_t m, int64_t row_begin,
     pr.a = a_dev;
     pr.b = b_dev;
     finish_problem(ctx);
+}
+
+// ---- point-cloud problems ------------------------------------------------------------------------
+// cost = |x_i - y_j|^2 / max (problem.h:53-61, 124-132), formed on the device with the arithmetic of
+// cloud_sqdist (sweep.cuh) so it equals the host generators' matrix bit for bit.
+constexpr int kCloudCols = 256;
+
+// maximum of the un-normalised cost over this rank's rows: one partial per block
+__global__ void __launch_bounds__(kCloudCols) k_cloud_max(int nloc, int m, const CloudGeom c, double* __restrict__ blockmax)
+{
+    __shared__ double wmax[kCloudCols / 32];
+    const int j = blockIdx.x * kCloudCols + threadIdx.x;
+    double mx = 0.0;
+    if (j < m) {
+        const double* yj = c.Y + (size_t)j * c.d;
+        for (int i = blockIdx.y; i < nloc; i += gridDim.y) mx = fmax(mx, cloud_sqdist(c.X + (size_t)i * c.d, yj, c.d));
+    }
+    mx = warp_max(mx);
+    if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < kCloudCols / 32; ++w) mx = fmax(mx, wmax[w]);
+        blockmax[(size_t)blockIdx.y * gridDim.x + blockIdx.x] = mx;
+    }
+}
+
+__global__ void __launch_bounds__(kCloudCols) k_cloud_materialize(int nloc, int m, long ld, const CloudGeom c,
+                                                                  double* __restrict__ M)
+{
+    const int j = blockIdx.x * kCloudCols + threadIdx.x;
+    if (j >= m) return;
+    const double* yj = c.Y + (size_t)j * c.d;
+    for (int i = blockIdx.y; i < nloc; i += gridDim.y)
+        M[(size_t)i * ld + j] = __ddiv_rn(cloud_sqdist(c.X + (size_t)i * c.d, yj, c.d), c.cmax);
+}
+
+void set_pointcloud(regot_ctx* ctx, int64_t n, int64_t m, int64_t row_begin, int64_t row_count, int d, const double* X,
+                    const double* Y, const double* a, const double* b, double eta, bool on_the_fly)
+{
+    check_shape(n, m, row_begin, row_count, eta);
+    if (!X || !Y || !a || !b) raise(REGOT_E_VALIDATION, "problem: null input");
+    if (d < 1 || d > 4096) raise(REGOT_E_VALIDATION, "set_pointcloud: need 1 <= d <= 4096");
+    for (int64_t q = row_begin * d; q < (row_begin + row_count) * d; ++q)
+        if (!std::isfinite(X[q])) raise(REGOT_E_VALIDATION, "problem: non-finite entries");
+    for (int64_t q = 0; q < m * d; ++q)
+        if (!std::isfinite(Y[q])) raise(REGOT_E_VALIDATION, "problem: non-finite entries");
+    RG_CUDA(cudaSetDevice(ctx->device));
+    DeviceProblem& pr = ctx->prob;
+    pr.loaded = false;
+    pr.n = n;
+    pr.m = m;
+    pr.row_begin = row_begin;
+    pr.nloc = row_count;
+    pr.eta = eta;
+    pr.cloud_d = d;
+    pr.on_the_fly = on_the_fly;
+    pr.X_own.ensure((size_t)pr.nloc * (size_t)d);
+    pr.Y_own.ensure((size_t)m * (size_t)d);
+    pr.a_own.ensure((size_t)pr.nloc);
+    pr.b_own.ensure((size_t)m);
+    pr.a = pr.a_own.p;
+    pr.b = pr.b_own.p;
+    cudaStream_t st = ctx->stream;
+    RG_CUDA(cudaMemcpyAsync(pr.X_own.p, X + row_begin * d, sizeof(double) * (size_t)pr.nloc * (size_t)d, cudaMemcpyHostToDevice, st));
+    RG_CUDA(cudaMemcpyAsync(pr.Y_own.p, Y, sizeof(double) * (size_t)m * (size_t)d, cudaMemcpyHostToDevice, st));
+    RG_CUDA(cudaMemcpyAsync(pr.a_own.p, a + row_begin, sizeof(double) * (size_t)pr.nloc, cudaMemcpyHostToDevice, st));
+    RG_CUDA(cudaMemcpyAsync(pr.b_own.p, b, sizeof(double) * (size_t)m, cudaMemcpyHostToDevice, st));
+
+    // exact maximum of the un-normalised cost (normalize_cost, problem.h:53-61), over all ranks
+    CloudGeom c;
+    c.X = pr.X_own.p;
+    c.Y = pr.Y_own.p;
+    c.d = d;
+    c.cmax = 1.0;
+    const dim3 grid((unsigned)((m + kCloudCols - 1) / kCloudCols),
+                    (unsigned)std::max<int64_t>(1, std::min<int64_t>(pr.nloc, 8L * ctx->sm_count)));
+    DevBuf<double> bm;
+    const size_t nb = (size_t)grid.x * grid.y;
+    bm.ensure(nb + 1);
+    k_cloud_max<<<grid, kCloudCols, 0, st>>>((int)pr.nloc, (int)m, c, bm.p);
+    RG_CUDA(cudaGetLastError());
+    ++ctx->launches;
+    std::vector<double> hb(nb);
+    RG_CUDA(cudaMemcpyAsync(hb.data(), bm.p, sizeof(double) * nb, cudaMemcpyDeviceToHost, st));
+    RG_CUDA(cudaStreamSynchronize(st));
+    double cmax = 0.0;
+    for (double v : hb) cmax = std::max(cmax, v);
+    if (ctx->world > 1) {
+        RG_CUDA(cudaMemcpyAsync(bm.p, &cmax, sizeof(double), cudaMemcpyHostToDevice, st));
+        allreduce_max(ctx, ctx->comm, bm.p, 1, st);
+        RG_CUDA(cudaMemcpyAsync(&cmax, bm.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+        RG_CUDA(cudaStreamSynchronize(st));
+    }
+    if (!(cmax > 0.0)) raise(REGOT_E_DEGENERATE_COST, "normalize_cost: no strictly positive entry");
+    pr.cloud_max = cmax;
+    c.cmax = cmax;
+    if (on_the_fly) {
+        pr.M_own.release();
+        pr.M = nullptr;
+        pr.ld = 0;
+    } else {
+        pr.ld = (m + 15) / 16 * 16;
+        pr.M_own.ensure((size_t)pr.nloc * (size_t)pr.ld);
+        pr.M = pr.M_own.p;
+        RG_CUDA(cudaMemsetAsync(pr.M_own.p, 0, sizeof(double) * (size_t)pr.nloc * (size_t)pr.ld, st));
+        k_cloud_materialize<<<grid, kCloudCols, 0, st>>>((int)pr.nloc, (int)m, (long)pr.ld, c, pr.M_own.p);
+        RG_CUDA(cudaGetLastError());
+        ++ctx->launches;
+        RG_CUDA(cudaStreamSynchronize(st));
+    }
+    finish_problem(ctx);
+}
+
+// the cost block of this rank, row-major nloc x m, to the host (formed on the fly if it is not resident)
+void get_cost_host(regot_ctx* ctx, double* out)
+{
+    const DeviceProblem& pr = ctx->prob;
+    cudaStream_t st = ctx->stream;
+    if (!pr.on_the_fly) {
+        RG_CUDA(cudaMemcpy2DAsync(out, (size_t)pr.m * 8, pr.M, (size_t)pr.ld * 8, (size_t)pr.m * 8, (size_t)pr.nloc,
+                                  cudaMemcpyDeviceToHost, st));
+        RG_CUDA(cudaStreamSynchronize(st));
+        return;
+    }
+    DevBuf<double> tmp;
+    tmp.ensure((size_t)pr.nloc * (size_t)pr.m);
+    const dim3 grid((unsigned)((pr.m + kCloudCols - 1) / kCloudCols),
+                    (unsigned)std::max<int64_t>(1, std::min<int64_t>(pr.nloc, 8L * ctx->sm_count)));
+    k_cloud_materialize<<<grid, kCloudCols, 0, st>>>((int)pr.nloc, (int)pr.m, (long)pr.m, cloud_geom(ctx), tmp.p);
+    RG_CUDA(cudaGetLastError());
+    ++ctx->launches;
+    RG_CUDA(cudaMemcpyAsync(out, tmp.p, sizeof(double) * (size_t)pr.nloc * (size_t)pr.m, cudaMemcpyDeviceToHost, st));
+    RG_CUDA(cudaStreamSynchronize(st));
 }
 
 // ---- host <-> device vectors ---------------------------------------------------------------------
@@ -403,9 +541,11 @@ void validate_problem_device(regot_ctx* ctx)
     DevBuf<unsigned int> flag;
     flag.ensure(1);
     RG_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(unsigned int), ctx->stream));
-    k_count_nonfinite<<<4 * ctx->sm_count, 256, 0, ctx->stream>>>((int)pr.nloc, (int)pr.m, (long)pr.ld, pr.M, flag.p);
-    RG_CUDA(cudaGetLastError());
-    ++ctx->launches;
+    if (!pr.on_the_fly) {  // point clouds were checked at upload
+        k_count_nonfinite<<<4 * ctx->sm_count, 256, 0, ctx->stream>>>((int)pr.nloc, (int)pr.m, (long)pr.ld, pr.M, flag.p);
+        RG_CUDA(cudaGetLastError());
+        ++ctx->launches;
+    }
     unsigned int bad = 0;
     RG_CUDA(cudaMemcpyAsync(&bad, flag.p, sizeof(bad), cudaMemcpyDeviceToHost, ctx->stream));
     RG_CUDA(cudaStreamSynchronize(ctx->stream));

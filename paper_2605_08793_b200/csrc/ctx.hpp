@@ -124,6 +124,12 @@ struct DeviceProblem {
     DevBuf<double> M_own, a_own, b_own;
     CUtensorMap tmap;  // 2-D map over M for the sweep kernels
     bool loaded = false;
+    // point-cloud problems (regot_b200_set_pointcloud): cost = |x_i - y_j|^2 / max.  on_the_fly: M is
+    // never materialised (M == nullptr); the sweeps form their tiles from X and Y.
+    bool on_the_fly = false;
+    int cloud_d = 0;
+    double cloud_max = 0.0;
+    DevBuf<double> X_own, Y_own;  // nloc x d, m x d
 };
 
 // A dual-space vector on the device: alpha block (nloc, row-sharded) + beta

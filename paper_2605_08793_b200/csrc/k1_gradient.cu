@@ -90,15 +90,16 @@ __device__ __forceinline__ void gradient_segment(RingCursor& ring, int lane, int
     }
 }
 
-__global__ void __launch_bounds__(kSweepThreads, 1)
+template <bool kCloud>
+__global__ void __launch_bounds__(sweep_threads<kCloud>(), 1)
 k_gradient_sweep(const __grid_constant__ CUtensorMap tmap, const GradParams p)
 {
     extern __shared__ __align__(128) unsigned char smem[];
-    const SweepSmem sm = sweep_prologue(smem, &tmap, p.exp_table);
+    const SweepSmem sm = sweep_prologue(smem, &tmap, p.exp_table, kCloud ? kCloudWarps : 1);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
-    if (warp == kTR) {
-        sweep_producer(&tmap, p.g, sm.tiles, sm.full, sm.empty);
+    if (warp >= kTR) {
+        sweep_feed<kCloud>(&tmap, p.g, sm.tiles, sm.full, sm.empty, warp, lane);
         return;
     }
 
@@ -308,7 +309,7 @@ __global__ void __launch_bounds__(kFinThreads) k_gradient_fin2(const Fin2Params 
 }
 
 // ---- dense plan (tests / diagnostics; dual.h:83-94) ---------------------------------
-__global__ void k_plan(int nloc, int m, long ld, const double* __restrict__ M, const double* __restrict__ alpha,
+__global__ void k_plan(int nloc, int m, const CostViewDev cost, const double* __restrict__ alpha,
                        const double* __restrict__ beta, const ExpScale E, const double* __restrict__ exp_table,
                        double* __restrict__ T)
 {
@@ -319,7 +320,7 @@ __global__ void k_plan(int nloc, int m, long ld, const double* __restrict__ M, c
     const long total = (long)nloc * m;
     for (long q = (long)blockIdx.x * blockDim.x + threadIdx.x; q < total; q += (long)gridDim.x * blockDim.x) {
         const int i = (int)(q / m), j = (int)(q % m);
-        T[q] = plan_entry_dev((alpha[i] + beta[j]) - M[(size_t)i * ld + j], E, tbl_lane);
+        T[q] = plan_entry_dev((alpha[i] + beta[j]) - cost_at(cost, i, j), E, tbl_lane);
     }
 }
 
@@ -341,6 +342,7 @@ static GradParams make_params(regot_ctx* ctx, SweepWS& ws, const double* alpha, 
     p.g.cta_seg0 = ctx->plan.d_cta_seg0.p;
     // M larger than ~half of L2 streams through with evict-first; small problems stay L2 resident
     p.g.evict_first = ((double)ctx->prob.nloc * (double)ctx->prob.ld * 8.0 > 48e6) ? 1 : 0;
+    p.g.cloud = cloud_geom(ctx);
     p.alpha = alpha;
     p.beta = beta;
     p.E = make_exp_scale(ctx->prob.eta);
@@ -354,12 +356,16 @@ void launch_gradient_sweep_only(regot_ctx* ctx, cudaStream_t st, SweepWS& ws, co
 {
     static bool attr_set = false;
     if (!attr_set) {
-        RG_CUDA(cudaFuncSetAttribute(k_gradient_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, kSweepSmem));
+        RG_CUDA(cudaFuncSetAttribute(k_gradient_sweep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSweepSmem));
+        RG_CUDA(cudaFuncSetAttribute(k_gradient_sweep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSweepSmem));
         attr_set = true;
     }
     const GradParams p = make_params(ctx, ws, alpha, beta);
     ProfScope prof(ctx, st, 0);
-    k_gradient_sweep<<<ctx->plan.grid, kSweepThreads, kSweepSmem, st>>>(ctx->prob.tmap, p);
+    if (ctx->prob.on_the_fly)
+        k_gradient_sweep<true><<<ctx->plan.grid, kCloudSweepThreads, kSweepSmem, st>>>(ctx->prob.tmap, p);
+    else
+        k_gradient_sweep<false><<<ctx->plan.grid, kSweepThreads, kSweepSmem, st>>>(ctx->prob.tmap, p);
     RG_CUDA(cudaGetLastError());
     ++ctx->launches;
 }
@@ -424,7 +430,7 @@ void launch_plan(regot_ctx* ctx, cudaStream_t st, const double* alpha, const dou
     const DeviceProblem& pr = ctx->prob;
     const long total = (long)pr.nloc * pr.m;
     const int grid = (int)std::max<long>(1, std::min<long>((total + 255) / 256, 8L * ctx->sm_count));
-    k_plan<<<grid, 256, 0, st>>>((int)pr.nloc, (int)pr.m, (long)pr.ld, pr.M, alpha, beta,
+    k_plan<<<grid, 256, 0, st>>>((int)pr.nloc, (int)pr.m, cost_view_dev(ctx), alpha, beta,
                                  make_exp_scale(pr.eta), ctx->exp_table.p, T_rowmajor);
     RG_CUDA(cudaGetLastError());
     ++ctx->launches;

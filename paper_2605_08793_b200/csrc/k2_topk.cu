@@ -57,20 +57,20 @@ struct TopkParams {
     double* cand_m;
 };
 
-template <int kPass, int kSrc>
-__global__ void __launch_bounds__(kSweepThreads, 1)
+template <int kPass, int kSrc, bool kCloud>
+__global__ void __launch_bounds__(sweep_threads<kCloud>(), 1)
 k_topk_sweep(const __grid_constant__ CUtensorMap tmap, const TopkParams p)
 {
     extern __shared__ __align__(128) unsigned char smem[];
-    const SweepSmem sm = sweep_prologue(smem, &tmap, p.exp_table);
+    const SweepSmem sm = sweep_prologue(smem, &tmap, p.exp_table, kCloud ? kCloudWarps : 1);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     unsigned int* shist = reinterpret_cast<unsigned int*>(sm.scratch);
     if (kPass == kPassHist) {
         for (int q = threadIdx.x; q < kCoarseBins; q += blockDim.x) shist[q] = 0u;
         __syncthreads();
     }
-    if (warp == kTR) {
-        sweep_producer(&tmap, p.g, sm.tiles, sm.full, sm.empty);
+    if (warp >= kTR) {
+        sweep_feed<kCloud>(&tmap, p.g, sm.tiles, sm.full, sm.empty, warp, lane);
         return;
     }
     long t0, t1;
@@ -280,11 +280,11 @@ __global__ void k_build_csc(int nnz, const int* __restrict__ src, const int* __r
         slot[t] = q;
     }
 }
-__global__ void k_gather_cost(int nnz, const int* __restrict__ row, const int* __restrict__ col, const double* __restrict__ M,
-                              long ld, double* __restrict__ mval)
+__global__ void k_gather_cost(int nnz, const int* __restrict__ row, const int* __restrict__ col, const CostViewDev cost,
+                              double* __restrict__ mval)
 {
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nnz; t += gridDim.x * blockDim.x)
-        mval[t] = M[(size_t)row[t] * ld + col[t]];
+        mval[t] = cost_at(cost, row[t], col[t]);
 }
 
 // ---- host side ----------------------------------------------------------------------------------
@@ -325,9 +325,14 @@ static void fetch_hist(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, size_t bin
 template <int kPass, int kSrc>
 static void launch_sweep(regot_ctx* ctx, cudaStream_t st, const TopkParams& p)
 {
-    RG_CUDA(cudaFuncSetAttribute(k_topk_sweep<kPass, kSrc>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSweepSmem));
     ProfScope prof(ctx, st, 3);
-    k_topk_sweep<kPass, kSrc><<<ctx->plan.grid, kSweepThreads, kSweepSmem, st>>>(ctx->prob.tmap, p);
+    if (kSrc == kFromDual && ctx->prob.on_the_fly) {
+        RG_CUDA(cudaFuncSetAttribute(k_topk_sweep<kPass, kFromDual, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSweepSmem));
+        k_topk_sweep<kPass, kFromDual, true><<<ctx->plan.grid, kCloudSweepThreads, kSweepSmem, st>>>(ctx->prob.tmap, p);
+    } else {
+        RG_CUDA(cudaFuncSetAttribute(k_topk_sweep<kPass, kSrc, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSweepSmem));
+        k_topk_sweep<kPass, kSrc, false><<<ctx->plan.grid, kSweepThreads, kSweepSmem, st>>>(ctx->prob.tmap, p);
+    }
     RG_CUDA(cudaGetLastError());
     ++ctx->launches;
 }
@@ -368,6 +373,7 @@ void topk_build_pattern(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, TopkSourc
     p.g.total_tiles = ctx->plan.total_tiles;
     p.g.cta_seg0 = ctx->plan.d_cta_seg0.p;
     p.g.evict_first = ((double)pr.nloc * (double)pr.ld * 8.0 > 48e6) ? 1 : 0;
+    p.g.cloud = cloud_geom(ctx);
     p.alpha = alpha;
     p.beta = beta;
     p.E = make_exp_scale(pr.eta);
@@ -527,7 +533,7 @@ void pattern_from_coords(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, const in
     if (nnz) {
         RG_CUDA(cudaMemcpyAsync(S.row.p, rows.data(), sizeof(int) * (size_t)nnz, cudaMemcpyHostToDevice, st));
         RG_CUDA(cudaMemcpyAsync(S.col.p, cols.data(), sizeof(int) * (size_t)nnz, cudaMemcpyHostToDevice, st));
-        k_gather_cost<<<lin_grid(ctx, nnz), 256, 0, st>>>(nnz, S.row.p, S.col.p, pr.M, (long)pr.ld, S.mval.p);
+        k_gather_cost<<<lin_grid(ctx, nnz), 256, 0, st>>>(nnz, S.row.p, S.col.p, cost_view_dev(ctx), S.mval.p);
         RG_CUDA(cudaGetLastError());
         ++ctx->launches;
     }

@@ -73,14 +73,15 @@ __device__ __forceinline__ void row_lse_row(const double2* __restrict__ trow, in
     lsum = ((sacc[0] + sacc[1]) + (sacc[2] + sacc[3])) + ((sacc[4] + sacc[5]) + (sacc[6] + sacc[7]));
 }
 
-__global__ void __launch_bounds__(kSweepThreads, 1)
+template <bool kCloud>
+__global__ void __launch_bounds__(sweep_threads<kCloud>(), 1)
 k_row_lse_sweep(const __grid_constant__ CUtensorMap tmap, const LseParams p)
 {
     extern __shared__ __align__(128) unsigned char smem[];
-    const SweepSmem sm = sweep_prologue(smem, &tmap, p.exp_table);
+    const SweepSmem sm = sweep_prologue(smem, &tmap, p.exp_table, kCloud ? kCloudWarps : 1);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (warp == kTR) {
-        sweep_producer(&tmap, p.g, sm.tiles, sm.full, sm.empty);
+    if (warp >= kTR) {
+        sweep_feed<kCloud>(&tmap, p.g, sm.tiles, sm.full, sm.empty, warp, lane);
         return;
     }
     long t0, t1;
@@ -180,14 +181,15 @@ __global__ void k_row_lse_fin(int nloc, int n_panels, double eta, const double* 
 // v_ij = (alpha_i - M_ij) / eta.  Each lane keeps an online (max, sum) pair for
 // its 8 columns across the rows of a segment: one exp per element,
 //   d = v - max;  d > 0: sum = sum e^{-d} + 1, max = v;  else: sum += e^{d}.
-__global__ void __launch_bounds__(kSweepThreads, 1)
+template <bool kCloud>
+__global__ void __launch_bounds__(sweep_threads<kCloud>(), 1)
 k_col_lse_sweep(const __grid_constant__ CUtensorMap tmap, const LseParams p)
 {
     extern __shared__ __align__(128) unsigned char smem[];
-    const SweepSmem sm = sweep_prologue(smem, &tmap, p.exp_table);
+    const SweepSmem sm = sweep_prologue(smem, &tmap, p.exp_table, kCloud ? kCloudWarps : 1);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (warp == kTR) {
-        sweep_producer(&tmap, p.g, sm.tiles, sm.full, sm.empty);
+    if (warp >= kTR) {
+        sweep_feed<kCloud>(&tmap, p.g, sm.tiles, sm.full, sm.empty, warp, lane);
         return;
     }
     long t0, t1;
@@ -361,6 +363,7 @@ static LseParams make_lse_params(regot_ctx* ctx, const double* vec, double* psum
     p.g.total_tiles = ctx->plan.total_tiles;
     p.g.cta_seg0 = ctx->plan.d_cta_seg0.p;
     p.g.evict_first = ((double)ctx->prob.nloc * (double)ctx->prob.ld * 8.0 > 48e6) ? 1 : 0;
+    p.g.cloud = cloud_geom(ctx);
     p.vec = vec;
     p.inv_eta = 1.0 / ctx->prob.eta;
     p.exp_table = ctx->exp_table.p;
@@ -378,12 +381,14 @@ void launch_row_lse_sweep_only(regot_ctx* ctx, cudaStream_t st, SweepWS& ws, con
 {
     static bool attr_set = false;
     if (!attr_set) {
-        RG_CUDA(cudaFuncSetAttribute(k_row_lse_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, kSweepSmem));
+        RG_CUDA(cudaFuncSetAttribute(k_row_lse_sweep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSweepSmem));
+        RG_CUDA(cudaFuncSetAttribute(k_row_lse_sweep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSweepSmem));
         attr_set = true;
     }
     const LseParams p = make_lse_params(ctx, beta, ws.rowpart.p, ws.rowpart2.p);
     ProfScope prof(ctx, st, 1);
-    k_row_lse_sweep<<<ctx->plan.grid, kSweepThreads, kSweepSmem, st>>>(ctx->prob.tmap, p);
+    if (ctx->prob.on_the_fly) k_row_lse_sweep<true><<<ctx->plan.grid, kCloudSweepThreads, kSweepSmem, st>>>(ctx->prob.tmap, p);
+    else k_row_lse_sweep<false><<<ctx->plan.grid, kSweepThreads, kSweepSmem, st>>>(ctx->prob.tmap, p);
     RG_CUDA(cudaGetLastError());
     ++ctx->launches;
 }
@@ -392,12 +397,14 @@ void launch_col_lse_sweep_only(regot_ctx* ctx, cudaStream_t st, SweepWS& ws, con
 {
     static bool attr_set = false;
     if (!attr_set) {
-        RG_CUDA(cudaFuncSetAttribute(k_col_lse_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, kSweepSmem));
+        RG_CUDA(cudaFuncSetAttribute(k_col_lse_sweep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSweepSmem));
+        RG_CUDA(cudaFuncSetAttribute(k_col_lse_sweep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSweepSmem));
         attr_set = true;
     }
     const LseParams p = make_lse_params(ctx, alpha, ws.colpart.p, ws.colpart2.p);
     ProfScope prof(ctx, st, 2);
-    k_col_lse_sweep<<<ctx->plan.grid, kSweepThreads, kSweepSmem, st>>>(ctx->prob.tmap, p);
+    if (ctx->prob.on_the_fly) k_col_lse_sweep<true><<<ctx->plan.grid, kCloudSweepThreads, kSweepSmem, st>>>(ctx->prob.tmap, p);
+    else k_col_lse_sweep<false><<<ctx->plan.grid, kSweepThreads, kSweepSmem, st>>>(ctx->prob.tmap, p);
     RG_CUDA(cudaGetLastError());
     ++ctx->launches;
 }

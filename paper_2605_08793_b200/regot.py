@@ -427,6 +427,33 @@ class Solver:
         self.n, self.m, self.row_begin, self.row_count = p.n, p.m, begin, count
         self._problem_key = (id(p), p.eta, begin, count)
 
+    def set_pointcloud(self, X: np.ndarray, Y: np.ndarray, a, b, eta: float, on_the_fly: bool = False,
+                       rows: Optional[Tuple[int, int]] = None) -> None:
+        """Squared-Euclidean cost of the clouds X (n x d), Y (m x d) divided by its maximum, formed on the
+        device (bit-identical to problems.problem_from_points).  on_the_fly=True never stores the matrix."""
+        X = np.ascontiguousarray(X, dtype=np.float64)
+        Y = np.ascontiguousarray(Y, dtype=np.float64)
+        if X.ndim != 2 or Y.ndim != 2 or X.shape[1] != Y.shape[1]:
+            raise ValidationError("set_pointcloud: X and Y must be (n x d) and (m x d)")
+        n, m, d = X.shape[0], Y.shape[0], X.shape[1]
+        a = _vec(a, n, "problem: marginal")
+        b = _vec(b, m, "problem: marginal")
+        begin, count = rows if rows is not None else (0, n)
+        if rows is None and self.world == 1:
+            st = self._lib.regot_b200_set_pointcloud(self._h, n, m, d, _ptr(X), _ptr(Y), _ptr(a), _ptr(b), eta, int(on_the_fly))
+        else:
+            st = self._lib.regot_b200_set_pointcloud_rows(
+                self._h, n, m, begin, count, d, _ptr(X), _ptr(Y), _ptr(a), _ptr(b), eta, int(on_the_fly))
+        self._check(st)
+        self.n, self.m, self.row_begin, self.row_count = n, m, begin, count
+        self._problem_key = None
+
+    def get_cost(self) -> np.ndarray:
+        """This context's cost block (row_count x m), as the kernels see it."""
+        out = np.empty((self.row_count, self.m))
+        self._check(self._lib.regot_b200_get_cost(self._h, _ptr(out)))
+        return out
+
     def set_problem_block(self, p: ProblemInstance, M_block: np.ndarray, row_begin: int, row_count: int) -> None:
         """Upload rows [row_begin, row_begin + row_count) given as a C-contiguous (row_count x m) array
         (e.g. a view of pinned memory); p supplies n, m, the global marginals and eta (p.M is not read)."""

@@ -1,5 +1,5 @@
 """Solve one BASELINE config on the GPU and print where the time goes.
-Usage: python scripts/solve_config.py B|C|A [overlap] [cg_rtol]"""
+Usage: python scripts/solve_config.py A|B|C|D|Dsmall|<side> [overlap] [cg_rtol]"""
 import json
 import os
 import sys
@@ -21,6 +21,19 @@ elif which == "B":
     p = problems.gen_image(100, 0.001)
 elif which == "C":
     p = problems.gen_synthetic2(20000, 5000, 0.0005)
+elif which in ("D", "Dsmall"):
+    # config D: Gaussian-mixture clouds in R^10, eta = 0.001; the 20 GB cost matrix is built in row chunks
+    n = m = 50000 if which == "D" else 8000
+    X, Y = problems.gen_gmm_points(n, m, 10, 21)
+    M = np.empty((n, m))
+    mx = 0.0
+    for r0 in range(0, n, 2500):
+        blk = problems.sqeuclid_cost(X[r0:r0 + 2500], Y)
+        mx = max(mx, float(blk.max()))
+        M[r0:r0 + 2500] = blk
+    for r0 in range(0, n, 2500):
+        M[r0:r0 + 2500] /= mx
+    p = rg.ProblemInstance(n, m, M, np.full(n, 1.0 / n), np.full(m, 1.0 / m), 0.001)
 else:
     side = int(which)
     p = problems.gen_image(side, 0.001)

@@ -392,6 +392,22 @@ __global__ void __launch_bounds__(kCloudCols) k_cloud_max(int nloc, int m, const
     }
 }
 
+// does cloud_div_fast reproduce true division on every entry of the block?  flag |= 1 if not
+__global__ void __launch_bounds__(kCloudCols) k_cloud_verify_div(int nloc, int m, const CloudGeom c, unsigned int* flag)
+{
+    const int j = blockIdx.x * kCloudCols + threadIdx.x;
+    bool bad = false;
+    if (j < m) {
+        const double* yj = c.Y + (size_t)j * c.d;
+        for (int i = blockIdx.y; i < nloc; i += gridDim.y) {
+            const double s = cloud_sqdist(c.X + (size_t)i * c.d, yj, c.d);
+            const double q = cloud_div_fast(s, c.cmax, c.inv_cmax), e = __ddiv_rn(s, c.cmax);
+            bad |= __double_as_longlong(q) != __double_as_longlong(e);
+        }
+    }
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1u);
+}
+
 __global__ void __launch_bounds__(kCloudCols) k_cloud_materialize(int nloc, int m, long ld, const CloudGeom c,
                                                                   double* __restrict__ M)
 {
@@ -399,7 +415,7 @@ __global__ void __launch_bounds__(kCloudCols) k_cloud_materialize(int nloc, int 
     if (j >= m) return;
     const double* yj = c.Y + (size_t)j * c.d;
     for (int i = blockIdx.y; i < nloc; i += gridDim.y)
-        M[(size_t)i * ld + j] = __ddiv_rn(cloud_sqdist(c.X + (size_t)i * c.d, yj, c.d), c.cmax);
+        M[(size_t)i * ld + j] = cloud_div(cloud_sqdist(c.X + (size_t)i * c.d, yj, c.d), c);
 }
 
 void set_pointcloud(regot_ctx* ctx, int64_t n, int64_t m, int64_t row_begin, int64_t row_count, int d, const double* X,
@@ -408,6 +424,9 @@ void set_pointcloud(regot_ctx* ctx, int64_t n, int64_t m, int64_t row_begin, int
     check_shape(n, m, row_begin, row_count, eta);
     if (!X || !Y || !a || !b) raise(REGOT_E_VALIDATION, "problem: null input");
     if (d < 1 || d > 4096) raise(REGOT_E_VALIDATION, "set_pointcloud: need 1 <= d <= 4096");
+    if (on_the_fly && d > kCloudMaxD)
+        raise(REGOT_E_UNSUPPORTED, "set_pointcloud: on-the-fly cost supports d <= " + std::to_string(kCloudMaxD) +
+                                       " (a panel of target points must fit in shared memory); materialise instead");
     for (int64_t q = row_begin * d; q < (row_begin + row_count) * d; ++q)
         if (!std::isfinite(X[q])) raise(REGOT_E_VALIDATION, "problem: non-finite entries");
     for (int64_t q = 0; q < m * d; ++q)
@@ -440,6 +459,8 @@ void set_pointcloud(regot_ctx* ctx, int64_t n, int64_t m, int64_t row_begin, int
     c.Y = pr.Y_own.p;
     c.d = d;
     c.cmax = 1.0;
+    c.inv_cmax = 1.0;
+    c.fast_div = 0;
     const dim3 grid((unsigned)((m + kCloudCols - 1) / kCloudCols),
                     (unsigned)std::max<int64_t>(1, std::min<int64_t>(pr.nloc, 8L * ctx->sm_count)));
     DevBuf<double> bm;
@@ -462,6 +483,21 @@ void set_pointcloud(regot_ctx* ctx, int64_t n, int64_t m, int64_t row_begin, int
     if (!(cmax > 0.0)) raise(REGOT_E_DEGENERATE_COST, "normalize_cost: no strictly positive entry");
     pr.cloud_max = cmax;
     c.cmax = cmax;
+    c.inv_cmax = 1.0 / cmax;
+    c.fast_div = 0;
+    {   // the fast division is used only if it equals true division on every entry of this block
+        DevBuf<unsigned int> flag;
+        flag.ensure(1);
+        RG_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(unsigned int), st));
+        k_cloud_verify_div<<<grid, kCloudCols, 0, st>>>((int)pr.nloc, (int)m, c, flag.p);
+        RG_CUDA(cudaGetLastError());
+        ++ctx->launches;
+        unsigned int bad = 1;
+        RG_CUDA(cudaMemcpyAsync(&bad, flag.p, sizeof(bad), cudaMemcpyDeviceToHost, st));
+        RG_CUDA(cudaStreamSynchronize(st));
+        pr.cloud_fast_div = (bad == 0) && std::getenv("REGOT_B200_CLOUD_EXACT_DIV") == nullptr;
+        c.fast_div = pr.cloud_fast_div ? 1 : 0;
+    }
     if (on_the_fly) {
         pr.M_own.release();
         pr.M = nullptr;

@@ -129,6 +129,7 @@ struct DeviceProblem {
     bool on_the_fly = false;
     int cloud_d = 0;
     double cloud_max = 0.0;
+    bool cloud_fast_div = false;  // the reciprocal-based division was verified against true division on this block
     DevBuf<double> X_own, Y_own;  // nloc x d, m x d
 };
 

@@ -51,8 +51,8 @@ __device__ __forceinline__ double gradient_row(const double (&mv)[kEPL], double 
 // The rows of one segment (the part of this CTA's tile range inside one column panel) for one
 // consumer warp: `row` is the warp's row in the segment's first tile.  Row partials are staged per
 // lane and flushed every kRowGroup tiles with one transposing sum.
-template <bool kRagged>
-__device__ __forceinline__ void gradient_segment(RingCursor& ring, int lane, int row, int seg_tiles, int nloc,
+template <bool kRagged, bool kCloud>
+__device__ __forceinline__ void gradient_segment(const CloudRows& rows, RingCursor& ring, int lane, int row, int seg_tiles, int nloc,
                                                  const double* __restrict__ alpha, const double (&bj)[kEPL],
                                                  double (&colacc)[kEPL], unsigned cmask, const ExpScale& E,
                                                  uint32_t tbl_lane, double* stage, double* rowdst)
@@ -67,9 +67,19 @@ __device__ __forceinline__ void gradient_segment(RingCursor& ring, int lane, int
             const double ai = ai_next;
             ai_next = __ldg(alpha + min(row + kTR, nloc - 1));
             double mv[kEPL];
-            ring.wait();
-            ring.load_row(mv);
-            ring.release(lane);  // the costs are in registers: the slot refills while we compute
+            if (kCloud) {
+                double2 m2[4];
+                rows.row(m2, row, lane);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    mv[2 * q] = m2[q].x;
+                    mv[2 * q + 1] = m2[q].y;
+                }
+            } else {
+                ring.wait();
+                ring.load_row(mv);
+                ring.release(lane);
+            }  // the costs are in registers: the slot refills while we compute
             double rs = 0.0;
             if (row < nloc) rs = gradient_row<kRagged>(mv, ai, bj, colacc, cmask, E, tbl_lane);
             stage[k * 32 + lane] = rs;
@@ -95,13 +105,15 @@ __global__ void __launch_bounds__(sweep_threads<kCloud>(), 1)
 k_gradient_sweep(const __grid_constant__ CUtensorMap tmap, const GradParams p)
 {
     extern __shared__ __align__(128) unsigned char smem[];
-    const SweepSmem sm = sweep_prologue(smem, &tmap, p.exp_table, kCloud ? kCloudWarps : 1);
+    const SweepSmem sm = sweep_prologue(smem, &tmap, p.exp_table, !kCloud);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
-    if (warp >= kTR) {
-        sweep_feed<kCloud>(&tmap, p.g, sm.tiles, sm.full, sm.empty, warp, lane);
+    if (!kCloud && warp == kTR) {
+        sweep_producer(&tmap, p.g, sm.tiles, sm.full, sm.empty);
         return;
     }
+    CloudRows rows;
+    if (kCloud) rows.init(p.g, sm.tiles);
 
     // ---- consumer warp `warp` owns row `warp` of every tile ----
     long t0, t1;
@@ -136,12 +148,13 @@ k_gradient_sweep(const __grid_constant__ CUtensorMap tmap, const GradParams p)
                 colacc[2 * q + e] = 0.0;
             }
         }
+        if (kCloud) rows.load_panel(col0);
         double* const rowdst = p.rowpart + (size_t)panel * nloc;
         if (col0 + kTC > m)
-            gradient_segment<true>(ring, lane, rt * kTR + warp, seg_tiles, nloc, p.alpha, bj, colacc, cmask, E, tbl_lane,
+            gradient_segment<true, kCloud>(rows, ring, lane, rt * kTR + warp, seg_tiles, nloc, p.alpha, bj, colacc, cmask, E, tbl_lane,
                                    stage, rowdst);
         else
-            gradient_segment<false>(ring, lane, rt * kTR + warp, seg_tiles, nloc, p.alpha, bj, colacc, cmask, E, tbl_lane,
+            gradient_segment<false, kCloud>(rows, ring, lane, rt * kTR + warp, seg_tiles, nloc, p.alpha, bj, colacc, cmask, E, tbl_lane,
                                     stage, rowdst);
         left -= seg_tiles;
         rt += seg_tiles;

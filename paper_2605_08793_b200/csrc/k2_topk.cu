@@ -62,17 +62,19 @@ __global__ void __launch_bounds__(sweep_threads<kCloud>(), 1)
 k_topk_sweep(const __grid_constant__ CUtensorMap tmap, const TopkParams p)
 {
     extern __shared__ __align__(128) unsigned char smem[];
-    const SweepSmem sm = sweep_prologue(smem, &tmap, p.exp_table, kCloud ? kCloudWarps : 1);
+    const SweepSmem sm = sweep_prologue(smem, &tmap, p.exp_table, !kCloud);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     unsigned int* shist = reinterpret_cast<unsigned int*>(sm.scratch);
     if (kPass == kPassHist) {
         for (int q = threadIdx.x; q < kCoarseBins; q += blockDim.x) shist[q] = 0u;
         __syncthreads();
     }
-    if (warp >= kTR) {
-        sweep_feed<kCloud>(&tmap, p.g, sm.tiles, sm.full, sm.empty, warp, lane);
+    if (!kCloud && warp == kTR) {
+        sweep_producer(&tmap, p.g, sm.tiles, sm.full, sm.empty);
         return;
     }
+    CloudRows rows;
+    if (kCloud) rows.init(p.g, sm.tiles);
     long t0, t1;
     sweep_range(p.g, t0, t1);
     const uint32_t tbl_lane = smem_u32(sm.table) + (uint32_t)(lane & 15) * 8u;
@@ -101,14 +103,19 @@ k_topk_sweep(const __grid_constant__ CUtensorMap tmap, const TopkParams p)
                 cmask |= (ok ? 1u : 0u) << (2 * q + e);
             }
         }
+        if (kCloud) rows.load_panel(col0);
         for (int it = 0; it < seg_tiles; ++it) {
             const int row = rt * kTR + warp;
-            mbar_wait(&sm.full[s], ph);
+            if (!kCloud) mbar_wait(&sm.full[s], ph);
             if (row < nloc) {
-                const double2* trow = tile_row + (size_t)s * (kTileElems / 2);
                 double2 mv[4];
+                if (kCloud) {
+                    rows.row(mv, row, lane);
+                } else {
+                    const double2* trow = tile_row + (size_t)s * (kTileElems / 2);
 #pragma unroll
-                for (int q = 0; q < 4; ++q) mv[q] = trow[q * 32 + lane];
+                    for (int q = 0; q < 4; ++q) mv[q] = trow[q * 32 + lane];
+                }
                 double T[kEPL], cost[kEPL];
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
@@ -182,11 +189,13 @@ k_topk_sweep(const __grid_constant__ CUtensorMap tmap, const TopkParams p)
                     }
                 }
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&sm.empty[s]);
-            if (++s == kStages) {
-                s = 0;
-                ph ^= 1u;
+            if (!kCloud) {
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&sm.empty[s]);
+                if (++s == kStages) {
+                    s = 0;
+                    ph ^= 1u;
+                }
             }
             ++rt;
             --left;

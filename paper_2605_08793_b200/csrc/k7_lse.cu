@@ -34,13 +34,9 @@ __device__ __forceinline__ double dmax(double a, double b) { return a > b ? a : 
 // v_ij = (beta_j - M_ij) / eta.  Warp w owns row w of each tile: lane max ->
 // warp max (shuffles) -> sum of exp(v - max) -> staged transposing flush.
 template <bool kRagged>
-__device__ __forceinline__ void row_lse_row(const double2* __restrict__ trow, int lane, const double (&bj)[kEPL],
-                                            unsigned cmask, double inv_eta, uint32_t tbl_lane, double& wmax,
-                                            double& lsum)
+__device__ __forceinline__ void row_lse_row(const double2 (&mv)[4], const double (&bj)[kEPL], unsigned cmask,
+                                            double inv_eta, uint32_t tbl_lane, double& wmax, double& lsum)
 {
-    double2 mv[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) mv[q] = trow[q * 32 + lane];
     double v[kEPL];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -78,12 +74,14 @@ __global__ void __launch_bounds__(sweep_threads<kCloud>(), 1)
 k_row_lse_sweep(const __grid_constant__ CUtensorMap tmap, const LseParams p)
 {
     extern __shared__ __align__(128) unsigned char smem[];
-    const SweepSmem sm = sweep_prologue(smem, &tmap, p.exp_table, kCloud ? kCloudWarps : 1);
+    const SweepSmem sm = sweep_prologue(smem, &tmap, p.exp_table, !kCloud);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (warp >= kTR) {
-        sweep_feed<kCloud>(&tmap, p.g, sm.tiles, sm.full, sm.empty, warp, lane);
+    if (!kCloud && warp == kTR) {
+        sweep_producer(&tmap, p.g, sm.tiles, sm.full, sm.empty);
         return;
     }
+    CloudRows rows;
+    if (kCloud) rows.init(p.g, sm.tiles);
     long t0, t1;
     sweep_range(p.g, t0, t1);
     if (t0 >= t1) return;
@@ -114,6 +112,7 @@ k_row_lse_sweep(const __grid_constant__ CUtensorMap tmap, const LseParams p)
             }
         }
         const bool ragged = (col0 + kTC > m);
+        if (kCloud) rows.load_panel(col0);
         int done = 0;
         while (done < seg_tiles) {
             const int cnt = min(kRowGroup, seg_tiles - done);
@@ -121,18 +120,27 @@ k_row_lse_sweep(const __grid_constant__ CUtensorMap tmap, const LseParams p)
             double my_max = 0.0;  // lane k of the group keeps the warp max of staged row k
             for (int k = 0; k < cnt; ++k) {
                 const int row = rt * kTR + warp;
-                mbar_wait(&sm.full[s], ph);
+                if (!kCloud) mbar_wait(&sm.full[s], ph);
                 double wmax = -INFINITY, lsum = 0.0;
                 if (row < nloc) {
-                    const double2* trow = tile_row + (size_t)s * (kTileElems / 2);
-                    if (ragged) row_lse_row<true>(trow, lane, bj, cmask, inv_eta, tbl_lane, wmax, lsum);
-                    else row_lse_row<false>(trow, lane, bj, cmask, inv_eta, tbl_lane, wmax, lsum);
+                    double2 mv[4];
+                    if (kCloud) {
+                        rows.row(mv, row, lane);
+                    } else {
+                        const double2* trow = tile_row + (size_t)s * (kTileElems / 2);
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) mv[q] = trow[q * 32 + lane];
+                    }
+                    if (ragged) row_lse_row<true>(mv, bj, cmask, inv_eta, tbl_lane, wmax, lsum);
+                    else row_lse_row<false>(mv, bj, cmask, inv_eta, tbl_lane, wmax, lsum);
                 }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&sm.empty[s]);
-                if (++s == kStages) {
-                    s = 0;
-                    ph ^= 1u;
+                if (!kCloud) {
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&sm.empty[s]);
+                    if (++s == kStages) {
+                        s = 0;
+                        ph ^= 1u;
+                    }
                 }
                 stage[k * 32 + lane] = lsum;
                 if (lane == 4 * k) my_max = wmax;
@@ -186,12 +194,14 @@ __global__ void __launch_bounds__(sweep_threads<kCloud>(), 1)
 k_col_lse_sweep(const __grid_constant__ CUtensorMap tmap, const LseParams p)
 {
     extern __shared__ __align__(128) unsigned char smem[];
-    const SweepSmem sm = sweep_prologue(smem, &tmap, p.exp_table, kCloud ? kCloudWarps : 1);
+    const SweepSmem sm = sweep_prologue(smem, &tmap, p.exp_table, !kCloud);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (warp >= kTR) {
-        sweep_feed<kCloud>(&tmap, p.g, sm.tiles, sm.full, sm.empty, warp, lane);
+    if (!kCloud && warp == kTR) {
+        sweep_producer(&tmap, p.g, sm.tiles, sm.full, sm.empty);
         return;
     }
+    CloudRows rows;
+    if (kCloud) rows.init(p.g, sm.tiles);
     long t0, t1;
     sweep_range(p.g, t0, t1);
     if (t0 >= t1) return;
@@ -210,6 +220,7 @@ k_col_lse_sweep(const __grid_constant__ CUtensorMap tmap, const LseParams p)
 
     while (left > 0) {
         const int seg_tiles = (int)min((long)(nrt - rt), left);
+        if (kCloud) rows.load_panel(panel * kTC);
         double cmax[kEPL], csum[kEPL];
 #pragma unroll
         for (int k = 0; k < kEPL; ++k) {
@@ -224,12 +235,16 @@ k_col_lse_sweep(const __grid_constant__ CUtensorMap tmap, const LseParams p)
                 if (rt + 1 == nrt) nrow = warp;
                 ai_next = (nrow < nloc && left > 1) ? __ldg(p.vec + nrow) : 0.0;
             }
-            mbar_wait(&sm.full[s], ph);
+            if (!kCloud) mbar_wait(&sm.full[s], ph);
             if (row < nloc) {
-                const double2* trow = tile_row + (size_t)s * (kTileElems / 2);
                 double2 mv[4];
+                if (kCloud) {
+                    rows.row(mv, row, lane);
+                } else {
+                    const double2* trow = tile_row + (size_t)s * (kTileElems / 2);
 #pragma unroll
-                for (int q = 0; q < 4; ++q) mv[q] = trow[q * 32 + lane];
+                    for (int q = 0; q < 4; ++q) mv[q] = trow[q * 32 + lane];
+                }
                 double v[kEPL], e[kEPL];
                 unsigned amax = 0;
 #pragma unroll
@@ -256,11 +271,13 @@ k_col_lse_sweep(const __grid_constant__ CUtensorMap tmap, const LseParams p)
                     cmax[k] = up ? v[k] : cmax[k];
                 }
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&sm.empty[s]);
-            if (++s == kStages) {
-                s = 0;
-                ph ^= 1u;
+            if (!kCloud) {
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&sm.empty[s]);
+                if (++s == kStages) {
+                    s = 0;
+                    ph ^= 1u;
+                }
             }
             ++rt;
             --left;

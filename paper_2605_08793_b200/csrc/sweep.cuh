@@ -29,10 +29,11 @@ constexpr int kTileBytes = kTileElems * 8;
 constexpr int kConsumerThreads = kTR * kWarp;
 constexpr int kSweepThreads = kConsumerThreads + kWarp;
 constexpr int kRowGroup = 8;          // row partials staged per warp before a flush
-// point-cloud problems whose cost is formed on the fly: the TMA producer warp is replaced by
-// kCloudWarps warps that compute the tiles into the same ring
-constexpr int kCloudWarps = 4;
-constexpr int kCloudSweepThreads = kConsumerThreads + kCloudWarps * kWarp;
+// point-cloud problems whose cost is formed on the fly have no producer warp and no tile ring: every
+// consumer warp computes its own row from the row's point and a shared-memory copy of the panel's
+// 256 target points (CloudRows below), which takes the ring's place in shared memory
+constexpr int kCloudSweepThreads = kConsumerThreads;
+constexpr int kCloudMaxD = (kStages * kTileBytes) / (kTC * 8);  // coordinates that fit: 64
 
 // dynamic shared memory carve-up (bytes)
 constexpr int kSmemTiles = 0;
@@ -50,8 +51,25 @@ struct CloudGeom {
     const double* X;  // nloc x d, this rank's rows
     const double* Y;  // m x d
     int d;
-    double cmax;  // maximum of the un-normalised cost over the GLOBAL matrix
+    double cmax;      // maximum of the un-normalised cost over the GLOBAL matrix
+    double inv_cmax;  // RN(1 / cmax)
+    int fast_div;     // set_pointcloud verified cloud_div_fast == true division on every entry of this block
 };
+// s / cmax, correctly rounded, from the reciprocal and two residual corrections (Markstein): 5 fused
+// multiply-adds that interleave across entries, where the generic division is a ~20-instruction
+// dependent sequence with a slow-path call.  The identity with true division is not assumed: it is
+// CHECKED on every entry of the block when the problem is set (k_cloud_verify_div) and the exact
+// division is used if a single entry differs.
+__device__ __forceinline__ double cloud_div_fast(double s, double cmax, double inv_cmax)
+{
+    const double q0 = s * inv_cmax;
+    const double q1 = __fma_rn(__fma_rn(-q0, cmax, s), inv_cmax, q0);
+    return __fma_rn(__fma_rn(-q1, cmax, s), inv_cmax, q1);
+}
+__device__ __forceinline__ double cloud_div(double s, const CloudGeom& c)
+{
+    return c.fast_div ? cloud_div_fast(s, c.cmax, c.inv_cmax) : __ddiv_rn(s, c.cmax);
+}
 __device__ __forceinline__ double cloud_sqdist(const double* __restrict__ xi, const double* __restrict__ yj, int d)
 {
     double s = 0.0;
@@ -63,7 +81,7 @@ __device__ __forceinline__ double cloud_sqdist(const double* __restrict__ xi, co
 }
 __device__ __forceinline__ double cloud_cost(const CloudGeom& c, int i, int j)
 {
-    return __ddiv_rn(cloud_sqdist(c.X + (size_t)i * c.d, c.Y + (size_t)j * c.d, c.d), c.cmax);
+    return cloud_div(cloud_sqdist(c.X + (size_t)i * c.d, c.Y + (size_t)j * c.d, c.d), c);
 }
 
 struct SweepGeom {
@@ -80,12 +98,6 @@ __device__ __forceinline__ void sweep_range(const SweepGeom& g, long& t0, long& 
     t0 = (g.total_tiles * (long)blockIdx.x) / (long)gridDim.x;
     t1 = (g.total_tiles * (long)(blockIdx.x + 1)) / (long)gridDim.x;
 }
-
-// Body of the warps above the consumers: stream (kCloud == false, one TMA warp) or compute
-// (kCloud == true, kCloudWarps warps) this CTA's tiles into the ring.
-template <bool kCloud>
-__device__ __forceinline__ void sweep_feed(const CUtensorMap* tmap, const SweepGeom& g, double* tiles, uint64_t* full,
-                                           uint64_t* empty, int warp, int lane);
 
 // Producer warp body: stream this CTA's tile range through the ring.
 __device__ __forceinline__ void sweep_producer(const CUtensorMap* tmap, const SweepGeom& g, double* tiles,
@@ -110,53 +122,6 @@ __device__ __forceinline__ void sweep_producer(const CUtensorMap* tmap, const Sw
     }
 }
 
-// Producer warps of the on-the-fly kernels: thread p of the kCloudWarps * 32 producers owns columns
-// 2p, 2p + 1 of every 256-wide tile and computes them for the tile's 16 rows (32 running sums, the
-// coordinate loop outermost so any d works), then stores them with one conflict-free 16-byte store
-// per row.  Rows / columns outside the block get finite dummies; consumers mask them like TMA's
-// zero fill.
-__device__ __forceinline__ void cloud_producer(const SweepGeom& g, double* tiles, uint64_t* full, uint64_t* empty, int pw,
-                                               int lane)
-{
-    long t0, t1;
-    sweep_range(g, t0, t1);
-    const int p = pw * kWarp + lane;
-    const CloudGeom& c = g.cloud;
-    int s = 0;
-    uint32_t ph = 0;
-    for (long t = t0; t < t1; ++t) {
-        const int panel = (int)(t / g.n_row_tiles), rt = (int)(t % g.n_row_tiles);
-        const int j0 = min(panel * kTC + 2 * p, g.m - 1), j1 = min(panel * kTC + 2 * p + 1, g.m - 1);
-        const double* y0 = c.Y + (size_t)j0 * c.d;
-        const double* y1 = c.Y + (size_t)j1 * c.d;
-        const int row0 = rt * kTR;
-        double acc0[kTR], acc1[kTR];
-#pragma unroll
-        for (int r = 0; r < kTR; ++r) acc0[r] = acc1[r] = 0.0;
-        for (int k = 0; k < c.d; ++k) {
-            const double ya = __ldg(y0 + k), yb = __ldg(y1 + k);
-#pragma unroll
-            for (int r = 0; r < kTR; ++r) {
-                const double x = __ldg(c.X + (size_t)min(row0 + r, g.nloc - 1) * c.d + k);
-                const double da = __dsub_rn(x, ya), db = __dsub_rn(x, yb);
-                acc0[r] = __dadd_rn(acc0[r], __dmul_rn(da, da));
-                acc1[r] = __dadd_rn(acc1[r], __dmul_rn(db, db));
-            }
-        }
-        mbar_wait(&empty[s], ph ^ 1u);
-        double* dst = tiles + (size_t)s * kTileElems + 2 * p;
-#pragma unroll
-        for (int r = 0; r < kTR; ++r)
-            *reinterpret_cast<double2*>(dst + r * kTC) = make_double2(__ddiv_rn(acc0[r], c.cmax), __ddiv_rn(acc1[r], c.cmax));
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&full[s]);
-        if (++s == kStages) {
-            s = 0;
-            ph ^= 1u;
-        }
-    }
-}
-
 // Common prologue: barriers + exp table.  Returns pointers into dynamic smem.
 struct SweepSmem {
     double* tiles;
@@ -165,9 +130,9 @@ struct SweepSmem {
     uint64_t* full;
     uint64_t* empty;
 };
-// full_count: arrivals that complete a stage (1 for the TMA producer, kCloudWarps for on-the-fly tiles)
+// use_tma == false (on-the-fly cost): the ring and its barriers stay unused
 __device__ __forceinline__ SweepSmem sweep_prologue(unsigned char* smem, const CUtensorMap* tmap,
-                                                    const double* __restrict__ exp_table, int full_count = 1)
+                                                    const double* __restrict__ exp_table, bool use_tma = true)
 {
     SweepSmem s;
     s.tiles = reinterpret_cast<double*>(smem + kSmemTiles);
@@ -176,9 +141,9 @@ __device__ __forceinline__ SweepSmem sweep_prologue(unsigned char* smem, const C
     s.full = reinterpret_cast<uint64_t*>(smem + kSmemBars);
     s.empty = s.full + kStages;
     if (threadIdx.x == 0) {
-        if (full_count == 1) tma_prefetch_desc(tmap);
+        if (use_tma) tma_prefetch_desc(tmap);
         for (int i = 0; i < kStages; ++i) {
-            mbar_init(&s.full[i], full_count);
+            mbar_init(&s.full[i], 1);
             mbar_init(&s.empty[i], kTR);
         }
         fence_mbar_init();
@@ -189,14 +154,64 @@ __device__ __forceinline__ SweepSmem sweep_prologue(unsigned char* smem, const C
 }
 
 template <bool kCloud>
-__device__ __forceinline__ void sweep_feed(const CUtensorMap* tmap, const SweepGeom& g, double* tiles, uint64_t* full,
-                                           uint64_t* empty, int warp, int lane)
-{
-    if (kCloud) cloud_producer(g, tiles, full, empty, warp - kTR, lane);
-    else sweep_producer(tmap, g, tiles, full, empty);
-}
-template <bool kCloud>
 constexpr int sweep_threads() { return kCloud ? kCloudSweepThreads : kSweepThreads; }
+
+// Consumer side of the on-the-fly kernels.  load_panel(): the consumer warps copy the panel's 256
+// target points into shared memory, coordinate-major ([k][256], so a lane's 8 columns of one
+// coordinate are four conflict-free 16-byte loads).  row(): the lane's 8 cost entries of one row, in
+// the column order of the resident-matrix tiles (columns 2 lane + 64 q + {0, 1}), with the arithmetic
+// of cloud_sqdist / cloud_div -- the same bits as the materialised matrix.
+struct CloudRows {
+    uint32_t ysm;
+    CloudGeom c;
+    int nloc, m;
+    __device__ __forceinline__ void init(const SweepGeom& g, const double* tiles)
+    {
+        ysm = smem_u32(tiles);
+        c = g.cloud;
+        nloc = g.nloc;
+        m = g.m;
+    }
+    // all kConsumerThreads threads; named barrier 2 fences the previous panel's readers and this copy
+    __device__ __forceinline__ void load_panel(int col0) const
+    {
+        bar_sync(2, kConsumerThreads);
+        for (int q = threadIdx.x; q < kTC * c.d; q += kConsumerThreads) {
+            const int col = q / c.d, k = q - col * c.d;  // consecutive threads read consecutive doubles of Y
+            const int j = min(col0 + col, m - 1);        // columns past the block: finite dummies, masked by the caller
+            const double y = __ldg(c.Y + (size_t)j * c.d + k);
+            asm volatile("st.shared.f64 [%0], %1;" ::"r"(ysm + (uint32_t)(k * kTC + col) * 8u), "d"(y) : "memory");
+        }
+        bar_sync(2, kConsumerThreads);
+    }
+    __device__ __forceinline__ void row(double2 (&mv)[4], int row, int lane) const
+    {
+        const double* xr = c.X + (size_t)min(row, nloc - 1) * c.d;
+        double acc[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[e] = 0.0;
+        uint32_t yk = ysm + (uint32_t)lane * 16u;
+        for (int k = 0; k < c.d; ++k) {
+            const double x = __ldg(xr + k);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const double2 y = lds_f64x2(yk + (uint32_t)q * 512u);
+                const double da = __dsub_rn(x, y.x), db = __dsub_rn(x, y.y);
+                acc[2 * q] = __dadd_rn(acc[2 * q], __dmul_rn(da, da));
+                acc[2 * q + 1] = __dadd_rn(acc[2 * q + 1], __dmul_rn(db, db));
+            }
+            yk += kTC * 8u;
+        }
+        if (c.fast_div) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                mv[q] = make_double2(cloud_div_fast(acc[2 * q], c.cmax, c.inv_cmax), cloud_div_fast(acc[2 * q + 1], c.cmax, c.inv_cmax));
+        } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) mv[q] = make_double2(__ddiv_rn(acc[2 * q], c.cmax), __ddiv_rn(acc[2 * q + 1], c.cmax));
+        }
+    }
+};
 
 // single cost entry for the low-volume kernels (dense plan, pattern gathers)
 struct CostViewDev {
@@ -267,6 +282,8 @@ inline CloudGeom cloud_geom(const regot_ctx* ctx)
     c.Y = ctx->prob.Y_own.p;
     c.d = ctx->prob.cloud_d;
     c.cmax = ctx->prob.cloud_max;
+    c.inv_cmax = 1.0 / ctx->prob.cloud_max;
+    c.fast_div = ctx->prob.cloud_fast_div ? 1 : 0;
     return c;
 }
 inline CostViewDev cost_view_dev(const regot_ctx* ctx)

@@ -617,6 +617,9 @@ void finish_structure(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, regot_spars
         cut(i, rp[(size_t)i], rp[(size_t)i + 1]);
         bin(i, rp[(size_t)i + 1] - rp[(size_t)i]);
     }
+    S.n_chunks_rows = (int)chunk.size() / 4;
+    S.n_lines_s_rows = (int)ls.size();
+    S.n_lines_m_rows = (int)lm.size();
     for (int j = 0; j < mm1; ++j) {
         cut(nloc + j, cp[(size_t)j], cp[(size_t)j + 1]);
         bin(nloc + j, cp[(size_t)j + 1] - cp[(size_t)j]);

@@ -51,6 +51,7 @@ struct regot_sparse {
     mutable rg::DevBuf<double> chunk_part;
     mutable rg::DevBuf<unsigned int> chunk_cnt;
     int n_chunks = 0, n_long = 0;
+    int n_chunks_rows = 0, n_lines_s_rows = 0, n_lines_m_rows = 0;  // rows come first in chunks / lines_s / lines_m
     // the other lines, binned by length so the mat-vec can give each line a fitting number of
     // lanes: short (<= kShortLine entries, 8 lanes) and medium (<= kLongLine, one warp)
     rg::DevBuf<int> lines_s, lines_m;

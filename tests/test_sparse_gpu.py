@@ -167,6 +167,69 @@ def test_direction_matches_cholesky_oracle(solver, oracle):
     assert np.abs(d0).max() == 0.0
 
 
+@pytest.fixture(scope="module")
+def multikernel_solver():
+    """A context that takes the kernel-by-kernel Schur PCG (the path of row-sharded runs and of problems
+    whose iterated vector does not fit in shared memory) on one GPU."""
+    import os
+
+    os.environ["REGOT_B200_MULTIKERNEL_PCG"] = "1"
+    try:
+        s = rg.Solver(0)
+    finally:
+        del os.environ["REGOT_B200_MULTIKERNEL_PCG"]
+    yield s
+    s.close()
+
+
+def test_multikernel_pcg_matches_oracle_and_persistent_kernel(solver, multikernel_solver, oracle):
+    p = oracle.gen_problem("rand", 300, 257, 0.1, seed=6701)
+    a0, b0 = oracle.rand_dual(300, 257, 0.2, 6801)
+    coords = oracle.select_topk(oracle.plan(p, a0, b0), 6000)
+    x = rg.DualPoint(a0, b0)
+    dim = 300 + 257 - 1
+    rng = np.random.default_rng(7)
+    got = []
+    for s in (solver, multikernel_solver):
+        s.set_problem(to_problem(p))
+        g = s.fused_gradient(x)
+        tau = min(1.0, g.grad_norm2)
+        A = s.assemble(x, rg.SparsityPattern(300, 256, coords), tau, g)
+        d, its = s.compute_direction(A, g.grad, cg_rtol=1e-13)
+        assert its > 0 and g.grad @ d < 0
+        sv = 0.05 * rng.uniform(-1, 1, dim) if not got else sv
+        R = oracle.assemble(p, a0, b0, coords, tau)
+        u, v = R.matvec(sv) + 0.3 * sv, R.matvec(sv)
+        xi, zeta = 1.0 / (u @ sv), -1.0 / (v @ sv)
+        d2, _ = s.compute_direction(A, g.grad, u, v, xi, zeta, cg_rtol=1e-13)
+        dr, _ = R.compute_direction(oracle.gradient(p, a0, b0)["grad"])
+        dr2, _ = R.compute_direction(oracle.gradient(p, a0, b0)["grad"], u, v, xi, zeta)
+        assert np.linalg.norm(d - dr) <= 1e-8 * np.linalg.norm(dr)
+        assert np.linalg.norm(d2 - dr2) <= 1e-8 * np.linalg.norm(dr2)
+        got.append((d, d2))
+    assert np.linalg.norm(got[0][0] - got[1][0]) <= 1e-9 * np.linalg.norm(got[0][0])
+
+
+def test_multikernel_pcg_solve_agrees_with_persistent_kernel(solver, multikernel_solver):
+    from paper_2605_08793_b200 import problems
+
+    p = problems.gen_synthetic2(96, 80, 0.01)
+    cfg = rg.SplrConfig(max_iter=200, tol=1e-8)
+    res = []
+    for s in (solver, multikernel_solver):
+        s.set_problem(p)
+        res.append(s.run_splr(rg.DualPoint.zeros(p.n, p.m), cfg))
+    a, b = res[0].trace.rows[-1], res[1].trace.rows[-1]
+    assert a.marginal_error <= 1e-8 and b.marginal_error <= 1e-8
+    # the same trajectory to rounding; the last few iterations sit on a plateau just above the tolerance,
+    # so the crossing itself may move by a few iterations
+    for u, v in zip(res[0].steps[:40], res[1].steps[:40]):
+        assert abs(u.f_after - v.f_after) <= 1e-12 * (1 + abs(u.f_after))
+        assert u.sinkhorn_selected == v.sinkhorn_selected and u.ls_evals == v.ls_evals
+    assert abs(a.iter - b.iter) <= max(1, round(0.15 * a.iter))
+    assert abs(a.f - b.f) <= 1e-9 * (1 + abs(a.f))
+
+
 def test_foreign_and_invalid_inputs_rejected(solver, oracle):
     p = oracle.gen_problem("rand", 8, 6, 0.1, seed=3601)
     solver.set_problem(to_problem(p))

@@ -648,7 +648,7 @@ int sparse_pcg(regot_ctx* ctx, cudaStream_t st, ncclComm* comm, SparseWS& ws, co
 {
     if (nrhs < 1 || nrhs > kMaxRhs) raise(REGOT_E_VALIDATION, "pcg: bad number of right-hand sides");
     // one GPU and both iterated vectors fit in shared memory: the persistent kernel; else kernel by kernel
-    if (ctx->world == 1 && !ctx->force_multikernel_pcg && S.pcg.vec_smem_r && S.pcg.vec_smem_c)
+    if (ctx->world == 1 && !ctx->force_multikernel_pcg && S.pcg.fits)
         return pcg_schur_persistent(ctx, st, ws, S, nrhs, rhs, sol, rtol, max_iter);
     return pcg_schur_multikernel(ctx, st, comm, ws, S, nrhs, rhs, sol, rtol, max_iter);
 }

@@ -15,20 +15,19 @@
 // One iteration = row phase (t = D1^-1 B z) | barrier | column phase (w = D2 z - B' t, delta
 // partials) | grid reduction | vector update (gamma partials) | grid reduction.
 //
-// What bounds a phase is the number of L2 requests an SM can issue (a scattered gather is one
-// request per entry, about 0.5 requests / clk / SM measured), not bytes.  So, per phase:
-//   * if the gathered vector fits in shared memory (16 B x length), every CTA copies it there with
-//     coalesced loads at the start of the phase and gathers from shared memory; the matrix streams
-//     from global memory, coalesced;
-//   * otherwise the warps keep THEIR part of the matrix in a shared-memory log (below) and only the
-//     gathers go to L2.
+// What bounds a scattered gather through L2 is the number of requests an SM can issue (one per entry,
+// a fraction of a request per clock measured), not bytes, and a grid-wide barrier costs ~2400 clk
+// (tools/barrier_bench.cu).  So this kernel runs only when the gathered vector (16 B x length) fits
+// in shared memory: every CTA copies it there with coalesced loads at the start of a phase and
+// gathers from shared memory, while the matrix streams from global memory, coalesced.  Larger
+// problems take the kernel-by-kernel form of the same algorithm (k4_sparse.cu), where the two half
+// mat-vecs run at 32 warps / SM.
 // Work schedule (built on the host per pattern, sparse.hpp PcgSchedule): rows and columns of B are
 // cut into warp-sized items -- 4 short lines (8 lanes each), one medium line, or one 256-entry
-// chunk of a long line -- dealt to the grid's warps longest-first.  The assignment is static over
-// the CG iterations, so in log mode every warp copies its items' (index, value) pairs and diagonals
-// into a private shared-memory log once per solve and replays it each iteration; items that do not
-// fit are read from global memory.  Every sum has a fixed order (lane-sequential partials,
-// butterfly, chunk order, CTA order): results are bitwise reproducible.  No float atomics.
+// chunk of a long line -- dealt to the grid's warps longest-first; the assignment is static over the
+// CG iterations and each warp caches its item descriptors in shared memory.  Every sum has a fixed
+// order (lane-sequential partials, butterfly, chunk order, CTA order): results are bitwise
+// reproducible.  No float atomics.
 #include "common.cuh"
 #include "ctx.hpp"
 #include "sparse.hpp"
@@ -42,7 +41,6 @@ namespace rg {
 constexpr int kSchurThreads = 512;
 constexpr int kSchurWarps = kSchurThreads / 32;
 static_assert(kSchurWarps == kPcgWarpsPerCta, "schedule and kernel disagree on warps per CTA");
-constexpr int kLogRowBytes = 32 * 12;  // 32 doubles + 32 ints
 constexpr int kMaxGrid = 160;     // CTAs whose partials are staged in shared memory by grid_sum4
 constexpr int kLongStage = 256;   // long lines whose dot contributions are staged likewise
 constexpr int kSchurScratchBytes = (4 * kSchurWarps + 8 + 4 * kMaxGrid + 2 * kLongStage) * 8;
@@ -51,8 +49,7 @@ enum { kRowMain = 0, kRowFinal = 1, kColInit = 2, kColMain = 3 };
 
 struct SchurParams {
     int nloc, mfree, nrhs, max_iter, n_long, nw, fixed_iters;
-    int vec_smem_r, vec_smem_c;  // phase gathers from a shared-memory copy of the vector
-    int vec_bytes, desc_cap, log_rows;  // shared-memory carve-up: vector buffer, desc_cap descriptors and log_rows log rows per warp
+    int vec_bytes, desc_cap;  // shared-memory carve-up: vector buffer, then desc_cap descriptors per warp
     double tol2;
     const int* col;  // CSR of B
     const double* val;
@@ -62,7 +59,6 @@ struct SchurParams {
     const double* dB;
     const int* items;  // kPcgItemInts per item
     const int* wptr;   // 2 x (nw + 1)
-    const int* wres;   // 2 x nw: leading items of each warp that live in the shared-memory log
     double* chunk_part;  // n_chunks x 2
     unsigned int* chunk_cnt;
     double* longdot;  // n_long x 2
@@ -131,11 +127,10 @@ __device__ __noinline__ void grid_sum4(const SchurParams& P, double (&v)[4], dou
     __syncthreads();
 }
 
-// This warp's log, as 32-bit shared-window addresses
+// shared-memory carve-up as 32-bit shared-window addresses
 struct WarpLog {
-    uint32_t val0, idx0;  // lane 0's slot of row 0: row r of lane l at val0 + 256 r + 8 l / idx0 + 128 r + 4 l
-    uint32_t vec;         // the shared copy of the gathered vector (x2)
-    uint32_t desc;        // this warp's cached item descriptors (kPcgItemInts ints each)
+    uint32_t vec;   // the shared copy of the gathered vector (x2)
+    uint32_t desc;  // this warp's cached item descriptors (kPcgItemInts ints each)
 };
 __device__ __forceinline__ int lds_i32(uint32_t addr)
 {
@@ -156,41 +151,6 @@ __device__ __forceinline__ void sts_f64x2(uint32_t addr, double2 v)
     asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(addr), "d"(v.x), "d"(v.y) : "memory");
 }
 
-// Copy the leading `n_res` items of one phase into the warp's log, starting at log row `row`.
-// Row layout of an item: header {idx: line ids at lanes 0/8/16/24, meta (kind, nE, chunk, slot,
-// first, cnt) at lanes 1..6; val: the diagonal entry at the group leaders' lanes}, then nE rows of
-// (byte offset of the gathered x2 entry, value), lane-major.  Padding entries are (0, 0.0).
-__device__ __noinline__ int fill_log(const SchurParams& P, const bool rows, const WarpLog& L, int i0, int n_res, int row,
-                                    int lane)
-{
-    const int* __restrict__ src_idx = rows ? P.col : P.cscrow;
-    const double* __restrict__ src_val = rows ? P.val : P.cscval;
-    const double* __restrict__ diagv = rows ? P.dA : P.dB;
-    for (int q = i0; q < i0 + n_res; ++q) {
-        const int* d = P.items + (size_t)q * kPcgItemInts;
-        const int kind = __ldg(d), nE = __ldg(d + 1);
-        const int sub = kind == 0 ? lane >> 3 : 0, gl = kind == 0 ? lane & 7 : lane, stride = kind == 0 ? 8 : 32;
-        const int line = __ldg(d + 8 + sub), beg = __ldg(d + 12 + sub), len = __ldg(d + 16 + sub);
-        int h = (gl == 0) ? line : -1;
-        if (lane >= 1 && lane <= 6) h = __ldg(d + lane - 1);
-        double hv = 0.0;
-        if (gl == 0 && line >= 0) hv = __ldg(diagv + line);
-        sts_i32(L.idx0 + 128u * row + 4u * lane, h);
-        sts_f64(L.val0 + 256u * row + 8u * lane, hv);
-#pragma unroll 4
-        for (int e = 0; e < nE; ++e) {
-            const int t = gl + stride * e;
-            const bool ok = t < len;
-            const int c = ok ? __ldg(src_idx + beg + t) : 0;
-            const double v = ok ? __ldg(src_val + beg + t) : 0.0;
-            sts_i32(L.idx0 + 128u * (row + 1 + e) + 4u * lane, c * 16);
-            sts_f64(L.val0 + 256u * (row + 1 + e) + 8u * lane, v);
-        }
-        row += nE + 1;
-    }
-    return row;
-}
-
 // Transposing reduction of (a0, a1) over groups of 8 lanes (full == false) or the warp: on return
 // even lanes hold the group sum of a0, odd lanes that of a1.  3 / 5 shuffles; fixed order.
 __device__ __forceinline__ double reduce2(double a0, double a1, int lane, bool full)
@@ -206,16 +166,12 @@ __device__ __forceinline__ double reduce2(double a0, double a1, int lane, bool f
     return c;
 }
 
-// gathered x2 entry at byte offset `off`: from the shared copy or through L2
-template <bool kVecSmem>
-__device__ __forceinline__ double2 gather2(const char* gxb, uint32_t vec, unsigned off)
+// gathered x2 entry at byte offset `off` of the shared copy of the vector
+__device__ __forceinline__ double2 gather2(uint32_t vec, unsigned off)
 {
-    if (kVecSmem) {
-        double2 v;
-        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(vec + off));
-        return v;
-    }
-    return __ldcg(reinterpret_cast<const double2*>(gxb + off));
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(vec + off));
+    return v;
 }
 
 // Head of one item as every lane needs it, and the first 8 (index, value) pairs of the lane
@@ -257,118 +213,41 @@ __device__ __forceinline__ ItemHead load_head(const SchurParams& P, const double
     h.diag = h.line >= 0 ? __ldg(diagv + h.line) : 1.0;
     return h;
 }
-// One mat-vec phase over this warp's items.  kRows: lines are rows of B, gx is a beta-space vector
-// (x2); else lines are columns of B, gx is the alpha-space vector ta (x2).  `dot` accumulates this
-// lane's component (lane & 1) of gamma (kColInit) or delta (kColMain) over the lines this warp
-// finished.  Items [i0, i0 + n_res) replay the shared-memory log; the others stream the matrix from
-// global memory, the next item's descriptor and first entries prefetched while the current one is
-// reduced (descriptors of the first n_desc streamed items are cached in shared memory at `desc`).
-template <bool kRows, bool kVecSmem>
-__device__ __forceinline__ void run_phase(const SchurParams& P, int mode, const double* gx, const WarpLog& L, int i0,
-                                          int i1, int n_res, int row, uint32_t desc, int n_desc, int lane, double& dot)
+// One mat-vec phase over this warp's items.  kRows: lines are rows of B and the staged vector is a
+// beta-space vector (x2); else lines are columns of B and it is the alpha-space vector ta (x2).  `dot`
+// accumulates this lane's component (lane & 1) of gamma (kColInit) or delta (kColMain) over the lines
+// this warp finished.  The matrix streams from global memory, coalesced, 8 entries per lane in
+// flight; descriptors of the first n_desc items are cached in shared memory at `desc`.
+template <bool kRows>
+__device__ __forceinline__ void run_phase(const SchurParams& P, int mode, const WarpLog& L, int i0, int i1,
+                                          uint32_t desc, int n_desc, int lane, double& dot)
 {
     const int* __restrict__ src_idx = kRows ? P.col : P.cscrow;
     const double* __restrict__ src_val = kRows ? P.val : P.cscval;
     const double* __restrict__ diagv = kRows ? P.dA : P.dB;
-    const char* gxb = reinterpret_cast<const char*>(gx);
     const int kk = lane & 1;
-    // a phase that gathers from shared memory has no log (the vector took its place)
-    const int s0 = kVecSmem ? i0 : i0 + n_res;  // first streamed item
     for (int q = i0; q < i1; ++q) {
-        const bool resident = !kVecSmem && q < s0;
-        int kind, nE, chunk = 0, slot = 0, first = 0, cnt = 0, line;
-        double diag;
         double a0 = 0.0, a1 = 0.0;
-        if (!kVecSmem && resident) {
-            const uint32_t h = L.idx0 + 128u * row;
-            kind = lds_i32(h + 4);
-            nE = lds_i32(h + 8);
-            if (kind == 2) {
-                chunk = lds_i32(h + 12);
-                slot = lds_i32(h + 16);
-                first = lds_i32(h + 20);
-                cnt = lds_i32(h + 24);
+        const int qs = q - i0;
+        const ItemHead h = load_head(P, diagv, desc + (uint32_t)qs * (kPcgItemInts * 4), qs < n_desc, q, lane);
+        const int kind = h.kind, nE = h.nE, chunk = h.chunk, slot = h.slot, first = h.first, cnt = h.cnt, line = h.line;
+        const double diag = h.diag;
+        const int gl = kind == 0 ? lane & 7 : lane, stride = kind == 0 ? 8 : 32;
+        for (int e0 = 0; e0 < nE; e0 += 8) {
+            int c[8];
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int t = gl + stride * (e0 + u);
+                const bool ok = (e0 + u) < nE && t < h.len;
+                c[u] = ok ? __ldg(src_idx + h.beg + t) : 0;
+                v[u] = ok ? __ldg(src_val + h.beg + t) : 0.0;
             }
-            const uint32_t lead = kind == 0 ? (uint32_t)(lane & 24) : 0u;  // the group leader's lane
-            line = lds_i32(h + 4u * lead);
-            diag = lds_f64v(L.val0 + 256u * row + 8u * lead);
-            uint32_t ai = L.idx0 + 128u * (row + 1) + 4u * lane, av = L.val0 + 256u * (row + 1) + 8u * lane;
-            int e = 0;
-            for (; e + 8 <= nE; e += 8) {
-                int id[8];
-                double v[8];
-                double2 g[8];
 #pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    id[u] = lds_i32(ai + 128u * u);
-                    v[u] = lds_f64v(av + 256u * u);
-                }
-#pragma unroll
-                for (int u = 0; u < 8; ++u) g[u] = gather2<kVecSmem>(gxb, L.vec, (unsigned)id[u]);
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    a0 += v[u] * g[u].x;
-                    a1 += v[u] * g[u].y;
-                }
-                ai += 8 * 128u;
-                av += 8 * 256u;
-            }
-            for (; e + 2 <= nE; e += 2) {
-                int id[2];
-                double v[2];
-                double2 g[2];
-#pragma unroll
-                for (int u = 0; u < 2; ++u) {
-                    id[u] = lds_i32(ai + 128u * u);
-                    v[u] = lds_f64v(av + 256u * u);
-                }
-#pragma unroll
-                for (int u = 0; u < 2; ++u) g[u] = gather2<kVecSmem>(gxb, L.vec, (unsigned)id[u]);
-#pragma unroll
-                for (int u = 0; u < 2; ++u) {
-                    a0 += v[u] * g[u].x;
-                    a1 += v[u] * g[u].y;
-                }
-                ai += 2 * 128u;
-                av += 2 * 256u;
-            }
-            if (e < nE) {
-                const int id = lds_i32(ai);
-                const double v = lds_f64v(av);
-                const double2 g = gather2<kVecSmem>(gxb, L.vec, (unsigned)id);
-                a0 += v * g.x;
-                a1 += v * g.y;
-            }
-            row += nE + 1;
-        } else {
-            // matrix from global memory, coalesced, 8 entries per lane in flight
-            const int qs = q - s0;
-            const ItemHead h = load_head(P, diagv, desc + (uint32_t)qs * (kPcgItemInts * 4), qs < n_desc, q, lane);
-            kind = h.kind;
-            nE = h.nE;
-            chunk = h.chunk;
-            slot = h.slot;
-            first = h.first;
-            cnt = h.cnt;
-            line = h.line;
-            diag = h.diag;
-            const int gl = kind == 0 ? lane & 7 : lane, stride = kind == 0 ? 8 : 32;
-            for (int e0 = 0; e0 < nE; e0 += 8) {
-                int c[8];
-                double v[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const int t = gl + stride * (e0 + u);
-                    const bool ok = (e0 + u) < nE && t < h.len;
-                    c[u] = ok ? __ldg(src_idx + h.beg + t) : 0;
-                    v[u] = ok ? __ldg(src_val + h.beg + t) : 0.0;
-                }
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const double2 g = gather2<kVecSmem>(gxb, L.vec, (unsigned)c[u] * 16u);
-                    a0 += v[u] * g.x;
-                    a1 += v[u] * g.y;
-                }
+            for (int u = 0; u < 8; ++u) {
+                const double2 g = gather2(L.vec, (unsigned)c[u] * 16u);
+                a0 += v[u] * g.x;
+                a1 += v[u] * g.y;
             }
         }
         double sum = reduce2(a0, a1, lane, kind != 0);
@@ -462,11 +341,7 @@ __global__ void __launch_bounds__(kSchurThreads, 1) k_pcg_schur(const __grid_con
     L.vec = smem_u32(smem);
     const uint32_t desc_bytes = (uint32_t)P.desc_cap * (kPcgItemInts * 4);
     L.desc = L.vec + (uint32_t)P.vec_bytes + (uint32_t)warp * desc_bytes;
-    const uint32_t log0 = L.vec + (uint32_t)P.vec_bytes + (uint32_t)kSchurWarps * desc_bytes;
-    L.val0 = log0 + (uint32_t)warp * ((uint32_t)P.log_rows * 256u);
-    L.idx0 = log0 + (uint32_t)kSchurWarps * ((uint32_t)P.log_rows * 256u) + (uint32_t)warp * ((uint32_t)P.log_rows * 128u);
-    double* scratch = reinterpret_cast<double*>(smem + P.vec_bytes + (size_t)kSchurWarps * desc_bytes +
-                                                (size_t)kSchurWarps * P.log_rows * kLogRowBytes);
+    double* scratch = reinterpret_cast<double*>(smem + P.vec_bytes + (size_t)kSchurWarps * desc_bytes);
     double* bcast = scratch + 4 * kSchurWarps;
 
     const int tid = blockIdx.x * blockDim.x + threadIdx.x, nthr = gridDim.x * blockDim.x;
@@ -486,14 +361,12 @@ __global__ void __launch_bounds__(kSchurThreads, 1) k_pcg_schur(const __grid_con
 #define RG_TICK(i)
 #endif
 
-    const int r0 = P.wptr[gw], r1 = P.wptr[gw + 1], rres = P.wres[gw];
-    const int c0 = P.wptr[P.nw + 1 + gw], c1 = P.wptr[P.nw + 1 + gw + 1], cres = P.wres[P.nw + gw];
-    const int col_row0 = fill_log(P, true, L, r0, rres, 0, lane);
-    fill_log(P, false, L, c0, cres, col_row0, lane);
-    // descriptors of the streamed items (those not in the log), rows first
-    const int nd_r = min(r1 - r0 - rres, P.desc_cap), nd_c = min(c1 - c0 - cres, P.desc_cap - nd_r);
+    const int r0 = P.wptr[gw], r1 = P.wptr[gw + 1];
+    const int c0 = P.wptr[P.nw + 1 + gw], c1 = P.wptr[P.nw + 1 + gw + 1];
+    // this warp's item descriptors, rows first
+    const int nd_r = min(r1 - r0, P.desc_cap), nd_c = min(c1 - c0, P.desc_cap - nd_r);
     for (int q = 0; q < nd_r + nd_c; ++q) {
-        const int item = q < nd_r ? r0 + rres + q : c0 + cres + (q - nd_r);
+        const int item = q < nd_r ? r0 + q : c0 + (q - nd_r);
         if (lane < kPcgItemInts) sts_i32(L.desc + (uint32_t)q * (kPcgItemInts * 4) + 4u * lane, __ldg(P.items + (size_t)item * kPcgItemInts + lane));
     }
     const uint32_t desc_r = L.desc, desc_c = L.desc + (uint32_t)nd_r * (kPcgItemInts * 4);
@@ -534,12 +407,8 @@ __global__ void __launch_bounds__(kSchurThreads, 1) k_pcg_schur(const __grid_con
             // kRowMain: t = D1^-1 B z;  kRowFinal: x_a = D1^-1 (r_a - B x_b)
             double none = 0.0;
             const double* gx = row_mode == kRowMain ? P.zb : P.xb;
-            if (P.vec_smem_r) {
-                stage_vector(L.vec, gx, mfree);
-                run_phase<true, true>(P, row_mode, gx, L, r0, r1, 0, 0, desc_r, nd_r, lane, none);
-            } else {
-                run_phase<true, false>(P, row_mode, gx, L, r0, r1, rres, 0, desc_r, nd_r, lane, none);
-            }
+            stage_vector(L.vec, gx, mfree);
+            run_phase<true>(P, row_mode, L, r0, r1, desc_r, nd_r, lane, none);
             if (row_mode == kRowFinal) break;
         }
         RG_TICK(1)
@@ -549,12 +418,8 @@ __global__ void __launch_bounds__(kSchurThreads, 1) k_pcg_schur(const __grid_con
         // kColMain: w = D2 z - B' t, delta = z'w
         {
             double dot = 0.0;
-            if (P.vec_smem_c) {
-                stage_vector(L.vec, P.ta, nloc);
-                run_phase<false, true>(P, col_mode, P.ta, L, c0, c1, 0, 0, desc_c, nd_c, lane, dot);
-            } else {
-                run_phase<false, false>(P, col_mode, P.ta, L, c0, c1, cres, col_row0, desc_c, nd_c, lane, dot);
-            }
+            stage_vector(L.vec, P.ta, nloc);
+            run_phase<false>(P, col_mode, L, c0, c1, desc_c, nd_c, lane, dot);
 #pragma unroll
             for (int k = 0; k < 2; ++k) {
                 const double dk = ((lane & 1) == k) ? dot : 0.0;
@@ -678,22 +543,16 @@ void build_pcg_schedule(regot_ctx* ctx, regot_sparse& S, const std::vector<int>&
     const int nloc = (int)S.nloc, mm1 = std::max((int)S.m - 1, 0);
     const int grid = ctx->sm_count, nw = grid * kPcgWarpsPerCta;
     Q.nw = nw;
-    // shared-memory plan (see the header comment): a phase whose gathered vector fits next to the
-    // reduction scratch gathers from a shared copy; the other phase(s) get the rest as matrix log
+    // shared-memory plan: the larger of the two gathered vectors (16 B per entry), then the descriptor
+    // cache.  fits == false: sparse_pcg takes the kernel-by-kernel path and this schedule is not used.
     const int budget = kPcgSmemBudget - kSchurScratchBytes;
-    const long need_r = 16L * std::max(mm1, 1), need_c = 16L * std::max(nloc, 1);  // row phase gathers beta-space
-    Q.vec_smem_r = need_r <= kPcgVecSmemMax;
-    Q.vec_smem_c = need_c <= kPcgVecSmemMax;
-    Q.vec_bytes = (int)std::max(Q.vec_smem_r ? need_r : 0L, Q.vec_smem_c ? need_c : 0L);
-    Q.vec_bytes = (Q.vec_bytes + 127) / 128 * 128;
-    Q.desc_cap = std::min(40, (budget - Q.vec_bytes) / (kPcgWarpsPerCta * kPcgItemInts * 4) / 2);
-    const int left = budget - Q.vec_bytes - kPcgWarpsPerCta * Q.desc_cap * kPcgItemInts * 4;
-    Q.log_rows = (Q.vec_smem_r && Q.vec_smem_c) ? 0 : left / (kPcgWarpsPerCta * kLogRowBytes);
-    const int phase_logs[2] = {Q.vec_smem_r ? 0 : 1, Q.vec_smem_c ? 0 : 1};
+    const long need = 16L * std::max(std::max(mm1, nloc), 1);
+    Q.fits = need <= kPcgVecSmemMax;
+    Q.vec_bytes = (int)((std::min<long>(need, kPcgVecSmemMax) + 127) / 128 * 128);
+    Q.desc_cap = std::min(40, (budget - Q.vec_bytes) / (kPcgWarpsPerCta * kPcgItemInts * 4));
+    if (!Q.fits) return;
     int n_long = 0, n_chunks = 0;
-    std::vector<int> h_items, h_wptr((size_t)2 * (nw + 1), 0), h_wres((size_t)2 * nw, 0);
-    std::vector<int> used_rows((size_t)nw, 0);
-    long resident_entries = 0, global_entries = 0;
+    std::vector<int> h_items, h_wptr((size_t)2 * (nw + 1), 0);
 
     for (int phase = 0; phase < 2; ++phase) {
         const std::vector<int>& ptr = phase == 0 ? rp : cp;
@@ -767,20 +626,8 @@ void build_pcg_schedule(regot_ctx* ctx, regot_sparse& S, const std::vector<int>&
         int cursor = base;
         for (int w = 0; w < nw; ++w) {
             h_wptr[(size_t)phase * (nw + 1) + w] = cursor;
-            bool open = true;
-            int nres = 0;
             for (int q : mine[(size_t)w]) {
                 const HostItem& it = items[(size_t)q];
-                long entries = 0;
-                for (int s = 0; s < 4; ++s) entries += it.len[s];
-                if (open && phase_logs[phase] && used_rows[(size_t)w] + it.nE + 1 <= Q.log_rows) {
-                    used_rows[(size_t)w] += it.nE + 1;
-                    ++nres;
-                    resident_entries += entries;
-                } else {
-                    open = false;
-                    global_entries += entries;
-                }
                 const int rec[kPcgItemInts] = {it.kind, it.nE, it.chunk, it.slot, it.first, it.cnt, 0, 0,
                                                it.line[0], it.line[1], it.line[2], it.line[3],
                                                it.beg[0], it.beg[1], it.beg[2], it.beg[3],
@@ -788,24 +635,19 @@ void build_pcg_schedule(regot_ctx* ctx, regot_sparse& S, const std::vector<int>&
                 h_items.insert(h_items.end(), rec, rec + kPcgItemInts);
                 ++cursor;
             }
-            h_wres[(size_t)phase * nw + w] = nres;
         }
         h_wptr[(size_t)phase * (nw + 1) + nw] = cursor;
     }
     Q.n_long = n_long;
     Q.n_chunks = n_chunks;
-    Q.resident_entries = resident_entries;
-    Q.global_entries = global_entries;
     Q.items.ensure(h_items.size() + kPcgItemInts);
     Q.wptr.ensure(h_wptr.size());
-    Q.wres.ensure(h_wres.size());
     Q.chunk_part.ensure((size_t)n_chunks * 2 + 2);
     Q.chunk_cnt.ensure((size_t)n_long + 1);
     Q.longdot.ensure((size_t)n_long * 2 + 2);
     if (!h_items.empty())
         RG_CUDA(cudaMemcpy(Q.items.p, h_items.data(), sizeof(int) * h_items.size(), cudaMemcpyHostToDevice));
     RG_CUDA(cudaMemcpy(Q.wptr.p, h_wptr.data(), sizeof(int) * h_wptr.size(), cudaMemcpyHostToDevice));
-    RG_CUDA(cudaMemcpy(Q.wres.p, h_wres.data(), sizeof(int) * h_wres.size(), cudaMemcpyHostToDevice));
     RG_CUDA(cudaMemset(Q.chunk_cnt.p, 0, sizeof(unsigned int) * ((size_t)n_long + 1)));
     RG_CUDA(cudaMemset(Q.longdot.p, 0, sizeof(double) * ((size_t)n_long * 2 + 2)));
 }
@@ -820,7 +662,8 @@ static int pcg_schur_launch(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, const
     const int grid = ctx->sm_count;
     if (Q.nw != grid * kPcgWarpsPerCta || grid > kMaxGrid)
         raise(REGOT_E_CUDA, "pcg: schedule was built for a different grid (internal error)");
-    const int smem = Q.vec_bytes + kPcgWarpsPerCta * (Q.desc_cap * kPcgItemInts * 4 + Q.log_rows * kLogRowBytes) + kSchurScratchBytes;
+    if (!Q.fits) raise(REGOT_E_CUDA, "pcg: the persistent kernel needs the iterated vectors in shared memory (internal error)");
+    const int smem = Q.vec_bytes + kPcgWarpsPerCta * Q.desc_cap * kPcgItemInts * 4 + kSchurScratchBytes;
     static bool attr_set = false;
     if (!attr_set) {
         RG_CUDA(cudaFuncSetAttribute(k_pcg_schur, cudaFuncAttributeMaxDynamicSharedMemorySize, kPcgSmemBudget));
@@ -847,10 +690,7 @@ static int pcg_schur_launch(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, const
     P.nw = Q.nw;
     P.fixed_iters = 0;
     if (const char* e = std::getenv("REGOT_B200_PCG_FIXED_ITERS")) P.fixed_iters = std::atoi(e);
-    P.vec_smem_r = Q.vec_smem_r;
-    P.vec_smem_c = Q.vec_smem_c;
     P.vec_bytes = Q.vec_bytes;
-    P.log_rows = Q.log_rows;
     P.desc_cap = Q.desc_cap;
 #ifdef REGOT_PCG_TIMING
     const bool timing = true;
@@ -866,7 +706,6 @@ static int pcg_schur_launch(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, const
     P.dB = S.dB.p;
     P.items = Q.items.p;
     P.wptr = Q.wptr.p;
-    P.wres = Q.wres.p;
     P.chunk_part = Q.chunk_part.p;
     P.chunk_cnt = Q.chunk_cnt.p;
     P.longdot = Q.longdot.p;
@@ -911,8 +750,7 @@ static int pcg_schur_launch(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, const
             }
             std::fprintf(stderr, " %s %.0f/%.0f/%.0f", nm[k], mn * 1e-3, sum / grid * 1e-3, mx * 1e-3);
         }
-        std::fprintf(stderr, " | iters %.0f resident %ld global %ld entries, %d long lines, vec_smem %d/%d log rows %d\n", ws.h_cg[0],
-                     Q.resident_entries, Q.global_entries, Q.n_long, Q.vec_smem_r, Q.vec_smem_c, Q.log_rows);
+        std::fprintf(stderr, " | iters %.0f, %d long lines\n", ws.h_cg[0], Q.n_long);
     }
     if (ws.h_cg[3] != 0.0) return -1;
     int it = 0;

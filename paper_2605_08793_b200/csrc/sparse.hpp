@@ -15,20 +15,19 @@ namespace rg {
 // pattern: rows and columns of B cut into warp-sized items (4 short lines / 1 medium line / 1 chunk
 // of a long line), dealt to the grid's warps longest-first.  items: kPcgItemInts ints each
 // {kind, nE, chunk, slot, first, cnt, -, -, line[4], beg[4], len[4], -...}; wptr: per phase
-// (rows, columns) nw + 1 offsets into items; wres: per phase and warp, how many of the warp's
-// leading items fit its shared-memory log.
+// (rows, columns) nw + 1 offsets into items.  The kernel keeps the gathered vector in shared memory;
+// fits == false (vector too long) sends the solve down the kernel-by-kernel path instead.
 constexpr int kPcgWarpsPerCta = 16;
 constexpr int kPcgItemInts = 24;
 constexpr int kPcgSmemBudget = 227 * 1024;     // dynamic shared memory of the persistent kernel
 constexpr int kPcgVecSmemMax = 168 * 1024;     // largest gathered vector (16 B / entry) staged in shared memory
 struct PcgSchedule {
-    DevBuf<int> items, wptr, wres;
+    DevBuf<int> items, wptr;
     mutable DevBuf<double> chunk_part, longdot;
     mutable DevBuf<unsigned int> chunk_cnt;
     int nw = 0, n_long = 0, n_chunks = 0;
-    int vec_smem_r = 0, vec_smem_c = 0;  // row / column phase gathers from a shared-memory copy of the vector
-    int vec_bytes = 0, desc_cap = 0, log_rows = 0;  // shared-memory carve-up (vector buffer; descriptors, log rows per warp)
-    long resident_entries = 0, global_entries = 0;
+    bool fits = false;                // both gathered vectors fit the shared-memory buffer
+    int vec_bytes = 0, desc_cap = 0;  // shared-memory carve-up: vector buffer, descriptors per warp
 };
 }  // namespace rg
 

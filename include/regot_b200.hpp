@@ -262,6 +262,18 @@ public:
         m_m = p.m;
         m_bound = &p;
     }
+    // squared-Euclidean cost of point clouds / max, formed on the device (problem.h:124-132, 53-61);
+    // on_the_fly: the matrix is never stored (every pass recomputes its tiles)
+    void set_pointcloud(Index n, Index m, int d, const Vector& X, const Vector& Y, const Vector& a, const Vector& b,
+                        double eta, bool on_the_fly = false)
+    {
+        if ((Index)X.size() != n * d || (Index)Y.size() != m * d) throw ValidationError("set_pointcloud: cloud shape mismatch");
+        if ((Index)a.size() != n || (Index)b.size() != m) throw ValidationError("problem: marginal length mismatch");
+        check(regot_b200_set_pointcloud(m_ctx, n, m, d, X.data(), Y.data(), a.data(), b.data(), eta, on_the_fly ? 1 : 0));
+        m_n = n;
+        m_m = m;
+        m_bound = nullptr;
+    }
     void ensure_problem(const ProblemInstance& p)
     {
         if (m_bound != &p) set_problem(p);

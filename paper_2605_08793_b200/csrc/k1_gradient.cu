@@ -229,8 +229,16 @@ __global__ void __launch_bounds__(kFinThreads) k_gradient_fin1(const Fin1Params 
     double acc[6] = {0, 0, 0, 0, 0, 0};
     const int stride = gridDim.x * blockDim.x;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < p.nloc; i += stride) {
+        // panel order (fixed), 8 loads in flight
         double r = 0.0;
-        for (int P = 0; P < p.n_panels; ++P) r += p.rowpart[(size_t)P * p.nloc + i];
+        for (int P0 = 0; P0 < p.n_panels; P0 += 8) {
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = (P0 + u < p.n_panels) ? p.rowpart[(size_t)(P0 + u) * p.nloc + i] : 0.0;
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (P0 + u < p.n_panels) r += v[u];
+        }
         const double al = p.alpha[i], ai = p.a[i];
         const double ga = r - ai;
         p.row_sums[i] = r;
@@ -245,7 +253,15 @@ __global__ void __launch_bounds__(kFinThreads) k_gradient_fin1(const Fin1Params 
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < p.m; j += stride) {
         const int P = j / kTC, off = j - P * kTC;
         double c = 0.0;
-        for (int sg = p.panel_seg0[P]; sg < p.panel_seg0[P + 1]; ++sg) c += p.colpart[(size_t)sg * kTC + off];
+        const int s1 = p.panel_seg0[P + 1];
+        for (int sg = p.panel_seg0[P]; sg < s1; sg += 8) {  // segment order (fixed), 8 loads in flight
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = (sg + u < s1) ? p.colpart[(size_t)(sg + u) * kTC + off] : 0.0;
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (sg + u < s1) c += v[u];
+        }
         p.pack[j] = c;
     }
     block_sum<6>(acc, scratch);

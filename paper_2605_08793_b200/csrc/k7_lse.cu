@@ -177,10 +177,26 @@ __global__ void k_row_lse_fin(int nloc, int n_panels, double eta, const double* 
 {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nloc; i += gridDim.x * blockDim.x) {
         double M = -INFINITY;
-        for (int P = 0; P < n_panels; ++P) M = dmax(M, part_max[(size_t)P * nloc + i]);
+        for (int P0 = 0; P0 < n_panels; P0 += 8) {  // 8 loads in flight
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = (P0 + u < n_panels) ? part_max[(size_t)(P0 + u) * nloc + i] : -INFINITY;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) M = dmax(M, v[u]);
+        }
         double S = 0.0;
-        for (int P = 0; P < n_panels; ++P)
-            S += part_sum[(size_t)P * nloc + i] * exp(part_max[(size_t)P * nloc + i] - M);
+        for (int P0 = 0; P0 < n_panels; P0 += 8) {  // panel order (fixed)
+            double ps[8], pm[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const bool ok = P0 + u < n_panels;
+                ps[u] = ok ? part_sum[(size_t)(P0 + u) * nloc + i] : 0.0;
+                pm[u] = ok ? part_max[(size_t)(P0 + u) * nloc + i] : M;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (P0 + u < n_panels) S += ps[u] * exp(pm[u] - M);
+        }
         alpha_out[i] = eta * (log(a[i]) - (M + log(S)));
     }
 }

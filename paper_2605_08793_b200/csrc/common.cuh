@@ -344,6 +344,15 @@ __device__ __forceinline__ double plan_entry_dev_g(double d, const ExpScale& E, 
     return __fma_rn(s, rw * p, s);
 }
 
+// ---- host mailbox (ctx.hpp HostMailbox): one thread posts n doubles, then the sequence number ----
+__device__ __forceinline__ void mailbox_post(double* mbox, const double* vals, int n, unsigned long long seq)
+{
+    volatile double* d = mbox;
+    for (int k = 0; k < n; ++k) d[k] = vals[k];
+    __threadfence_system();
+    reinterpret_cast<volatile unsigned long long*>(mbox)[31] = seq;
+}
+
 // ---- warp reductions ---------------------------------------------------------
 __device__ __forceinline__ double shfl_xor_d(double v, int mask) { return __shfl_xor_sync(0xffffffffu, v, mask); }
 __device__ __forceinline__ double shfl_idx_d(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }

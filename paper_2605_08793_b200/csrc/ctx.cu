@@ -254,7 +254,7 @@ void ensure_sweep_ws(regot_ctx* ctx, SweepWS& ws)
         RG_CUDA(cudaMemset(ws.ticket.p, 0, 8 * sizeof(unsigned int)));
     }
     ws.d_scal.ensure(1);
-    if (!ws.h_scal) RG_CUDA(cudaMallocHost((void**)&ws.h_scal, sizeof(GradScalars)));
+    ws.mbox.ensure();
 }
 
 // ---- problem upload ---------------------------------------------------------------------------

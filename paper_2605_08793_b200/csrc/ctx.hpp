@@ -71,6 +71,48 @@ struct DevBuf {
     }
 };
 
+// A slot of mapped pinned host memory: the last thread of a kernel writes its scalars there, then a
+// sequence number (device side: mailbox_post in common.cuh); the host spins on the sequence number
+// instead of paying a copy + stream synchronisation for every decision it takes (a line-search
+// evaluation, a set of dot products, the end of a PCG solve: ~6 per quasi-Newton iteration).
+struct HostMailbox {
+    static constexpr int kSlots = 31;  // payload doubles; the sequence number follows them
+    double* data = nullptr;
+    unsigned long long expected = 0;
+    HostMailbox() = default;
+    HostMailbox(const HostMailbox&) = delete;
+    HostMailbox& operator=(const HostMailbox&) = delete;
+    ~HostMailbox()
+    {
+        if (data) cudaFreeHost(data);
+    }
+    void ensure()
+    {
+        if (data) return;
+        RG_CUDA(cudaHostAlloc((void**)&data, sizeof(double) * (kSlots + 1), cudaHostAllocMapped));
+        for (int k = 0; k <= kSlots; ++k) data[k] = 0.0;
+        reinterpret_cast<volatile unsigned long long*>(data)[kSlots] = 0ULL;
+    }
+    // the value the next post must carry
+    unsigned long long next() { return ++expected; }
+    // block until the post with sequence number `expected` has landed (all earlier work of the posting
+    // stream is then complete); a failed launch or kernel shows up through cudaStreamQuery
+    void wait(cudaStream_t st) const
+    {
+        const volatile unsigned long long* seq = reinterpret_cast<const volatile unsigned long long*>(data) + kSlots;
+        for (unsigned long spins = 0; *seq != expected; ++spins) {
+            if ((spins & 0xffffUL) == 0xffffUL) {
+                const cudaError_t e = cudaStreamQuery(st);
+                if (e != cudaErrorNotReady && *seq != expected) {
+                    if (e == cudaSuccess) raise(REGOT_E_CUDA, "mailbox: stream drained without the expected post (internal error)");
+                    raise(REGOT_E_CUDA, std::string("mailbox: ") + cudaGetErrorString(e));
+                }
+            }
+        }
+        __sync_synchronize();
+    }
+};
+
 // Geometry of the panel sweep shared by the fused-gradient and LSE kernels:
 // M is cut into tiles of tile_rows x tile_cols, ordered column-panel-major
 // (tile id = panel * n_row_tiles + row_tile); CTA b owns the contiguous tile
@@ -105,11 +147,7 @@ struct SweepWS {
     DevBuf<double> partials;  // per-CTA scalar partials of the finalize kernels
     DevBuf<unsigned int> ticket;
     DevBuf<GradScalars> d_scal;
-    GradScalars* h_scal = nullptr;  // pinned
-    ~SweepWS()
-    {
-        if (h_scal) cudaFreeHost(h_scal);
-    }
+    HostMailbox mbox;  // the pass's scalars, posted by k_gradient_fin2
 };
 
 // Problem resident on the device (one row block).

@@ -16,6 +16,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstring>
 
 namespace rg {
 
@@ -291,6 +292,8 @@ struct Fin2Params {
     double* partials;
     unsigned int* ticket;
     GradScalars* out;
+    double* mbox;  // host mailbox: the scalars go straight to pinned host memory
+    unsigned long long seq;
 };
 
 __global__ void __launch_bounds__(kFinThreads) k_gradient_fin2(const Fin2Params p)
@@ -332,6 +335,8 @@ __global__ void __launch_bounds__(kFinThreads) k_gradient_fin2(const Fin2Params 
                 o.g_dot_d = S[5] + c[4];
                 *p.out = o;
                 *p.ticket = 0u;
+                static_assert(sizeof(GradScalars) == 8 * sizeof(double), "GradScalars is 8 doubles");
+                mailbox_post(p.mbox, reinterpret_cast<const double*>(&o), 8, p.seq);
             }
         }
     }
@@ -441,17 +446,18 @@ void launch_gradient(regot_ctx* ctx, cudaStream_t st, SweepWS& ws, ncclComm* com
     f2.partials = ws.partials.p;
     f2.ticket = ws.ticket.p + 1;
     f2.out = ws.d_scal.p;
+    f2.mbox = ws.mbox.data;
+    f2.seq = ws.mbox.next();
     k_gradient_fin2<<<g2, kFinThreads, 0, st>>>(f2);
     RG_CUDA(cudaGetLastError());
     ++ctx->launches;
-    RG_CUDA(cudaMemcpyAsync(ws.h_scal, ws.d_scal.p, sizeof(GradScalars), cudaMemcpyDeviceToHost, st));
 }
 
 void sync_scalars(regot_ctx* ctx, cudaStream_t st, SweepWS& ws, GradOut& out)
 {
     (void)ctx;
-    RG_CUDA(cudaStreamSynchronize(st));
-    out.sc = *ws.h_scal;
+    ws.mbox.wait(st);
+    std::memcpy(&out.sc, ws.mbox.data, sizeof(GradScalars));
 }
 
 void launch_plan(regot_ctx* ctx, cudaStream_t st, const double* alpha, const double* beta, double* T_rowmajor)

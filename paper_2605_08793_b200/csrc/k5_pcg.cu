@@ -70,6 +70,8 @@ struct SchurParams {
     double* blockpart;                         // gridDim.x x 4
     unsigned int* barrier;
     double* out;  // iters[2], -, breakdown flag, then timing
+    double* mbox;  // host mailbox for out[0..3]
+    unsigned long long seq;
 };
 
 __device__ __forceinline__ double2 ldcg_x2(const double* p) { return __ldcg(reinterpret_cast<const double2*>(p)); }
@@ -257,12 +259,12 @@ __device__ __forceinline__ void run_phase(const SchurParams& P, int mode, const 
         if (kind == 2) {
             // chunk of a long line: publish the partial; the last chunk to arrive sums them in chunk order
             if (finish) P.chunk_part[(size_t)chunk * 2 + kk] = sum;
-            __threadfence();
+            __syncwarp();  // lanes 0 and 1 wrote the partial: ordered before lane 0's release
             unsigned int prev = 0;
-            if (lane == 0) prev = atomicAdd(&P.chunk_cnt[slot], 1u);
+            if (lane == 0)  // one acquire-release atomic instead of two sequentially-consistent fences per warp
+                asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(P.chunk_cnt + slot) : "memory");
             prev = __shfl_sync(0xffffffffu, prev, 0);
             if ((int)prev == cnt - 1) {
-                __threadfence();
                 double s0_ = 0.0, s1_ = 0.0;
                 for (int c = lane; c < cnt; c += 32) {
                     s0_ += __ldcg(P.chunk_part + (size_t)(first + c) * 2);
@@ -521,6 +523,11 @@ __global__ void __launch_bounds__(kSchurThreads, 1) k_pcg_schur(const __grid_con
 #pragma unroll
         for (int k = 0; k < 2; ++k) P.out[k] = (double)iters[k];
         P.out[3] = broke ? 1.0 : 0.0;
+        // the host only needs these flags; everything it launches next is ordered behind this kernel
+        if (P.mbox) {
+            const double post[4] = {(double)iters[0], (double)iters[1], 0.0, broke ? 1.0 : 0.0};
+            mailbox_post(P.mbox, post, 4, P.seq);
+        }
     }
 #ifdef REGOT_PCG_TIMING
     if (threadIdx.x == 0)
@@ -729,14 +736,22 @@ static int pcg_schur_launch(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, const
     P.barrier = ws.cg_barrier.p;
     P.out = ws.cg_scal.p;
     RG_CUDA(cudaMemsetAsync(P.barrier, 0, sizeof(unsigned int), st));
+    ws.cg_mbox.ensure();
+    P.mbox = timing ? nullptr : ws.cg_mbox.data;
+    P.seq = timing ? 0ULL : ws.cg_mbox.next();
     void* args[] = {&P};
     {
         ProfScope prof(ctx, st, 5);
         RG_CUDA(cudaLaunchCooperativeKernel((const void*)k_pcg_schur, dim3(grid), dim3(kSchurThreads), args, (size_t)smem, st));
     }
     ++ctx->launches;
-    RG_CUDA(cudaMemcpyAsync(ws.h_cg, ws.cg_scal.p, sizeof(double) * (timing ? 4 + (size_t)grid * 8 : 4), cudaMemcpyDeviceToHost, st));
-    RG_CUDA(cudaStreamSynchronize(st));
+    if (timing) {
+        RG_CUDA(cudaMemcpyAsync(ws.h_cg, ws.cg_scal.p, sizeof(double) * (4 + (size_t)grid * 8), cudaMemcpyDeviceToHost, st));
+        RG_CUDA(cudaStreamSynchronize(st));
+    } else {
+        ws.cg_mbox.wait(st);
+        for (int k = 0; k < 4; ++k) ws.h_cg[k] = ws.cg_mbox.data[k];
+    }
     if (timing) {
         const char* nm[8] = {"init", "row", "bar1", "col", "reduce_delta", "update", "reduce_gamma", "final"};
         std::fprintf(stderr, "pcg_schur kcycles min/avg/max over CTAs:");

@@ -84,6 +84,7 @@ struct SparseWS {
     DevBuf<unsigned int> cg_ticket;
     DevBuf<unsigned int> cg_barrier;
     double* h_cg = nullptr;  // pinned
+    HostMailbox cg_mbox;     // iteration counts / breakdown flag of the persistent PCG kernel
     ~SparseWS()
     {
         if (h_hist) cudaFreeHost(h_hist);

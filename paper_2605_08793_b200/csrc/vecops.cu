@@ -90,7 +90,10 @@ __global__ void __launch_bounds__(256) k_multidot(const DotJob job)
                 s = warp_sum(s);
                 if (threadIdx.x == 0) job.out[k] = s;
             }
-            if (threadIdx.x == 0) *job.ticket = 0u;
+            if (threadIdx.x == 0) {
+                *job.ticket = 0u;
+                if (job.mbox) mailbox_post(job.mbox, job.out, 2 * kMaxDots, job.seq);
+            }
         }
     }
 }
@@ -177,11 +180,20 @@ void vec_dots(regot_ctx* ctx, cudaStream_t st, ncclComm* comm, DotScratch& ws, i
     job.partials = ws.partials.p;
     job.out = ws.out.p;
     job.ticket = ws.ticket.p;
+    const bool post = ctx->world == 1;  // sharded: the alpha parts are summed over ranks first
+    ws.mbox.ensure();
+    job.mbox = post ? ws.mbox.data : nullptr;
+    job.seq = post ? ws.mbox.next() : 0ULL;
     k_multidot<<<grid, 256, 0, st>>>(job);
     RG_CUDA(cudaGetLastError());
     ++ctx->launches;
+    if (post) {
+        ws.mbox.wait(st);
+        for (int k = 0; k < count; ++k) out_host[k] = ws.mbox.data[k] + ws.mbox.data[kMaxDots + k];
+        return;
+    }
     // alpha parts are partial sums over this rank's rows; beta parts are replicated
-    if (ctx->world > 1) allreduce_sum(ctx, comm, ws.out.p, (size_t)count, st);
+    allreduce_sum(ctx, comm, ws.out.p, (size_t)count, st);
     RG_CUDA(cudaMemcpyAsync(ws.h_out, ws.out.p, sizeof(double) * 2 * kMaxDots, cudaMemcpyDeviceToHost, st));
     RG_CUDA(cudaStreamSynchronize(st));
     for (int k = 0; k < count; ++k) out_host[k] = ws.h_out[k] + ws.h_out[kMaxDots + k];

@@ -17,12 +17,15 @@ struct DotJob {
     double* partials;
     double* out;
     unsigned int* ticket;
+    double* mbox;  // nullable: host mailbox for the 2 kMaxDots results (single-rank runs)
+    unsigned long long seq;
 };
 
 struct DotScratch {
     DevBuf<double> partials, out;
     DevBuf<unsigned int> ticket;
     double* h_out = nullptr;
+    HostMailbox mbox;
     ~DotScratch()
     {
         if (h_out) cudaFreeHost(h_out);

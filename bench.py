@@ -309,7 +309,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": WORKLOAD, "parallelism": f"row-sharded x{world}" if world > 1 else "single GPU",
                    "l2": "cost matrix (0.8 GB) larger than L2 (126 MB); streamed with an evict-first policy",
-                   "solver": "run_splr via C ABI (libregot_b200.so), library defaults (PCG direction rtol 1e-10)"},
+                   "solver": "run_splr via C ABI (libregot_b200.so), library defaults (Schur-complement PCG direction, rtol 1e-10)"},
         "solve": {"iterations": final.iter, "marginal_error": final.marginal_error, "f": final.f,
                   "gradient_passes": last.stats.gradient_passes, "lse_passes": last.stats.lse_passes,
                   "cg_iters": sum(s.cg_iters for s in last.steps), "ls_evals": sum(s.ls_evals for s in last.steps),

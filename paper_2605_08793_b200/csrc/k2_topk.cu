@@ -595,8 +595,13 @@ void finish_structure(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, regot_spars
     RG_CUDA(cudaStreamSynchronize(st));
     std::vector<int> chunk;      // 4 ints per chunk: line, beg, end, long-line slot
     std::vector<int> longline;   // 2 ints per long line: first chunk, chunk count
+    // The threshold grows with the problem: once a warp of the mat-vec grid has thousands of entries to
+    // process anyway, a line of that length is balanced work for ONE warp, and chunking it would only
+    // add the cross-warp combine (a fence and an atomic per chunk).  At config B it stays kLongLine.
+    const long spmv_warps = 8L * ctx->sm_count * 8;
+    const int long_thr = (int)std::max<long>(kLongLine, std::min<long>(4096, (long)nnz / (2 * spmv_warps)));
     auto cut = [&](int line, int beg, int end) {
-        if (end - beg <= kLongLine) return;
+        if (end - beg <= long_thr) return;
         const int slot = (int)longline.size() / 2;
         longline.push_back((int)chunk.size() / 4);
         int cnt = 0;
@@ -611,7 +616,7 @@ void finish_structure(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, regot_spars
     std::vector<int> ls, lm;  // short / medium lines
     auto bin = [&](int line, int len) {
         if (len <= kShortLine) ls.push_back(line);
-        else if (len <= kLongLine) lm.push_back(line);
+        else if (len <= long_thr) lm.push_back(line);
     };
     for (int i = 0; i < nloc; ++i) {
         cut(i, rp[(size_t)i], rp[(size_t)i + 1]);

@@ -82,6 +82,8 @@ struct SpmvMat {
 // part of one matrix line (row of B or column of B) against nrhs vectors: kLanes lanes stride
 // over [beg, end) with kUnroll independent index/value loads and gathers in flight per lane
 // (the mat-vec is latency-bound, not bandwidth-bound: everything lives in L2)
+constexpr long kInterleaved4 = -4;  // stride value: right-hand sides interleaved 4 doubles per index
+
 template <int kLanes, int kUnroll>
 __device__ __forceinline__ void line_dot(int beg, int end, int gl, const int* __restrict__ idx,
                                          const double* __restrict__ v, const double* x, long sx, int nrhs,
@@ -97,11 +99,30 @@ __device__ __forceinline__ void line_dot(int beg, int end, int gl, const int* __
             c[u] = ok ? __ldg(idx + tt) : 0;
             a[u] = ok ? __ldg(v + tt) : 0.0;
         }
+        if (sx == kInterleaved4) {
+            // the right-hand sides interleaved 4 doubles per index: ONE 32-byte sector per gather (what bounds
+            // a scattered gather through L2 is the number of requests, not bytes)
+            double2 g01[kUnroll];
+            double g2[kUnroll];
 #pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
+            for (int u = 0; u < kUnroll; ++u) {
+                const double* q = x + (size_t)c[u] * 4;
+                g01[u] = *reinterpret_cast<const double2*>(q);
+                g2[u] = q[2];
+            }
 #pragma unroll
-            for (int k = 0; k < kMaxRhs; ++k)
-                if (k < nrhs) acc[k] += a[u] * x[(size_t)k * sx + c[u]];
+            for (int u = 0; u < kUnroll; ++u) {
+                acc[0] += a[u] * g01[u].x;
+                acc[1] += a[u] * g01[u].y;
+                acc[2] += a[u] * g2[u];
+            }
+        } else {
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u) {
+#pragma unroll
+                for (int k = 0; k < kMaxRhs; ++k)
+                    if (k < nrhs) acc[k] += a[u] * x[(size_t)k * sx + c[u]];
+            }
         }
     }
 }
@@ -110,6 +131,7 @@ __device__ __forceinline__ void line_dot(int beg, int end, int gl, const int* __
 //   kEpiFull        y = diag * v_line + s       (A v over rows and columns, K4)
 //   kEpiRowsScaled  y_a = s / dA                (rows only: t = D1^-1 B v_b, first half of S v)
 //   kEpiColsPlain   y_b = s                     (columns only: u = B' v_a, second half; partial over row blocks)
+// The two halves read and write vectors interleaved 4 doubles per index (stride argument kInterleaved4).
 enum { kEpiFull = 0, kEpiRowsScaled = 1, kEpiColsPlain = 2 };
 
 template <int kEpi>
@@ -121,9 +143,9 @@ __device__ __forceinline__ void line_store(const SpmvMat& A, int line, int k, do
         if (line < A.nloc) ya[(size_t)k * sa + line] = y;
         else yb[(size_t)k * sb + (line - A.nloc)] = y;
     } else if (kEpi == kEpiRowsScaled) {
-        ya[(size_t)k * sa + line] = s / diag;
+        ya[(size_t)line * 4 + k] = s / diag;  // the Schur halves keep their vectors interleaved x4
     } else {
-        yb[(size_t)k * sb + (line - A.nloc)] = s;
+        yb[(size_t)(line - A.nloc) * 4 + k] = s;
     }
 }
 
@@ -352,7 +374,7 @@ constexpr int kCgThreads = 256;
 
 struct CgVecs {
     int nloc, mfree, nrhs;
-    long sa, sb;
+    // all interleaved 4 doubles per index (entry 3 is padding)
     double *ta;                      // alpha space: t = D1^-1 (...)
     double *ub, *xb, *rb, *pb, *qb;  // beta space: u = B' t, x, r, p, q = S p
     const double *dA, *dB;
@@ -396,7 +418,7 @@ __global__ void __launch_bounds__(kCgThreads) k_schur_init_a(const CgVecs v, con
     for (int k = 0; k < v.nrhs; ++k)
         for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < v.nloc; i += stride) {
             const double r = rhs_a[k][i], t = r / v.dA[i];
-            v.ta[k * v.sa + i] = t;
+            v.ta[(size_t)i * 4 + k] = t;
             acc[k] += r * t;
         }
     two_stage_store<kMaxRhs>(acc, scratch, v.partials, v.ticket, v.scal + kScalG0a);
@@ -411,10 +433,10 @@ __global__ void __launch_bounds__(kCgThreads) k_schur_init_b(const CgVecs v, con
     for (int k = 0; k < v.nrhs; ++k)
         for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < v.mfree; j += stride) {
             const double d = v.dB[j], rb = rhs_b[k][j];
-            const double c = rb - v.ub[k * v.sb + j], z = c / d;
-            v.rb[k * v.sb + j] = c;
-            v.pb[k * v.sb + j] = z;
-            v.xb[k * v.sb + j] = 0.0;
+            const double c = rb - v.ub[(size_t)j * 4 + k], z = c / d;
+            v.rb[(size_t)j * 4 + k] = c;
+            v.pb[(size_t)j * 4 + k] = z;
+            v.xb[(size_t)j * 4 + k] = 0.0;
             acc[k] += c * z;
             acc[kMaxRhs + k] += rb * (rb / d);
         }
@@ -456,9 +478,9 @@ __global__ void __launch_bounds__(kCgThreads) k_schur_q(const CgVecs v)
     const int stride = gridDim.x * blockDim.x;
     for (int k = 0; k < v.nrhs; ++k)
         for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < v.mfree; j += stride) {
-            const double p = v.pb[k * v.sb + j];
-            const double q = v.dB[j] * p - v.ub[k * v.sb + j];
-            v.qb[k * v.sb + j] = q;
+            const double p = v.pb[(size_t)j * 4 + k];
+            const double q = v.dB[j] * p - v.ub[(size_t)j * 4 + k];
+            v.qb[(size_t)j * 4 + k] = q;
             acc[k] += p * q;
         }
     two_stage_store<kMaxRhs>(acc, scratch, v.partials, v.ticket, v.scal + kScalPap);
@@ -475,9 +497,9 @@ __global__ void __launch_bounds__(kCgThreads) k_schur_update(const CgVecs v, int
         const bool live = v.scal[kScalDone + k] == 0.0 && pap > 0.0;
         const double a = live ? v.scal[kScalRz + parity * kMaxRhs + k] / pap : 0.0;
         for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < v.mfree; j += stride) {
-            v.xb[k * v.sb + j] += a * v.pb[k * v.sb + j];
-            const double r = v.rb[k * v.sb + j] - a * v.qb[k * v.sb + j];
-            v.rb[k * v.sb + j] = r;
+            v.xb[(size_t)j * 4 + k] += a * v.pb[(size_t)j * 4 + k];
+            const double r = v.rb[(size_t)j * 4 + k] - a * v.qb[(size_t)j * 4 + k];
+            v.rb[(size_t)j * 4 + k] = r;
             acc[k] += r * (r / v.dB[j]);
         }
     }
@@ -495,7 +517,7 @@ __global__ void __launch_bounds__(kCgThreads) k_schur_direction(const CgVecs v, 
         const double b = (!done && rz > 0.0) ? rzn / rz : 0.0;
         if (!done)
             for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < v.mfree; j += stride)
-                v.pb[k * v.sb + j] = v.rb[k * v.sb + j] / v.dB[j] + b * v.pb[k * v.sb + j];
+                v.pb[(size_t)j * 4 + k] = v.rb[(size_t)j * 4 + k] / v.dB[j] + b * v.pb[(size_t)j * 4 + k];
     }
 }
 
@@ -530,9 +552,9 @@ __global__ void __launch_bounds__(kCgThreads) k_schur_final(const CgVecs v, cons
     const int stride = gridDim.x * blockDim.x;
     for (int k = 0; k < v.nrhs; ++k) {
         for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < v.nloc; i += stride)
-            sol_a[k][i] = rhs_a[k][i] / v.dA[i] - v.ta[k * v.sa + i];
+            sol_a[k][i] = rhs_a[k][i] / v.dA[i] - v.ta[(size_t)i * 4 + k];
         for (int j = blockIdx.x * blockDim.x + threadIdx.x; j <= v.mfree; j += stride)
-            sol_b[k][j] = j < v.mfree ? v.xb[k * v.sb + j] : 0.0;
+            sol_b[k][j] = j < v.mfree ? v.xb[(size_t)j * 4 + k] : 0.0;
     }
 }
 
@@ -540,9 +562,9 @@ static int pcg_schur_multikernel(regot_ctx* ctx, cudaStream_t st, ncclComm* comm
                                  int nrhs, const DVec* const* rhs, DVec* const* sol, double rtol, int max_iter)
 {
     const int nloc = (int)S.nloc, mfree = std::max((int)S.m - 1, 0);
-    const long sa = std::max(nloc, 1), sb = std::max(mfree, 1);
-    // layout of ws.cg: t | u | x | r | p | q
-    ws.cg.ensure((size_t)kMaxRhs * (size_t)(sa + 5 * sb) + 16);
+    const size_t la = 4 * (size_t)std::max(nloc, 1), lb = 4 * (size_t)std::max(mfree, 1);
+    // layout of ws.cg: t | u | x | r | p | q, interleaved x4
+    ws.cg.ensure(la + 5 * lb + 16);
     ws.cg_scal.ensure(kScalCount + 8 * kMaxRhs);
     ws.cg_partials.ensure((size_t)(2 * ctx->sm_count + 8) * 2 * kMaxRhs);
     if (!ws.cg_ticket.p) {
@@ -556,15 +578,15 @@ static int pcg_schur_multikernel(regot_ctx* ctx, cudaStream_t st, ncclComm* comm
     v.nloc = nloc;
     v.mfree = mfree;
     v.nrhs = nrhs;
-    v.sa = sa;
-    v.sb = sb;
     double* base = ws.cg.p;
     v.ta = base;
-    v.ub = base + (size_t)kMaxRhs * sa;
-    v.xb = v.ub + (size_t)kMaxRhs * sb;
-    v.rb = v.xb + (size_t)kMaxRhs * sb;
-    v.pb = v.rb + (size_t)kMaxRhs * sb;
-    v.qb = v.pb + (size_t)kMaxRhs * sb;
+    v.ub = base + la;
+    v.xb = v.ub + lb;
+    v.rb = v.xb + lb;
+    v.pb = v.rb + lb;
+    v.qb = v.pb + lb;
+    // the padding entries are gathered (and multiplied into an unused accumulator): keep them finite
+    RG_CUDA(cudaMemsetAsync(base, 0, sizeof(double) * (la + 5 * lb), st));
     v.dA = S.dA.p;
     v.dB = S.dB.p;
     v.scal = ws.cg_scal.p;
@@ -593,9 +615,8 @@ static int pcg_schur_multikernel(regot_ctx* ctx, cudaStream_t st, ncclComm* comm
     const double tol2 = rtol * rtol;
     // u = B' t, summed over the row blocks
     auto half_cols = [&]() {
-        launch_spmv<kEpiColsPlain>(ctx, st, S, nrhs, v.ta, nullptr, nullptr, v.ub, sa, sb);
-        if (ctx->world > 1)
-            for (int k = 0; k < nrhs; ++k) allreduce_sum(ctx, comm, v.ub + (size_t)k * sb, (size_t)mfree, st);
+        launch_spmv<kEpiColsPlain>(ctx, st, S, nrhs, v.ta, nullptr, nullptr, v.ub, kInterleaved4, kInterleaved4);
+        if (ctx->world > 1) allreduce_sum(ctx, comm, v.ub, 4 * (size_t)mfree, st);
     };
 
     k_schur_init_a<<<grid_a, kCgThreads, 0, st>>>(v, d_rhs_a);
@@ -621,7 +642,7 @@ static int pcg_schur_multikernel(regot_ctx* ctx, cudaStream_t st, ncclComm* comm
     while (it < max_iter && !finished && !broke) {
         const int burst = std::min(check_every, max_iter - it);
         for (int b = 0; b < burst; ++b, ++it) {
-            launch_spmv<kEpiRowsScaled>(ctx, st, S, nrhs, nullptr, v.pb, v.ta, nullptr, sa, sb);  // t = D1^-1 B p
+            launch_spmv<kEpiRowsScaled>(ctx, st, S, nrhs, nullptr, v.pb, v.ta, nullptr, kInterleaved4, kInterleaved4);  // t = D1^-1 B p
             half_cols();                                                                            // u = B' t
             k_schur_q<<<grid_b, kCgThreads, 0, st>>>(v);
             k_schur_update<<<grid_b, kCgThreads, 0, st>>>(v, parity);
@@ -636,7 +657,7 @@ static int pcg_schur_multikernel(regot_ctx* ctx, cudaStream_t st, ncclComm* comm
     if (broke) return -1;
     it = 0;  // report the slowest system's exact count, not the burst-rounded loop count
     for (int k = 0; k < nrhs; ++k) it = std::max(it, (int)ws.h_cg[kScalIters + k]);
-    launch_spmv<kEpiRowsScaled>(ctx, st, S, nrhs, nullptr, v.xb, v.ta, nullptr, sa, sb);  // t = D1^-1 B x_b
+    launch_spmv<kEpiRowsScaled>(ctx, st, S, nrhs, nullptr, v.xb, v.ta, nullptr, kInterleaved4, kInterleaved4);  // t = D1^-1 B x_b
     k_schur_final<<<std::max(grid_a, grid_b), kCgThreads, 0, st>>>(v, d_rhs_a, d_sol_a, d_sol_b);
     RG_CUDA(cudaGetLastError());
     ++ctx->launches;

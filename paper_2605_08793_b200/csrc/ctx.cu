@@ -132,6 +132,8 @@ regot_ctx* ctx_create(int device)
         ctx->device = device;
         ctx->sm_count = prop.multiProcessorCount;
         if (const char* e = std::getenv("REGOT_B200_MULTIKERNEL_PCG")) ctx->force_multikernel_pcg = e[0] == '1';
+        if (const char* e = std::getenv("REGOT_B200_EXACT_LSE")) ctx->fast_sinkhorn = e[0] != '1';
+        if (const char* e = std::getenv("REGOT_B200_FAST_CHAIN")) ctx->fast_sinkhorn_chain = e[0] == '1';
         RG_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
         RG_CUDA(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
         RG_CUDA(cudaEventCreate(&ctx->ev_a));
@@ -254,6 +256,10 @@ void ensure_sweep_ws(regot_ctx* ctx, SweepWS& ws)
         RG_CUDA(cudaMemset(ws.ticket.p, 0, 8 * sizeof(unsigned int)));
     }
     ws.d_scal.ensure(1);
+    if (!ws.sk_flag.p) {
+        ws.sk_flag.ensure(1);
+        RG_CUDA(cudaMemset(ws.sk_flag.p, 0, sizeof(unsigned int)));
+    }
     ws.mbox.ensure();
 }
 

@@ -133,6 +133,7 @@ struct SweepPlan {
 struct GradScalars {
     double f, marginal_error, duality_gap, grad_sqnorm, total_mass, g_dot_d;
     double row_abs, col_abs;  // the two halves of the marginal error
+    double lse_flag;          // != 0: a fast Sinkhorn update on this stream left its safe range since the last check
 };
 
 // Per-stream scratch of one sweep (gradient or LSE) so the main stream and the
@@ -147,6 +148,7 @@ struct SweepWS {
     DevBuf<double> partials;  // per-CTA scalar partials of the finalize kernels
     DevBuf<unsigned int> ticket;
     DevBuf<GradScalars> d_scal;
+    DevBuf<unsigned int> sk_flag;  // set by the fast Sinkhorn updates (k7_lse.cu), reported with the next gradient pass
     HostMailbox mbox;  // the pass's scalars, posted by k_gradient_fin2
 };
 
@@ -234,6 +236,11 @@ struct regot_ctx {
 
     // tests: run the sharded (multi-kernel + NCCL) PCG path on one GPU (REGOT_B200_MULTIKERNEL_PCG=1)
     bool force_multikernel_pcg = false;
+    // run_sinkhorn's updates take the gradient-sweep form (k7_lse.cu) unless REGOT_B200_EXACT_LSE=1; the
+    // candidate chain of run_splr only with REGOT_B200_FAST_CHAIN=1 (see solver.cu); the stand-alone entry
+    // points always use the log-sum-exp kernels
+    bool fast_sinkhorn = true;
+    bool fast_sinkhorn_chain = false;
 
     // optional per-kernel timing (regot_b200_set_profiling): event pairs around the sweep kernels
     bool profiling = false;
@@ -294,6 +301,13 @@ void launch_optimal_beta(regot_ctx* ctx, cudaStream_t st, SweepWS& ws, ncclComm*
                          double* beta_out, int gauge);
 void launch_sinkhorn_step(regot_ctx* ctx, cudaStream_t st, SweepWS& ws, ncclComm* comm, double* alpha_io,
                           double* beta_io);
+// The same update from two fused-gradient sweeps (row sums at (alpha, beta), column sums at (alpha', beta)):
+//   alpha_i += eta (log a_i - log r_i),  beta_j += eta (log b_j - log c_j),  then the gauge shift.
+// Identical to the log-sum-exp form whenever every sum lies in [e^-600, e^600] (no entry that matters was
+// clamped); otherwise ws.sk_flag is set and the caller must redo the update with launch_sinkhorn_step.
+void launch_sinkhorn_step_fast(regot_ctx* ctx, cudaStream_t st, SweepWS& ws, ncclComm* comm, double* alpha_io,
+                               double* beta_io);
+void reset_sinkhorn_flag(regot_ctx* ctx, cudaStream_t st, SweepWS& ws);
 
 // host <-> device helpers (ctx.cu)
 void upload_dual(regot_ctx* ctx, const double* alpha_host, const double* beta_host, DVec& x, bool check_gauge,

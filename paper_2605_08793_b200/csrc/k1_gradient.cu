@@ -294,6 +294,7 @@ struct Fin2Params {
     GradScalars* out;
     double* mbox;  // host mailbox: the scalars go straight to pinned host memory
     unsigned long long seq;
+    const unsigned int* sk_flag;
 };
 
 __global__ void __launch_bounds__(kFinThreads) k_gradient_fin2(const Fin2Params p)
@@ -333,10 +334,11 @@ __global__ void __launch_bounds__(kFinThreads) k_gradient_fin2(const Fin2Params 
                 o.duality_gap = S[3] + c[2];     // dual.h:225-229
                 o.grad_sqnorm = S[4] + c[3];
                 o.g_dot_d = S[5] + c[4];
+                o.lse_flag = (double)*p.sk_flag;
                 *p.out = o;
                 *p.ticket = 0u;
-                static_assert(sizeof(GradScalars) == 8 * sizeof(double), "GradScalars is 8 doubles");
-                mailbox_post(p.mbox, reinterpret_cast<const double*>(&o), 8, p.seq);
+                static_assert(sizeof(GradScalars) == 9 * sizeof(double), "GradScalars is 9 doubles");
+                mailbox_post(p.mbox, reinterpret_cast<const double*>(&o), 9, p.seq);
             }
         }
     }
@@ -448,6 +450,7 @@ void launch_gradient(regot_ctx* ctx, cudaStream_t st, SweepWS& ws, ncclComm* com
     f2.out = ws.d_scal.p;
     f2.mbox = ws.mbox.data;
     f2.seq = ws.mbox.next();
+    f2.sk_flag = ws.sk_flag.p;
     k_gradient_fin2<<<g2, kFinThreads, 0, st>>>(f2);
     RG_CUDA(cudaGetLastError());
     ++ctx->launches;

@@ -483,6 +483,91 @@ void launch_optimal_beta(regot_ctx* ctx, cudaStream_t st, SweepWS& ws, ncclComm*
     ++ctx->launches;
 }
 
+// ---- the Sinkhorn update from fused-gradient sweeps ---------------------------------------------------
+// T(alpha, beta) row sums r give LSE_j((beta_j - M_ij) / eta) = log r_i - alpha_i / eta, so
+// optimal_alpha (sinkhorn.h:44-74) is alpha_i + eta (log a_i - log r_i); likewise for beta.  One exp per
+// entry and no row maxima: the pass runs at K1's speed.  K1 clamps its exponents to +-700 (dual.h:65-69)
+// where the LSE does not, so the identity is exact only while no clamped entry matters: a sum inside
+// [e^-600, e^600] has its largest exponent above -600 - log(m), every clamped entry is below e^-700, and
+// nothing was clamped from above.  Sums outside that range (or non-finite) raise the flag instead.
+constexpr double kSafeLo = 0x1.4dd4d0d12c071p-866;  // e^-600
+constexpr double kSafeHi = 0x1.88a122d234b39p+865;  // e^600
+
+__global__ void k_sk_alpha_fin(int nloc, int n_panels, double eta, const double* __restrict__ rowpart,
+                               const double* __restrict__ a, double* __restrict__ alpha_io, unsigned int* flag)
+{
+    bool bad = false;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nloc; i += gridDim.x * blockDim.x) {
+        double r = 0.0;
+        for (int P = 0; P < n_panels; ++P) r += rowpart[(size_t)P * nloc + i];  // panel order, as k_gradient_fin1
+        if (r >= kSafeLo && r <= kSafeHi) alpha_io[i] += eta * (log(a[i]) - log(r));
+        else bad = true;
+    }
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1u);
+}
+
+__global__ void k_sk_cols(int m, const int* __restrict__ panel_seg0, const double* __restrict__ colpart,
+                          double* __restrict__ pack)
+{
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < m; j += gridDim.x * blockDim.x) {
+        const int P = j / kTC, off = j - P * kTC;
+        double c = 0.0;
+        for (int sg = panel_seg0[P]; sg < panel_seg0[P + 1]; ++sg) c += colpart[(size_t)sg * kTC + off];
+        pack[j] = c;
+    }
+}
+
+// beta_j += eta (log b_j - log c_j), then the gauge shift of sinkhorn_step (sinkhorn.h:110-113)
+__global__ void k_sk_beta_fin(int nloc, int m, double eta, const double* __restrict__ colsum,
+                              const double* __restrict__ b, double* __restrict__ beta_io, double* __restrict__ alpha_io,
+                              unsigned int* flag)
+{
+    const double cl = colsum[m - 1];
+    const bool last_ok = cl >= kSafeLo && cl <= kSafeHi;
+    const double c = last_ok ? beta_io[m - 1] + eta * (log(b[m - 1]) - log(cl)) : 0.0;  // the new beta[m-1]
+    bool bad = !last_ok;
+    const int stride = gridDim.x * blockDim.x;
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < m - 1; j += stride) {
+        const double cj = colsum[j];
+        if (cj >= kSafeLo && cj <= kSafeHi) beta_io[j] = (beta_io[j] + eta * (log(b[j]) - log(cj))) - c;
+        else bad = true;
+    }
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nloc; i += stride) alpha_io[i] += c;
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1u);
+}
+// beta[m-1] is read by every block above, so it is zeroed by a separate launch
+__global__ void k_sk_gauge_zero(double* beta_io, int m)
+{
+    if (threadIdx.x == 0 && blockIdx.x == 0) beta_io[m - 1] = 0.0;
+}
+
+void launch_sinkhorn_step_fast(regot_ctx* ctx, cudaStream_t st, SweepWS& ws, ncclComm* comm, double* alpha_io,
+                               double* beta_io)
+{
+    const DeviceProblem& pr = ctx->prob;
+    const int nloc = (int)pr.nloc, m = (int)pr.m;
+    // alpha from the row sums at (alpha, beta): rows are local, no collective
+    launch_gradient_sweep_only(ctx, st, ws, alpha_io, beta_io);
+    k_sk_alpha_fin<<<vec_grid(ctx, nloc), 256, 0, st>>>(nloc, ctx->plan.n_panels, pr.eta, ws.rowpart.p, pr.a, alpha_io,
+                                                        ws.sk_flag.p);
+    // beta from the column sums at (alpha', beta), summed over the row blocks
+    launch_gradient_sweep_only(ctx, st, ws, alpha_io, beta_io);
+    k_sk_cols<<<vec_grid(ctx, m), 256, 0, st>>>(m, ctx->plan.d_panel_seg0.p, ws.colpart.p, ws.pack.p);
+    RG_CUDA(cudaGetLastError());
+    if (ctx->world > 1) allreduce_sum(ctx, comm, ws.pack.p, (size_t)m, st);
+    k_sk_beta_fin<<<vec_grid(ctx, std::max(nloc, m)), 256, 0, st>>>(nloc, m, pr.eta, ws.pack.p, pr.b, beta_io, alpha_io,
+                                                                    ws.sk_flag.p);
+    k_sk_gauge_zero<<<1, 32, 0, st>>>(beta_io, m);
+    RG_CUDA(cudaGetLastError());
+    ctx->launches += 4;
+}
+
+void reset_sinkhorn_flag(regot_ctx* ctx, cudaStream_t st, SweepWS& ws)
+{
+    (void)ctx;
+    RG_CUDA(cudaMemsetAsync(ws.sk_flag.p, 0, sizeof(unsigned int), st));
+}
+
 // sinkhorn_step (sinkhorn.h:105-115) in place on (alpha, beta)
 void launch_sinkhorn_step(regot_ctx* ctx, cudaStream_t st, SweepWS& ws, ncclComm* comm, double* alpha_io,
                           double* beta_io)

@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <functional>
 #include <cstring>
 #include <limits>
 
@@ -97,19 +98,35 @@ void solve_sinkhorn(regot_ctx* ctx, const double* alpha0, const double* beta0, c
     Timer tm(ctx);
     cudaStream_t st = ctx->stream;
 
+    reset_sinkhorn_flag(ctx, st, ctx->ws_main);
     gradient_sync(ctx, st, ctx->ws_main, ctx->comm, W.x, nullptr, W.cur, &out);
     append_row(out, 0, clk.ms(), W.cur.sc);
     long it = 0;
     bool fresh = true;
     while (it < cfg.max_iter) {
         if (cfg.tol > 0.0 && W.cur.sc.marginal_error <= cfg.tol) break;
-        launch_sinkhorn_step(ctx, st, ctx->ws_main, ctx->comm, W.x.a.p, W.x.b.p);
+        // the gradient-sweep form of the update when a gradient pass follows at once (its scalars report
+        // whether the update stayed in its safe range; if not it is redone with the log-sum-exp kernels)
+        const bool rec = (it + 1 ) % cfg.record_every == 0 || it + 1 == cfg.max_iter;
+        const bool checked = cfg.tol > 0.0 || rec;
+        const bool fast = ctx->fast_sinkhorn && checked;
+        if (fast) {
+            vec_copy(ctx, st, W.x, W.x_prev);
+            launch_sinkhorn_step_fast(ctx, st, ctx->ws_main, ctx->comm, W.x.a.p, W.x.b.p);
+        } else {
+            launch_sinkhorn_step(ctx, st, ctx->ws_main, ctx->comm, W.x.a.p, W.x.b.p);
+        }
         out.lse_passes += 2;
         ++it;
         fresh = false;
-        const bool rec = (it % cfg.record_every == 0) || it == cfg.max_iter;
-        if (cfg.tol > 0.0 || rec) {
+        if (checked) {
             gradient_sync(ctx, st, ctx->ws_main, ctx->comm, W.x, nullptr, W.cur, &out);
+            if (fast && W.cur.sc.lse_flag != 0.0) {
+                reset_sinkhorn_flag(ctx, st, ctx->ws_main);
+                vec_copy(ctx, st, W.x_prev, W.x);
+                launch_sinkhorn_step(ctx, st, ctx->ws_main, ctx->comm, W.x.a.p, W.x.b.p);
+                gradient_sync(ctx, st, ctx->ws_main, ctx->comm, W.x, nullptr, W.cur, &out);
+            }
             fresh = true;
             if (rec) append_row(out, it, clk.ms(), W.cur.sc);
         }
@@ -367,6 +384,8 @@ void solve_splr(regot_ctx* ctx, const double* alpha0, const double* beta0, const
     const int cg_max = cfg.cg_max_iter > 0 ? cfg.cg_max_iter : (int)std::min<long>(20 * dim, 200000);
 
     // splr_init (splr.h:326-334)
+    reset_sinkhorn_flag(ctx, st, ctx->ws_main);
+    reset_sinkhorn_flag(ctx, ctx->side, ctx->ws_side);
     gradient_sync(ctx, st, ctx->ws_main, ctx->comm, W.x, nullptr, W.cur, &out);
     bool has_prev = false;
     long iter = 0;
@@ -384,6 +403,8 @@ void solve_splr(regot_ctx* ctx, const double* alpha0, const double* beta0, const
             const bool refresh = (k % cfg.S == 0);
             double tau = std::min(cfg.tau_max, std::sqrt(W.cur.sc.grad_sqnorm));  // splr.h:353
             bool have_s = false;
+            std::function<void(bool)> run_chain;
+            std::function<void()> join_chain;
 
             if (refresh) {
                 // plan + select_topk + assemble (splr.h:361-364); T is never materialised
@@ -402,13 +423,38 @@ void solve_splr(regot_ctx* ctx, const double* alpha0, const double* beta0, const
                         RG_CUDA(cudaStreamWaitEvent(cs, ctx->ev_fork, 0));
                     }
                     W.xs.ensure(pr.nloc, pr.m);
-                    RG_CUDA(cudaMemcpyAsync(W.xs.a.p, W.x.a.p, sizeof(double) * (size_t)pr.nloc, cudaMemcpyDeviceToDevice, cs));
-                    RG_CUDA(cudaMemcpyAsync(W.xs.b.p, W.x.b.p, sizeof(double) * (size_t)pr.m, cudaMemcpyDeviceToDevice, cs));
-                    for (long j = 0; j < cfg.J; ++j) launch_sinkhorn_step(ctx, cs, cws, ccomm, W.xs.a.p, W.xs.b.p);
-                    out.lse_passes += 2 * cfg.J;
-                    launch_gradient(ctx, cs, cws, ccomm, W.xs.a.p, W.xs.b.p, nullptr, nullptr, W.cand);
-                    ++out.gradient_passes;
-                    if (!cfg.overlap) sync_scalars(ctx, cs, cws, W.cand);
+                    // J Sinkhorn steps from the snapshot, then a gradient pass.  By default the steps are the
+                    // log-sum-exp kernels: the hybrid trajectory is sensitive to the last bits of the
+                    // candidate (a rounding-level change flips synth1-diff 64^2 between a 61- and a
+                    // 71-iteration path), and the LSE form rounds like the reference's.  With
+                    // REGOT_B200_FAST_CHAIN=1 they take the gradient-sweep form (3 % faster on config B); a
+                    // step that left its safe range is reported with the gradient pass's scalars and the
+                    // chain is redone with the log-sum-exp kernels.
+                    run_chain = [&, cs, ccomm](bool fast) {
+                        SweepWS& w = cfg.overlap ? ctx->ws_side : ctx->ws_main;
+                        RG_CUDA(cudaMemcpyAsync(W.xs.a.p, W.x.a.p, sizeof(double) * (size_t)pr.nloc, cudaMemcpyDeviceToDevice, cs));
+                        RG_CUDA(cudaMemcpyAsync(W.xs.b.p, W.x.b.p, sizeof(double) * (size_t)pr.m, cudaMemcpyDeviceToDevice, cs));
+                        for (long j = 0; j < cfg.J; ++j) {
+                            if (fast) launch_sinkhorn_step_fast(ctx, cs, w, ccomm, W.xs.a.p, W.xs.b.p);
+                            else launch_sinkhorn_step(ctx, cs, w, ccomm, W.xs.a.p, W.xs.b.p);
+                        }
+                        out.lse_passes += 2 * cfg.J;
+                        launch_gradient(ctx, cs, w, ccomm, W.xs.a.p, W.xs.b.p, nullptr, nullptr, W.cand);
+                        ++out.gradient_passes;
+                    };
+                    auto finish_chain = [&, cs]() {
+                        SweepWS& w = cfg.overlap ? ctx->ws_side : ctx->ws_main;
+                        sync_scalars(ctx, cs, w, W.cand);
+                        if (W.cand.sc.lse_flag != 0.0) {
+                            reset_sinkhorn_flag(ctx, cs, w);
+                            run_chain(false);
+                            sync_scalars(ctx, cs, w, W.cand);
+                        }
+                    };
+                    (void)cws;
+                    run_chain(ctx->fast_sinkhorn_chain);
+                    if (!cfg.overlap) finish_chain();
+                    else join_chain = finish_chain;
                     have_s = true;
                 }
             } else {
@@ -448,10 +494,7 @@ void solve_splr(regot_ctx* ctx, const double* alpha0, const double* beta0, const
             }
             const double f_qn = ls_failed ? W.cur.sc.f : ls_engine.tg[ls.slot].sc.f;
 
-            if (have_s && cfg.overlap) {
-                // join the side stream, then read its scalars
-                sync_scalars(ctx, ctx->side, ctx->ws_side, W.cand);
-            }
+            if (have_s && cfg.overlap) join_chain();  // join the side stream, then read its scalars
             // hybrid selection, ties to the Sinkhorn candidate (splr.h:442-443)
             const bool pick_s = have_s && std::isfinite(W.cand.sc.f) && (ls_failed || W.cand.sc.f <= f_qn);
 

@@ -111,3 +111,22 @@ def test_config_validation(solver):
         rg.SinkhornConfig(max_iter=0).validate()
     with pytest.raises(rg.ValidationError):
         rg.SinkhornConfig(tol=-1.0).validate()
+
+
+def test_solver_sinkhorn_updates_match_exact_kernels_and_fall_back(solver, oracle):
+    """Inside run_sinkhorn / run_splr the update takes the gradient-sweep form (alpha += eta (log a - log r)):
+    same iterates as the log-sum-exp kernels to rounding; a start whose plan overflows the clamp range
+    (sums outside [e^-600, e^600]) must take the exact path and still match the oracle."""
+    p = oracle.gen_problem("rand", 70, 300, 0.01, seed=4242)
+    solver.set_problem(to_problem(p))
+    cfg = rg.SinkhornConfig(max_iter=12, tol=1e-300, record_every=1)
+    for scale in (0.05, 9.0):  # 9.0 / eta = 900 > 700: clamped entries, row sums ~ e^700: fallback
+        al, be = oracle.rand_dual(70, 300, scale, 99)
+        res = solver.run_sinkhorn(rg.DualPoint(al, be), cfg)
+        ref = oracle.run_sinkhorn(p, al, be, cfg._c())
+        np.testing.assert_allclose(res.x.alpha, ref["alpha"], atol=1e-11)
+        np.testing.assert_allclose(res.x.beta, ref["beta"], atol=1e-11)
+        fs = [r.f for r in res.trace.rows]
+        fr = [r[2] for r in ref["trace"]]
+        assert len(fs) == len(fr)
+        np.testing.assert_allclose(fs[1:], fr[1:], rtol=1e-10)

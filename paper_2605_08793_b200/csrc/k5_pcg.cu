@@ -13,7 +13,7 @@
 //   beta = gamma / gamma_old, alpha = gamma / (delta - beta gamma / alpha_old),
 //   p = z + beta p, s = w + beta s, x += alpha p, r -= alpha s.
 // One iteration = row phase (t = D1^-1 B z) | barrier | column phase (w = D2 z - B' t, delta
-// partials) | grid reduction | vector update (gamma partials) | grid reduction.
+// partials) | grid reduction of (gamma, delta) | vector update (gamma partials) | barrier.
 //
 // What bounds a scattered gather through L2 is the number of requests an SM can issue (one per entry,
 // a fraction of a request per clock measured), not bytes, and a grid-wide barrier costs ~2400 clk
@@ -426,10 +426,7 @@ __global__ void __launch_bounds__(kSchurThreads, 1) k_pcg_schur(const __grid_con
             for (int k = 0; k < 2; ++k) {
                 const double dk = ((lane & 1) == k) ? dot : 0.0;
                 if (col_mode == kColInit) red[k] = dk;
-                else {
-                    red[k] = 0.0;
-                    red[2 + k] = dk;
-                }
+                else red[2 + k] = dk;  // red[k] still holds the gamma partial of the last update
             }
         }
         RG_TICK(3)
@@ -442,6 +439,7 @@ __global__ void __launch_bounds__(kSchurThreads, 1) k_pcg_schur(const __grid_con
                 gamma0[k] = red[2 + k];
                 done[k] = (k >= nrhs) || gamma0[k] == 0.0 || !(gamma[k] > P.tol2 * gamma0[k]);
                 if (P.fixed_iters > 0 && k < nrhs) done[k] = false;
+                red[k] = 0.0;  // no update yet: no gamma partial for the first combined reduction
             }
             col_mode = kColMain;
         } else {
@@ -450,6 +448,13 @@ __global__ void __launch_bounds__(kSchurThreads, 1) k_pcg_schur(const __grid_con
             for (int k = 0; k < 2; ++k) {
                 al[k] = be[k] = 0.0;
                 if (done[k]) continue;
+                if (it > 0) {  // gamma = r'z of the last update arrives with this reduction
+                    gamma[k] = red[k];
+                    if (!(gamma[k] > P.tol2 * gamma0[k]) && P.fixed_iters == 0) {
+                        done[k] = true;
+                        continue;
+                    }
+                }
                 const double delta = red[2 + k];
                 be[k] = (it == 0) ? 0.0 : gamma[k] / gamma_old[k];
                 const double denom = delta - be[k] * gamma[k] / alpha_old[k];  // = p'Sp
@@ -460,7 +465,7 @@ __global__ void __launch_bounds__(kSchurThreads, 1) k_pcg_schur(const __grid_con
                 ++iters[k];
             }
             ++it;
-            if (!broke) {
+            if (!broke && !(done[0] && done[1])) {
                 // p = z + beta p, s = w + beta s, x += alpha p, r -= alpha s, z = D2^-1 r, gamma = r'z
 #pragma unroll
                 for (int k = 0; k < 4; ++k) red[k] = 0.0;
@@ -495,16 +500,11 @@ __global__ void __launch_bounds__(kSchurThreads, 1) k_pcg_schur(const __grid_con
                     *reinterpret_cast<double2*>(P.rb + o) = make_double2(rn[0], rn[1]);
                     *reinterpret_cast<double2*>(P.zb + o) = make_double2(zn[0], zn[1]);
                 }
-                // gamma is needed by every CTA before the next decision; z by the next row phase
+                // z is needed by the next row phase; the gamma partials ride on the next reduction
+                // (one grid reduction per iteration: Chronopoulos-Gear)
                 RG_TICK(5)
-                grid_sum4(P, red, scratch, bcast, bar_target, -1);
+                grid_barrier(P.barrier, bar_target);
                 RG_TICK(6)
-#pragma unroll
-                for (int k = 0; k < 2; ++k) {
-                    if (done[k]) continue;
-                    gamma[k] = red[k];
-                    if (!(gamma[k] > P.tol2 * gamma0[k]) && P.fixed_iters == 0) done[k] = true;
-                }
             }
         }
         bool all_done = done[0] && done[1];

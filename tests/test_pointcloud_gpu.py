@@ -121,3 +121,23 @@ def test_degenerate_cloud_is_rejected(solver):
         solver.set_pointcloud(X, Y, a, b, 0.01)
     with pytest.raises(rg.ValidationError):
         solver.set_pointcloud(np.array([[np.nan, 0.0]] * 4), Y, a, b, 0.01)
+
+
+def test_high_dimension_clouds(solver):
+    # on the fly the panel of target points lives in shared memory: d <= 64; above that only the materialised mode
+    n, m, eta = 130, 270, 0.05
+    for d in (33, 64):
+        X, Y = clouds("normal", n, m, d, d)
+        a, b = marginals(n, m)
+        want = problems.problem_from_points(X, Y, eta).M
+        solver.set_pointcloud(X, Y, a, b, eta, on_the_fly=True)
+        assert np.array_equal(solver.get_cost(), want)
+        g1 = solver.fused_gradient(rg.DualPoint.zeros(n, m))
+        solver.set_pointcloud(X, Y, a, b, eta, on_the_fly=False)
+        g0 = solver.fused_gradient(rg.DualPoint.zeros(n, m))
+        assert g0.f == g1.f and np.array_equal(g0.row_sums, g1.row_sums) and np.array_equal(g0.col_sums, g1.col_sums)
+    X, Y = clouds("normal", n, m, 65, 1)
+    with pytest.raises(rg.RegotError):
+        solver.set_pointcloud(X, Y, *marginals(n, m), eta, on_the_fly=True)
+    solver.set_pointcloud(X, Y, *marginals(n, m), eta, on_the_fly=False)
+    assert np.array_equal(solver.get_cost(), problems.problem_from_points(X, Y, eta).M)

@@ -305,8 +305,9 @@ void launch_sinkhorn_step(regot_ctx* ctx, cudaStream_t st, SweepWS& ws, ncclComm
 //   alpha_i += eta (log a_i - log r_i),  beta_j += eta (log b_j - log c_j),  then the gauge shift.
 // Identical to the log-sum-exp form whenever every sum lies in [e^-600, e^600] (no entry that matters was
 // clamped); otherwise ws.sk_flag is set and the caller must redo the update with launch_sinkhorn_step.
+// row_sums_here (nullable): row sums of T at (alpha, beta) from a gradient pass made at this very point.
 void launch_sinkhorn_step_fast(regot_ctx* ctx, cudaStream_t st, SweepWS& ws, ncclComm* comm, double* alpha_io,
-                               double* beta_io);
+                               double* beta_io, const double* row_sums_here = nullptr);
 void reset_sinkhorn_flag(regot_ctx* ctx, cudaStream_t st, SweepWS& ws);
 
 // host <-> device helpers (ctx.cu)

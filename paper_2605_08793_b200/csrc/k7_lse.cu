@@ -506,6 +506,19 @@ __global__ void k_sk_alpha_fin(int nloc, int n_panels, double eta, const double*
     if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1u);
 }
 
+// the same from row sums already on the device (the gradient pass at this very point)
+__global__ void k_sk_alpha_from_sums(int nloc, double eta, const double* __restrict__ row_sums, const double* __restrict__ a,
+                                     double* __restrict__ alpha_io, unsigned int* flag)
+{
+    bool bad = false;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nloc; i += gridDim.x * blockDim.x) {
+        const double r = row_sums[i];
+        if (r >= kSafeLo && r <= kSafeHi) alpha_io[i] += eta * (log(a[i]) - log(r));
+        else bad = true;
+    }
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1u);
+}
+
 __global__ void k_sk_cols(int m, const int* __restrict__ panel_seg0, const double* __restrict__ colpart,
                           double* __restrict__ pack)
 {
@@ -542,14 +555,19 @@ __global__ void k_sk_gauge_zero(double* beta_io, int m)
 }
 
 void launch_sinkhorn_step_fast(regot_ctx* ctx, cudaStream_t st, SweepWS& ws, ncclComm* comm, double* alpha_io,
-                               double* beta_io)
+                               double* beta_io, const double* row_sums_here)
 {
     const DeviceProblem& pr = ctx->prob;
     const int nloc = (int)pr.nloc, m = (int)pr.m;
-    // alpha from the row sums at (alpha, beta): rows are local, no collective
-    launch_gradient_sweep_only(ctx, st, ws, alpha_io, beta_io);
-    k_sk_alpha_fin<<<vec_grid(ctx, nloc), 256, 0, st>>>(nloc, ctx->plan.n_panels, pr.eta, ws.rowpart.p, pr.a, alpha_io,
-                                                        ws.sk_flag.p);
+    // alpha from the row sums at (alpha, beta): rows are local, no collective.  When a gradient pass was
+    // just made at this point its row sums are those very numbers and the sweep is skipped.
+    if (row_sums_here) {
+        k_sk_alpha_from_sums<<<vec_grid(ctx, nloc), 256, 0, st>>>(nloc, pr.eta, row_sums_here, pr.a, alpha_io, ws.sk_flag.p);
+    } else {
+        launch_gradient_sweep_only(ctx, st, ws, alpha_io, beta_io);
+        k_sk_alpha_fin<<<vec_grid(ctx, nloc), 256, 0, st>>>(nloc, ctx->plan.n_panels, pr.eta, ws.rowpart.p, pr.a, alpha_io,
+                                                            ws.sk_flag.p);
+    }
     // beta from the column sums at (alpha', beta), summed over the row blocks
     launch_gradient_sweep_only(ctx, st, ws, alpha_io, beta_io);
     k_sk_cols<<<vec_grid(ctx, m), 256, 0, st>>>(m, ctx->plan.d_panel_seg0.p, ws.colpart.p, ws.pack.p);

@@ -112,7 +112,9 @@ void solve_sinkhorn(regot_ctx* ctx, const double* alpha0, const double* beta0, c
         const bool fast = ctx->fast_sinkhorn && checked;
         if (fast) {
             vec_copy(ctx, st, W.x, W.x_prev);
-            launch_sinkhorn_step_fast(ctx, st, ctx->ws_main, ctx->comm, W.x.a.p, W.x.b.p);
+            // W.cur is the gradient pass at W.x when `fresh`: its row sums are the first sweep's result
+            launch_sinkhorn_step_fast(ctx, st, ctx->ws_main, ctx->comm, W.x.a.p, W.x.b.p, fresh ? W.cur.sums.a.p : nullptr);
+            if (fresh) --out.lse_passes;
         } else {
             launch_sinkhorn_step(ctx, st, ctx->ws_main, ctx->comm, W.x.a.p, W.x.b.p);
         }

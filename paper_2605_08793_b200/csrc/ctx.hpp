@@ -71,6 +71,29 @@ struct DevBuf {
     }
 };
 
+// RAII pinned host buffer of T (grow-only): staging for asynchronous copies
+template <class T>
+struct PinnedBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    PinnedBuf() = default;
+    PinnedBuf(const PinnedBuf&) = delete;
+    PinnedBuf& operator=(const PinnedBuf&) = delete;
+    ~PinnedBuf()
+    {
+        if (p) cudaFreeHost(p);
+    }
+    void ensure(size_t count)
+    {
+        if (count <= n && p) return;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        const size_t want = count + count / 4 + 64;  // slack: sizes drift from refresh to refresh
+        RG_CUDA(cudaMallocHost((void**)&p, sizeof(T) * want));
+        n = want;
+    }
+};
+
 // A slot of mapped pinned host memory: the last thread of a kernel writes its scalars there, then a
 // sequence number (device side: mailbox_post in common.cuh); the host spins on the sequence number
 // instead of paying a copy + stream synchronisation for every decision it takes (a line-search
@@ -255,7 +278,7 @@ namespace rg {
 
 void ctx_require_problem(const regot_ctx* ctx);
 // kind: 0 gradient sweep (K1), 1 row LSE (K7), 2 column LSE (K8), 3 top-k sweeps (K2), 4 spmv (K4),
-// 5 persistent PCG solve (K5)
+// 5 persistent PCG solve (K5), 6 a whole pattern refresh (top-k sweeps + selection + structure, host gaps included)
 struct ProfScope {
     regot_ctx* ctx;
     cudaStream_t st;

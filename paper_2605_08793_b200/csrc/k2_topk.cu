@@ -19,6 +19,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
 #include <cstring>
 
 namespace rg {
@@ -297,6 +298,28 @@ __global__ void k_gather_cost(int nnz, const int* __restrict__ row, const int* _
 }
 
 // ---- host side ----------------------------------------------------------------------------------
+namespace {
+struct RefreshTimer {  // experiments: REGOT_B200_REFRESH_TIMING=1 prints the host wall time of each section
+    bool on;
+    cudaStream_t st;
+    std::chrono::steady_clock::time_point t0;
+    std::string line;
+    RefreshTimer(cudaStream_t s) : on(std::getenv("REGOT_B200_REFRESH_TIMING") != nullptr), st(s), t0(std::chrono::steady_clock::now()) {}
+    void tick(const char* name)
+    {
+        if (!on) return;
+        cudaStreamSynchronize(st);
+        const auto t1 = std::chrono::steady_clock::now();
+        line += std::string(name) + " " + std::to_string((int)std::chrono::duration<double, std::micro>(t1 - t0).count()) + " us | ";
+        t0 = t1;
+    }
+    ~RefreshTimer()
+    {
+        if (on) std::fprintf(stderr, "refresh: %s\n", line.c_str());
+    }
+};
+}  // namespace
+
 static int lin_grid(const regot_ctx* ctx, long work)
 {
     return (int)std::max<long>(1, std::min<long>((work + 255) / 256, 8L * ctx->sm_count));
@@ -373,6 +396,7 @@ void topk_build_pattern(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, TopkSourc
     const long long total = (long long)pr.n * (long long)mm1;
     const long long take = std::min<long long>(k, total);
 
+    RefreshTimer rt(st);
     TopkParams p;
     std::memset(&p, 0, sizeof(p));
     p.g.nloc = nloc;
@@ -407,6 +431,7 @@ void topk_build_pattern(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, TopkSourc
         need = take - above;
     }
 
+    rt.tick("hist sweep + pick");
     // ---- pass 2 + 3: count and write the candidates in row-major order ----
     const size_t np = (size_t)ctx->plan.n_panels * (size_t)nloc;
     ws.cnt.ensure(np);
@@ -435,7 +460,9 @@ void topk_build_pattern(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, TopkSourc
     p.cand_col = ws.cand_col.p;
     p.cand_row = ws.cand_row.p;
     p.cand_m = ws.cand_m.p;
+    rt.tick("count sweep + scan");
     launch_sweep_src<kPassWrite>(ctx, st, src, p);
+    rt.tick("write sweep");
 
     // ---- exact threshold K* inside bin b*: 4 x 13-bit radix refinement ----
     unsigned long long kstar = 0;
@@ -461,6 +488,7 @@ void topk_build_pattern(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, TopkSourc
         need_eq = rem;  // ties at K* taken in row-major order
     }
 
+    rt.tick("radix refinement");
     // ---- flags, tie ranking, compaction into CSR ----
     k_flag<<<lin_grid(ctx, nc), 256, 0, st>>>(nc, ws.cand_key.p, ws.cand_col.p, ws.cand_row.p, (int)pr.row_begin, kstar,
                                               take > 0 ? 1 : 0, ws.keep.p, ws.tie.p);
@@ -495,7 +523,9 @@ void topk_build_pattern(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, TopkSourc
     RG_CUDA(cudaGetLastError());
     ++ctx->launches;
     exclusive_scan(ctx, st, ws, ws.rowtot.p, S.rowptr.p, nloc);
+    rt.tick("flags + compaction");
     finish_structure(ctx, st, ws, S);
+    rt.tick("finish_structure (CSC, line lists, PCG schedule)");
 }
 
 void pattern_from_coords(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, const int32_t* coords, int64_t ncoords,
@@ -586,66 +616,91 @@ void finish_structure(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, regot_spars
         RG_CUDA(cudaGetLastError());
         ctx->launches += 4;
     }
-    // Lines (rows of B, columns of B) longer than kLongLine entries -- always row 0 and column 0 of
-    // Omega* at scale -- are cut into chunks of kChunkLen entries that different warps process; the
-    // last warp to finish a line sums its chunk partials in chunk order (deterministic).
-    std::vector<int> rp((size_t)nloc + 1), cp((size_t)std::max(mm1, 0) + 1);
-    RG_CUDA(cudaMemcpyAsync(rp.data(), S.rowptr.p, sizeof(int) * rp.size(), cudaMemcpyDeviceToHost, st));
-    RG_CUDA(cudaMemcpyAsync(cp.data(), S.cscptr.p, sizeof(int) * cp.size(), cudaMemcpyDeviceToHost, st));
+    // Lines (rows of B, columns of B) longer than a threshold -- always row 0 and column 0 of Omega*
+    // at scale -- are cut into chunks of kChunkLen entries that different warps process; the last warp
+    // to finish a line sums its chunk partials in chunk order (deterministic).  The others are binned
+    // by length.  All of this is host work on the two pointer arrays: pinned staging both ways, no
+    // allocation, one synchronisation.
+    const size_t np = (size_t)nloc + 1 + (size_t)std::max(mm1, 0) + 1;
+    ws.h_ptrs.ensure(np);
+    int* rp = ws.h_ptrs.p;
+    int* cp = rp + nloc + 1;
+    RG_CUDA(cudaMemcpyAsync(rp, S.rowptr.p, sizeof(int) * ((size_t)nloc + 1), cudaMemcpyDeviceToHost, st));
+    RG_CUDA(cudaMemcpyAsync(cp, S.cscptr.p, sizeof(int) * ((size_t)std::max(mm1, 0) + 1), cudaMemcpyDeviceToHost, st));
     RG_CUDA(cudaStreamSynchronize(st));
-    std::vector<int> chunk;      // 4 ints per chunk: line, beg, end, long-line slot
-    std::vector<int> longline;   // 2 ints per long line: first chunk, chunk count
     // The threshold grows with the problem: once a warp of the mat-vec grid has thousands of entries to
     // process anyway, a line of that length is balanced work for ONE warp, and chunking it would only
     // add the cross-warp combine (a fence and an atomic per chunk).  At config B it stays kLongLine.
     const long spmv_warps = 8L * ctx->sm_count * 8;
     const int long_thr = (int)std::max<long>(kLongLine, std::min<long>(4096, (long)nnz / (2 * spmv_warps)));
-    auto cut = [&](int line, int beg, int end) {
-        if (end - beg <= long_thr) return;
-        const int slot = (int)longline.size() / 2;
-        longline.push_back((int)chunk.size() / 4);
-        int cnt = 0;
-        for (int b0 = beg; b0 < end; b0 += kChunkLen, ++cnt) {
-            chunk.push_back(line);
-            chunk.push_back(b0);
-            chunk.push_back(std::min(end, b0 + kChunkLen));
-            chunk.push_back(slot);
+    // pass 1: sizes (rows first in every list)
+    int n_s[2] = {0, 0}, n_m[2] = {0, 0}, n_c[2] = {0, 0}, n_l[2] = {0, 0};
+    for (int side = 0; side < 2; ++side) {
+        const int* ptr = side == 0 ? rp : cp;
+        const int nl = side == 0 ? nloc : mm1;
+        for (int l = 0; l < nl; ++l) {
+            const int len = ptr[l + 1] - ptr[l];
+            if (len <= kShortLine) ++n_s[side];
+            else if (len <= long_thr) ++n_m[side];
+            else {
+                ++n_l[side];
+                n_c[side] += (len + kChunkLen - 1) / kChunkLen;
+            }
         }
-        longline.push_back(cnt);
-    };
-    std::vector<int> ls, lm;  // short / medium lines
-    auto bin = [&](int line, int len) {
-        if (len <= kShortLine) ls.push_back(line);
-        else if (len <= long_thr) lm.push_back(line);
-    };
-    for (int i = 0; i < nloc; ++i) {
-        cut(i, rp[(size_t)i], rp[(size_t)i + 1]);
-        bin(i, rp[(size_t)i + 1] - rp[(size_t)i]);
     }
-    S.n_chunks_rows = (int)chunk.size() / 4;
-    S.n_lines_s_rows = (int)ls.size();
-    S.n_lines_m_rows = (int)lm.size();
-    for (int j = 0; j < mm1; ++j) {
-        cut(nloc + j, cp[(size_t)j], cp[(size_t)j + 1]);
-        bin(nloc + j, cp[(size_t)j + 1] - cp[(size_t)j]);
+    S.n_lines_s_rows = n_s[0];
+    S.n_lines_m_rows = n_m[0];
+    S.n_chunks_rows = n_c[0];
+    S.n_lines_s = n_s[0] + n_s[1];
+    S.n_lines_m = n_m[0] + n_m[1];
+    S.n_chunks = n_c[0] + n_c[1];
+    S.n_long = n_l[0] + n_l[1];
+    // pass 2: fill the staging  [lines_s | lines_m | chunks (4 ints) | longlines (2 ints)]
+    const size_t o_s = 0, o_m = o_s + (size_t)S.n_lines_s, o_c = o_m + (size_t)S.n_lines_m, o_l = o_c + 4 * (size_t)S.n_chunks;
+    const size_t used = o_l + 2 * (size_t)S.n_long;
+    // room for the PCG schedule behind the lists: one item per 1..4 lines / chunk, 2 pointer tables
+    const size_t sched_max = (size_t)kPcgItemInts * ((size_t)S.n_lines_s + S.n_lines_m + S.n_chunks + 16) +
+                             2 * ((size_t)ctx->sm_count * kPcgWarpsPerCta + 1);
+    ws.h_lines.ensure(used + sched_max + 64);
+    int* hs = ws.h_lines.p;
+    {
+        size_t is = o_s, im = o_m, ic = 0, il = 0;  // ic / il count chunks / long lines
+        for (int side = 0; side < 2; ++side) {
+            const int* ptr = side == 0 ? rp : cp;
+            const int nl = side == 0 ? nloc : mm1, base = side == 0 ? 0 : nloc;
+            for (int l = 0; l < nl; ++l) {
+                const int beg = ptr[l], end = ptr[l + 1], len = end - beg;
+                if (len <= kShortLine) hs[is++] = base + l;
+                else if (len <= long_thr) hs[im++] = base + l;
+                else {
+                    hs[o_l + 2 * il] = (int)ic;
+                    int cnt = 0;
+                    for (int b0 = beg; b0 < end; b0 += kChunkLen, ++cnt, ++ic) {
+                        int* c4 = hs + o_c + 4 * ic;
+                        c4[0] = base + l;
+                        c4[1] = b0;
+                        c4[2] = std::min(end, b0 + kChunkLen);
+                        c4[3] = (int)il;
+                    }
+                    hs[o_l + 2 * il + 1] = cnt;
+                    ++il;
+                }
+            }
+        }
     }
-    S.n_lines_s = (int)ls.size();
-    S.n_lines_m = (int)lm.size();
-    S.lines_s.ensure(ls.size() + 1);
-    S.lines_m.ensure(lm.size() + 1);
-    if (!ls.empty()) RG_CUDA(cudaMemcpy(S.lines_s.p, ls.data(), sizeof(int) * ls.size(), cudaMemcpyHostToDevice));
-    if (!lm.empty()) RG_CUDA(cudaMemcpy(S.lines_m.p, lm.data(), sizeof(int) * lm.size(), cudaMemcpyHostToDevice));
-    S.n_chunks = (int)chunk.size() / 4;
-    S.n_long = (int)longline.size() / 2;
-    S.chunks.ensure(chunk.size() + 4);
-    S.longlines.ensure(longline.size() + 2);
+    S.lines_s.ensure((size_t)S.n_lines_s + 1);
+    S.lines_m.ensure((size_t)S.n_lines_m + 1);
+    S.chunks.ensure(4 * (size_t)S.n_chunks + 4);
+    S.longlines.ensure(2 * (size_t)S.n_long + 2);
     S.chunk_part.ensure((size_t)S.n_chunks * 3 + 3);
     S.chunk_cnt.ensure((size_t)S.n_long + 1);
-    RG_CUDA(cudaMemset(S.chunk_cnt.p, 0, sizeof(unsigned int) * ((size_t)S.n_long + 1)));
-    if (!chunk.empty()) RG_CUDA(cudaMemcpy(S.chunks.p, chunk.data(), sizeof(int) * chunk.size(), cudaMemcpyHostToDevice));
-    if (!longline.empty())
-        RG_CUDA(cudaMemcpy(S.longlines.p, longline.data(), sizeof(int) * longline.size(), cudaMemcpyHostToDevice));
-    if (ctx->world == 1) build_pcg_schedule(ctx, S, rp, cp);
+    RG_CUDA(cudaMemsetAsync(S.chunk_cnt.p, 0, sizeof(unsigned int) * ((size_t)S.n_long + 1), st));
+    if (S.n_lines_s) RG_CUDA(cudaMemcpyAsync(S.lines_s.p, hs + o_s, sizeof(int) * (size_t)S.n_lines_s, cudaMemcpyHostToDevice, st));
+    if (S.n_lines_m) RG_CUDA(cudaMemcpyAsync(S.lines_m.p, hs + o_m, sizeof(int) * (size_t)S.n_lines_m, cudaMemcpyHostToDevice, st));
+    if (S.n_chunks) RG_CUDA(cudaMemcpyAsync(S.chunks.p, hs + o_c, sizeof(int) * 4 * (size_t)S.n_chunks, cudaMemcpyHostToDevice, st));
+    if (S.n_long) RG_CUDA(cudaMemcpyAsync(S.longlines.p, hs + o_l, sizeof(int) * 2 * (size_t)S.n_long, cudaMemcpyHostToDevice, st));
+    if (ctx->world == 1) build_pcg_schedule(ctx, st, S, rp, cp, ws.h_lines, used);
+    RG_CUDA(cudaStreamSynchronize(st));  // the staging is free again
 }
 
 }  // namespace rg

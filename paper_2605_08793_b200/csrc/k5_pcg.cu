@@ -35,6 +35,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <vector>
 
 namespace rg {
 
@@ -537,14 +538,12 @@ __global__ void __launch_bounds__(kSchurThreads, 1) k_pcg_schur(const __grid_con
 }
 
 // ---- host: the work schedule ------------------------------------------------------------------
-namespace {
-struct HostItem {
-    int kind = 0, nE = 0, chunk = 0, slot = 0, first = 0, cnt = 0;
-    int line[4] = {-1, -1, -1, -1}, beg[4] = {0, 0, 0, 0}, len[4] = {0, 0, 0, 0};
-};
-}  // namespace
-
-void build_pcg_schedule(regot_ctx* ctx, regot_sparse& S, const std::vector<int>& rp, const std::vector<int>& cp)
+// Items of one phase are produced in order of decreasing row count nE (a counting sort: nE <= 16), then
+// dealt over the warps in a snake (position q of the sorted order -> round q / nw, warp q % nw, reversed
+// on odd rounds) so the loads stay level; warp w's items are contiguous in `items`.  Everything is
+// written straight into pinned staging and uploaded asynchronously: no allocation, no sort call.
+void build_pcg_schedule(regot_ctx* ctx, cudaStream_t st, regot_sparse& S, const int* rp, const int* cp, PinnedBuf<int>& staging,
+                        size_t staging_used)
 {
     PcgSchedule& Q = S.pcg;
     const int nloc = (int)S.nloc, mm1 = std::max((int)S.m - 1, 0);
@@ -558,105 +557,146 @@ void build_pcg_schedule(regot_ctx* ctx, regot_sparse& S, const std::vector<int>&
     Q.vec_bytes = (int)((std::min<long>(need, kPcgVecSmemMax) + 127) / 128 * 128);
     Q.desc_cap = std::min(40, (budget - Q.vec_bytes) / (kPcgWarpsPerCta * kPcgItemInts * 4));
     if (!Q.fits) return;
-    int n_long = 0, n_chunks = 0;
-    std::vector<int> h_items, h_wptr((size_t)2 * (nw + 1), 0);
 
-    for (int phase = 0; phase < 2; ++phase) {
-        const std::vector<int>& ptr = phase == 0 ? rp : cp;
-        const int nlines = phase == 0 ? nloc : mm1;
-        std::vector<HostItem> items;
-        // short lines, bucketed by length (descending) so a quad holds lines of similar length
-        std::vector<std::vector<int>> bucket((size_t)kShortLine + 1);
-        for (int l = 0; l < nlines; ++l) {
-            const int beg = ptr[(size_t)l], len = ptr[(size_t)l + 1] - beg;
-            if (len > kLongLine) {
-                const int slot = n_long++, first = n_chunks;
-                const int cnt = (len + kChunkLen - 1) / kChunkLen;
-                for (int c = 0; c < cnt; ++c) {
-                    HostItem it;
-                    it.kind = 2;
-                    it.line[0] = l;
-                    it.beg[0] = beg + c * kChunkLen;
-                    it.len[0] = std::min(kChunkLen, len - c * kChunkLen);
-                    it.nE = (it.len[0] + 31) / 32;
-                    it.chunk = n_chunks++;
-                    it.slot = slot;
-                    it.first = first;
-                    it.cnt = cnt;
-                    items.push_back(it);
+    constexpr int kMaxNE = 16;
+    int* const h_items = staging.p + staging_used;  // room was reserved by the caller
+    int n_items_total = 0, n_long = 0, n_chunks = 0;
+    // per phase: count items by nE, then place
+    int* h_wptr = nullptr;
+    static thread_local std::vector<int> bucket_cnt, bucket_pos, short_sorted;
+    for (int pass = 0; pass < 2; ++pass) {  // pass 0 sizes the item array (the pointer tables go behind it)
+        int n_long_p = 0, n_chunks_p = 0, cursor_items = 0;
+        for (int phase = 0; phase < 2; ++phase) {
+            const int* ptr = phase == 0 ? rp : cp;
+            const int nlines = phase == 0 ? nloc : mm1;
+            // short lines sorted by decreasing length (counting sort) so a quad holds lines of similar length
+            bucket_cnt.assign((size_t)kShortLine + 2, 0);
+            int n_short = 0;
+            for (int l = 0; l < nlines; ++l) {
+                const int len = ptr[l + 1] - ptr[l];
+                if (len <= kShortLine) {
+                    ++bucket_cnt[(size_t)(kShortLine - len)];
+                    ++n_short;
                 }
-            } else if (len > kShortLine) {
-                HostItem it;
-                it.kind = 1;
-                it.line[0] = l;
-                it.beg[0] = beg;
-                it.len[0] = len;
-                it.nE = (len + 31) / 32;
-                items.push_back(it);
-            } else {
-                bucket[(size_t)len].push_back(l);
             }
-        }
-        {
-            HostItem it;
-            int fill = 0;
-            auto flush = [&]() {
-                if (!fill) return;
-                int mx = 0;
-                for (int s = 0; s < fill; ++s) mx = std::max(mx, it.len[s]);
-                it.kind = 0;
-                it.nE = (mx + 7) / 8;
-                items.push_back(it);
-                it = HostItem();
-                fill = 0;
+            bucket_pos.assign((size_t)kShortLine + 2, 0);
+            for (int k = 1; k <= kShortLine + 1; ++k) bucket_pos[(size_t)k] = bucket_pos[(size_t)k - 1] + bucket_cnt[(size_t)k - 1];
+            short_sorted.resize((size_t)n_short + 4);
+            for (int l = 0; l < nlines; ++l) {
+                const int len = ptr[l + 1] - ptr[l];
+                if (len <= kShortLine) short_sorted[(size_t)bucket_pos[(size_t)(kShortLine - len)]++] = l;
+            }
+            // items by nE: count[nE]
+            int cnt_ne[kMaxNE + 1] = {0};
+            for (int l = 0; l < nlines; ++l) {
+                const int len = ptr[l + 1] - ptr[l];
+                if (len > kLongLine) {
+                    const int full = len / kChunkLen, rest = len - full * kChunkLen;
+                    cnt_ne[kChunkLen / 32] += full;
+                    if (rest) ++cnt_ne[(rest + 31) / 32];
+                } else if (len > kShortLine) {
+                    ++cnt_ne[(len + 31) / 32];
+                }
+            }
+            for (int q = 0; q < n_short; q += 4) {
+                const int l0 = short_sorted[(size_t)q];
+                ++cnt_ne[(ptr[l0 + 1] - ptr[l0] + 7) / 8];  // the quad's longest line comes first
+            }
+            int n_items = 0;
+            for (int e = 0; e <= kMaxNE; ++e) n_items += cnt_ne[e];
+            if (pass == 0) {
+                cursor_items += n_items;
+                continue;
+            }
+            // sorted position of the first item of each nE class (decreasing nE)
+            int start_ne[kMaxNE + 1];
+            {
+                int acc = 0;
+                for (int e = kMaxNE; e >= 0; --e) {
+                    start_ne[e] = acc;
+                    acc += cnt_ne[e];
+                }
+            }
+            // warp w holds the items at sorted positions q with (q / nw even ? q % nw : nw - 1 - q % nw) == w,
+            // in round order: its count is the number of rounds that reach it
+            const int full_rounds = n_items / nw, tail = n_items % nw;
+            const int base = cursor_items;
+            int* wp = h_wptr + (size_t)phase * (nw + 1);
+            {
+                int acc = base;
+                for (int w = 0; w < nw; ++w) {
+                    wp[w] = acc;
+                    const bool in_tail = (full_rounds & 1) ? (nw - 1 - w) < tail : w < tail;
+                    acc += full_rounds + (in_tail ? 1 : 0);
+                }
+                wp[nw] = acc;
+            }
+            auto place = [&](int q) -> int* {  // slot of the item at sorted position q
+                const int round = q / nw, pos = q % nw;
+                const int w = (round & 1) ? nw - 1 - pos : pos;
+                return h_items + (size_t)kPcgItemInts * (size_t)(wp[w] + round);
             };
-            for (int len = kShortLine; len >= 0; --len)
-                for (int l : bucket[(size_t)len]) {
-                    it.line[fill] = l;
-                    it.beg[fill] = ptr[(size_t)l];
-                    it.len[fill] = len;
-                    if (++fill == 4) flush();
+            auto emit = [&](int nE, int kind, int chunk, int slot, int first, int cnt, const int (&line)[4], const int (&beg)[4],
+                            const int (&len)[4]) {
+                int* r = place(start_ne[nE]++);
+                r[0] = kind; r[1] = nE; r[2] = chunk; r[3] = slot; r[4] = first; r[5] = cnt; r[6] = 0; r[7] = 0;
+                for (int k = 0; k < 4; ++k) {
+                    r[8 + k] = line[k];
+                    r[12 + k] = beg[k];
+                    r[16 + k] = len[k];
+                    r[20 + k] = 0;
                 }
-            flush();
-        }
-        // longest first (stable), dealt over the warps in a snake so the loads stay level
-        std::vector<int> order(items.size());
-        for (size_t q = 0; q < order.size(); ++q) order[q] = (int)q;
-        std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return items[(size_t)x].nE > items[(size_t)y].nE; });
-        std::vector<std::vector<int>> mine((size_t)nw);
-        for (size_t q = 0; q < order.size(); ++q) {
-            const size_t round = q / (size_t)nw, pos = q % (size_t)nw;
-            const size_t w = (round & 1) ? (size_t)nw - 1 - pos : pos;
-            mine[w].push_back(order[q]);
-        }
-        const int base = (int)(h_items.size() / kPcgItemInts);
-        int cursor = base;
-        for (int w = 0; w < nw; ++w) {
-            h_wptr[(size_t)phase * (nw + 1) + w] = cursor;
-            for (int q : mine[(size_t)w]) {
-                const HostItem& it = items[(size_t)q];
-                const int rec[kPcgItemInts] = {it.kind, it.nE, it.chunk, it.slot, it.first, it.cnt, 0, 0,
-                                               it.line[0], it.line[1], it.line[2], it.line[3],
-                                               it.beg[0], it.beg[1], it.beg[2], it.beg[3],
-                                               it.len[0], it.len[1], it.len[2], it.len[3], 0, 0, 0, 0};
-                h_items.insert(h_items.end(), rec, rec + kPcgItemInts);
-                ++cursor;
+            };
+            for (int l = 0; l < nlines; ++l) {
+                const int beg = ptr[l], len = ptr[l + 1] - beg;
+                if (len > kLongLine) {
+                    const int slot = n_long + n_long_p++, first = n_chunks + n_chunks_p;
+                    const int cnt = (len + kChunkLen - 1) / kChunkLen;
+                    for (int c = 0; c < cnt; ++c) {
+                        const int clen = std::min(kChunkLen, len - c * kChunkLen);
+                        const int line4[4] = {l, -1, -1, -1}, beg4[4] = {beg + c * kChunkLen, 0, 0, 0}, len4[4] = {clen, 0, 0, 0};
+                        emit((clen + 31) / 32, 2, n_chunks + n_chunks_p++, slot, first, cnt, line4, beg4, len4);
+                    }
+                } else if (len > kShortLine) {
+                    const int line4[4] = {l, -1, -1, -1}, beg4[4] = {beg, 0, 0, 0}, len4[4] = {len, 0, 0, 0};
+                    emit((len + 31) / 32, 1, 0, 0, 0, 0, line4, beg4, len4);
+                }
             }
+            for (int q = 0; q < n_short; q += 4) {
+                int line4[4] = {-1, -1, -1, -1}, beg4[4] = {0, 0, 0, 0}, len4[4] = {0, 0, 0, 0};
+                for (int k = 0; k < 4 && q + k < n_short; ++k) {
+                    const int l = short_sorted[(size_t)(q + k)];
+                    line4[k] = l;
+                    beg4[k] = ptr[l];
+                    len4[k] = ptr[l + 1] - ptr[l];
+                }
+                emit((len4[0] + 7) / 8, 0, 0, 0, 0, 0, line4, beg4, len4);
+            }
+            cursor_items += n_items;
         }
-        h_wptr[(size_t)phase * (nw + 1) + nw] = cursor;
+        if (pass == 0) {
+            n_items_total = cursor_items;
+            h_wptr = h_items + (size_t)kPcgItemInts * (size_t)n_items_total;
+            if (staging_used + (size_t)kPcgItemInts * n_items_total + 2 * ((size_t)nw + 1) > staging.n)
+                raise(REGOT_E_CUDA, "pcg: schedule staging too small (internal error)");
+        } else {
+            n_long += n_long_p;
+            n_chunks += n_chunks_p;
+        }
     }
     Q.n_long = n_long;
     Q.n_chunks = n_chunks;
-    Q.items.ensure(h_items.size() + kPcgItemInts);
-    Q.wptr.ensure(h_wptr.size());
+    Q.items.ensure((size_t)kPcgItemInts * ((size_t)n_items_total + 1));
+    Q.wptr.ensure(2 * ((size_t)nw + 1));
     Q.chunk_part.ensure((size_t)n_chunks * 2 + 2);
     Q.chunk_cnt.ensure((size_t)n_long + 1);
     Q.longdot.ensure((size_t)n_long * 2 + 2);
-    if (!h_items.empty())
-        RG_CUDA(cudaMemcpy(Q.items.p, h_items.data(), sizeof(int) * h_items.size(), cudaMemcpyHostToDevice));
-    RG_CUDA(cudaMemcpy(Q.wptr.p, h_wptr.data(), sizeof(int) * h_wptr.size(), cudaMemcpyHostToDevice));
-    RG_CUDA(cudaMemset(Q.chunk_cnt.p, 0, sizeof(unsigned int) * ((size_t)n_long + 1)));
-    RG_CUDA(cudaMemset(Q.longdot.p, 0, sizeof(double) * ((size_t)n_long * 2 + 2)));
+    if (n_items_total)
+        RG_CUDA(cudaMemcpyAsync(Q.items.p, h_items, sizeof(int) * (size_t)kPcgItemInts * (size_t)n_items_total,
+                                cudaMemcpyHostToDevice, st));
+    RG_CUDA(cudaMemcpyAsync(Q.wptr.p, h_wptr, sizeof(int) * 2 * ((size_t)nw + 1), cudaMemcpyHostToDevice, st));
+    RG_CUDA(cudaMemsetAsync(Q.chunk_cnt.p, 0, sizeof(unsigned int) * ((size_t)n_long + 1), st));
+    RG_CUDA(cudaMemsetAsync(Q.longdot.p, 0, sizeof(double) * ((size_t)n_long * 2 + 2), st));
 }
 
 // ---- host: launch --------------------------------------------------------------------------------

@@ -410,8 +410,11 @@ void solve_splr(regot_ctx* ctx, const double* alpha0, const double* beta0, const
 
             if (refresh) {
                 // plan + select_topk + assemble (splr.h:361-364); T is never materialised
-                topk_build_pattern(ctx, st, W.sparse, kFromDual, W.x.a.p, W.x.b.p,
-                                   regot_b200_topk_budget(pr.n, pr.m, cfg.density), W.A);
+                {
+                    ProfScope prof(ctx, st, 6);  // the whole pattern refresh: sweeps, selection, structure, host work
+                    topk_build_pattern(ctx, st, W.sparse, kFromDual, W.x.a.p, W.x.b.p,
+                                       regot_b200_topk_budget(pr.n, pr.m, cfg.density), W.A);
+                }
                 out.gradient_passes += 3;  // three sweeps over M
                 sparse_fill_values(ctx, st, W.A, W.x.a.p, W.x.b.p, tau, W.cur.sums.a.p, W.cur.sums.b.p);
                 if (cfg.J > 0) {

@@ -83,6 +83,8 @@ struct SparseWS {
     DevBuf<double> cg_partials;
     DevBuf<unsigned int> cg_ticket;
     DevBuf<unsigned int> cg_barrier;
+    PinnedBuf<int> h_ptrs;   // rowptr | cscptr of the current pattern (device -> host)
+    PinnedBuf<int> h_lines;  // line lists and the PCG schedule (host -> device)
     double* h_cg = nullptr;  // pinned
     HostMailbox cg_mbox;     // iteration counts / breakdown flag of the persistent PCG kernel
     ~SparseWS()
@@ -118,8 +120,10 @@ void sparse_matvec(regot_ctx* ctx, cudaStream_t st, ncclComm* comm, const regot_
 // Jacobi-PCG (K5): solves A x_k = rhs_k for k < nrhs simultaneously.  Returns
 // iterations, or -1 on breakdown (p'Ap <= 0: "not positive definite").
 // k5_pcg.cu -- the single-GPU path of sparse_pcg: Schur-complement PCG in one persistent kernel
-void build_pcg_schedule(regot_ctx* ctx, regot_sparse& S, const std::vector<int>& rowptr_host,
-                        const std::vector<int>& cscptr_host);
+// rowptr_host / cscptr_host: nloc + 1 / m entries; staging: pinned scratch the uploads are issued from
+// (asynchronously on st; the caller synchronises before the staging is reused)
+void build_pcg_schedule(regot_ctx* ctx, cudaStream_t st, regot_sparse& S, const int* rowptr_host, const int* cscptr_host,
+                        PinnedBuf<int>& staging, size_t staging_used);
 int pcg_schur_persistent(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, const regot_sparse& S, int nrhs,
                          const DVec* const* rhs, DVec* const* sol, double rtol, int max_iter);
 int sparse_pcg(regot_ctx* ctx, cudaStream_t st, ncclComm* comm, SparseWS& ws, const regot_sparse& S, int nrhs,

@@ -9,6 +9,7 @@
 #include "capi_util.hpp"
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <functional>
 #include <cstring>
@@ -142,6 +143,31 @@ void solve_sinkhorn(regot_ctx* ctx, const double* alpha0, const double* beta0, c
 
 // ---- SPLR pieces ---------------------------------------------------------------------------------
 namespace {
+
+// experiments: REGOT_B200_STEP_TIMING=1 prints the host wall time per section of run_splr (each tick
+// drains the stream, so the numbers are only meaningful relative to each other)
+struct SectionTimer {
+    bool on;
+    cudaStream_t st;
+    std::chrono::steady_clock::time_point t0;
+    double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    SectionTimer(cudaStream_t s) : on(std::getenv("REGOT_B200_STEP_TIMING") != nullptr), st(s), t0(std::chrono::steady_clock::now()) {}
+    void tick(int k)
+    {
+        if (!on) return;
+        cudaStreamSynchronize(st);
+        const auto t1 = std::chrono::steady_clock::now();
+        acc[k] += std::chrono::duration<double, std::milli>(t1 - t0).count();
+        t0 = t1;
+    }
+    ~SectionTimer()
+    {
+        if (on)
+            std::fprintf(stderr, "run_splr sections (ms): refresh %.2f | candidate chain %.2f | value refresh %.2f | low rank %.2f | "
+                                 "direction %.2f | line search %.2f | bookkeeping %.2f\n",
+                         acc[0], acc[1], acc[2], acc[3], acc[4], acc[5], acc[6]);
+    }
+};
 
 struct LowRankDev {
     bool active = false;
@@ -393,6 +419,7 @@ void solve_splr(regot_ctx* ctx, const double* alpha0, const double* beta0, const
     long iter = 0;
     append_row(out, 0, clk.ms(), W.cur.sc);
     LineSearch ls_engine{ctx, W, out};
+    SectionTimer sect(st);
 
     while (iter < cfg.max_iter) {
         if (W.cur.sc.marginal_error <= cfg.tol) break;
@@ -417,6 +444,7 @@ void solve_splr(regot_ctx* ctx, const double* alpha0, const double* beta0, const
                 }
                 out.gradient_passes += 3;  // three sweeps over M
                 sparse_fill_values(ctx, st, W.A, W.x.a.p, W.x.b.p, tau, W.cur.sums.a.p, W.cur.sums.b.p);
+                sect.tick(0);
                 if (cfg.J > 0) {
                     // candidate chain from the same snapshot (splr.h:366-372); on the side
                     // stream when cfg.overlap is set (splr.h:373-378)
@@ -462,8 +490,10 @@ void solve_splr(regot_ctx* ctx, const double* alpha0, const double* beta0, const
                     else join_chain = finish_chain;
                     have_s = true;
                 }
+                sect.tick(1);
             } else {
                 sparse_fill_values(ctx, st, W.A, W.x.a.p, W.x.b.p, tau, W.cur.sums.a.p, W.cur.sums.b.p);  // update_values
+                sect.tick(2);
             }
 
             // direction; PCG breakdown plays the role of NotPositiveDefiniteError (splr.h:391-408)
@@ -472,6 +502,7 @@ void solve_splr(regot_ctx* ctx, const double* alpha0, const double* beta0, const
             LowRankDev R;
             for (;;) {
                 R = build_low_rank(ctx, W, has_prev);
+                sect.tick(3);
                 if (compute_direction(ctx, W, W.A, W.cur.g, W.cur.sc.grad_sqnorm, R, W.ydiff, W.v, cg_rtol, cg_max, W.d,
                                       g_dot_d, cg_iters, &W.sdiff))
                     break;
@@ -481,6 +512,7 @@ void solve_splr(regot_ctx* ctx, const double* alpha0, const double* beta0, const
                 ++retries;
             }
 
+            sect.tick(4);
             // Wolfe line search on the fused gradient (splr.h:414-436)
             LsOut ls;
             bool ls_failed = false;
@@ -498,6 +530,7 @@ void solve_splr(regot_ctx* ctx, const double* alpha0, const double* beta0, const
                 ls.slot = -1;
             }
             const double f_qn = ls_failed ? W.cur.sc.f : ls_engine.tg[ls.slot].sc.f;
+            sect.tick(5);
 
             if (have_s && cfg.overlap) join_chain();  // join the side stream, then read its scalars
             // hybrid selection, ties to the Sinkhorn candidate (splr.h:442-443)
@@ -537,6 +570,7 @@ void solve_splr(regot_ctx* ctx, const double* alpha0, const double* beta0, const
             }
             rec.f_after = W.cur.sc.f;
             iter = k + 1;
+            sect.tick(6);
         } catch (const Error& e) {
             if (e.code == REGOT_E_CUDA || e.code == REGOT_E_NCCL || e.code == REGOT_E_NOMEM) throw;
             // StepError (splr.h:315-324, 520-525): partial trace, no point

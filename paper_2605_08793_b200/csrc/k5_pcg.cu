@@ -807,6 +807,8 @@ static int pcg_schur_launch(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, const
         }
         std::fprintf(stderr, " | iters %.0f, %d long lines\n", ws.h_cg[0], Q.n_long);
     }
+    static const bool show_iters = std::getenv("REGOT_B200_PCG_ITERS") != nullptr;  // experiments
+    if (show_iters) std::fprintf(stderr, "pcg iters: g-system %d, u-system %d\n", (int)ws.h_cg[0], nrhs > 1 ? (int)ws.h_cg[1] : -1);
     if (ws.h_cg[3] != 0.0) return -1;
     int it = 0;
     for (int k = 0; k < nrhs; ++k) it = std::max(it, (int)ws.h_cg[k]);

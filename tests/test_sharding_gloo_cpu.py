@@ -1,5 +1,5 @@
 """CPU, world_size = 2 over gloo: the row-sharded protocol of the multi-GPU path (SURVEY.md 5.8,
-C1/C2/C5) -- what each rank reduces locally, what crosses the wire, and how the pieces are combined --
+C1/C2/C3/C5 and the point-cloud maximum) -- what each rank reduces locally, what crosses the wire, and how the pieces are combined --
 checked against the unsharded oracle.  Per-rank kernel work is stood in by the oracle on the rank's row
 block; the partition and the threshold search are the product's own host functions
 (regot_b200_host_row_block / regot_b200_host_pick_bucket, also used by the device path)."""
@@ -114,6 +114,44 @@ def sharded_topk(T, k, rank):
     return np.concatenate(gathered)  # rank order == row order
 
 
+def sharded_schur_pcg(B, D1, D2, ra, rb, rank, rtol=1e-12, max_iter=500):
+    """The kernel-by-kernel Schur-complement PCG of k4_sparse.cu (pcg_schur_multikernel) on a row block:
+    alpha-space quantities and the rows of B are local, beta-space vectors are replicated, and the ONLY
+    collectives are one allreduce(SUM) of B' t per mat-vec plus the alpha part of the reference norm."""
+    n = B.shape[0]
+    r0, cnt = row_block(n, rank, WORLD)
+    Bl, D1l, ral = B[r0:r0 + cnt], D1[r0:r0 + cnt], ra[r0:r0 + cnt]
+    t = ral / D1l
+    g0 = allreduce(np.array([ral @ t]))[0] + rb @ (rb / D2)     # r' D^-1 r of the FULL system
+    u = allreduce(Bl.T @ t)                                       # C3: the one vector collective
+    r = rb - u
+    z = r / D2
+    p, x = z.copy(), np.zeros_like(rb)
+    rz = r @ z
+    its = 0
+    while rz > rtol * rtol * g0 and its < max_iter:
+        t = (Bl @ p) / D1l
+        u = allreduce(Bl.T @ t)
+        q = D2 * p - u
+        a = rz / (p @ q)                                           # beta-space dots: identical on every rank
+        x += a * p
+        r -= a * q
+        z = r / D2
+        rzn = r @ z
+        p = z + (rzn / rz) * p
+        rz = rzn
+        its += 1
+    xa = ral / D1l - (Bl @ x) / D1l
+    return xa, x, its, r0
+
+
+def sharded_cloud_max(X, Y, rank):
+    """regot_b200_set_pointcloud_rows: the normalising maximum is taken over all ranks (allreduce MAX)."""
+    r0, cnt = row_block(X.shape[0], rank, WORLD)
+    d2 = ((X[r0:r0 + cnt, None, :] - Y[None, :, :]) ** 2).sum(axis=2)
+    return allreduce(np.array([d2.max()]), dist.ReduceOp.MAX)[0]
+
+
 def worker(rank, port, out):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=WORLD)
@@ -143,6 +181,20 @@ def worker(rank, port, out):
             assert np.array_equal(got, want), (t, n, m, k)
         got = sharded_topk(T, 0, rank)
         assert np.array_equal(got, o.select_topk(T, 0))
+        # Schur-complement PCG over row blocks == dense solve of A = [D1 B; B' D2]
+        n, m = 41, 23
+        B = np.where(rng.random((n, m)) < 0.3, rng.random((n, m)), 0.0)
+        D1, D2 = B.sum(axis=1) + 0.5 + rng.random(n), B.sum(axis=0) + 0.5 + rng.random(m)  # diagonally dominant: SPD
+        ra, rb = rng.normal(size=n), rng.normal(size=m)
+        xa, xb, its, r0 = sharded_schur_pcg(B, D1, D2, ra, rb, rank)
+        A = np.block([[np.diag(D1), B], [B.T, np.diag(D2)]])
+        ref = np.linalg.solve(A, np.concatenate([ra, rb]))
+        assert 0 < its < 200
+        np.testing.assert_allclose(xa, ref[r0:r0 + len(xa)], rtol=0, atol=1e-10 * np.abs(ref).max())
+        np.testing.assert_allclose(xb, ref[n:], rtol=0, atol=1e-10 * np.abs(ref).max())
+        # point clouds: global maximum of the cost
+        X, Y = rng.normal(size=(19, 3)), rng.normal(size=(11, 3))
+        assert sharded_cloud_max(X, Y, rank) == ((X[:, None, :] - Y[None, :, :]) ** 2).sum(axis=2).max()
         out[rank] = True
     finally:
         dist.destroy_process_group()

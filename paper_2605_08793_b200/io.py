@@ -299,3 +299,88 @@ def run_benchmark(spec: BenchSpec, solver=None) -> BenchReport:
             ar.rows.append(stat)
         report.algos.append(ar)
     return report
+
+
+# ---- spec file (bench.h:509-586) ------------------------------------------------------------------------------------
+_GENERATED_KINDS = ("synth1-iid", "synth1-diff", "synth2")
+
+
+def _stol(val: str, what: str) -> int:
+    """std::stol: leading integer, trailing text ignored; nothing parsable is an error (the reference
+    lets std::invalid_argument escape; here it is a ValidationError naming the key)."""
+    s = val.lstrip()
+    k = 1 if s[:1] in "+-" else 0
+    e = k
+    while e < len(s) and s[e].isdigit():
+        e += 1
+    if e == k:
+        raise ValidationError(f"parse_bench_spec: '{what}' needs an integer, got '{val}'")
+    return int(s[:e])
+
+
+def _strtod(val: str) -> float:
+    """strtod(val, nullptr): longest parsable prefix, 0 when there is none."""
+    s = val.strip()
+    for e in range(len(s), 0, -1):
+        try:
+            return float(s[:e])
+        except ValueError:
+            continue
+    return 0.0
+
+
+def parse_bench_spec(path: str) -> BenchSpec:
+    """Flat `key = value` lines, `#` comments; same keys, defaults and errors as bench.h:509-586
+    (`parallel-repeats` is accepted and ignored: one GPU context runs its repeats in sequence)."""
+    try:
+        with open(path, "r") as fh:
+            lines = fh.read().split("\n")
+    except OSError as e:
+        raise IoError(f"parse_bench_spec: cannot open {path}") from e
+    spec = BenchSpec()
+    spec.algos = []
+    have_eta = False
+    ws = " \t\r\n"
+    for lineno, line in enumerate(lines, 1):
+        t = line.strip(ws)
+        if not t or t[0] == "#":
+            continue
+        eq = t.find("=")
+        if eq < 0:
+            raise ValidationError(f"parse_bench_spec: line {lineno} is not 'key = value'")
+        key, val = t[:eq].strip(ws), t[eq + 1:].strip(ws)
+        if key == "problem":
+            if val in _GENERATED_KINDS:
+                spec.gen.kind = val
+            else:
+                spec.gen.kind, spec.gen.path = "file", val
+        elif key in ("n", "m", "d", "seed"):
+            setattr(spec.gen, key, _stol(val, key))
+        elif key == "eta":
+            spec.eta, have_eta = _strtod(val), True
+        elif key == "algo":
+            spec.algos += [a.strip(ws) for a in val.split(",") if a.strip(ws)]
+        elif key == "checkpoints":
+            spec.checkpoints = [_stol(c, key) for c in val.split(",") if c.strip(ws)]
+        elif key in ("repeats", "warmup"):
+            setattr(spec, key, _stol(val, key))
+        elif key == "tau-max":
+            spec.splr.tau_max = _strtod(val)
+        elif key in ("S", "J"):
+            setattr(spec.splr, key, _stol(val, key))
+        elif key in ("density", "c1", "c2"):
+            setattr(spec.splr, key, _strtod(val))
+        elif key == "max-ls-trials":
+            spec.splr.max_ls_trials = _stol(val, key)
+        elif key == "overlap":
+            spec.splr.overlap = val in ("1", "true")
+        elif key == "parallel-repeats":
+            pass
+        else:
+            raise ValidationError(f"parse_bench_spec: unknown key '{key}'")
+    if not spec.algos:
+        spec.algos = ["sinkhorn", "splr"]
+    if spec.gen.kind == "file" and not have_eta:
+        spec.eta = 0.0  # keep the eta stored in the file
+    spec.validate()
+    return spec

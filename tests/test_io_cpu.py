@@ -136,3 +136,43 @@ def test_medians_and_spec_validation():
             io.BenchSpec(**bad).validate()
     with pytest.raises(rg.ValidationError):
         io.BenchSpec(splr=rg.SplrConfig(c1=0.7)).validate()
+
+
+def test_bench_spec_keyfiles_parse_and_validate(tmp_path):
+    # test_bench.cpp:304-348 (same file contents, same expectations)
+    path = str(tmp_path / "spec.cfg")
+    with open(path, "w") as fh:
+        fh.write("# benchmark configuration\nproblem = synth2\nn = 32\nm = 24\neta = 0.005\nalgo = sinkhorn,splr\n"
+                 "checkpoints = 5, 10, 20\nrepeats = 3\nwarmup = 1\nS = 7\nJ = 2\ndensity = 0.05\n")
+    spec = io.parse_bench_spec(path)
+    assert (spec.gen.kind, spec.gen.n, spec.gen.m, spec.eta) == ("synth2", 32, 24, 0.005)
+    assert spec.algos == ["sinkhorn", "splr"] and spec.checkpoints == [5, 10, 20]
+    assert (spec.repeats, spec.warmup, spec.splr.S, spec.splr.J, spec.splr.density) == (3, 1, 7, 2, 0.05)
+    for body in ("problem = synth2\nbogus = 1\n", "problem = synth2\ncheckpoints = 10,5\n", "problem = synth2\njust a line\n",
+                 "problem = synth2\nn = many\n"):
+        with open(path, "w") as fh:
+            fh.write(body)
+        with pytest.raises(rg.ValidationError):
+            io.parse_bench_spec(path)
+    with pytest.raises(rg.IoError):
+        io.parse_bench_spec(str(tmp_path / "absent.cfg"))
+    # bench.h:534-543, 580-583: anything else is a file path whose stored eta is kept; default algorithms
+    with open(path, "w") as fh:
+        fh.write("problem = some/file.rotb\ntau-max = 0.5\nmax-ls-trials = 12\noverlap = true\nparallel-repeats = 1\n")
+    spec = io.parse_bench_spec(path)
+    assert (spec.gen.kind, spec.gen.path, spec.eta) == ("file", "some/file.rotb", 0.0)
+    assert spec.algos == ["sinkhorn", "splr"] and spec.splr.tau_max == 0.5 and spec.splr.max_ls_trials == 12 and spec.splr.overlap
+
+
+def test_command_line_gen_and_errors(tmp_path, capsys):
+    # regot.cpp:104-113, 185-189: `gen` writes the ROTB file and reports it; errors print "error: ..." and exit 1
+    from paper_2605_08793_b200.__main__ import main
+    out = str(tmp_path / "p.rotb")
+    assert main(["gen", "synth1-iid", "--n", "12", "--m", "9", "--d", "3", "--seed", "5", "--eta", "0.01", "-o", out]) == 0
+    assert capsys.readouterr().out == f"wrote synth1-iid 12x9 d=3 seed=5 eta=0.01 to {out}\n"
+    p, q = io.load_problem(out), problems.gen_synthetic1(12, 9, "iid", 3, 5, 0.01)
+    assert np.array_equal(p.M, q.M) and np.array_equal(p.a, q.a) and p.eta == 0.01
+    assert main(["gen", "not-a-generator", "-o", out]) == 1
+    assert "error: gen: kind must be a synthetic generator" in capsys.readouterr().err
+    assert main(["bench", "--spec", str(tmp_path / "absent.cfg"), "-o", out]) == 1
+    assert "cannot open" in capsys.readouterr().err

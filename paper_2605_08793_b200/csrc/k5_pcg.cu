@@ -49,7 +49,7 @@ constexpr int kSchurScratchBytes = (4 * kSchurWarps + 8 + 4 * kMaxGrid + 2 * kLo
 enum { kRowMain = 0, kRowFinal = 1, kColInit = 2, kColMain = 3 };
 
 struct SchurParams {
-    int nloc, mfree, nrhs, max_iter, n_long, nw, fixed_iters;
+    int nloc, mfree, nrhs, max_iter, n_long, n_long_rows, nw, fixed_iters;  // long lines: rows first; only columns carry dots
     int vec_bytes, desc_cap;  // shared-memory carve-up: vector buffer, then desc_cap descriptors per warp
     double tol2;
     const int* col;  // CSR of B
@@ -62,13 +62,12 @@ struct SchurParams {
     const int* wptr;   // 2 x (nw + 1)
     double* chunk_part;  // n_chunks x 2
     unsigned int* chunk_cnt;
-    double* longdot;  // n_long x 2
     const double* rhs_a[2];
     const double* rhs_b[2];
     double* sol_a[2];
     double* sol_b[2];
     double *ta, *zb, *wb, *pb, *sb, *rb, *xb;  // interleaved x2
-    double* blockpart;                         // gridDim.x x 4
+    unsigned long long* xchg;                  // flagged words of the partial-sum exchange: (gridDim.x x 4 + n_long x 2) x 2
     unsigned int* barrier;
     double* out;  // iters[2], -, breakdown flag, then timing
     double* mbox;  // host mailbox for out[0..3]
@@ -93,41 +92,104 @@ __device__ __forceinline__ void grid_barrier(unsigned int* ctr, unsigned int& ta
     __syncthreads();
 }
 
+// A double travels as two 64-bit words, each carrying 32 bits of the value and the 32-bit sequence number
+// of the exchange it belongs to: a reader that sees both numbers has the value, with no fence, atomic or
+// barrier in between (an aligned 8-byte store is single-copy atomic).
+__device__ __forceinline__ void xchg_post(unsigned long long* slot, double v, unsigned int seq)
+{
+    const unsigned long long b = (unsigned long long)__double_as_longlong(v), f = (unsigned long long)seq << 32;
+    asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(slot), "l"((b & 0xffffffffull) | f), "l"((b >> 32) | f) : "memory");
+}
+__device__ __forceinline__ double xchg_wait(const unsigned long long* slot, unsigned int seq)
+{
+    unsigned long long lo, hi;
+    do {
+        asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(lo), "=l"(hi) : "l"(slot) : "memory");
+    } while ((unsigned int)(lo >> 32) != seq || (unsigned int)(hi >> 32) != seq);
+    return __longlong_as_double((long long)((lo & 0xffffffffull) | (hi << 32)));
+}
+
+#ifdef REGOT_PCG_TIMING
+__device__ long long g_tsub[8];
+#define RG_SUB(i)                                                     \
+    if (blockIdx.x == 3 && threadIdx.x == 37) {                       \
+        const long long now__ = clock64();                            \
+        g_tsub[i] += now__ - tsub_prev;                               \
+        tsub_prev = now__;                                            \
+    }
+#else
+#define RG_SUB(i)
+#endif
 // sum of 4 per-thread values over the grid, in CTA order (+ the long lines' dot contributions added
-// to components [2 long_range, 2 long_range + 2)); result in every thread.  Contains a grid barrier.
-// All partials are fetched with ONE round of independent loads into shared memory and summed there.
-__device__ __noinline__ void grid_sum4(const SchurParams& P, double (&v)[4], double* scratch, double* bcast,
-                                       unsigned int& target, int long_range)
+// to components [2 long_range, 2 long_range + 2)); result in every thread.  Every CTA posts its 4
+// partials as flagged words and reads everybody's: one store-to-poll latency instead of a grid barrier
+// followed by a round of loads.  It is also a barrier for memory: the partials are posted behind a
+// fence that follows the CTA's own writes, and every reader fences after it has seen them.
+// Written for instruction count: with 16 warps on 4 schedulers every instruction on this path costs
+// ~4 clk per iteration of the solve (transposing warp reduction: 6 shuffles for 4 values, not 20).
+__device__ __noinline__ void grid_sum4(const SchurParams& P, double (&v)[4], double* scratch, double* bcast, unsigned int seq,
+                                       int long_range)
 {
     double* stage = bcast + 8;
     double* stage_long = stage + 4 * kMaxGrid;
-    block_sum<4>(v, scratch);
-    if (threadIdx.x == 0) {
-#pragma unroll
-        for (int k = 0; k < 4; ++k) P.blockpart[(size_t)blockIdx.x * 4 + k] = v[k];
-    }
-    grid_barrier(P.barrier, target);
-    const int nvals = (int)gridDim.x * 4, nlong = long_range >= 0 ? min(P.n_long, kLongStage) * 2 : 0;
-    for (int i = threadIdx.x; i < nvals + nlong; i += kSchurThreads) {
-        if (i < nvals) stage[i] = __ldcg(P.blockpart + i);
-        else stage_long[i - nvals] = __ldcg(P.longdot + (i - nvals));
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#ifdef REGOT_PCG_TIMING
+    long long tsub_prev = clock64();
+#endif
+    {
+        // lanes with (bit 4, bit 3) = (h, b) end up with the warp's sum of v[2h + b]
+        const bool up = lane & 16, b3 = lane & 8;
+        const double c0 = (up ? v[2] : v[0]) + shfl_xor_d(up ? v[0] : v[2], 16);
+        const double c1 = (up ? v[3] : v[1]) + shfl_xor_d(up ? v[1] : v[3], 16);
+        double d = (b3 ? c1 : c0) + shfl_xor_d(b3 ? c0 : c1, 8);
+        d += shfl_xor_d(d, 4);
+        d += shfl_xor_d(d, 2);
+        d += shfl_xor_d(d, 1);
+        if ((lane & 7) == 0) scratch[(lane >> 3) * kSchurWarps + warp] = d;
     }
     __syncthreads();
-    if (threadIdx.x < 32 * 4) {
-        const int k = threadIdx.x >> 5, l = threadIdx.x & 31;
+    RG_SUB(0)
+    if (threadIdx.x < 4 * kSchurWarps) {  // 16 lanes per component
+        double d = scratch[threadIdx.x];
+        d += shfl_xor_d(d, 8);
+        d += shfl_xor_d(d, 4);
+        d += shfl_xor_d(d, 2);
+        d += shfl_xor_d(d, 1);
+        if ((threadIdx.x & (kSchurWarps - 1)) == 0) {
+            __threadfence();
+            xchg_post(P.xchg + ((size_t)blockIdx.x * 4 + (threadIdx.x / kSchurWarps)) * 2, d, seq);
+        }
+    }
+    const int nvals = (int)gridDim.x * 4, n_dots = P.n_long - P.n_long_rows;  // the column phase's long lines
+    const int nlong = long_range >= 0 ? min(n_dots, kLongStage) * 2 : 0;
+#pragma unroll 1
+    for (int i = threadIdx.x; i < nvals + nlong; i += kSchurThreads) {
+        const double x = xchg_wait(P.xchg + (size_t)i * 2, seq);
+        if (i < nvals) stage[i] = x;
+        else stage_long[i - nvals] = x;
+    }
+    RG_SUB(1)
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    RG_SUB(2)
+    __syncthreads();
+    RG_SUB(3)
+    if (warp < 4) {
+        const int k = warp;
         double s = 0.0;
-        for (int b = l; b < (int)gridDim.x; b += 32) s += stage[b * 4 + k];
+#pragma unroll 1
+        for (int b = lane; b < (int)gridDim.x; b += 32) s += stage[b * 4 + k];
         if (k / 2 == long_range) {
-            for (int q = l; q < P.n_long; q += 32)
-                s += q < kLongStage ? stage_long[q * 2 + (k % 2)] : __ldcg(P.longdot + (size_t)q * 2 + (k % 2));
+#pragma unroll 1
+            for (int q = lane; q < n_dots; q += 32)
+                s += q < kLongStage ? stage_long[q * 2 + (k % 2)] : xchg_wait(P.xchg + ((size_t)nvals + (size_t)q * 2 + (k % 2)) * 2, seq);
         }
         s = warp_sum(s);
-        if (l == 0) bcast[k] = s;
+        if (lane == 0) bcast[k] = s;
     }
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < 4; ++k) v[k] = bcast[k];
-    __syncthreads();
+    RG_SUB(4)
 }
 
 // shared-memory carve-up as 32-bit shared-window addresses
@@ -223,7 +285,7 @@ __device__ __forceinline__ ItemHead load_head(const SchurParams& P, const double
 // flight; descriptors of the first n_desc items are cached in shared memory at `desc`.
 template <bool kRows>
 __device__ __forceinline__ void run_phase(const SchurParams& P, int mode, const WarpLog& L, int i0, int i1,
-                                          uint32_t desc, int n_desc, int lane, double& dot)
+                                          uint32_t desc, int n_desc, int lane, double& dot, unsigned int seq)
 {
     const int* __restrict__ src_idx = kRows ? P.col : P.cscrow;
     const double* __restrict__ src_val = kRows ? P.val : P.cscval;
@@ -309,8 +371,8 @@ __device__ __forceinline__ void run_phase(const SchurParams& P, int mode, const 
                     dk = z * w;
                 }
                 // which warp finishes a long line varies from run to run: its dot product goes to a fixed
-                // slot of the ordered grid reduction instead of this lane's partial
-                if (is_long) P.longdot[(size_t)slot * 2 + kk] = dk;
+                // slot of the ordered grid reduction (sequence number `seq`) instead of this lane's partial
+                if (is_long) xchg_post(P.xchg + ((size_t)gridDim.x * 4 + (size_t)(slot - P.n_long_rows) * 2 + kk) * 2, dk, seq);
                 else dot += dk;
             }
         }
@@ -351,7 +413,7 @@ __global__ void __launch_bounds__(kSchurThreads, 1) k_pcg_schur(const __grid_con
     // the schedule deals items CTA-first so the heaviest ones land on different SMs
     const int gw = warp * gridDim.x + blockIdx.x;
     const int nloc = P.nloc, mfree = P.mfree, nrhs = P.nrhs;
-    unsigned int bar_target = 0;
+    unsigned int bar_target = 0, xchg_seq = 0;
 #ifdef REGOT_PCG_TIMING  // per-section cycle counts per CTA (experiments only; costs registers)
     long long tsec[8] = {0, 0, 0, 0, 0, 0, 0, 0}, tprev = clock64();
 #define RG_TICK(i)                         \
@@ -411,7 +473,7 @@ __global__ void __launch_bounds__(kSchurThreads, 1) k_pcg_schur(const __grid_con
             double none = 0.0;
             const double* gx = row_mode == kRowMain ? P.zb : P.xb;
             stage_vector(L.vec, gx, mfree);
-            run_phase<true>(P, row_mode, L, r0, r1, desc_r, nd_r, lane, none);
+            run_phase<true>(P, row_mode, L, r0, r1, desc_r, nd_r, lane, none, 0u);
             if (row_mode == kRowFinal) break;
         }
         RG_TICK(1)
@@ -422,7 +484,8 @@ __global__ void __launch_bounds__(kSchurThreads, 1) k_pcg_schur(const __grid_con
         {
             double dot = 0.0;
             stage_vector(L.vec, P.ta, nloc);
-            run_phase<false>(P, col_mode, L, c0, c1, desc_c, nd_c, lane, dot);
+            ++xchg_seq;
+            run_phase<false>(P, col_mode, L, c0, c1, desc_c, nd_c, lane, dot, xchg_seq);
 #pragma unroll
             for (int k = 0; k < 2; ++k) {
                 const double dk = ((lane & 1) == k) ? dot : 0.0;
@@ -431,7 +494,7 @@ __global__ void __launch_bounds__(kSchurThreads, 1) k_pcg_schur(const __grid_con
             }
         }
         RG_TICK(3)
-        grid_sum4(P, red, scratch, bcast, bar_target, col_mode == kColInit ? 0 : 1);
+        grid_sum4(P, red, scratch, bcast, xchg_seq, col_mode == kColInit ? 0 : 1);
         RG_TICK(4)
         if (col_mode == kColInit) {
 #pragma unroll
@@ -673,6 +736,7 @@ void build_pcg_schedule(regot_ctx* ctx, cudaStream_t st, regot_sparse& S, const 
                 emit((len4[0] + 7) / 8, 0, 0, 0, 0, 0, line4, beg4, len4);
             }
             cursor_items += n_items;
+            if (pass == 1 && phase == 0) Q.n_long_rows = n_long_p;
         }
         if (pass == 0) {
             n_items_total = cursor_items;
@@ -690,13 +754,11 @@ void build_pcg_schedule(regot_ctx* ctx, cudaStream_t st, regot_sparse& S, const 
     Q.wptr.ensure(2 * ((size_t)nw + 1));
     Q.chunk_part.ensure((size_t)n_chunks * 2 + 2);
     Q.chunk_cnt.ensure((size_t)n_long + 1);
-    Q.longdot.ensure((size_t)n_long * 2 + 2);
     if (n_items_total)
         RG_CUDA(cudaMemcpyAsync(Q.items.p, h_items, sizeof(int) * (size_t)kPcgItemInts * (size_t)n_items_total,
                                 cudaMemcpyHostToDevice, st));
     RG_CUDA(cudaMemcpyAsync(Q.wptr.p, h_wptr, sizeof(int) * 2 * ((size_t)nw + 1), cudaMemcpyHostToDevice, st));
     RG_CUDA(cudaMemsetAsync(Q.chunk_cnt.p, 0, sizeof(unsigned int) * ((size_t)n_long + 1), st));
-    RG_CUDA(cudaMemsetAsync(Q.longdot.p, 0, sizeof(double) * ((size_t)n_long * 2 + 2), st));
 }
 
 // ---- host: launch --------------------------------------------------------------------------------
@@ -722,9 +784,7 @@ static int pcg_schur_launch(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, const
     if (smem > kPcgSmemBudget) raise(REGOT_E_CUDA, "pcg: shared-memory plan exceeds the budget (internal error)");
     const size_t va = (size_t)std::max(nloc, 1) * 2, vb = (size_t)std::max(mfree, 1) * 2;
     ws.cg.ensure(va + 6 * vb + 16);
-    ws.cg_partials.ensure((size_t)grid * 4 + 8);
     ws.cg_scal.ensure(16 + (size_t)grid * 8);
-    ws.cg_barrier.ensure(4);
     if (!ws.h_cg) RG_CUDA(cudaMallocHost((void**)&ws.h_cg, sizeof(double) * 4096));
 
     SchurParams P;
@@ -734,6 +794,7 @@ static int pcg_schur_launch(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, const
     P.nrhs = nrhs;
     P.max_iter = max_iter;
     P.n_long = Q.n_long;
+    P.n_long_rows = Q.n_long_rows;
     P.nw = Q.nw;
     P.fixed_iters = 0;
     if (const char* e = std::getenv("REGOT_B200_PCG_FIXED_ITERS")) P.fixed_iters = std::atoi(e);
@@ -755,7 +816,6 @@ static int pcg_schur_launch(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, const
     P.wptr = Q.wptr.p;
     P.chunk_part = Q.chunk_part.p;
     P.chunk_cnt = Q.chunk_cnt.p;
-    P.longdot = Q.longdot.p;
     for (int k = 0; k < 2; ++k) {
         const int kk = k < nrhs ? k : 0;
         P.rhs_a[k] = rhs[kk]->a.p;
@@ -772,10 +832,13 @@ static int pcg_schur_launch(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, const
     P.sb = P.pb + vb;
     P.rb = P.sb + vb;
     P.xb = P.rb + vb;
-    P.blockpart = ws.cg_partials.p;
-    P.barrier = ws.cg_barrier.p;
+    // [barrier counter | flagged words of the exchange], zeroed together: sequence numbers start at 1 in every launch
+    const size_t xchg_words = ((size_t)grid * 4 + (size_t)Q.n_long * 2) * 2;
+    ws.cg_xchg.ensure(2 + xchg_words);
+    P.barrier = reinterpret_cast<unsigned int*>(ws.cg_xchg.p);
+    P.xchg = ws.cg_xchg.p + 2;  // 16-byte aligned
     P.out = ws.cg_scal.p;
-    RG_CUDA(cudaMemsetAsync(P.barrier, 0, sizeof(unsigned int), st));
+    RG_CUDA(cudaMemsetAsync(ws.cg_xchg.p, 0, sizeof(unsigned long long) * (2 + xchg_words), st));
     ws.cg_mbox.ensure();
     P.mbox = timing ? nullptr : ws.cg_mbox.data;
     P.seq = timing ? 0ULL : ws.cg_mbox.next();
@@ -806,6 +869,14 @@ static int pcg_schur_launch(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, const
             std::fprintf(stderr, " %s %.0f/%.0f/%.0f", nm[k], mn * 1e-3, sum / grid * 1e-3, mx * 1e-3);
         }
         std::fprintf(stderr, " | iters %.0f, %d long lines\n", ws.h_cg[0], Q.n_long);
+#ifdef REGOT_PCG_TIMING
+        long long tsub[8];
+        RG_CUDA(cudaMemcpyFromSymbol(tsub, g_tsub, sizeof(tsub)));
+        std::fprintf(stderr, "  grid_sum4 kcycles (one thread, cumulative): block_sum %lld | post+poll %lld | fence %lld | sync %lld | sum %lld\n",
+                     tsub[0] / 1000, tsub[1] / 1000, tsub[2] / 1000, tsub[3] / 1000, tsub[4] / 1000);
+        std::memset(tsub, 0, sizeof(tsub));
+        RG_CUDA(cudaMemcpyToSymbol(g_tsub, tsub, sizeof(tsub)));
+#endif
     }
     static const bool show_iters = std::getenv("REGOT_B200_PCG_ITERS") != nullptr;  // experiments
     if (show_iters) std::fprintf(stderr, "pcg iters: g-system %d, u-system %d\n", (int)ws.h_cg[0], nrhs > 1 ? (int)ws.h_cg[1] : -1);

@@ -23,9 +23,9 @@ constexpr int kPcgSmemBudget = 227 * 1024;     // dynamic shared memory of the p
 constexpr int kPcgVecSmemMax = 168 * 1024;     // largest gathered vector (16 B / entry) staged in shared memory
 struct PcgSchedule {
     DevBuf<int> items, wptr;
-    mutable DevBuf<double> chunk_part, longdot;
+    mutable DevBuf<double> chunk_part;
     mutable DevBuf<unsigned int> chunk_cnt;
-    int nw = 0, n_long = 0, n_chunks = 0;
+    int nw = 0, n_long = 0, n_long_rows = 0, n_chunks = 0;  // long lines: the row phase's come first
     bool fits = false;                // both gathered vectors fit the shared-memory buffer
     int vec_bytes = 0, desc_cap = 0;  // shared-memory carve-up: vector buffer, descriptors per warp
 };
@@ -83,6 +83,7 @@ struct SparseWS {
     DevBuf<double> cg_partials;
     DevBuf<unsigned int> cg_ticket;
     DevBuf<unsigned int> cg_barrier;
+    DevBuf<unsigned long long> cg_xchg;  // persistent PCG: grid-barrier counter + flagged words of the partial-sum exchange
     PinnedBuf<int> h_ptrs;   // rowptr | cscptr of the current pattern (device -> host)
     PinnedBuf<int> h_lines;  // line lists and the PCG schedule (host -> device)
     double* h_cg = nullptr;  // pinned

@@ -34,6 +34,9 @@ elif which in ("D", "Dsmall"):
     for r0 in range(0, n, 2500):
         M[r0:r0 + 2500] /= mx
     p = rg.ProblemInstance(n, m, M, np.full(n, 1.0 / n), np.full(m, 1.0 / m), 0.001)
+elif ":" in which:  # kind:n:m:eta, e.g. synth1-iid:1600:1200:0.001 (d = 2, seed = 7)
+    kind, n_, m_, eta_ = which.split(":")
+    p = problems.make_problem(kind, int(n_), int(m_), float(eta_), 2, 7)
 else:
     side = int(which)
     p = problems.gen_image(side, 0.001)

@@ -132,6 +132,11 @@ regot_ctx* ctx_create(int device)
         ctx->device = device;
         ctx->sm_count = prop.multiProcessorCount;
         if (const char* e = std::getenv("REGOT_B200_MULTIKERNEL_PCG")) ctx->force_multikernel_pcg = e[0] == '1';
+        // off by default: measured 11 % (config A) / 1 % (1600 x 1200) of the direction solve, slower above ~50k entries
+        ctx->pcg_cluster_size = 0;
+        ctx->pcg_cluster_max_entries = 50000;
+        if (const char* e = std::getenv("REGOT_B200_PCG_CLUSTER")) ctx->pcg_cluster_size = std::atoi(e);
+        if (const char* e = std::getenv("REGOT_B200_PCG_CLUSTER_ENTRIES")) ctx->pcg_cluster_max_entries = std::atol(e);
         if (const char* e = std::getenv("REGOT_B200_EXACT_LSE")) ctx->fast_sinkhorn = e[0] != '1';
         if (const char* e = std::getenv("REGOT_B200_FAST_CHAIN")) ctx->fast_sinkhorn_chain = e[0] == '1';
         RG_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));

@@ -259,6 +259,11 @@ struct regot_ctx {
 
     // tests: run the sharded (multi-kernel + NCCL) PCG path on one GPU (REGOT_B200_MULTIKERNEL_PCG=1)
     bool force_multikernel_pcg = false;
+    // persistent PCG on one thread-block cluster when a CG iteration touches at most this many matrix entries
+    // (REGOT_B200_PCG_CLUSTER = 0 | 8 | 16, REGOT_B200_PCG_CLUSTER_ENTRIES)
+    int pcg_cluster_size = 0;
+    bool pcg_cluster_probed = false;
+    long pcg_cluster_max_entries = 0;
     // run_sinkhorn's updates take the gradient-sweep form (k7_lse.cu) unless REGOT_B200_EXACT_LSE=1; the
     // candidate chain of run_splr only with REGOT_B200_FAST_CHAIN=1 (see solver.cu); the stand-alone entry
     // points always use the log-sum-exp kernels

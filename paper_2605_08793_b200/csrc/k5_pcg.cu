@@ -49,7 +49,7 @@ constexpr int kSchurScratchBytes = (4 * kSchurWarps + 8 + 4 * kMaxGrid + 2 * kLo
 enum { kRowMain = 0, kRowFinal = 1, kColInit = 2, kColMain = 3 };
 
 struct SchurParams {
-    int nloc, mfree, nrhs, max_iter, n_long, n_long_rows, nw, fixed_iters;  // long lines: rows first; only columns carry dots
+    int nloc, mfree, nrhs, max_iter, n_long, n_long_rows, nw, fixed_iters, cluster;  // long lines: rows first; only columns carry dots
     int vec_bytes, desc_cap;  // shared-memory carve-up: vector buffer, then desc_cap descriptors per warp
     double tol2;
     const int* col;  // CSR of B
@@ -107,6 +107,18 @@ __device__ __forceinline__ double xchg_wait(const unsigned long long* slot, unsi
         asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(lo), "=l"(hi) : "l"(slot) : "memory");
     } while ((unsigned int)(lo >> 32) != seq || (unsigned int)(hi >> 32) != seq);
     return __longlong_as_double((long long)((lo & 0xffffffffull) | (hi << 32)));
+}
+
+// Small systems run on ONE thread-block cluster (16 CTAs) instead of the whole GPU: the work per
+// iteration is a few entries per lane either way, and the hardware cluster barrier costs a fraction of a
+// barrier through L2 among 148 CTAs.
+__device__ __forceinline__ void sync_all(const SchurParams& P, unsigned int& target)
+{
+    if (P.cluster) {
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    } else {
+        grid_barrier(P.barrier, target);
+    }
 }
 
 #ifdef REGOT_PCG_TIMING
@@ -477,7 +489,7 @@ __global__ void __launch_bounds__(kSchurThreads, 1) k_pcg_schur(const __grid_con
             if (row_mode == kRowFinal) break;
         }
         RG_TICK(1)
-        grid_barrier(P.barrier, bar_target);
+        sync_all(P, bar_target);
         RG_TICK(2)
         // kColInit: c = r_b - B' t, r = c, z = D2^-1 c, x = p = s = 0, gamma = r'z
         // kColMain: w = D2 z - B' t, delta = z'w
@@ -533,7 +545,9 @@ __global__ void __launch_bounds__(kSchurThreads, 1) k_pcg_schur(const __grid_con
                 // p = z + beta p, s = w + beta s, x += alpha p, r -= alpha s, z = D2^-1 r, gamma = r'z
 #pragma unroll
                 for (int k = 0; k < 4; ++k) red[k] = 0.0;
-                for (int j = tid; j < mfree; j += nthr) {
+                // groups of 32 entries dealt CTA-first: on the critical path between two grid-wide waits it matters
+                // that no SM has more than a warp or two of this to issue
+                for (int j = (warp * (int)gridDim.x + (int)blockIdx.x) * 32 + lane; j < mfree; j += nthr) {
                     const size_t o = (size_t)j * 2;
                     const double2 z2 = ldcg_x2(P.zb + o), p2 = ldcg_x2(P.pb + o), w2 = ldcg_x2(P.wb + o);
                     const double2 s2 = ldcg_x2(P.sb + o), x2 = ldcg_x2(P.xb + o), r2 = ldcg_x2(P.rb + o);
@@ -567,7 +581,7 @@ __global__ void __launch_bounds__(kSchurThreads, 1) k_pcg_schur(const __grid_con
                 // z is needed by the next row phase; the gamma partials ride on the next reduction
                 // (one grid reduction per iteration: Chronopoulos-Gear)
                 RG_TICK(5)
-                grid_barrier(P.barrier, bar_target);
+                sync_all(P, bar_target);
                 RG_TICK(6)
             }
         }
@@ -605,12 +619,45 @@ __global__ void __launch_bounds__(kSchurThreads, 1) k_pcg_schur(const __grid_con
 // dealt over the warps in a snake (position q of the sorted order -> round q / nw, warp q % nw, reversed
 // on odd rounds) so the loads stay level; warp w's items are contiguous in `items`.  Everything is
 // written straight into pinned staging and uploaded asynchronously: no allocation, no sort call.
+// largest cluster (<= the requested size) of CTAs with the kernel's full shared-memory budget that this device can host
+static int probe_cluster_size(int want)
+{
+    RG_CUDA(cudaFuncSetAttribute(k_pcg_schur, cudaFuncAttributeMaxDynamicSharedMemorySize, kPcgSmemBudget));
+    RG_CUDA(cudaFuncSetAttribute(k_pcg_schur, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    for (int size = want; size >= 2; size /= 2) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(size);
+        cfg.blockDim = dim3(kSchurThreads);
+        cfg.dynamicSmemBytes = kPcgSmemBudget;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = (unsigned)size;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, (const void*)k_pcg_schur, &cfg) == cudaSuccess && n >= 1) return size;
+        (void)cudaGetLastError();
+    }
+    return 0;
+}
+
 void build_pcg_schedule(regot_ctx* ctx, cudaStream_t st, regot_sparse& S, const int* rp, const int* cp, PinnedBuf<int>& staging,
                         size_t staging_used)
 {
+    if (ctx->pcg_cluster_size > 0 && !ctx->pcg_cluster_probed) {
+        ctx->pcg_cluster_size = probe_cluster_size(std::min(ctx->pcg_cluster_size, 16));
+        ctx->pcg_cluster_probed = true;
+    }
     PcgSchedule& Q = S.pcg;
     const int nloc = (int)S.nloc, mm1 = std::max((int)S.m - 1, 0);
-    const int grid = ctx->sm_count, nw = grid * kPcgWarpsPerCta;
+    // small systems: one cluster of CTAs (hardware barrier) instead of the whole GPU
+    const long entries_per_iter = 2L * (long)rp[nloc];
+    int grid = ctx->sm_count;
+    if (ctx->pcg_cluster_size > 0 && entries_per_iter <= ctx->pcg_cluster_max_entries) grid = ctx->pcg_cluster_size;
+    const int nw = grid * kPcgWarpsPerCta;
+    Q.grid = grid;
     Q.nw = nw;
     // shared-memory plan: the larger of the two gathered vectors (16 B per entry), then the descriptor
     // cache.  fits == false: sparse_pcg takes the kernel-by-kernel path and this schedule is not used.
@@ -768,7 +815,8 @@ static int pcg_schur_launch(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, const
 {
     const PcgSchedule& Q = S.pcg;
     const int nloc = (int)S.nloc, mfree = std::max((int)S.m - 1, 0);
-    const int grid = ctx->sm_count;
+    const int grid = Q.grid;
+    const bool cluster = grid != ctx->sm_count;
     if (Q.nw != grid * kPcgWarpsPerCta || grid > kMaxGrid)
         raise(REGOT_E_CUDA, "pcg: schedule was built for a different grid (internal error)");
     if (!Q.fits) raise(REGOT_E_CUDA, "pcg: the persistent kernel needs the iterated vectors in shared memory (internal error)");
@@ -796,6 +844,7 @@ static int pcg_schur_launch(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, const
     P.n_long = Q.n_long;
     P.n_long_rows = Q.n_long_rows;
     P.nw = Q.nw;
+    P.cluster = cluster ? 1 : 0;
     P.fixed_iters = 0;
     if (const char* e = std::getenv("REGOT_B200_PCG_FIXED_ITERS")) P.fixed_iters = std::atoi(e);
     P.vec_bytes = Q.vec_bytes;
@@ -845,7 +894,23 @@ static int pcg_schur_launch(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, const
     void* args[] = {&P};
     {
         ProfScope prof(ctx, st, 5);
-        RG_CUDA(cudaLaunchCooperativeKernel((const void*)k_pcg_schur, dim3(grid), dim3(kSchurThreads), args, (size_t)smem, st));
+        if (cluster) {
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(grid);
+            cfg.blockDim = dim3(kSchurThreads);
+            cfg.dynamicSmemBytes = (size_t)smem;
+            cfg.stream = st;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = (unsigned)grid;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            RG_CUDA(cudaLaunchKernelExC(&cfg, (const void*)k_pcg_schur, args));
+        } else {
+            RG_CUDA(cudaLaunchCooperativeKernel((const void*)k_pcg_schur, dim3(grid), dim3(kSchurThreads), args, (size_t)smem, st));
+        }
     }
     ++ctx->launches;
     if (timing) {

@@ -25,6 +25,7 @@ struct PcgSchedule {
     DevBuf<int> items, wptr;
     mutable DevBuf<double> chunk_part;
     mutable DevBuf<unsigned int> chunk_cnt;
+    int grid = 0;  // CTAs the schedule was dealt over: all SMs, or one cluster for a small system
     int nw = 0, n_long = 0, n_long_rows = 0, n_chunks = 0;  // long lines: the row phase's come first
     bool fits = false;                // both gathered vectors fit the shared-memory buffer
     int vec_bytes = 0, desc_cap = 0;  // shared-memory carve-up: vector buffer, descriptors per warp

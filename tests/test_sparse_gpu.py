@@ -230,6 +230,34 @@ def test_multikernel_pcg_solve_agrees_with_persistent_kernel(solver, multikernel
     assert abs(a.f - b.f) <= 1e-9 * (1 + abs(a.f))
 
 
+def test_single_cluster_pcg_agrees_with_whole_grid_kernel(solver):
+    """REGOT_B200_PCG_CLUSTER=16: the persistent kernel on one thread-block cluster with the hardware cluster
+    barrier (an opt-in for small systems).  Same schedule code dealt over 16 CTAs instead of 148."""
+    import os
+
+    from paper_2605_08793_b200 import problems
+
+    os.environ["REGOT_B200_PCG_CLUSTER"] = "16"
+    try:
+        clustered = rg.Solver(0)
+    finally:
+        del os.environ["REGOT_B200_PCG_CLUSTER"]
+    try:
+        p = problems.gen_synthetic1(300, 260, "iid", 2, 7, 0.01)
+        cfg = rg.SplrConfig(max_iter=200, tol=1e-8)
+        res = []
+        for s in (solver, clustered):
+            s.set_problem(p)
+            res.append(s.run_splr(rg.DualPoint.zeros(p.n, p.m), cfg))
+        a, b = res[0].trace.rows[-1], res[1].trace.rows[-1]
+        assert a.marginal_error <= 1e-8 and b.marginal_error <= 1e-8
+        for u, v in zip(res[0].steps[:15], res[1].steps[:15]):
+            assert abs(u.f_after - v.f_after) <= 1e-11 * (1 + abs(u.f_after)) and u.cg_iters == v.cg_iters
+        assert abs(a.iter - b.iter) <= max(1, round(0.15 * a.iter)) and abs(a.f - b.f) <= 1e-9 * (1 + abs(a.f))
+    finally:
+        clustered.close()
+
+
 def test_foreign_and_invalid_inputs_rejected(solver, oracle):
     p = oracle.gen_problem("rand", 8, 6, 0.1, seed=3601)
     solver.set_problem(to_problem(p))

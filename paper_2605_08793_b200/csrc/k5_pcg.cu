@@ -51,6 +51,7 @@ enum { kRowMain = 0, kRowFinal = 1, kColInit = 2, kColMain = 3 };
 struct SchurParams {
     int nloc, mfree, nrhs, max_iter, n_long, n_long_rows, nw, fixed_iters, cluster;  // long lines: rows first; only columns carry dots
     int vec_bytes, desc_cap;  // shared-memory carve-up: vector buffer, then desc_cap descriptors per warp
+    int stage_rows, stage_cols;  // whether the vector a phase gathers is staged in shared memory (else: gathered through L2)
     double tol2;
     const int* col;  // CSR of B
     const double* val;
@@ -297,7 +298,8 @@ __device__ __forceinline__ ItemHead load_head(const SchurParams& P, const double
 // flight; descriptors of the first n_desc items are cached in shared memory at `desc`.
 template <bool kRows>
 __device__ __forceinline__ void run_phase(const SchurParams& P, int mode, const WarpLog& L, int i0, int i1,
-                                          uint32_t desc, int n_desc, int lane, double& dot, unsigned int seq)
+                                          uint32_t desc, int n_desc, int lane, double& dot, unsigned int seq, const double* gx,
+                                          bool staged)
 {
     const int* __restrict__ src_idx = kRows ? P.col : P.cscrow;
     const double* __restrict__ src_val = kRows ? P.val : P.cscval;
@@ -322,7 +324,7 @@ __device__ __forceinline__ void run_phase(const SchurParams& P, int mode, const 
             }
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
-                const double2 g = gather2(L.vec, (unsigned)c[u] * 16u);
+                const double2 g = staged ? gather2(L.vec, (unsigned)c[u] * 16u) : ldcg_x2(gx + (size_t)c[u] * 2);
                 a0 += v[u] * g.x;
                 a1 += v[u] * g.y;
             }
@@ -484,8 +486,8 @@ __global__ void __launch_bounds__(kSchurThreads, 1) k_pcg_schur(const __grid_con
             // kRowMain: t = D1^-1 B z;  kRowFinal: x_a = D1^-1 (r_a - B x_b)
             double none = 0.0;
             const double* gx = row_mode == kRowMain ? P.zb : P.xb;
-            stage_vector(L.vec, gx, mfree);
-            run_phase<true>(P, row_mode, L, r0, r1, desc_r, nd_r, lane, none, 0u);
+            if (P.stage_rows) stage_vector(L.vec, gx, mfree);
+            run_phase<true>(P, row_mode, L, r0, r1, desc_r, nd_r, lane, none, 0u, gx, P.stage_rows != 0);
             if (row_mode == kRowFinal) break;
         }
         RG_TICK(1)
@@ -495,9 +497,9 @@ __global__ void __launch_bounds__(kSchurThreads, 1) k_pcg_schur(const __grid_con
         // kColMain: w = D2 z - B' t, delta = z'w
         {
             double dot = 0.0;
-            stage_vector(L.vec, P.ta, nloc);
+            if (P.stage_cols) stage_vector(L.vec, P.ta, nloc);
             ++xchg_seq;
-            run_phase<false>(P, col_mode, L, c0, c1, desc_c, nd_c, lane, dot, xchg_seq);
+            run_phase<false>(P, col_mode, L, c0, c1, desc_c, nd_c, lane, dot, xchg_seq, P.ta, P.stage_cols != 0);
 #pragma unroll
             for (int k = 0; k < 2; ++k) {
                 const double dk = ((lane & 1) == k) ? dot : 0.0;
@@ -662,9 +664,15 @@ void build_pcg_schedule(regot_ctx* ctx, cudaStream_t st, regot_sparse& S, const 
     // shared-memory plan: the larger of the two gathered vectors (16 B per entry), then the descriptor
     // cache.  fits == false: sparse_pcg takes the kernel-by-kernel path and this schedule is not used.
     const int budget = kPcgSmemBudget - kSchurScratchBytes;
-    const long need = 16L * std::max(std::max(mm1, nloc), 1);
-    Q.fits = need <= kPcgVecSmemMax;
-    Q.vec_bytes = (int)((std::min<long>(need, kPcgVecSmemMax) + 127) / 128 * 128);
+    // a phase whose gathered vector does not fit gathers it through L2 instead (request-rate bound, ~14 k clk per
+    // phase at 10^6 entries -- still one kernel per solve, against ~95 us per iteration kernel by kernel)
+    const long need_r = 16L * std::max(mm1, 1), need_c = 16L * std::max(nloc, 1);
+    Q.stage_rows = need_r <= kPcgVecSmemMax;
+    Q.stage_cols = need_c <= kPcgVecSmemMax;
+    Q.fits = (Q.stage_rows || Q.stage_cols) && rp[nloc] <= kPcgMaxEntriesL2Gather;
+    if (Q.stage_rows && Q.stage_cols) Q.fits = true;
+    const long need = std::max<long>(Q.stage_rows ? need_r : 0, Q.stage_cols ? need_c : 0);
+    Q.vec_bytes = (int)((std::max<long>(need, 16) + 127) / 128 * 128);
     Q.desc_cap = std::min(40, (budget - Q.vec_bytes) / (kPcgWarpsPerCta * kPcgItemInts * 4));
     if (!Q.fits) return;
 
@@ -848,6 +856,8 @@ static int pcg_schur_launch(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, const
     P.fixed_iters = 0;
     if (const char* e = std::getenv("REGOT_B200_PCG_FIXED_ITERS")) P.fixed_iters = std::atoi(e);
     P.vec_bytes = Q.vec_bytes;
+    P.stage_rows = Q.stage_rows ? 1 : 0;
+    P.stage_cols = Q.stage_cols ? 1 : 0;
     P.desc_cap = Q.desc_cap;
 #ifdef REGOT_PCG_TIMING
     const bool timing = true;

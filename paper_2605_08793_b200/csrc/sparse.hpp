@@ -21,13 +21,15 @@ constexpr int kPcgWarpsPerCta = 16;
 constexpr int kPcgItemInts = 24;
 constexpr int kPcgSmemBudget = 227 * 1024;     // dynamic shared memory of the persistent kernel
 constexpr int kPcgVecSmemMax = 168 * 1024;     // largest gathered vector (16 B / entry) staged in shared memory
+constexpr long kPcgMaxEntriesL2Gather = 4000000;  // one phase gathering through L2: only up to this many entries of B
 struct PcgSchedule {
     DevBuf<int> items, wptr;
     mutable DevBuf<double> chunk_part;
     mutable DevBuf<unsigned int> chunk_cnt;
     int grid = 0;  // CTAs the schedule was dealt over: all SMs, or one cluster for a small system
     int nw = 0, n_long = 0, n_long_rows = 0, n_chunks = 0;  // long lines: the row phase's come first
-    bool fits = false;                // both gathered vectors fit the shared-memory buffer
+    bool fits = false;                // the persistent kernel takes this pattern (else: kernel by kernel)
+    bool stage_rows = false, stage_cols = false;  // which phase's gathered vector is staged in shared memory
     int vec_bytes = 0, desc_cap = 0;  // shared-memory carve-up: vector buffer, descriptors per warp
 };
 }  // namespace rg

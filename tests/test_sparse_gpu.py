@@ -230,6 +230,26 @@ def test_multikernel_pcg_solve_agrees_with_persistent_kernel(solver, multikernel
     assert abs(a.f - b.f) <= 1e-9 * (1 + abs(a.f))
 
 
+@pytest.mark.parametrize("n,m", [(11000, 300), (300, 11000)])
+def test_persistent_pcg_with_one_phase_gathering_through_l2(solver, multikernel_solver, n, m):
+    """One side longer than the shared-memory vector buffer (10,752 entries): that phase of the persistent kernel
+    gathers through L2 instead.  Same trajectory as the kernel-by-kernel solve (config C's shape class)."""
+    from paper_2605_08793_b200 import problems
+
+    p = problems.gen_synthetic2(n, m, 0.01)
+    cfg = rg.SplrConfig(max_iter=60, tol=1e-8)
+    res = []
+    for s in (solver, multikernel_solver):
+        s.set_problem(p)
+        res.append(s.run_splr(rg.DualPoint.zeros(p.n, p.m), cfg))
+    assert len(res[0].steps) >= 10
+    for u, v in zip(res[0].steps[:25], res[1].steps[:25]):
+        assert abs(u.f_after - v.f_after) <= 1e-11 * (1 + abs(u.f_after)) and u.ls_evals == v.ls_evals
+        assert abs(u.cg_iters - v.cg_iters) <= 1
+    a, b = res[0].trace.rows[-1], res[1].trace.rows[-1]
+    assert abs(a.iter - b.iter) <= max(1, round(0.15 * a.iter)) and abs(a.f - b.f) <= 1e-9 * (1 + abs(a.f))
+
+
 def test_single_cluster_pcg_agrees_with_whole_grid_kernel(solver):
     """REGOT_B200_PCG_CLUSTER=16: the persistent kernel on one thread-block cluster with the hardware cluster
     barrier (an opt-in for small systems).  Same schedule code dealt over 16 CTAs instead of 148."""

@@ -627,7 +627,17 @@ void finish_structure(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, regot_spars
     int* cp = rp + nloc + 1;
     RG_CUDA(cudaMemcpyAsync(rp, S.rowptr.p, sizeof(int) * ((size_t)nloc + 1), cudaMemcpyDeviceToHost, st));
     RG_CUDA(cudaMemcpyAsync(cp, S.cscptr.p, sizeof(int) * ((size_t)std::max(mm1, 0) + 1), cudaMemcpyDeviceToHost, st));
-    RG_CUDA(cudaStreamSynchronize(st));
+    if (ws.after_pointer_download) {
+        // wait for the pointers only; what the hook enqueues behind them keeps the GPU busy during the host work below
+        if (!ws.ev_ptrs) RG_CUDA(cudaEventCreateWithFlags(&ws.ev_ptrs, cudaEventDisableTiming));
+        RG_CUDA(cudaEventRecord(ws.ev_ptrs, st));
+        auto hook = std::move(ws.after_pointer_download);
+        ws.after_pointer_download = nullptr;
+        hook();
+        RG_CUDA(cudaEventSynchronize(ws.ev_ptrs));
+    } else {
+        RG_CUDA(cudaStreamSynchronize(st));
+    }
     // The threshold grows with the problem: once a warp of the mat-vec grid has thousands of entries to
     // process anyway, a line of that length is balanced work for ONE warp, and chunking it would only
     // add the cross-warp combine (a fence and an atomic per chunk).  At config B it stays kLongLine.

@@ -436,56 +436,67 @@ void solve_splr(regot_ctx* ctx, const double* alpha0, const double* beta0, const
             std::function<void()> join_chain;
 
             if (refresh) {
+                // candidate chain from the same snapshot (splr.h:366-372): J Sinkhorn steps, then a gradient pass; on
+                // the side stream when cfg.overlap is set (splr.h:373-378).  By default the steps are the
+                // log-sum-exp kernels: the hybrid trajectory is sensitive to the last bits of the
+                // candidate (a rounding-level change flips synth1-diff 64^2 between a 61- and a
+                // 71-iteration path), and the LSE form rounds like the reference's.  With
+                // REGOT_B200_FAST_CHAIN=1 they take the gradient-sweep form (3 % faster on config B); a
+                // step that left its safe range is reported with the gradient pass's scalars and the
+                // chain is redone with the log-sum-exp kernels.
+                cudaStream_t cs = cfg.overlap ? ctx->side : st;
+                ncclComm* ccomm = cfg.overlap ? ctx->comm_side : ctx->comm;
+                run_chain = [&, cs, ccomm](bool fast) {
+                    SweepWS& w = cfg.overlap ? ctx->ws_side : ctx->ws_main;
+                    W.xs.ensure(pr.nloc, pr.m);
+                    RG_CUDA(cudaMemcpyAsync(W.xs.a.p, W.x.a.p, sizeof(double) * (size_t)pr.nloc, cudaMemcpyDeviceToDevice, cs));
+                    RG_CUDA(cudaMemcpyAsync(W.xs.b.p, W.x.b.p, sizeof(double) * (size_t)pr.m, cudaMemcpyDeviceToDevice, cs));
+                    for (long j = 0; j < cfg.J; ++j) {
+                        if (fast) launch_sinkhorn_step_fast(ctx, cs, w, ccomm, W.xs.a.p, W.xs.b.p);
+                        else launch_sinkhorn_step(ctx, cs, w, ccomm, W.xs.a.p, W.xs.b.p);
+                    }
+                    out.lse_passes += 2 * cfg.J;
+                    launch_gradient(ctx, cs, w, ccomm, W.xs.a.p, W.xs.b.p, nullptr, nullptr, W.cand);
+                    ++out.gradient_passes;
+                };
+                auto finish_chain = [&, cs]() {
+                    SweepWS& w = cfg.overlap ? ctx->ws_side : ctx->ws_main;
+                    sync_scalars(ctx, cs, w, W.cand);
+                    if (W.cand.sc.lse_flag != 0.0) {
+                        reset_sinkhorn_flag(ctx, cs, w);
+                        run_chain(false);
+                        sync_scalars(ctx, cs, w, W.cand);
+                    }
+                };
+                // Without a side stream the chain is enqueued in the middle of the refresh, behind the selection
+                // sweeps: it does not depend on the pattern, and it keeps the GPU busy while the host turns the
+                // pattern's pointer arrays into line lists and the PCG schedule.  Same kernels, same order of
+                // arithmetic, same results.
+                bool chain_started = false;
+                if (cfg.J > 0 && !cfg.overlap && !ctx->profiling)
+                    W.sparse.after_pointer_download = [&]() {
+                        run_chain(ctx->fast_sinkhorn_chain);
+                        chain_started = true;
+                    };
                 // plan + select_topk + assemble (splr.h:361-364); T is never materialised
-                {
+                try {
                     ProfScope prof(ctx, st, 6);  // the whole pattern refresh: sweeps, selection, structure, host work
                     topk_build_pattern(ctx, st, W.sparse, kFromDual, W.x.a.p, W.x.b.p,
                                        regot_b200_topk_budget(pr.n, pr.m, cfg.density), W.A);
+                } catch (...) {
+                    W.sparse.after_pointer_download = nullptr;
+                    throw;
                 }
+                W.sparse.after_pointer_download = nullptr;
                 out.gradient_passes += 3;  // three sweeps over M
                 sparse_fill_values(ctx, st, W.A, W.x.a.p, W.x.b.p, tau, W.cur.sums.a.p, W.cur.sums.b.p);
                 sect.tick(0);
                 if (cfg.J > 0) {
-                    // candidate chain from the same snapshot (splr.h:366-372); on the side
-                    // stream when cfg.overlap is set (splr.h:373-378)
-                    cudaStream_t cs = cfg.overlap ? ctx->side : st;
-                    SweepWS& cws = cfg.overlap ? ctx->ws_side : ctx->ws_main;
-                    ncclComm* ccomm = cfg.overlap ? ctx->comm_side : ctx->comm;
                     if (cfg.overlap) {
                         RG_CUDA(cudaEventRecord(ctx->ev_fork, st));
                         RG_CUDA(cudaStreamWaitEvent(cs, ctx->ev_fork, 0));
                     }
-                    W.xs.ensure(pr.nloc, pr.m);
-                    // J Sinkhorn steps from the snapshot, then a gradient pass.  By default the steps are the
-                    // log-sum-exp kernels: the hybrid trajectory is sensitive to the last bits of the
-                    // candidate (a rounding-level change flips synth1-diff 64^2 between a 61- and a
-                    // 71-iteration path), and the LSE form rounds like the reference's.  With
-                    // REGOT_B200_FAST_CHAIN=1 they take the gradient-sweep form (3 % faster on config B); a
-                    // step that left its safe range is reported with the gradient pass's scalars and the
-                    // chain is redone with the log-sum-exp kernels.
-                    run_chain = [&, cs, ccomm](bool fast) {
-                        SweepWS& w = cfg.overlap ? ctx->ws_side : ctx->ws_main;
-                        RG_CUDA(cudaMemcpyAsync(W.xs.a.p, W.x.a.p, sizeof(double) * (size_t)pr.nloc, cudaMemcpyDeviceToDevice, cs));
-                        RG_CUDA(cudaMemcpyAsync(W.xs.b.p, W.x.b.p, sizeof(double) * (size_t)pr.m, cudaMemcpyDeviceToDevice, cs));
-                        for (long j = 0; j < cfg.J; ++j) {
-                            if (fast) launch_sinkhorn_step_fast(ctx, cs, w, ccomm, W.xs.a.p, W.xs.b.p);
-                            else launch_sinkhorn_step(ctx, cs, w, ccomm, W.xs.a.p, W.xs.b.p);
-                        }
-                        out.lse_passes += 2 * cfg.J;
-                        launch_gradient(ctx, cs, w, ccomm, W.xs.a.p, W.xs.b.p, nullptr, nullptr, W.cand);
-                        ++out.gradient_passes;
-                    };
-                    auto finish_chain = [&, cs]() {
-                        SweepWS& w = cfg.overlap ? ctx->ws_side : ctx->ws_main;
-                        sync_scalars(ctx, cs, w, W.cand);
-                        if (W.cand.sc.lse_flag != 0.0) {
-                            reset_sinkhorn_flag(ctx, cs, w);
-                            run_chain(false);
-                            sync_scalars(ctx, cs, w, W.cand);
-                        }
-                    };
-                    (void)cws;
-                    run_chain(ctx->fast_sinkhorn_chain);
+                    if (!chain_started) run_chain(ctx->fast_sinkhorn_chain);
                     if (!cfg.overlap) finish_chain();
                     else join_chain = finish_chain;
                     have_s = true;

@@ -8,6 +8,7 @@
 // on export only.
 #pragma once
 
+#include <functional>
 #include "ctx.hpp"
 
 namespace rg {
@@ -87,6 +88,10 @@ struct SparseWS {
     DevBuf<unsigned int> cg_ticket;
     DevBuf<unsigned int> cg_barrier;
     DevBuf<unsigned long long> cg_xchg;  // persistent PCG: grid-barrier counter + flagged words of the partial-sum exchange
+    // called by finish_structure once the pointer arrays are on their way to the host: GPU work that does not
+    // depend on the pattern (the solver's candidate chain) is enqueued here and runs while the host builds the lists
+    std::function<void()> after_pointer_download;
+    cudaEvent_t ev_ptrs = nullptr;
     PinnedBuf<int> h_ptrs;   // rowptr | cscptr of the current pattern (device -> host)
     PinnedBuf<int> h_lines;  // line lists and the PCG schedule (host -> device)
     double* h_cg = nullptr;  // pinned

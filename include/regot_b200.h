@@ -257,6 +257,12 @@ regot_status regot_b200_sparse_info(const regot_sparse* A, int32_t* dim, int64_t
                                     uint64_t* pattern_id);
 regot_status regot_b200_sparse_export(regot_ctx* ctx, const regot_sparse* A, int32_t* colptr, int32_t* rowidx,
                                       double* values, int32_t* coords);
+/* This context's rows of the pattern (global row index, column) with the off-diagonal values B_ij =
+ * T_ij / eta, in row-major order -- the one export that also works on a row-sharded context (the
+ * concatenation over the ranks is the global pattern).  *count receives the number of local entries;
+ * up to `cap` of them are written (coords: 2 ints per entry; either array may be NULL). */
+regot_status regot_b200_sparse_export_local(regot_ctx* ctx, const regot_sparse* A, int32_t* coords, double* values,
+                                            int64_t cap, int64_t* count);
 void regot_b200_sparse_free(regot_sparse* A);
 
 /* ---- SPLR (splr.h) ---------------------------------------------------------- */
@@ -269,6 +275,31 @@ regot_status regot_b200_compute_direction(regot_ctx* ctx, const regot_sparse* A,
 /* run_splr (splr.h:487-534) */
 regot_status regot_b200_run_splr(regot_ctx* ctx, const double* alpha0, const double* beta0,
                                  const regot_splr_config* cfg, regot_result* out);
+
+/* Step-level interface: SplrState (splr.h:82-97) as an opaque device-resident handle -- the iterate, its
+ * gradient, the previous accepted iterate, the frozen pattern and its matrix -- with splr_init
+ * (splr.h:326-334) and splr_step (splr.h:348-478).  run_splr is exactly init + the loop of splr.h:509-531
+ * over step; a caller driving the steps itself gets bitwise the same iterates (the reference's tests do:
+ * test_splr.cpp:349-378).  A state belongs to the context and problem it was made with; it is the
+ * checkpoint / resume seam (state_point + state_info give everything a restart needs: x and iter --
+ * restarting at a multiple of S rebuilds the pattern like the reference would). */
+typedef struct regot_splr_state regot_splr_state;
+regot_status regot_b200_splr_init(regot_ctx* ctx, const double* alpha0, const double* beta0,
+                                  const regot_splr_config* cfg, regot_splr_state** out);
+/* One iteration; rec (nullable) receives the step record.  Failures are the reference's exception classes
+ * (REGOT_E_DIRECTION, REGOT_E_NOT_POSITIVE_DEFINITE, ...), not REGOT_E_STEP: wrapping is run_splr's job. */
+regot_status regot_b200_splr_step(regot_ctx* ctx, regot_splr_state* state, const regot_splr_config* cfg,
+                                  regot_step_record* rec);
+/* st.iter, st.has_prev and the scalars of st.cur (f, marginal error, duality gap, ||grad||, mass). */
+regot_status regot_b200_splr_state_info(regot_ctx* ctx, const regot_splr_state* state, int64_t* iter,
+                                        int32_t* has_prev, regot_gradient_info* cur);
+/* st.x (alpha: n, beta: m) and, optionally, st.cur's gradient (n+m-1), row sums (n), column sums (m). */
+regot_status regot_b200_splr_state_point(regot_ctx* ctx, const regot_splr_state* state, double* alpha,
+                                         double* beta, double* grad, double* row_sums, double* col_sums);
+/* st.A: borrowed handle to H_Omega + tau I at the frozen pattern (valid until the next refresh step or
+ * state_free; NULL before the first step).  Do not free it. */
+const regot_sparse* regot_b200_splr_state_matrix(const regot_splr_state* state);
+void regot_b200_splr_state_free(regot_splr_state* state);
 
 void regot_b200_splr_config_default(regot_splr_config* cfg);         /* SplrConfig{} */
 void regot_b200_sinkhorn_config_default(regot_sinkhorn_config* cfg); /* SinkhornConfig{} */

@@ -58,7 +58,7 @@ def _parser() -> argparse.ArgumentParser:
     b = sub.add_parser("bench", help="Run the benchmark protocol from a spec file")
     b.add_argument("--spec", required=True, help="flat key = value spec file")
     b.add_argument("-o", "--output", required=True, help="report CSV path")
-    b.add_argument("--parallel-repeats", action="store_true", help="accepted for compatibility; repeats run in sequence on one GPU")
+    b.add_argument("--parallel-repeats", action="store_true", help="run repeats concurrently (one device context per thread); timings not comparable")
 
     p = sub.add_parser("plot", help="(not provided: render the report CSV with the reference's `regot plot`)")
     p.add_argument("rest", nargs="*")
@@ -99,7 +99,10 @@ def main(argv=None) -> int:
                 io.emit_csv(trace, args.trace)
                 print(f"trace written to {args.trace}")
         elif args.cmd == "bench":
-            report = io.run_benchmark(io.parse_bench_spec(args.spec))
+            spec = io.parse_bench_spec(args.spec)
+            if args.parallel_repeats:  # regot.cpp:165-166
+                spec.parallel_repeats = True
+            report = io.run_benchmark(spec)
             io.emit_csv(report, args.output)
             print(f"report written to {args.output}")
             for ar in report.algos:

@@ -161,12 +161,19 @@ PROTOTYPES = {
     "regot_b200_matvec": (C.c_int, [_vp, _vp, _vp, _vp]),
     "regot_b200_sparse_info": (C.c_int, [_vp, c_int32_p, c_int64_p, c_int64_p, C.POINTER(C.c_uint64)]),
     "regot_b200_sparse_export": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
+    "regot_b200_sparse_export_local": (C.c_int, [_vp, _vp, _vp, _vp, C.c_int64, c_int64_p]),
     "regot_b200_sparse_free": (None, [_vp]),
     "regot_b200_compute_direction": (
         C.c_int,
         [_vp, _vp, _vp, _vp, _vp, C.c_double, C.c_double, C.c_double, C.c_int32, _vp, c_int32_p],
     ),
     "regot_b200_run_splr": (C.c_int, [_vp, _vp, _vp, C.POINTER(SplrConfigC), C.POINTER(ResultC)]),
+    "regot_b200_splr_init": (C.c_int, [_vp, _vp, _vp, C.POINTER(SplrConfigC), C.POINTER(_vp)]),
+    "regot_b200_splr_step": (C.c_int, [_vp, _vp, C.POINTER(SplrConfigC), C.POINTER(StepRecordC)]),
+    "regot_b200_splr_state_info": (C.c_int, [_vp, _vp, c_int64_p, c_int32_p, C.POINTER(GradientInfoC)]),
+    "regot_b200_splr_state_point": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "regot_b200_splr_state_matrix": (_vp, [_vp]),
+    "regot_b200_splr_state_free": (None, [_vp]),
     "regot_b200_splr_config_default": (None, [C.POINTER(SplrConfigC)]),
     "regot_b200_sinkhorn_config_default": (None, [C.POINTER(SinkhornConfigC)]),
     "regot_b200_splr_config_validate": (C.c_int, [C.POINTER(SplrConfigC)]),

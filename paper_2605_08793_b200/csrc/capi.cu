@@ -21,7 +21,7 @@ void validate_problem_device(regot_ctx* ctx);
 void set_pointcloud(regot_ctx* ctx, int64_t n, int64_t m, int64_t row_begin, int64_t row_count, int d, const double* X,
                     const double* Y, const double* a, const double* b, double eta, bool on_the_fly);
 void get_cost_host(regot_ctx* ctx, double* out);
-std::string g_create_error;
+thread_local std::string g_create_error;  // last create()/unique_id() failure of the calling thread
 }  // namespace rg
 
 using namespace rg;

@@ -230,6 +230,113 @@ regot_status regot_b200_run_splr(regot_ctx* ctx, const double* alpha0, const dou
     return st;
 }
 
+}  // extern "C"
+
+// SplrState (splr.h:82-97): the device state plus the context it belongs to
+struct regot_splr_state {
+    regot_ctx* ctx = nullptr;
+    int device = 0;
+    int64_t n = 0, m = 0, nloc = 0;
+    SplrStateDev dev;
+};
+
+namespace {
+void check_state(const regot_ctx* ctx, const regot_splr_state* s, const char* who)
+{
+    if (!s) raise(REGOT_E_VALIDATION, std::string(who) + ": null state");
+    if (s->ctx != ctx || s->n != ctx->prob.n || s->m != ctx->prob.m || s->nloc != ctx->prob.nloc)
+        raise(REGOT_E_VALIDATION, std::string(who) + ": dual point/problem dimension mismatch");
+}
+}  // namespace
+
+extern "C" {
+
+regot_status regot_b200_splr_init(regot_ctx* ctx, const double* alpha0, const double* beta0, const regot_splr_config* cfg,
+                                  regot_splr_state** out)
+{
+    return guard(ctx, [&] {
+        if (!cfg || !out) raise(REGOT_E_VALIDATION, "splr_init: null argument");
+        *out = nullptr;
+        ctx_require_problem(ctx);
+        auto s = std::make_unique<regot_splr_state>();
+        s->ctx = ctx;
+        s->device = ctx->device;
+        s->n = ctx->prob.n;
+        s->m = ctx->prob.m;
+        s->nloc = ctx->prob.nloc;
+        splr_init_state(ctx, alpha0, beta0, s->dev, nullptr);
+        *out = s.release();
+    });
+}
+
+regot_status regot_b200_splr_step(regot_ctx* ctx, regot_splr_state* state, const regot_splr_config* cfg,
+                                  regot_step_record* rec)
+{
+    return guard(ctx, [&] {
+        if (!cfg) raise(REGOT_E_VALIDATION, "splr_step: null argument");
+        validate_splr_config(*cfg);
+        ctx_require_problem(ctx);
+        check_state(ctx, state, "splr_step");
+        regot_step_record r;
+        splr_step_state(ctx, state->dev, *cfg, r, nullptr);
+        if (rec) *rec = r;
+    });
+}
+
+regot_status regot_b200_splr_state_info(regot_ctx* ctx, const regot_splr_state* state, int64_t* iter, int32_t* has_prev,
+                                        regot_gradient_info* cur)
+{
+    return guard(ctx, [&] {
+        check_state(ctx, state, "splr_state_info");
+        if (iter) *iter = state->dev.iter;
+        if (has_prev) *has_prev = state->dev.has_prev ? 1 : 0;
+        if (cur) {
+            const GradScalars& sc = state->dev.cur.sc;
+            cur->f = sc.f;
+            cur->marginal_error = sc.marginal_error;
+            cur->duality_gap = sc.duality_gap;
+            cur->grad_norm2 = std::sqrt(sc.grad_sqnorm);
+            cur->total_mass = sc.total_mass;
+        }
+    });
+}
+
+regot_status regot_b200_splr_state_point(regot_ctx* ctx, const regot_splr_state* state, double* alpha, double* beta,
+                                         double* grad, double* row_sums, double* col_sums)
+{
+    return guard(ctx, [&] {
+        check_state(ctx, state, "splr_state_point");
+        const DeviceProblem& pr = ctx->prob;
+        const SplrStateDev& S = state->dev;
+        if (alpha || beta) {
+            std::vector<double> a, b;
+            download_point(ctx, S.x, a, b);
+            if (alpha) std::memcpy(alpha, a.data(), sizeof(double) * a.size());
+            if (beta) std::memcpy(beta, b.data(), sizeof(double) * b.size());
+        }
+        // like fused_gradient: a sharded context fills its own row slice of the n-long outputs
+        if (grad) {
+            download(ctx, grad + pr.row_begin, S.cur.g.a.p, (size_t)pr.nloc);
+            download(ctx, grad + pr.n, S.cur.g.b.p, (size_t)pr.m - 1);
+        }
+        if (row_sums) download(ctx, row_sums + pr.row_begin, S.cur.sums.a.p, (size_t)pr.nloc);
+        if (col_sums) download(ctx, col_sums, S.cur.sums.b.p, (size_t)pr.m);
+        RG_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+const regot_sparse* regot_b200_splr_state_matrix(const regot_splr_state* state)
+{
+    return (state && state->dev.A.ctx) ? &state->dev.A : nullptr;
+}
+
+void regot_b200_splr_state_free(regot_splr_state* state)
+{
+    if (!state) return;
+    cudaSetDevice(state->device);
+    delete state;
+}
+
 regot_status regot_b200_select_topk_dense(regot_ctx* ctx, int64_t n, int64_t m, const double* T, int layout, int64_t k,
                                           int32_t* coords, int64_t cap, int64_t* count)
 {
@@ -352,10 +459,31 @@ regot_status regot_b200_sparse_export(regot_ctx* ctx, const regot_sparse* A, int
     });
 }
 
+regot_status regot_b200_sparse_export_local(regot_ctx* ctx, const regot_sparse* A, int32_t* coords, double* values,
+                                            int64_t cap, int64_t* count)
+{
+    return guard(ctx, [&] {
+        if (!A || !count) raise(REGOT_E_VALIDATION, "sparse_export_local: null argument");
+        *count = A->nnz;
+        const size_t take = (size_t)std::max<int64_t>(0, std::min<int64_t>(cap, A->nnz));
+        if (take == 0) return;
+        std::vector<int> row(take), col(take);
+        RG_CUDA(cudaMemcpyAsync(row.data(), A->row.p, sizeof(int) * take, cudaMemcpyDeviceToHost, ctx->stream));
+        RG_CUDA(cudaMemcpyAsync(col.data(), A->col.p, sizeof(int) * take, cudaMemcpyDeviceToHost, ctx->stream));
+        if (values) RG_CUDA(cudaMemcpyAsync(values, A->val.p, sizeof(double) * take, cudaMemcpyDeviceToHost, ctx->stream));
+        RG_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (coords)
+            for (size_t t = 0; t < take; ++t) {
+                coords[2 * t] = (int32_t)(row[t] + A->row_begin);
+                coords[2 * t + 1] = col[t];
+            }
+    });
+}
+
 void regot_b200_sparse_free(regot_sparse* A)
 {
     if (!A) return;
-    if (A->ctx) cudaSetDevice(A->ctx->device);
+    cudaSetDevice(A->device);  // not A->ctx->device: the context may already have been destroyed
     delete A;
 }
 

@@ -9,7 +9,7 @@
 
 namespace rg {
 
-extern std::string g_create_error;
+extern thread_local std::string g_create_error;
 
 // Run `body`, translate exceptions into a status + ctx->err.
 template <class F>

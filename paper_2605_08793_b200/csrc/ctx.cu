@@ -29,11 +29,21 @@ NcclApi& nccl()
     static NcclApi api;
     static std::once_flag once;
     std::call_once(once, [] {
+        // REGOT_B200_NCCL_LIB names another library with the same five entry points: the tests point it at a
+        // loopback communicator (tests/fake_nccl) that runs R ranks as R contexts of one process on one GPU
+        if (const char* path = std::getenv("REGOT_B200_NCCL_LIB")) {
+            api.lib = dlopen(path, RTLD_NOW | RTLD_LOCAL);
+            if (!api.lib) {
+                api.why = std::string("REGOT_B200_NCCL_LIB: ") + (dlerror() ? dlerror() : "dlopen failed");
+                return;
+            }
+        }
         // RTLD_NOLOAD first: reuse the copy torch already mapped (same SONAME)
-        api.lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!api.lib) api.lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
         if (!api.lib) api.lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
         if (!api.lib) {
-            api.why = dlerror() ? dlerror() : "dlopen(libnccl.so.2) failed";
+            const char* why = dlerror();
+            api.why = why ? why : "dlopen(libnccl.so.2) failed";
             return;
         }
         api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(api.lib, "ncclGetUniqueId");

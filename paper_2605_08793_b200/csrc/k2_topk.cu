@@ -382,6 +382,7 @@ void topk_build_pattern(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, TopkSourc
     if (k < 0) raise(REGOT_E_VALIDATION, "select_topk: k must be >= 0");
     const int nloc = (int)pr.nloc, m = (int)pr.m, mm1 = m - 1;
     S.ctx = ctx;
+    S.device = ctx->device;
     S.n = pr.n;
     S.m = pr.m;
     S.nloc = pr.nloc;
@@ -534,6 +535,7 @@ void pattern_from_coords(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, const in
     const DeviceProblem& pr = ctx->prob;
     const int nloc = (int)pr.nloc, mm1 = (int)pr.m - 1;
     S.ctx = ctx;
+    S.device = ctx->device;
     S.n = pr.n;
     S.m = pr.m;
     S.nloc = pr.nloc;

@@ -53,11 +53,13 @@ void gradient_sync(regot_ctx* ctx, cudaStream_t st, SweepWS& ws, ncclComm* comm,
 
 // copy the dual point back: this rank's rows of alpha (allgathered by summing a
 // zero-padded vector when sharded), all of beta
-void download_point(regot_ctx* ctx, const DVec& x, SolveOut& out)
+}  // namespace
+
+void download_point(regot_ctx* ctx, const DVec& x, std::vector<double>& alpha, std::vector<double>& beta)
 {
     const DeviceProblem& pr = ctx->prob;
-    out.alpha.assign((size_t)pr.n, 0.0);
-    out.beta.assign((size_t)pr.m, 0.0);
+    alpha.assign((size_t)pr.n, 0.0);
+    beta.assign((size_t)pr.m, 0.0);
     if (ctx->world > 1) {
         DevBuf<double> full;
         full.ensure((size_t)pr.n);
@@ -65,14 +67,16 @@ void download_point(regot_ctx* ctx, const DVec& x, SolveOut& out)
         RG_CUDA(cudaMemcpyAsync(full.p + pr.row_begin, x.a.p, sizeof(double) * (size_t)pr.nloc, cudaMemcpyDeviceToDevice,
                                 ctx->stream));
         allreduce_sum(ctx, ctx->comm, full.p, (size_t)pr.n, ctx->stream);
-        RG_CUDA(cudaMemcpyAsync(out.alpha.data(), full.p, sizeof(double) * (size_t)pr.n, cudaMemcpyDeviceToHost, ctx->stream));
+        RG_CUDA(cudaMemcpyAsync(alpha.data(), full.p, sizeof(double) * (size_t)pr.n, cudaMemcpyDeviceToHost, ctx->stream));
         RG_CUDA(cudaStreamSynchronize(ctx->stream));
     } else {
-        RG_CUDA(cudaMemcpyAsync(out.alpha.data(), x.a.p, sizeof(double) * (size_t)pr.nloc, cudaMemcpyDeviceToHost, ctx->stream));
+        RG_CUDA(cudaMemcpyAsync(alpha.data(), x.a.p, sizeof(double) * (size_t)pr.nloc, cudaMemcpyDeviceToHost, ctx->stream));
     }
-    RG_CUDA(cudaMemcpyAsync(out.beta.data(), x.b.p, sizeof(double) * (size_t)pr.m, cudaMemcpyDeviceToHost, ctx->stream));
+    RG_CUDA(cudaMemcpyAsync(beta.data(), x.b.p, sizeof(double) * (size_t)pr.m, cudaMemcpyDeviceToHost, ctx->stream));
     RG_CUDA(cudaStreamSynchronize(ctx->stream));
 }
+
+namespace {
 
 void append_row(SolveOut& out, long iter, double wall_ms, const GradScalars& sc)
 {
@@ -137,7 +141,7 @@ void solve_sinkhorn(regot_ctx* ctx, const double* alpha0, const double* beta0, c
     if (!fresh) gradient_sync(ctx, st, ctx->ws_main, ctx->comm, W.x, nullptr, W.cur, &out);
     if (out.trace.back().iter != it) append_row(out, it, clk.ms(), W.cur.sc);
     out.device_ms = tm.stop();
-    download_point(ctx, W.x, out);
+    download_point(ctx, W.x, out.alpha, out.beta);
     out.kernel_launches = ctx->launches - launches0;
 }
 
@@ -152,6 +156,10 @@ struct SectionTimer {
     std::chrono::steady_clock::time_point t0;
     double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     SectionTimer(cudaStream_t s) : on(std::getenv("REGOT_B200_STEP_TIMING") != nullptr), st(s), t0(std::chrono::steady_clock::now()) {}
+    void start()
+    {
+        if (on) t0 = std::chrono::steady_clock::now();
+    }
     void tick(int k)
     {
         if (!on) return;
@@ -162,16 +170,18 @@ struct SectionTimer {
     }
     ~SectionTimer()
     {
-        if (on)
+        if (on && acc[0] + acc[2] + acc[4] > 0.0)
             std::fprintf(stderr, "run_splr sections (ms): refresh %.2f | candidate chain %.2f | value refresh %.2f | low rank %.2f | "
                                  "direction %.2f | line search %.2f | bookkeeping %.2f\n",
                          acc[0], acc[1], acc[2], acc[3], acc[4], acc[5], acc[6]);
     }
 };
 
+thread_local SectionTimer* g_sect = nullptr;  // run_splr's timer while it drives splr_step_state
+
 struct LowRankDev {
     bool active = false;
-    double xi = 0.0, zeta = 0.0;  // u = W.ydiff, v = W.v
+    double xi = 0.0, zeta = 0.0;  // u = ydiff, v = v
 };
 
 double dot1(regot_ctx* ctx, SolverWS& W, const DVec& a, const DVec& b)
@@ -185,17 +195,17 @@ double dot1(regot_ctx* ctx, SolverWS& W, const DVec& a, const DVec& b)
 
 // build_low_rank (splr.h:102-122): s- and y- are differences of the free vectors of
 // the last two accepted iterates
-LowRankDev build_low_rank(regot_ctx* ctx, SolverWS& W, bool has_prev)
+LowRankDev build_low_rank(regot_ctx* ctx, SolverWS& W, SplrStateDev& S)
 {
     LowRankDev R;
-    if (!has_prev) return R;
+    if (!S.has_prev) return R;
     cudaStream_t st = ctx->stream;
-    vec_sub(ctx, st, W.x, W.x_prev, W.sdiff);
-    vec_sub(ctx, st, W.cur.g, W.g_prev, W.ydiff);
-    W.v.ensure(ctx->prob.nloc, ctx->prob.m);
-    sparse_matvec(ctx, st, ctx->comm, W.A, 1, W.sdiff.a.p, W.sdiff.b.p, W.v.a.p, W.v.b.p, 0, 0);
-    const DVec* xs[5] = {&W.ydiff, &W.ydiff, &W.v, &W.v, &W.sdiff};
-    const DVec* ys[5] = {&W.sdiff, &W.ydiff, &W.sdiff, &W.v, &W.sdiff};
+    vec_sub(ctx, st, S.x, S.x_prev, S.sdiff);
+    vec_sub(ctx, st, S.cur.g, S.g_prev, S.ydiff);
+    S.v.ensure(ctx->prob.nloc, ctx->prob.m);
+    sparse_matvec(ctx, st, ctx->comm, S.A, 1, S.sdiff.a.p, S.sdiff.b.p, S.v.a.p, S.v.b.p, 0, 0);
+    const DVec* xs[5] = {&S.ydiff, &S.ydiff, &S.v, &S.v, &S.sdiff};
+    const DVec* ys[5] = {&S.sdiff, &S.ydiff, &S.sdiff, &S.v, &S.sdiff};
     double r[5];
     vec_dots(ctx, st, ctx->comm, W.dots, 5, xs, ys, r);
     const double ys_ = r[0], yy = r[1], vs = r[2], vv = r[3], ss = r[4];
@@ -207,10 +217,15 @@ LowRankDev build_low_rank(regot_ctx* ctx, SolverWS& W, bool has_prev)
     return R;
 }
 
+// the three solutions compute_direction works with
+struct DirScratch {
+    DVec &ag, &au, &av;
+};
+
 // compute_direction (splr.h:128-167) with A^{-1} applied by batched PCG.
 // Returns false on PCG breakdown (the caller escalates tau like a failed
 // factorization, splr.h:400-407).  g_dot_d receives g . d.
-bool compute_direction(regot_ctx* ctx, SolverWS& W, const regot_sparse& A, const DVec& g, double g_sqnorm,
+bool compute_direction(regot_ctx* ctx, SolverWS& W, DirScratch D, const regot_sparse& A, const DVec& g, double g_sqnorm,
                        const LowRankDev& R, const DVec& u, const DVec& v, double rtol, int max_iter, DVec& d,
                        double& g_dot_d, int& cg_iters, const DVec* av_known = nullptr)
 {
@@ -222,11 +237,11 @@ bool compute_direction(regot_ctx* ctx, SolverWS& W, const regot_sparse& A, const
         return true;
     }
     const DVec* rhs[3] = {&g, &u, &v};
-    DVec* sol[3] = {&W.ag, &W.au, &W.av};
+    DVec* sol[3] = {&D.ag, &D.au, &D.av};
     // Inside the solver v = A s^- (build_low_rank) for the SAME matrix the solves use, so A^-1 v is
     // s^- itself: the reference's third solve (splr.h:136) reproduces it to rounding, and it is passed
     // in as av_known.  Only the stand-alone entry point (arbitrary v) solves three systems.
-    const DVec& av = av_known ? *av_known : W.av;
+    const DVec& av = av_known ? *av_known : D.av;
     const int nrhs = R.active ? (av_known ? 2 : 3) : 1;
     const int it = sparse_pcg(ctx, st, ctx->comm, W.sparse, A, nrhs, rhs, sol, rtol, max_iter);
     if (it < 0) return false;
@@ -234,7 +249,7 @@ bool compute_direction(regot_ctx* ctx, SolverWS& W, const regot_sparse& A, const
     bool woodbury = false;
     if (R.active) {
         const DVec* xs[5] = {&u, &u, &v, &u, &v};
-        const DVec* ys[5] = {&W.au, &av, &av, &W.ag, &W.ag};
+        const DVec* ys[5] = {&D.au, &av, &av, &D.ag, &D.ag};
         double r[5];
         vec_dots(ctx, st, ctx->comm, W.dots, 5, xs, ys, r);
         const double k11 = 1.0 / R.xi + r[0], k12 = r[1], k22 = 1.0 / R.zeta + r[2];
@@ -244,15 +259,15 @@ bool compute_direction(regot_ctx* ctx, SolverWS& W, const regot_sparse& A, const
             const double t1 = r[3], t2 = r[4];
             const double z1 = (k22 * t1 - k12 * t2) / det;
             const double z2 = (-k12 * t1 + k11 * t2) / det;
-            vec_lincomb(ctx, st, -1.0, W.ag, z1, &W.au, z2, &av, d);  // d = -(ag - au z1 - av z2)
+            vec_lincomb(ctx, st, -1.0, D.ag, z1, &D.au, z2, &av, d);  // d = -(ag - au z1 - av z2)
             woodbury = true;
         }
     }
-    if (!woodbury) vec_lincomb(ctx, st, -1.0, W.ag, 0.0, nullptr, 0.0, nullptr, d);
+    if (!woodbury) vec_lincomb(ctx, st, -1.0, D.ag, 0.0, nullptr, 0.0, nullptr, d);
     g_dot_d = dot1(ctx, W, g, d);
     if (g_dot_d < 0.0) return true;
     if (woodbury) {
-        vec_lincomb(ctx, st, -1.0, W.ag, 0.0, nullptr, 0.0, nullptr, d);
+        vec_lincomb(ctx, st, -1.0, D.ag, 0.0, nullptr, 0.0, nullptr, d);
         g_dot_d = dot1(ctx, W, g, d);
         if (g_dot_d < 0.0) return true;
     }
@@ -270,10 +285,8 @@ struct LsOut {
 // rotating device slots; only (f, phi') come back to the host per evaluation.
 struct LineSearch {
     regot_ctx* ctx;
-    SolverWS& W;
-    SolveOut& stats;
-    DVec tx[3];
-    GradOut tg[3];
+    SplrStateDev& S;
+    SolveOut* stats;
     bool used[3] = {false, false, false};
 
     int grab()
@@ -300,10 +313,10 @@ struct LineSearch {
             Trial e;
             e.gamma = gamma;
             e.slot = grab();
-            vec_axpy(ctx, ctx->stream, gamma, x0, d, tx[e.slot]);
-            gradient_sync(ctx, ctx->stream, ctx->ws_main, ctx->comm, tx[e.slot], &d, tg[e.slot], &stats);
-            e.f = tg[e.slot].sc.f;
-            e.dphi = tg[e.slot].sc.g_dot_d;
+            vec_axpy(ctx, ctx->stream, gamma, x0, d, S.tx[e.slot]);
+            gradient_sync(ctx, ctx->stream, ctx->ws_main, ctx->comm, S.tx[e.slot], &d, S.tg[e.slot], stats);
+            e.f = S.tg[e.slot].sc.f;
+            e.dphi = S.tg[e.slot].sc.g_dot_d;
             ++evals;
             return e;
         };
@@ -391,7 +404,204 @@ bool compute_direction_api(regot_ctx* ctx, const regot_sparse& A, const DVec& g,
     R.xi = xi;
     R.zeta = zeta;
     double gd = 0.0;
-    return compute_direction(ctx, solver_ws(ctx), A, g, g_sqnorm, R, u, v, rtol, max_iter, d, gd, cg_iters);
+    SolverWS& W = solver_ws(ctx);
+    return compute_direction(ctx, W, DirScratch{W.ag, W.au, W.av}, A, g, g_sqnorm, R, u, v, rtol, max_iter, d, gd, cg_iters);
+}
+
+// ---- splr_init (splr.h:326-334) ------------------------------------------------------------------
+void splr_init_state(regot_ctx* ctx, const double* alpha0, const double* beta0, SplrStateDev& S, SolveOut* stats)
+{
+    ctx_require_problem(ctx);
+    upload_dual(ctx, alpha0, beta0, S.x, true, "splr_init");
+    reset_sinkhorn_flag(ctx, ctx->stream, ctx->ws_main);
+    reset_sinkhorn_flag(ctx, ctx->side, ctx->ws_side);
+    gradient_sync(ctx, ctx->stream, ctx->ws_main, ctx->comm, S.x, nullptr, S.cur, stats);
+    S.has_prev = false;
+    S.iter = 0;
+}
+
+// ---- splr_step (splr.h:348-478) -------------------------------------------------------------------
+void splr_step_state(regot_ctx* ctx, SplrStateDev& S, const regot_splr_config& cfg, regot_step_record& rec, SolveOut* stats)
+{
+    const DeviceProblem& pr = ctx->prob;
+    SolverWS& W = solver_ws(ctx);
+    cudaStream_t st = ctx->stream;
+    SolveOut scratch_stats;
+    SolveOut& out = stats ? *stats : scratch_stats;
+    SectionTimer local_sect(st);
+    SectionTimer& sect = g_sect ? *g_sect : local_sect;
+    sect.start();
+
+    std::memset(&rec, 0, sizeof(rec));
+    rec.f_cand_sinkhorn = std::numeric_limits<double>::quiet_NaN();
+    const double cg_rtol = cfg.cg_rtol > 0.0 ? cfg.cg_rtol : kDefaultCgRtol;
+    const long dim = (long)pr.n + pr.m - 1;
+    const int cg_max = cfg.cg_max_iter > 0 ? cfg.cg_max_iter : (int)std::min<long>(20 * dim, 200000);
+
+    const long k = S.iter;
+    const bool refresh = (k % cfg.S == 0);
+    double tau = std::min(cfg.tau_max, std::sqrt(S.cur.sc.grad_sqnorm));  // splr.h:353
+    bool have_s = false;
+    std::function<void(bool)> run_chain;
+    std::function<void()> join_chain;
+
+    if (refresh) {
+        // candidate chain from the same snapshot (splr.h:366-372): J Sinkhorn steps, then a gradient pass; on
+        // the side stream when cfg.overlap is set (splr.h:373-378).  By default the steps are the
+        // log-sum-exp kernels: the hybrid trajectory is sensitive to the last bits of the
+        // candidate (a rounding-level change flips synth1-diff 64^2 between a 61- and a
+        // 71-iteration path), and the LSE form rounds like the reference's.  With
+        // REGOT_B200_FAST_CHAIN=1 they take the gradient-sweep form (3 % faster on config B); a
+        // step that left its safe range is reported with the gradient pass's scalars and the
+        // chain is redone with the log-sum-exp kernels.
+        cudaStream_t cs = cfg.overlap ? ctx->side : st;
+        ncclComm* ccomm = cfg.overlap ? ctx->comm_side : ctx->comm;
+        run_chain = [&, cs, ccomm](bool fast) {
+            SweepWS& w = cfg.overlap ? ctx->ws_side : ctx->ws_main;
+            S.xs.ensure(pr.nloc, pr.m);
+            RG_CUDA(cudaMemcpyAsync(S.xs.a.p, S.x.a.p, sizeof(double) * (size_t)pr.nloc, cudaMemcpyDeviceToDevice, cs));
+            RG_CUDA(cudaMemcpyAsync(S.xs.b.p, S.x.b.p, sizeof(double) * (size_t)pr.m, cudaMemcpyDeviceToDevice, cs));
+            for (long j = 0; j < cfg.J; ++j) {
+                if (fast) launch_sinkhorn_step_fast(ctx, cs, w, ccomm, S.xs.a.p, S.xs.b.p);
+                else launch_sinkhorn_step(ctx, cs, w, ccomm, S.xs.a.p, S.xs.b.p);
+            }
+            out.lse_passes += 2 * cfg.J;
+            launch_gradient(ctx, cs, w, ccomm, S.xs.a.p, S.xs.b.p, nullptr, nullptr, S.cand);
+            ++out.gradient_passes;
+        };
+        auto finish_chain = [&, cs]() {
+            SweepWS& w = cfg.overlap ? ctx->ws_side : ctx->ws_main;
+            sync_scalars(ctx, cs, w, S.cand);
+            if (S.cand.sc.lse_flag != 0.0) {
+                reset_sinkhorn_flag(ctx, cs, w);
+                run_chain(false);
+                sync_scalars(ctx, cs, w, S.cand);
+            }
+        };
+        // Without a side stream the chain is enqueued in the middle of the refresh, behind the selection
+        // sweeps: it does not depend on the pattern, and it keeps the GPU busy while the host turns the
+        // pattern's pointer arrays into line lists and the PCG schedule.  Same kernels, same order of
+        // arithmetic, same results.
+        bool chain_started = false;
+        if (cfg.J > 0 && !cfg.overlap && !ctx->profiling)
+            W.sparse.after_pointer_download = [&]() {
+                run_chain(ctx->fast_sinkhorn_chain);
+                chain_started = true;
+            };
+        // plan + select_topk + assemble (splr.h:361-364); T is never materialised
+        try {
+            ProfScope prof(ctx, st, 6);  // the whole pattern refresh: sweeps, selection, structure, host work
+            topk_build_pattern(ctx, st, W.sparse, kFromDual, S.x.a.p, S.x.b.p,
+                               regot_b200_topk_budget(pr.n, pr.m, cfg.density), S.A);
+        } catch (...) {
+            W.sparse.after_pointer_download = nullptr;
+            throw;
+        }
+        W.sparse.after_pointer_download = nullptr;
+        out.gradient_passes += 3;  // three sweeps over M
+        sparse_fill_values(ctx, st, S.A, S.x.a.p, S.x.b.p, tau, S.cur.sums.a.p, S.cur.sums.b.p);
+        sect.tick(0);
+        if (cfg.J > 0) {
+            if (cfg.overlap) {
+                RG_CUDA(cudaEventRecord(ctx->ev_fork, st));
+                RG_CUDA(cudaStreamWaitEvent(cs, ctx->ev_fork, 0));
+            }
+            if (!chain_started) run_chain(ctx->fast_sinkhorn_chain);
+            if (!cfg.overlap) finish_chain();
+            else join_chain = finish_chain;
+            have_s = true;
+        }
+        sect.tick(1);
+    } else {
+        if (S.A.ctx != ctx || S.A.n != pr.n || S.A.m != pr.m || S.A.nloc != pr.nloc)
+            raise(REGOT_E_STRUCTURE, "splr_step: the state holds no pattern for this problem");
+        sparse_fill_values(ctx, st, S.A, S.x.a.p, S.x.b.p, tau, S.cur.sums.a.p, S.cur.sums.b.p);  // update_values
+        sect.tick(2);
+    }
+
+    // direction; PCG breakdown plays the role of NotPositiveDefiniteError (splr.h:391-408)
+    int retries = 0, cg_iters = 0;
+    double g_dot_d = 0.0;
+    LowRankDev R;
+    try {
+        for (;;) {
+            R = build_low_rank(ctx, W, S);
+            sect.tick(3);
+            if (compute_direction(ctx, W, DirScratch{S.ag, S.au, S.av}, S.A, S.cur.g, S.cur.sc.grad_sqnorm, R, S.ydiff, S.v,
+                                  cg_rtol, cg_max, S.d, g_dot_d, cg_iters, &S.sdiff))
+                break;
+            if (retries >= 8) raise(REGOT_E_NOT_POSITIVE_DEFINITE, "pcg: matrix is not positive definite");
+            tau = (tau > 0.0) ? 2.0 * tau : 1e-8;
+            sparse_fill_values(ctx, st, S.A, S.x.a.p, S.x.b.p, tau, S.cur.sums.a.p, S.cur.sums.b.p);
+            ++retries;
+        }
+    } catch (...) {
+        if (have_s && cfg.overlap) cudaStreamSynchronize(ctx->side);  // the chain still writes into the state
+        throw;
+    }
+
+    sect.tick(4);
+    // Wolfe line search on the fused gradient (splr.h:414-436)
+    LsOut ls;
+    bool ls_failed = false;
+    LineSearch ls_engine{ctx, S, &out};
+    try {
+        ls = ls_engine.run(S.x, S.d, S.cur.sc.f, g_dot_d, cfg);
+    } catch (const Error& e) {
+        if (e.code != REGOT_E_LINE_SEARCH) {
+            if (have_s && cfg.overlap) cudaStreamSynchronize(ctx->side);
+            throw;
+        }
+        ls_failed = true;
+        ls.gamma = 0.0;
+        ls.g0_dot_d = g_dot_d;
+        ls.gnew_dot_d = g_dot_d;
+        ls.curvature_ok = false;
+        ls.evals = (int)cfg.max_ls_trials;
+        ls.slot = -1;
+    }
+    const double f_qn = ls_failed ? S.cur.sc.f : S.tg[ls.slot].sc.f;
+    sect.tick(5);
+
+    if (have_s && cfg.overlap) join_chain();  // join the side stream, then read its scalars
+    // hybrid selection, ties to the Sinkhorn candidate (splr.h:442-443)
+    const bool pick_s = have_s && std::isfinite(S.cand.sc.f) && (ls_failed || S.cand.sc.f <= f_qn);
+
+    rec.iter = k;
+    rec.refresh = refresh;
+    rec.sinkhorn_selected = pick_s;
+    rec.f_before = S.cur.sc.f;
+    rec.f_cand_qn = f_qn;
+    rec.f_cand_sinkhorn = have_s ? S.cand.sc.f : std::numeric_limits<double>::quiet_NaN();
+    rec.gamma = ls.gamma;
+    rec.g_dot_d = ls.g0_dot_d;
+    rec.gnew_dot_d = ls.gnew_dot_d;
+    rec.curvature_ok = ls.curvature_ok;
+    rec.ls_failed = ls_failed;
+    rec.lowrank_active = R.active;
+    rec.tau = tau;
+    rec.factor_retries = retries;
+    rec.ls_evals = ls.evals;
+    rec.cg_iters = cg_iters;
+
+    // rotate (x_prev, g_prev) <- (x, g) (splr.h:463-476)
+    S.x_prev.swap(S.x);
+    S.g_prev.swap(S.cur.g);
+    S.has_prev = true;
+    if (pick_s) {
+        S.x.swap(S.xs);
+        S.cur.swap(S.cand);
+    } else if (ls_failed) {
+        // zero step: x and its sums stay, only the gradient buffer was rotated away
+        vec_copy(ctx, st, S.x_prev, S.x);
+        vec_copy(ctx, st, S.g_prev, S.cur.g);
+    } else {
+        S.x.swap(S.tx[ls.slot]);
+        S.cur.swap(S.tg[ls.slot]);
+    }
+    rec.f_after = S.cur.sc.f;
+    S.iter = k + 1;
+    sect.tick(6);
 }
 
 // ---- run_splr (splr.h:487-534) -----------------------------------------------------------------
@@ -399,205 +609,44 @@ void solve_splr(regot_ctx* ctx, const double* alpha0, const double* beta0, const
 {
     validate_splr_config(cfg);
     ctx_require_problem(ctx);
-    const DeviceProblem& pr = ctx->prob;
     SolverWS& W = solver_ws(ctx);
+    SplrStateDev& S = W.splr;
     const int64_t launches0 = ctx->launches;
-    cudaStream_t st = ctx->stream;
-    upload_dual(ctx, alpha0, beta0, W.x, true, "run_splr");
+    // the gauge is checked before the clock starts, like check_dims (splr.h:491)
+    if (!alpha0 || !beta0) raise(REGOT_E_VALIDATION, "run_splr: null dual point");
+    if (beta0[ctx->prob.m - 1] != 0.0) raise(REGOT_E_VALIDATION, "run_splr: gauge violated, beta[m-1] must be 0");
     WallClock clk;
     Timer tm(ctx);
 
-    const double cg_rtol = cfg.cg_rtol > 0.0 ? cfg.cg_rtol : kDefaultCgRtol;
-    const long dim = (long)pr.n + pr.m - 1;
-    const int cg_max = cfg.cg_max_iter > 0 ? cfg.cg_max_iter : (int)std::min<long>(20 * dim, 200000);
+    splr_init_state(ctx, alpha0, beta0, S, &out);
+    append_row(out, 0, clk.ms(), S.cur.sc);
+    SectionTimer sect(ctx->stream);
+    struct SectScope {
+        explicit SectScope(SectionTimer* s) { g_sect = s; }
+        ~SectScope() { g_sect = nullptr; }
+    } sect_scope(&sect);
 
-    // splr_init (splr.h:326-334)
-    reset_sinkhorn_flag(ctx, st, ctx->ws_main);
-    reset_sinkhorn_flag(ctx, ctx->side, ctx->ws_side);
-    gradient_sync(ctx, st, ctx->ws_main, ctx->comm, W.x, nullptr, W.cur, &out);
-    bool has_prev = false;
-    long iter = 0;
-    append_row(out, 0, clk.ms(), W.cur.sc);
-    LineSearch ls_engine{ctx, W, out};
-    SectionTimer sect(st);
-
-    while (iter < cfg.max_iter) {
-        if (W.cur.sc.marginal_error <= cfg.tol) break;
+    while (S.iter < cfg.max_iter) {
+        if (S.cur.sc.marginal_error <= cfg.tol) break;
         regot_step_record rec;
-        std::memset(&rec, 0, sizeof(rec));
-        rec.f_cand_sinkhorn = std::numeric_limits<double>::quiet_NaN();
         try {
-            // ---------------- splr_step (splr.h:348-478) ----------------
-            const long k = iter;
-            const bool refresh = (k % cfg.S == 0);
-            double tau = std::min(cfg.tau_max, std::sqrt(W.cur.sc.grad_sqnorm));  // splr.h:353
-            bool have_s = false;
-            std::function<void(bool)> run_chain;
-            std::function<void()> join_chain;
-
-            if (refresh) {
-                // candidate chain from the same snapshot (splr.h:366-372): J Sinkhorn steps, then a gradient pass; on
-                // the side stream when cfg.overlap is set (splr.h:373-378).  By default the steps are the
-                // log-sum-exp kernels: the hybrid trajectory is sensitive to the last bits of the
-                // candidate (a rounding-level change flips synth1-diff 64^2 between a 61- and a
-                // 71-iteration path), and the LSE form rounds like the reference's.  With
-                // REGOT_B200_FAST_CHAIN=1 they take the gradient-sweep form (3 % faster on config B); a
-                // step that left its safe range is reported with the gradient pass's scalars and the
-                // chain is redone with the log-sum-exp kernels.
-                cudaStream_t cs = cfg.overlap ? ctx->side : st;
-                ncclComm* ccomm = cfg.overlap ? ctx->comm_side : ctx->comm;
-                run_chain = [&, cs, ccomm](bool fast) {
-                    SweepWS& w = cfg.overlap ? ctx->ws_side : ctx->ws_main;
-                    W.xs.ensure(pr.nloc, pr.m);
-                    RG_CUDA(cudaMemcpyAsync(W.xs.a.p, W.x.a.p, sizeof(double) * (size_t)pr.nloc, cudaMemcpyDeviceToDevice, cs));
-                    RG_CUDA(cudaMemcpyAsync(W.xs.b.p, W.x.b.p, sizeof(double) * (size_t)pr.m, cudaMemcpyDeviceToDevice, cs));
-                    for (long j = 0; j < cfg.J; ++j) {
-                        if (fast) launch_sinkhorn_step_fast(ctx, cs, w, ccomm, W.xs.a.p, W.xs.b.p);
-                        else launch_sinkhorn_step(ctx, cs, w, ccomm, W.xs.a.p, W.xs.b.p);
-                    }
-                    out.lse_passes += 2 * cfg.J;
-                    launch_gradient(ctx, cs, w, ccomm, W.xs.a.p, W.xs.b.p, nullptr, nullptr, W.cand);
-                    ++out.gradient_passes;
-                };
-                auto finish_chain = [&, cs]() {
-                    SweepWS& w = cfg.overlap ? ctx->ws_side : ctx->ws_main;
-                    sync_scalars(ctx, cs, w, W.cand);
-                    if (W.cand.sc.lse_flag != 0.0) {
-                        reset_sinkhorn_flag(ctx, cs, w);
-                        run_chain(false);
-                        sync_scalars(ctx, cs, w, W.cand);
-                    }
-                };
-                // Without a side stream the chain is enqueued in the middle of the refresh, behind the selection
-                // sweeps: it does not depend on the pattern, and it keeps the GPU busy while the host turns the
-                // pattern's pointer arrays into line lists and the PCG schedule.  Same kernels, same order of
-                // arithmetic, same results.
-                bool chain_started = false;
-                if (cfg.J > 0 && !cfg.overlap && !ctx->profiling)
-                    W.sparse.after_pointer_download = [&]() {
-                        run_chain(ctx->fast_sinkhorn_chain);
-                        chain_started = true;
-                    };
-                // plan + select_topk + assemble (splr.h:361-364); T is never materialised
-                try {
-                    ProfScope prof(ctx, st, 6);  // the whole pattern refresh: sweeps, selection, structure, host work
-                    topk_build_pattern(ctx, st, W.sparse, kFromDual, W.x.a.p, W.x.b.p,
-                                       regot_b200_topk_budget(pr.n, pr.m, cfg.density), W.A);
-                } catch (...) {
-                    W.sparse.after_pointer_download = nullptr;
-                    throw;
-                }
-                W.sparse.after_pointer_download = nullptr;
-                out.gradient_passes += 3;  // three sweeps over M
-                sparse_fill_values(ctx, st, W.A, W.x.a.p, W.x.b.p, tau, W.cur.sums.a.p, W.cur.sums.b.p);
-                sect.tick(0);
-                if (cfg.J > 0) {
-                    if (cfg.overlap) {
-                        RG_CUDA(cudaEventRecord(ctx->ev_fork, st));
-                        RG_CUDA(cudaStreamWaitEvent(cs, ctx->ev_fork, 0));
-                    }
-                    if (!chain_started) run_chain(ctx->fast_sinkhorn_chain);
-                    if (!cfg.overlap) finish_chain();
-                    else join_chain = finish_chain;
-                    have_s = true;
-                }
-                sect.tick(1);
-            } else {
-                sparse_fill_values(ctx, st, W.A, W.x.a.p, W.x.b.p, tau, W.cur.sums.a.p, W.cur.sums.b.p);  // update_values
-                sect.tick(2);
-            }
-
-            // direction; PCG breakdown plays the role of NotPositiveDefiniteError (splr.h:391-408)
-            int retries = 0, cg_iters = 0;
-            double g_dot_d = 0.0;
-            LowRankDev R;
-            for (;;) {
-                R = build_low_rank(ctx, W, has_prev);
-                sect.tick(3);
-                if (compute_direction(ctx, W, W.A, W.cur.g, W.cur.sc.grad_sqnorm, R, W.ydiff, W.v, cg_rtol, cg_max, W.d,
-                                      g_dot_d, cg_iters, &W.sdiff))
-                    break;
-                if (retries >= 8) raise(REGOT_E_NOT_POSITIVE_DEFINITE, "pcg: matrix is not positive definite");
-                tau = (tau > 0.0) ? 2.0 * tau : 1e-8;
-                sparse_fill_values(ctx, st, W.A, W.x.a.p, W.x.b.p, tau, W.cur.sums.a.p, W.cur.sums.b.p);
-                ++retries;
-            }
-
-            sect.tick(4);
-            // Wolfe line search on the fused gradient (splr.h:414-436)
-            LsOut ls;
-            bool ls_failed = false;
-            for (bool& u : ls_engine.used) u = false;
-            try {
-                ls = ls_engine.run(W.x, W.d, W.cur.sc.f, g_dot_d, cfg);
-            } catch (const Error& e) {
-                if (e.code != REGOT_E_LINE_SEARCH) throw;
-                ls_failed = true;
-                ls.gamma = 0.0;
-                ls.g0_dot_d = g_dot_d;
-                ls.gnew_dot_d = g_dot_d;
-                ls.curvature_ok = false;
-                ls.evals = (int)cfg.max_ls_trials;
-                ls.slot = -1;
-            }
-            const double f_qn = ls_failed ? W.cur.sc.f : ls_engine.tg[ls.slot].sc.f;
-            sect.tick(5);
-
-            if (have_s && cfg.overlap) join_chain();  // join the side stream, then read its scalars
-            // hybrid selection, ties to the Sinkhorn candidate (splr.h:442-443)
-            const bool pick_s = have_s && std::isfinite(W.cand.sc.f) && (ls_failed || W.cand.sc.f <= f_qn);
-
-            rec.iter = k;
-            rec.refresh = refresh;
-            rec.sinkhorn_selected = pick_s;
-            rec.f_before = W.cur.sc.f;
-            rec.f_cand_qn = f_qn;
-            rec.f_cand_sinkhorn = have_s ? W.cand.sc.f : std::numeric_limits<double>::quiet_NaN();
-            rec.gamma = ls.gamma;
-            rec.g_dot_d = ls.g0_dot_d;
-            rec.gnew_dot_d = ls.gnew_dot_d;
-            rec.curvature_ok = ls.curvature_ok;
-            rec.ls_failed = ls_failed;
-            rec.lowrank_active = R.active;
-            rec.tau = tau;
-            rec.factor_retries = retries;
-            rec.ls_evals = ls.evals;
-            rec.cg_iters = cg_iters;
-
-            // rotate (x_prev, g_prev) <- (x, g) (splr.h:463-476)
-            W.x_prev.swap(W.x);
-            W.g_prev.swap(W.cur.g);
-            has_prev = true;
-            if (pick_s) {
-                W.x.swap(W.xs);
-                W.cur.swap(W.cand);
-            } else if (ls_failed) {
-                // zero step: x and its sums stay, only the gradient buffer was rotated away
-                vec_copy(ctx, st, W.x_prev, W.x);
-                vec_copy(ctx, st, W.g_prev, W.cur.g);
-            } else {
-                W.x.swap(ls_engine.tx[ls.slot]);
-                W.cur.swap(ls_engine.tg[ls.slot]);
-            }
-            rec.f_after = W.cur.sc.f;
-            iter = k + 1;
-            sect.tick(6);
+            splr_step_state(ctx, S, cfg, rec, &out);
         } catch (const Error& e) {
             if (e.code == REGOT_E_CUDA || e.code == REGOT_E_NCCL || e.code == REGOT_E_NOMEM) throw;
             // StepError (splr.h:315-324, 520-525): partial trace, no point
             cudaStreamSynchronize(ctx->side);
             out.status = REGOT_E_STEP;
-            out.message = "run_splr: step " + std::to_string(iter) + " failed: " + e.what();
+            out.message = "run_splr: step " + std::to_string(S.iter) + " failed: " + e.what();
             out.device_ms = tm.stop();
             out.kernel_launches = ctx->launches - launches0;
             return;
         }
         out.steps.push_back(rec);
-        if (iter % cfg.record_every == 0 || iter == cfg.max_iter) append_row(out, iter, clk.ms(), W.cur.sc);
+        if (S.iter % cfg.record_every == 0 || S.iter == cfg.max_iter) append_row(out, S.iter, clk.ms(), S.cur.sc);
     }
-    if (out.trace.back().iter != iter) append_row(out, iter, clk.ms(), W.cur.sc);
+    if (out.trace.back().iter != S.iter) append_row(out, S.iter, clk.ms(), S.cur.sc);
     out.device_ms = tm.stop();
-    download_point(ctx, W.x, out);
+    download_point(ctx, S.x, out.alpha, out.beta);
     out.kernel_launches = ctx->launches - launches0;
 }
 

@@ -35,13 +35,29 @@ struct SolveOut {
     int64_t gradient_passes = 0, lse_passes = 0, kernel_launches = 0;
 };
 
+// SplrState (splr.h:82-97) on the device: the iterate and its gradient, the previous accepted iterate, the
+// frozen pattern with its matrix, plus the vectors one step works in (so a step allocates nothing).
+struct SplrStateDev {
+    DVec x, x_prev, g_prev;
+    GradOut cur;  // f, grad, row/col sums at x
+    bool has_prev = false;
+    regot_sparse A;  // H_Omega + tau I at the frozen pattern
+    long iter = 0;
+    // per-step scratch
+    DVec xs, d, sdiff, ydiff, v, ag, au, av;
+    GradOut cand;
+    DVec tx[3];  // line-search trial points and their gradients (three rotating slots)
+    GradOut tg[3];
+};
+
 // Everything the solvers keep on the device between calls.
 struct SolverWS {
-    DVec x, x_prev, g_prev, xs, d, trial, sdiff, ydiff, v, ag, au, av, tmp;
-    GradOut cur, cand, trial_g[2];
+    DVec x, x_prev;  // run_sinkhorn
+    GradOut cur;
+    DVec ag, au, av, d;  // stand-alone compute_direction
+    SplrStateDev splr;  // run_splr's state (splr_init / splr_step own theirs)
     DotScratch dots;
     SparseWS sparse;
-    regot_sparse A;  // H_Omega + tau I at the frozen pattern (SplrState::A)
 };
 
 SolverWS& solver_ws(regot_ctx* ctx);
@@ -49,6 +65,11 @@ SolverWS& solver_ws(regot_ctx* ctx);
 void solve_sinkhorn(regot_ctx* ctx, const double* alpha0, const double* beta0, const regot_sinkhorn_config& cfg,
                     SolveOut& out);
 void solve_splr(regot_ctx* ctx, const double* alpha0, const double* beta0, const regot_splr_config& cfg, SolveOut& out);
+// splr_init (splr.h:326-334) / splr_step (splr.h:348-478) on a caller-owned state; stats (nullable) counts passes
+void splr_init_state(regot_ctx* ctx, const double* alpha0, const double* beta0, SplrStateDev& S, SolveOut* stats);
+void splr_step_state(regot_ctx* ctx, SplrStateDev& S, const regot_splr_config& cfg, regot_step_record& rec, SolveOut* stats);
+// st.x to the host (alpha allgathered over the ranks when sharded)
+void download_point(regot_ctx* ctx, const DVec& x, std::vector<double>& alpha, std::vector<double>& beta);
 
 // compute_direction alone (regot_b200_compute_direction); false on PCG breakdown
 bool compute_direction_api(regot_ctx* ctx, const regot_sparse& A, const DVec& g, double g_sqnorm, bool active, double xi,

@@ -36,7 +36,8 @@ struct PcgSchedule {
 }  // namespace rg
 
 struct regot_sparse {
-    regot_ctx* ctx = nullptr;
+    regot_ctx* ctx = nullptr;  // owner; never dereferenced on the free path (the context may be gone by then)
+    int device = 0;
     int64_t n = 0, m = 0, nloc = 0, row_begin = 0;
     int64_t nnz = 0;  // |Omega| restricted to this rank's rows
     double tau = 0.0;

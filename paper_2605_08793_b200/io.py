@@ -8,8 +8,12 @@ the reference is read here (and vice versa) bit for bit.  Solves run on the GPU 
 from __future__ import annotations
 
 import math
+import os
+import queue
 import struct
+import threading
 import time
+from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass, field
 from typing import List, Optional, Sequence, Union
 
@@ -65,6 +69,13 @@ def load_problem(path: str) -> ProblemInstance:
         if n == 0 or m == 0 or n > _MAX_DIM or m > _MAX_DIM:
             raise FormatError("load_problem: implausible dimensions")
         (eta,) = struct.unpack("<d", take(8))
+        # a crafted or truncated header must not drive an allocation: compare the payload with what is left
+        try:
+            left = os.fstat(f.fileno()).st_size - f.tell()
+        except (OSError, AttributeError):
+            left = None
+        if left is not None and left < 8 * (n + m + n * m):
+            raise TruncationError("load_problem: truncated payload")
         a = np.frombuffer(take(8 * n), dtype="<f8").astype(np.float64)
         b = np.frombuffer(take(8 * m), dtype="<f8").astype(np.float64)
         M = np.frombuffer(take(8 * n * m), dtype="<f8").astype(np.float64).reshape(n, m)
@@ -235,6 +246,7 @@ class BenchSpec:
     checkpoints: List[int] = field(default_factory=lambda: [10, 20, 50, 100])
     repeats: int = 10
     warmup: int = 1
+    parallel_repeats: bool = False  # concurrent repeats; timings not comparable (bench.h:84)
 
     def validate(self) -> None:
         if self.repeats < 1:
@@ -268,6 +280,36 @@ def bench_solve(algo: str, p: ProblemInstance, splr_cfg: SplrConfig, iters: int,
     return s.run_splr(DualPoint.zeros(p.n, p.m), c).x
 
 
+_MAX_PARALLEL_CONTEXTS = 4
+_pool_lock = threading.Lock()
+
+
+def _context_pool(s, p: ProblemInstance, count: int):
+    """Extra device contexts of the same problem for concurrent repeats, cached on the primary solver."""
+    pool = getattr(s, "_bench_pool", None)
+    if pool is None:
+        pool = s._bench_pool = {"key": None, "free": queue.SimpleQueue(), "all": []}
+    key = (id(p), p.n, p.m, p.eta)
+    if pool["key"] != key:
+        for sv in pool["all"]:
+            sv.close()
+        pool.update(key=key, free=queue.SimpleQueue(), all=[])
+    while len(pool["all"]) < count:
+        sv = Solver(s.device)
+        sv.set_problem(p)
+        pool["all"].append(sv)
+        pool["free"].put(sv)
+    return pool
+
+
+def _with_context(pool, fn):
+    sv = pool["free"].get()
+    try:
+        return fn(sv)
+    finally:
+        pool["free"].put(sv)
+
+
 def run_benchmark(spec: BenchSpec, solver=None) -> BenchReport:
     """Per algorithm and checkpoint: `warmup` discarded runs, `repeats` timed runs of exactly that many
     iterations from x0 = 0, medians; a solver failure marks the cell failed (NaN) and the run goes on."""
@@ -283,12 +325,25 @@ def run_benchmark(spec: BenchSpec, solver=None) -> BenchReport:
             try:
                 for _ in range(spec.warmup):
                     bench_solve(algo, p, spec.splr, cp, s)
-                for _ in range(spec.repeats):
+
+                def one_repeat(sv):
                     t0 = time.perf_counter()
-                    x = bench_solve(algo, p, spec.splr, cp, s)
+                    x = bench_solve(algo, p, spec.splr, cp, sv)
                     wall = 1e3 * (time.perf_counter() - t0)
-                    g = s.fused_gradient(x)
-                    stat.samples.append(RepeatSample(wall, g.f, g.marginal_error, g.duality_gap))
+                    g = sv.fused_gradient(x)
+                    return RepeatSample(wall, g.f, g.marginal_error, g.duality_gap)
+
+                if spec.parallel_repeats:
+                    # property runs only (bench.h:203-211): the repeats run concurrently, one thread and one
+                    # device context each (entry points are re-entrant per handle); errors stay deterministic,
+                    # wall times reflect contention
+                    pool = _context_pool(s, p, min(spec.repeats, _MAX_PARALLEL_CONTEXTS))
+                    with ThreadPoolExecutor(max_workers=len(pool)) as ex:
+                        futs = [ex.submit(_with_context, pool, one_repeat) for _ in range(spec.repeats)]
+                        stat.samples.extend(f.result() for f in futs)
+                else:
+                    for _ in range(spec.repeats):
+                        stat.samples.append(one_repeat(s))
                 stat.wall_ms = median([q.wall_ms for q in stat.samples])
                 stat.f = median([q.f for q in stat.samples])
                 stat.marginal_error = median([q.marginal_error for q in stat.samples])
@@ -331,7 +386,7 @@ def _strtod(val: str) -> float:
 
 def parse_bench_spec(path: str) -> BenchSpec:
     """Flat `key = value` lines, `#` comments; same keys, defaults and errors as bench.h:509-586
-    (`parallel-repeats` is accepted and ignored: one GPU context runs its repeats in sequence)."""
+    (`parallel-repeats` runs the repeats from several threads, one device context each)."""
     try:
         with open(path, "r") as fh:
             lines = fh.read().split("\n")
@@ -375,7 +430,7 @@ def parse_bench_spec(path: str) -> BenchSpec:
         elif key == "overlap":
             spec.splr.overlap = val in ("1", "true")
         elif key == "parallel-repeats":
-            pass
+            spec.parallel_repeats = val in ("1", "true")
         else:
             raise ValidationError(f"parse_bench_spec: unknown key '{key}'")
     if not spec.algos:

@@ -11,13 +11,14 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import weakref
 from dataclasses import dataclass, field
 from typing import List, Optional, Sequence, Tuple
 
 import numpy as np
 
 from . import _lib
-from ._lib import GradientInfoC, ResultC, SinkhornConfigC, SplrConfigC
+from ._lib import GradientInfoC, ResultC, SinkhornConfigC, SplrConfigC, StepRecordC
 
 LAYOUT_COLMAJOR = 0
 LAYOUT_ROWMAJOR = 1
@@ -347,6 +348,24 @@ class SparsityPattern:
         return bool(row0.all() and col0.all())
 
 
+def _fingerprint(p: ProblemInstance) -> bytes:
+    """Cheap content hash of a ProblemInstance: both marginals and a strided sample of M (<= 64k entries), so
+    in-place edits of a resident instance are seen by Solver.ensure_problem."""
+    import hashlib
+
+    h = hashlib.blake2b(digest_size=16)
+    M = np.asarray(p.M)
+    h.update(repr((M.shape, M.strides, str(M.dtype))).encode())
+    h.update(np.ascontiguousarray(p.a, dtype=np.float64).tobytes())
+    h.update(np.ascontiguousarray(p.b, dtype=np.float64).tobytes())
+    flat = M.reshape(-1, order="A") if (M.flags.c_contiguous or M.flags.f_contiguous) else M.ravel()
+    step = max(1, flat.shape[0] // 65536)
+    h.update(np.ascontiguousarray(flat[::step]).tobytes())
+    if flat.shape[0]:
+        h.update(np.ascontiguousarray(flat[-1:]).tobytes())
+    return h.digest()
+
+
 def topk_budget(p: ProblemInstance, density: float) -> int:
     """splr.h:336-340."""
     return int(_lib.load().regot_b200_topk_budget(p.n, p.m, density))
@@ -363,14 +382,20 @@ class Solver:
         if st != 0:
             _raise(st, self._lib.regot_b200_last_error(None).decode())
         self._h = h
+        self.device = device
         self._problem_key = None
         self.n = self.m = 0
         self.row_begin = 0
         self.row_count = 0
         self.rank, self.world = 0, 1
+        self._sparse = weakref.WeakSet()  # live SparseSym handles: released before the context goes
 
     def close(self) -> None:
         if getattr(self, "_h", None):
+            for A in list(getattr(self, "_sparse", ())):
+                A.free()
+            for sv in (getattr(self, "_bench_pool", None) or {}).get("all", []):
+                sv.close()
             self._lib.regot_b200_destroy(self._h)
             self._h = None
 
@@ -425,7 +450,8 @@ class Solver:
             )
         self._check(st)
         self.n, self.m, self.row_begin, self.row_count = p.n, p.m, begin, count
-        self._problem_key = (id(p), p.eta, begin, count)
+        # the uploaded instance is held (a freed object's id() can be reused) together with a content fingerprint
+        self._problem_key = (p, p.n, p.m, p.eta, begin, count, _fingerprint(p))
 
     def set_pointcloud(self, X: np.ndarray, Y: np.ndarray, a, b, eta: float, on_the_fly: bool = False,
                        rows: Optional[Tuple[int, int]] = None) -> None:
@@ -476,7 +502,11 @@ class Solver:
         self._problem_key = None
 
     def ensure_problem(self, p: ProblemInstance) -> None:
-        if self._problem_key != (id(p), p.eta, self.row_begin, self.row_count) or self._problem_key is None:
+        """Upload p unless this very instance, unchanged, is the resident problem (the free functions below
+        call this on every invocation, like the reference passes `const ProblemInstance&`)."""
+        k = self._problem_key
+        if (k is None or k[0] is not p or k[1:6] != (p.n, p.m, p.eta, self.row_begin, self.row_count)
+                or k[6] != _fingerprint(p)):
             self.set_problem(p)
 
     def validate_problem(self) -> None:
@@ -524,6 +554,13 @@ class Solver:
         self._check(self._lib.regot_b200_sinkhorn_step(self._h, _ptr(al), _ptr(be)))
         return DualPoint(al, be)
 
+    @staticmethod
+    def _step_record(q) -> SplrStepRecord:
+        return SplrStepRecord(
+            q.iter, bool(q.refresh), bool(q.sinkhorn_selected), q.f_before, q.f_after, q.f_cand_sinkhorn,
+            q.f_cand_qn, q.gamma, q.g_dot_d, q.gnew_dot_d, bool(q.curvature_ok), bool(q.ls_failed),
+            bool(q.lowrank_active), q.tau, q.factor_retries, q.ls_evals, q.cg_iters)
+
     def _unpack(self, res: ResultC, want_steps: bool):
         trace = SolverTrace(res.algo.decode(), "", res.eta, res.config_hash.decode())
         for r in range(res.n_trace):
@@ -532,11 +569,7 @@ class Solver:
         steps = []
         if want_steps:
             for s in range(res.n_steps):
-                q = res.steps[s]
-                steps.append(SplrStepRecord(
-                    q.iter, bool(q.refresh), bool(q.sinkhorn_selected), q.f_before, q.f_after, q.f_cand_sinkhorn,
-                    q.f_cand_qn, q.gamma, q.g_dot_d, q.gnew_dot_d, bool(q.curvature_ok), bool(q.ls_failed),
-                    bool(q.lowrank_active), q.tau, q.factor_retries, q.ls_evals, q.cg_iters))
+                steps.append(self._step_record(res.steps[s]))
         x = None
         if res.alpha and res.beta:
             x = DualPoint(np.ctypeslib.as_array(res.alpha, (res.n,)).copy(),
@@ -570,6 +603,22 @@ class Solver:
             return SplrResult(x, trace, steps, stats)
         finally:
             self._lib.regot_b200_result_free(C.byref(res))
+
+    def splr_init(self, x0: DualPoint, cfg: SplrConfig) -> "SplrState":
+        """splr.h:326-334."""
+        al, be = self._dual(x0, "splr_init")
+        c = cfg._c()
+        h = C.c_void_p()
+        self._check(self._lib.regot_b200_splr_init(self._h, _ptr(al), _ptr(be), C.byref(c), C.byref(h)))
+        return SplrState(self, h)
+
+    def splr_step(self, st: "SplrState", cfg: SplrConfig) -> SplrStepRecord:
+        """splr.h:348-478: advances `st` in place (the reference moves the state through) and returns the record."""
+        st._live()
+        c = cfg._c()
+        rec = StepRecordC()
+        self._check(self._lib.regot_b200_splr_step(self._h, st._h, C.byref(c), C.byref(rec)))
+        return self._step_record(rec)
 
     # -- sparsification ---------------------------------------------------------------
     def select_topk(self, T: np.ndarray, k: int) -> SparsityPattern:
@@ -648,16 +697,25 @@ class SparseSym:
     def __init__(self, solver: Solver, handle):
         self._s = solver
         self._h = handle
+        solver._sparse.add(self)
+
+    def free(self) -> None:
+        if self._h:
+            self._s._lib.regot_b200_sparse_free(self._h)
+            self._h = None
 
     def __del__(self):
         try:
-            if self._h:
-                self._s._lib.regot_b200_sparse_free(self._h)
-                self._h = None
+            self.free()
         except Exception:
             pass
 
+    def _live(self):
+        if not self._h or not self._s._h:
+            raise ValidationError("SparseSym: the matrix or its solver was released")
+
     def info(self):
+        self._live()
         dim, nnz, nc, pid = C.c_int32(), C.c_int64(), C.c_int64(), C.c_uint64()
         self._s._check(self._s._lib.regot_b200_sparse_info(self._h, C.byref(dim), C.byref(nnz), C.byref(nc), C.byref(pid)))
         return dim.value, nnz.value, nc.value, pid.value
@@ -673,7 +731,21 @@ class SparseSym:
             self._s._h, self._h, _ptr(colptr), _ptr(rowidx), _ptr(values), _ptr(coords)))
         return colptr, rowidx, values, coords
 
+    def export_local(self):
+        """(coords, values) of this context's rows of the pattern: global (i, j) pairs in row-major order and
+        B_ij = T_ij / eta.  Works on row-sharded contexts (the ranks' pieces concatenate to the global pattern)."""
+        self._live()
+        cnt = C.c_int64(0)
+        self._s._check(self._s._lib.regot_b200_sparse_export_local(self._s._h, self._h, None, None, 0, C.byref(cnt)))
+        coords = np.zeros((cnt.value, 2), np.int32)
+        values = np.zeros(cnt.value)
+        if cnt.value:
+            self._s._check(self._s._lib.regot_b200_sparse_export_local(
+                self._s._h, self._h, _ptr(coords), _ptr(values), cnt.value, C.byref(cnt)))
+        return coords, values
+
     def update_values(self, x: DualPoint, tau: float, gr: Optional[GradientResult] = None) -> None:
+        self._live()
         al, be = self._s._dual(x, "update_values")
         if gr is None:
             gr = self._s.fused_gradient(x)
@@ -686,6 +758,74 @@ class SparseSym:
         y = np.zeros(dim)
         self._s._check(self._s._lib.regot_b200_matvec(self._s._h, self._h, _ptr(v), _ptr(y)))
         return y
+
+
+class SplrState:
+    """SplrState (splr.h:82-97), resident on the device."""
+
+    def __init__(self, solver: Solver, handle):
+        self._s = solver
+        self._h = handle
+        solver._sparse.add(self)  # released with the solver, like the matrices
+
+    def free(self) -> None:
+        if self._h:
+            self._s._lib.regot_b200_splr_state_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+    def _live(self):
+        if not self._h or not self._s._h:
+            raise ValidationError("SplrState: the state or its solver was released")
+
+    def _info(self):
+        self._live()
+        it, hp, info = C.c_int64(), C.c_int32(), GradientInfoC()
+        self._s._check(self._s._lib.regot_b200_splr_state_info(self._s._h, self._h, C.byref(it), C.byref(hp), C.byref(info)))
+        return it.value, bool(hp.value), info
+
+    @property
+    def iter(self) -> int:
+        return self._info()[0]
+
+    @property
+    def has_prev(self) -> bool:
+        return self._info()[1]
+
+    @property
+    def x(self) -> DualPoint:
+        self._live()
+        al, be = np.zeros(self._s.n), np.zeros(self._s.m)
+        self._s._check(self._s._lib.regot_b200_splr_state_point(self._s._h, self._h, _ptr(al), _ptr(be), None, None, None))
+        return DualPoint(al, be)
+
+    @property
+    def cur(self) -> GradientResult:
+        """GradientResult at st.x (on a sharded context: this rank's slice of the n-long arrays)."""
+        _, _, info = self._info()
+        s = self._s
+        grad, row, col = np.zeros(s.n + s.m - 1), np.zeros(s.n), np.zeros(s.m)
+        s._check(s._lib.regot_b200_splr_state_point(s._h, self._h, None, None, _ptr(grad), _ptr(row), _ptr(col)))
+        return GradientResult(info.f, grad, row, col, info.marginal_error, info.duality_gap, info.grad_norm2, info.total_mass)
+
+    @property
+    def A(self) -> Optional["SparseSym"]:
+        """st.A, borrowed: valid until the next refresh step."""
+        self._live()
+        h = self._s._lib.regot_b200_splr_state_matrix(self._h)
+        return _BorrowedSparse(self._s, C.c_void_p(h)) if h else None
+
+
+class _BorrowedSparse(SparseSym):
+    """A SparseSym owned by an SplrState: never freed from here."""
+
+    def free(self) -> None:
+        self._h = None
 
 
 # ---- free functions with the reference's signatures ------------------------------------------------
@@ -755,6 +895,19 @@ def run_sinkhorn(x0: DualPoint, p: ProblemInstance, cfg: SinkhornConfig) -> Sink
 def run_splr(x0: DualPoint, p: ProblemInstance, cfg: SplrConfig) -> SplrResult:
     """splr.h:487-534."""
     return _bound(p).run_splr(x0, cfg)
+
+
+def splr_init(x0: DualPoint, p: ProblemInstance, cfg: SplrConfig) -> SplrState:
+    """splr.h:326-334."""
+    return _bound(p).splr_init(x0, cfg)
+
+
+def splr_step(st: SplrState, p: ProblemInstance, cfg: SplrConfig) -> Tuple[SplrState, SplrStepRecord]:
+    """splr.h:348-478: `st = splr_step(std::move(st), p, cfg, &rec)` -- the state comes back with the record."""
+    s = _bound(p)
+    if st._s is not s:
+        raise ValidationError("splr_step: the state belongs to another solver")
+    return st, s.splr_step(st, cfg)
 
 
 def select_topk(T: np.ndarray, k: int) -> SparsityPattern:

@@ -1,18 +1,25 @@
 #!/usr/bin/env python
 """bench.py -- headline benchmark of the B200-native entropic-OT dual solver.
 
-Metric (BASELINE.json): time to marginal error <= 1e-8 (seconds per solve), plus the
-fused-gradient kernel's achieved HBM GB/s as the roofline.  Workload at every N: config B --
-n = m = 10,000 image-histogram OT (100 x 100 pixel grids), eta = 0.001, reference defaults
-(SplrConfig{}: S=10, J=5, density=0.01, tol=1e-8), x0 = 0.  At N > 1 the same problem is
-row-sharded over the ranks (strong scaling; NCCL allreduce of column sums / scalars).
+Metric (BASELINE.json): time to marginal error <= 1e-8 (seconds per solve), plus the fused-gradient
+kernel's achieved HBM GB/s as the roofline.
+
+Workload at EVERY N: BASELINE config D -- n = m = 50,000 Gaussian-mixture clouds in R^10 (3- and 4-component,
+Rng seed 21), squared-Euclidean cost normalised by its maximum (20 GB of fp64, resident in HBM), uniform
+marginals, eta = 0.001, reference defaults (SplrConfig{}: S=10, J=5, density=0.01, tol=1e-8), x0 = 0.  It is the
+largest configuration of the metric's range (n = m = 1e4 .. 5e4) that fits one GPU and the one north_star shards:
+at N > 1 rank r owns rows [n r / N, n (r+1) / N) (strong scaling; NCCL allreduce of column sums / scalars / B't).
+At N = 1 the line also carries, as secondary blocks measured the same way, config B (n = m = 10,000 image
+histograms, eta = 0.001: round 1's workload) and config A (n = m = 1000, eta = 0.01: the one size at which the
+reference's CPU code completes a full solve, so GPU and CPU are both MEASURED there).
 
     python bench.py --gpus N --steps K --warmup W            # our arm (one JSON line)
     python bench.py --impl reference --gpus N --steps K ...   # the reference's CPU path
 
-A "step" is one full run_splr solve from x0 = 0 to tolerance.  `value` times K solves with
-the problem already resident in HBM (CUDA events, max over ranks); `e2e` times the public
-C-ABI call sequence from pinned HOST buffers (upload + solve + result download).
+A "step" is one full run_splr solve from x0 = 0 to tolerance.  `value` times K solves with the problem already
+resident in HBM (CUDA events, max over ranks); `e2e` times the reference-facing call sequence from pinned HOST
+buffers: the dense cost block (what the reference's ProblemInstance holds) is uploaded, the solve runs, the dual
+point and trace come back.
 """
 from __future__ import annotations
 
@@ -29,11 +36,25 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-SIDE = 100  # config B: 100 x 100 grids -> n = m = 10,000
-ETA = 0.001
 TOL = 1e-8
-WORKLOAD = ("B: n=m=10000 image-histogram OT (100x100 grids, 3-blob marginals), eta=0.001, "
-            "SplrConfig defaults (S=10,J=5,density=0.01), x0=0, solve to marginal error<=1e-8")
+D_N = D_M = 50000
+D_DIM, D_SEED, D_ETA = 10, 21, 0.001
+WORKLOAD = ("D: n=m=50000 Gaussian-mixture clouds in R^10 (seed 21), squared-Euclidean cost / max (20 GB fp64 resident in "
+            "HBM), uniform marginals, eta=0.001, SplrConfig defaults (S=10,J=5,density=0.01), x0=0, solve to marginal "
+            "error<=1e-8")
+WORKLOAD_B = ("B: n=m=10000 image-histogram OT (100x100 grids, 3-blob marginals), eta=0.001, SplrConfig defaults, x0=0, "
+              "solve to marginal error<=1e-8")
+WORKLOAD_A = "A: n=m=1000 Gaussian clouds in R^2 (gen_synthetic1 iid, seed 7), eta=0.01, SplrConfig defaults, x0=0"
+
+# ONE pass-count model for every CPU estimate of config D (both arms use these constants): the reference's CPU
+# code cannot run D (dense T 20 GB + 40 GB of top-k scratch + Cholesky fill), so its time-to-tolerance is
+# ESTIMATED as passes x measured time per pass.  Counts of the device solve at D recorded on a B200
+# (profiles/r02_configs.txt): 62 iterations, 151 line-search evaluations, 7 refreshes.  In the reference
+# (splr.h:348-478) that is 1 + 151 gradient passes + per refresh one plan() pass and one candidate gradient
+# pass, and J = 5 Sinkhorn steps per refresh.
+PASS_MODEL_D = {"iterations": 62, "ls_evals": 151, "refreshes": 7,
+                "gradient_passes": 1 + 151 + 2 * 7, "sinkhorn_steps": 5 * 7}
+CPU_SAMPLE_ROWS = 2000  # rows of config D's cost matrix the CPU legs time (2000 x 50000 = 1e8 entries = config B's size)
 
 
 # ---- clocks -----------------------------------------------------------------------------------------
@@ -89,82 +110,140 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-# ---- the reference arm: CPU oracle on the host cores ---------------------------------------------------
-def cpu_sample(oracle, prob, reps: int = 1):
-    """Bounded sample of the workload on the CPU: fused-gradient passes and one Sinkhorn step of the
-    reference algorithm on the full config-B matrix, plus the pass structure of a complete solve
-    counted on a reduced instance (the full CPU solve is infeasible: dense T + sparse Cholesky)."""
-    n, m = prob["n"], prob["m"]
-    al, be = np.zeros(n), np.zeros(m)
-    t_grad = oracle.time_gradient(prob, al, be, reps)
+# ---- CPU legs (the oracle is the checker/baseline here, never the product path) ---------------------------
+def load_cpu():
+    """(oracle, kind): the reference's own headers compiled over the Eigen stand-in (oracle/_ref) when built, else
+    the restatement (bitwise identical to it, tests/test_ref_vs_oracle_cpu.py)."""
+    from tests import oracle_lib
+
+    port = oracle_lib.load()
+    ref = oracle_lib.load_ref()
+    return (ref, "reference") if ref is not None else (port, "port")
+
+
+def d_sample_block():
+    """CPU_SAMPLE_ROWS rows of config D's cost matrix (normalised by the block's own maximum: timing only)."""
+    from paper_2605_08793_b200 import problems
+
+    X, Y = problems.gen_gmm_points(CPU_SAMPLE_ROWS, D_M, D_DIM, D_SEED)
+    M = problems.sqeuclid_cost(X, Y)
+    M /= M.max()
+    return dict(n=CPU_SAMPLE_ROWS, m=D_M, M=np.asfortranarray(M), a=np.full(CPU_SAMPLE_ROWS, 1.0 / CPU_SAMPLE_ROWS),
+                b=np.full(D_M, 1.0 / D_M), eta=D_ETA)
+
+
+def cpu_sample(oracle, blk):
+    """One fused_gradient pass and one sinkhorn_step of the reference algorithm on the sample block (seconds)."""
+    al, be = np.zeros(blk["n"]), np.zeros(blk["m"])
+    t_grad = oracle.time_gradient(blk, al, be, 1)
     t0 = time.perf_counter()
-    oracle.sinkhorn_step(prob, al, be)
-    t_sink = time.perf_counter() - t0
-    return t_grad, t_sink
+    oracle.sinkhorn_step(blk, al, be)
+    return t_grad, time.perf_counter() - t0
 
 
-def reference_pass_structure(oracle, port):
-    """Gradient passes / Sinkhorn steps of one reference solve, counted by running the reference
-    algorithm (oracle restatement, sparse-Cholesky direction) to 1e-8 on the same generator at
-    n = m = 1024 (32 x 32 grids)."""
-    from paper_2605_08793_b200._lib import SplrConfigC
-    import ctypes as C
-    from paper_2605_08793_b200 import _lib
+def cpu_estimate_d(t_grad: float, t_sink: float) -> float:
+    scale = D_N / CPU_SAMPLE_ROWS
+    return scale * (PASS_MODEL_D["gradient_passes"] * t_grad + PASS_MODEL_D["sinkhorn_steps"] * t_sink)
 
-    small = port.gen_problem("image", 1024, 1024, ETA, d=32)  # config-B generator (not in the reference)
-    cfg = SplrConfigC()
-    _lib.load().regot_b200_splr_config_default(C.byref(cfg))
+
+def cpu_measured_a(oracle):
+    """A COMPLETE reference solve (run_splr to 1e-8, sparse-Cholesky direction) at config A, timed."""
+    import paper_2605_08793_b200 as rg  # value structs only: nothing here touches the CUDA library
+
+    from tests import oracle_lib
+
+    p = oracle_lib.load().gen_problem("synth1-iid", 1000, 1000, 0.01, d=2, seed=7)
+    cfg = rg.SplrConfig(tol=TOL)._c()
     t0 = time.perf_counter()
-    res = oracle.run_splr(small, np.zeros(1024), np.zeros(1024), cfg)
-    t_small = time.perf_counter() - t0
-    steps = res["steps"]
-    refreshes = sum(1 for s in steps if s["refresh"])
-    grad = 1 + sum(s["ls_evals"] for s in steps) + 2 * refreshes  # line search + plan() + candidate gradient
-    sink = 5 * refreshes
-    return {"iters": res["trace"][-1][0], "gradient_passes": grad, "sinkhorn_steps": sink,
-            "err": res["trace"][-1][3], "seconds_small": t_small}
+    res = oracle.run_splr(p, np.zeros(1000), np.zeros(1000), cfg)
+    sec = time.perf_counter() - t0
+    last = res["trace"][-1]
+    return {"seconds": sec, "iterations": last[0], "marginal_error": last[3],
+            "ls_evals": sum(s["ls_evals"] for s in res["steps"]), "measured": True}
 
 
 def run_reference(args, rank: int):
     if rank != 0:
         return
-    from tests import oracle_lib
-
-    # the reference's own code (oracle/_ref: its headers compiled over the Eigen stand-in) when it was
-    # built, else the restatement (bitwise identical to it, tests/test_ref_vs_oracle_cpu.py)
-    port = oracle_lib.load()
-    oracle = oracle_lib.load_ref() or port
-    kind = "reference" if oracle is not port else "port"
     t0 = time.time()
-    prob = port.gen_problem("image", SIDE * SIDE, SIDE * SIDE, ETA, d=SIDE)
-    structure = reference_pass_structure(oracle, port)
-    for _ in range(max(args.warmup, 0) and 1):
-        cpu_sample(oracle, prob)
-    samples = [cpu_sample(oracle, prob) for _ in range(args.steps)]
+    oracle, kind = load_cpu()
+    blk = d_sample_block()
+    for _ in range(1 if args.warmup > 0 else 0):
+        cpu_sample(oracle, blk)
+    samples = [cpu_sample(oracle, blk) for _ in range(args.steps)]
     t_grad = float(np.median([s[0] for s in samples]))
     t_sink = float(np.median([s[1] for s in samples]))
-    value = structure["gradient_passes"] * t_grad + structure["sinkhorn_steps"] * t_sink
-    sample = (f"per step: 1 fused_gradient pass ({t_grad:.3f} s) + 1 sinkhorn_step ({t_sink:.3f} s) of the CPU "
-              f"restatement on the full config-B matrix; time-to-tolerance extrapolated with the pass structure of a "
-              f"complete reference solve at n=m=1024 ({structure['iters']} iterations, {structure['gradient_passes']} "
-              f"gradient passes, {structure['sinkhorn_steps']} Sinkhorn steps); lower bound: dense plan(), top-k sort "
-              f"and sparse Cholesky at n=m=10000 are not included (they do not fit CPU time/memory)")
+    value = cpu_estimate_d(t_grad, t_sink)
+    a = cpu_measured_a(oracle)
+    sample = (f"ESTIMATE. Per step: 1 fused_gradient pass ({t_grad:.3f} s, {8e-9 * blk['n'] * blk['m'] / t_grad:.2f} GB/s) + 1 "
+              f"sinkhorn_step ({t_sink:.3f} s) of the reference CPU code on {CPU_SAMPLE_ROWS} of config D's 50000 rows; "
+              f"time-to-tolerance = (50000/{CPU_SAMPLE_ROWS}) x ({PASS_MODEL_D['gradient_passes']} gradient passes + "
+              f"{PASS_MODEL_D['sinkhorn_steps']} Sinkhorn steps), the pass counts of the device solve at D (bench.py "
+              f"PASS_MODEL_D); lower bound: the dense plan(), the top-k selection and the sparse Cholesky at dim 99,999 "
+              f"are not included and do not fit CPU memory/time.  The MEASURED pair is config A (measured_config_A).")
     line = {
-        "impl": "reference", "metric": "time_to_marginal_err_1e-8", "value": value, "unit": "s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * value,
+        "impl": "reference", "metric": "time_to_marginal_err_1e-8", "value": value, "value_kind": "estimated",
+        "unit": "s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * value,
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": WORKLOAD,
-                   "arm": ("the reference's own headers compiled over oracle/eigen_shim (oracle/_ref/libregot_ref.so)"
-                           if kind == "reference" else "CPU restatement of the reference (oracle/liboracle.so)")},
-        "cpu_baseline": {"value": value, "unit": "s", "cores": 1, "kind": kind, "sample": sample},
-        "e2e": {"value": value, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "fused_gradient_cpu_GBps": 8.0 * prob["n"] * prob["m"] / t_grad * 1e-9,
+                   "arm": ("the reference's own headers compiled over oracle/eigen_shim (oracle/_ref/libregot_ref.so), "
+                           "single thread (the reference is single-threaded)"
+                           if kind == "reference" else "CPU restatement of the reference (oracle/liboracle.so), single thread")},
+        "cpu_baseline": {"value": value, "value_kind": "estimated", "unit": "s", "cores": 1, "kind": kind, "sample": sample},
+        "e2e": {"value": value, "value_kind": "estimated", "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "measured_config_A": {"workload": WORKLOAD_A, "cpu_reference_s": a["seconds"], "iterations": a["iterations"],
+                              "marginal_error": a["marginal_error"], "ls_evals": a["ls_evals"], "cores": 1, "kind": kind},
+        "fused_gradient_cpu_GBps": 8.0 * blk["n"] * blk["m"] / t_grad * 1e-9,
         "wall_s": time.time() - t0,
     }
     print(json.dumps(line), flush=True)
 
 
 # ---- our arm ---------------------------------------------------------------------------------------------
+KINDS = ["fused_gradient_sweep", "row_lse", "col_lse", "topk_sweeps", "spmv", "pcg_persistent", "pattern_refresh",
+         "fused_gradient_whole_op"]
+
+
+def hbm_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy bandwidth)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def static_traffic(key: str):
+    """dram bytes per K1 launch from the committed `ncu --set full` capture (a profiler cannot run inside the bench)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "k1_traffic.json")) as f:
+            return json.load(f).get(key)
+    except (OSError, ValueError):
+        return None
+
+
+def profile_solve(solver, x0, cfg, nloc, m):
+    """One extra solve with per-kernel CUDA events: shares of the step and the K1 roofline figures."""
+    solver.set_profiling(True)
+    prof = solver.run_splr(x0, cfg)
+    shares = {}
+    for k, nm in enumerate(KINDS):
+        cnt, ms = solver.get_profile(k)
+        shares[nm] = {"launches": cnt, "total_ms": round(ms, 3), "avg_ms": round(ms / max(cnt, 1), 5)}
+    solver.set_profiling(False)
+    alg = 8.0 * nloc * m + 16.0 * (nloc + m)
+    sw, op = shares["fused_gradient_sweep"], shares["fused_gradient_whole_op"]
+    return prof, shares, alg, (alg / (sw["avg_ms"] * 1e-3) * 1e-9 if sw["launches"] else 0.0), \
+        (alg / (op["avg_ms"] * 1e-3) * 1e-9 if op["launches"] else 0.0)
+
+
+def check_converged(res, cfg, what):
+    last = res.trace.rows[-1]
+    if not (last.marginal_error <= TOL and last.iter < cfg.max_iter):
+        raise RuntimeError(f"{what}: the solve stopped at iteration {last.iter} with marginal error "
+                           f"{last.marginal_error:.3e} > {TOL}: a time-to-tolerance cannot be reported")
+    return last
+
+
 def run_ours(args, rank: int, world: int, local_rank: int):
     import torch
 
@@ -179,26 +258,6 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     torch.cuda.set_device(local_rank)
 
-    # ---- synthetic workload (host), this rank's row block in pinned memory ----
-    p = problems.gen_image(SIDE, ETA)
-    n, m = p.n, p.m
-    r0 = (n * rank) // world
-    r1 = (n * (rank + 1)) // world
-    nloc = r1 - r0
-    pinned = torch.empty((nloc, m), dtype=torch.float64).pin_memory()
-    Mblk = pinned.numpy()
-    Mblk[:] = p.M[r0:r1]
-    blockprob = rg.ProblemInstance(n, m, None, p.a, p.b, p.eta)
-
-    solver = rg.Solver(local_rank)
-    if world > 1:
-        ids = [rg.Solver.comm_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(ids, src=0)
-        solver.comm_init(rank, world, ids[0])
-
-    def upload():
-        solver.set_problem_block(blockprob, Mblk, r0, nloc)
-
     def barrier():
         torch.cuda.synchronize()
         if dist is not None:
@@ -211,10 +270,23 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    # ---- synthetic workload: config D clouds on the host, the cost block built on the device ----
+    n, m = D_N, D_M
+    X, Y = problems.gen_gmm_points(n, m, D_DIM, D_SEED)
+    a, b = np.full(n, 1.0 / n), np.full(m, 1.0 / m)
+    r0 = (n * rank) // world
+    nloc = (n * (rank + 1)) // world - r0
+
+    solver = rg.Solver(local_rank)
+    if world > 1:
+        ids = [rg.Solver.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(ids, src=0)
+        solver.comm_init(rank, world, ids[0])
+    rows = (r0, nloc) if world > 1 else None
+    solver.set_pointcloud(X, Y, a, b, D_ETA, on_the_fly=False, rows=rows)
+    solver.validate_problem()
     cfg = rg.SplrConfig(tol=TOL)
     x0 = rg.DualPoint.zeros(n, m)
-    upload()
-    solver.validate_problem()
 
     # ---- warm-up ----
     last = None
@@ -236,98 +308,179 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     region_s = time.perf_counter() - t_region
     gpu_launches = solver.launch_count - launches0
     clocks = sampler.stop() if sampler else None
+    final = check_converged(last, cfg, "config D")
     total_ms = max_over_ranks(float(np.sum(dev_ms)))
     ms_per_step = total_ms / args.steps
     value = ms_per_step / 1e3
 
-    # ---- timed region 2: end to end through the public API from pinned host buffers ----
+    # ---- timed region 2: end to end from pinned HOST buffers through the reference-facing calls ----
+    # The reference's ProblemInstance holds the dense cost matrix, so the host side holds this rank's block of it
+    # (fetched from the device once, outside the timed region) and every step uploads it again.
+    e2e = None
+    try:
+        pinned = torch.empty((nloc, m), dtype=torch.float64).pin_memory()
+        Mblk = pinned.numpy()
+        solver._check(solver._lib.regot_b200_get_cost(solver._h, Mblk.ctypes.data))
+        blockprob = rg.ProblemInstance(n, m, None, a, b, D_ETA)
+        barrier()
+        e2e_walls = []
+        for _ in range(args.steps):
+            barrier()
+            t0 = time.perf_counter()
+            solver.set_problem_block(blockprob, Mblk, r0, nloc)  # H2D of the cost block + marginals
+            res = solver.run_splr(x0, cfg)                        # uploads x0, downloads the dual point and trace
+            e2e_walls.append(time.perf_counter() - t0)
+        check_converged(res, cfg, "config D (e2e)")
+        e2e = {"value": max_over_ranks(float(np.mean(e2e_walls))), "unit": "s",
+               "h2d_bytes_per_step": 8 * nloc * m + 8 * (nloc + m) + 8 * (nloc + m),
+               "d2h_bytes_per_step": 8 * (n + m) + 40 * len(res.trace.rows) + 112 * len(res.steps),
+               "route": "dense host cost block (pinned) -> regot_b200_set_problem_rows -> regot_b200_run_splr"}
+        del pinned, Mblk
+    except (RuntimeError, MemoryError) as e:  # not enough pinnable host memory for 20 GB: say so, use the cloud route
+        e2e = {"dense_route_unavailable": str(e)[:200]}
+    # the same through the point-cloud entry (an extension: the cost is formed on the device, 8 MB cross the bus)
     barrier()
-    e2e_walls = []
-    for _ in range(args.steps):
+    pc_walls = []
+    for _ in range(max(2, args.steps // 2)):
         barrier()
         t0 = time.perf_counter()
-        upload()                              # H2D of this rank's cost block + marginals
-        res = solver.run_splr(x0, cfg)        # uploads x0, downloads the dual point and trace
-        e2e_walls.append(time.perf_counter() - t0)
-    e2e_s = max_over_ranks(float(np.mean(e2e_walls)))
-    h2d = 8 * nloc * m + 8 * (nloc + m) + 8 * (nloc + m)
-    d2h = 8 * (n + m) + 40 * len(res.trace.rows) + 112 * len(res.steps)
+        solver.set_pointcloud(X, Y, a, b, D_ETA, on_the_fly=False, rows=rows)
+        res = solver.run_splr(x0, cfg)
+        pc_walls.append(time.perf_counter() - t0)
+    pc = {"value": max_over_ranks(float(np.mean(pc_walls))), "unit": "s",
+          "h2d_bytes_per_step": 8 * (n + m) * D_DIM + 8 * (nloc + m) + 8 * (nloc + m),
+          "d2h_bytes_per_step": 8 * (n + m) + 40 * len(res.trace.rows) + 112 * len(res.steps),
+          "route": "host point clouds -> regot_b200_set_pointcloud(_rows) (cost block built on the device) -> regot_b200_run_splr"}
+    if "value" not in e2e:
+        e2e = {**pc, **e2e}
 
-    # ---- roofline of the dominant kernel (K1 fused gradient), measured inside a solve ----
-    solver.set_profiling(True)
-    prof = solver.run_splr(x0, cfg)
-    kinds = ["fused_gradient", "row_lse", "col_lse", "topk_sweeps", "spmv", "pcg_persistent"]
-    shares = {}
-    for k, nm in enumerate(kinds):
-        cnt, ms = solver.get_profile(k)
-        shares[nm] = {"launches": cnt, "total_ms": round(ms, 3), "avg_ms": round(ms / max(cnt, 1), 5)}
-    solver.set_profiling(False)
-    k1 = shares["fused_gradient"]
-    alg_bytes = 8.0 * nloc * m + 16.0 * (nloc + m)
-    achieved = alg_bytes / (k1["avg_ms"] * 1e-3) * 1e-9 if k1["launches"] else 0.0
-    peak, peak_src = 6650.0, "fallback"
-    try:
-        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            peak, peak_src = float(json.load(f)["hbm_gbs"]), "measured"
-    except (OSError, KeyError, ValueError):
-        pass
-    traffic = None
-    try:
-        with open(os.path.join(ROOT, "profiles", "k1_traffic.json")) as f:
-            traffic = json.load(f).get("dram_bytes_per_launch_configB")
-        if world > 1 and traffic is not None:
-            traffic = None  # the capture is for the unsharded block
-    except (OSError, ValueError):
-        pass
-    # K1 alone, back to back (the burst figure next to the in-solve average)
-    alone = solver.time_kernel(0, last.x, 10)
+    # ---- roofline of the dominant kernel class (K1 fused gradient), measured inside a solve ----
+    prof, shares, alg_bytes, ach_sweep, ach_op = profile_solve(solver, x0, cfg, nloc, m)
+    peak, peak_src = hbm_peak()
+    alone = solver.time_kernel(0, last.x, 5)
+    traffic = static_traffic("dram_bytes_per_launch_configD") if world == 1 else None
 
     if rank != 0:
         return
-
-    # ---- CPU baseline: the oracle restatement on this box's host cores (bounded sample) ----
-    cpu = None
-    if world == 1 and not args.no_cpu:
-        from tests import oracle_lib
-
-        port = oracle_lib.load()
-        oracle = oracle_lib.load_ref() or port
-        cpu_kind = "reference" if oracle is not port else "port"
-        oprob = dict(n=n, m=m, M=np.asfortranarray(p.M), a=p.a, b=p.b, eta=p.eta)
-        t_grad, t_sink = cpu_sample(oracle, oprob)
-        est = prof.stats.gradient_passes * t_grad + (prof.stats.lse_passes / 2) * t_sink
-        cpu = {"value": est, "unit": "s", "cores": 1, "kind": cpu_kind,
-               "sample": (f"1 fused_gradient pass ({t_grad:.3f} s, {8e-9 * n * m / t_grad:.2f} GB/s) + 1 sinkhorn_step "
-                          f"({t_sink:.3f} s) of the CPU oracle on the full config-B matrix, extrapolated to the "
-                          f"{prof.stats.gradient_passes} gradient-equivalent passes + {prof.stats.lse_passes // 2} Sinkhorn "
-                          f"steps this solve made; lower bound (no CPU top-k sort / sparse Cholesky)")}
-
-    final = last.trace.rows[-1]
     line = {
         "metric": "time_to_marginal_err_1e-8", "value": value, "unit": "s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": WORKLOAD, "parallelism": f"row-sharded x{world}" if world > 1 else "single GPU",
-                   "l2": "cost matrix (0.8 GB) larger than L2 (126 MB); streamed with an evict-first policy",
+                   "l2": "cost block (20 GB / N) far larger than L2 (126 MB); streamed with an evict-first policy",
                    "solver": "run_splr via C ABI (libregot_b200.so), library defaults (Schur-complement PCG direction, rtol 1e-10)"},
         "solve": {"iterations": final.iter, "marginal_error": final.marginal_error, "f": final.f,
                   "gradient_passes": last.stats.gradient_passes, "lse_passes": last.stats.lse_passes,
                   "cg_iters": sum(s.cg_iters for s in last.steps), "ls_evals": sum(s.ls_evals for s in last.steps),
-                  "per_iteration_ms": ms_per_step / max(final.iter, 1), "wall_ms_per_step": 1e3 * float(np.mean(walls))},
-        "roofline": {"bound": "hbm", "kernel": "k_gradient_sweep (K1 fused dual gradient)", "achieved": achieved,
-                     "peak": peak, "peak_source": f"{peak_src} HBM copy bandwidth", "unit": "GB/s", "frac": achieved / peak,
-                     "frac_of_8TBps_spec": achieved / 8000.0, "traffic": traffic,
-                     "algorithmic_bytes_per_launch": alg_bytes, "avg_launch_ms_in_solve": k1["avg_ms"],
+                  "refreshes": sum(1 for s in last.steps if s.refresh),
+                  "per_iteration_ms": ms_per_step / max(final.iter, 1), "wall_ms_per_step": 1e3 * float(np.mean(walls)),
+                  "hbm_frac_whole_step": (last.stats.gradient_passes + last.stats.lse_passes) * alg_bytes / (value * 1e9) / peak},
+        "roofline": {"bound": "hbm", "kernel": "k_gradient_sweep (K1 fused dual gradient)", "achieved": ach_sweep,
+                     "peak": peak, "peak_source": peak_src, "unit": "GB/s", "frac": ach_sweep / peak,
+                     "frac_of_8TBps_spec": ach_sweep / 8000.0,
+                     "whole_op": {"what": "fused_gradient = sweep + k_gradient_fin (+ allreduce)", "achieved": ach_op,
+                                  "frac": ach_op / peak, "avg_ms": shares["fused_gradient_whole_op"]["avg_ms"]},
+                     "traffic": traffic, "traffic_source": "static: ncu --set full capture, profiles/k1_traffic.json",
+                     "algorithmic_bytes_per_launch": alg_bytes,
+                     "avg_launch_ms_in_solve": shares["fused_gradient_sweep"]["avg_ms"],
                      "alone_GBps_median": alg_bytes / (float(np.median(alone)) * 1e-3) * 1e-9,
-                     "launches_timed": k1["launches"]},
+                     "launches_timed": shares["fused_gradient_sweep"]["launches"]},
         "kernel_shares_ms": shares,
-        "cpu_baseline": cpu,
-        "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "e2e": e2e,
+        "e2e_pointcloud": pc,
         "gpu_launches": gpu_launches,
         "clocks": clocks,
         "timed_region_wall_s": region_s,
     }
+
+    if world == 1:
+        line["secondary"] = {"B": secondary_b(solver, rg, problems, torch, args),
+                             "A": secondary_a(solver, rg, problems, args)}
+        line["cpu_baseline"] = None if args.no_cpu else cpu_baseline_leg(line, last)
     print(json.dumps(line), flush=True)
+
+
+def secondary_b(solver, rg, problems, torch, args):
+    """Config B (round 1's workload), measured like the headline: resident time, e2e from pinned host memory, K1."""
+    p = problems.gen_image(100, 0.001)
+    n, m = p.n, p.m
+    pinned = torch.empty((n, m), dtype=torch.float64).pin_memory()
+    Mblk = pinned.numpy()
+    Mblk[:] = p.M
+    blockprob = rg.ProblemInstance(n, m, None, p.a, p.b, p.eta)
+    solver.set_problem_block(blockprob, Mblk, 0, n)
+    cfg = rg.SplrConfig(tol=TOL)
+    x0 = rg.DualPoint.zeros(n, m)
+    for _ in range(max(3, args.warmup)):
+        res = solver.run_splr(x0, cfg)
+    dev = []
+    for _ in range(args.steps):
+        res = solver.run_splr(x0, cfg)
+        dev.append(res.stats.device_ms)
+    last = check_converged(res, cfg, "config B")
+    walls = []
+    for _ in range(args.steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        solver.set_problem_block(blockprob, Mblk, 0, n)
+        r2 = solver.run_splr(x0, cfg)
+        walls.append(time.perf_counter() - t0)
+    prof, shares, alg, ach_sweep, ach_op = profile_solve(solver, x0, cfg, n, m)
+    peak, _ = hbm_peak()
+    return {"workload": WORKLOAD_B, "value": float(np.mean(dev)) / 1e3, "unit": "s", "iterations": last.iter,
+            "marginal_error": last.marginal_error, "ls_evals": sum(s.ls_evals for s in res.steps),
+            "cg_iters": sum(s.cg_iters for s in res.steps),
+            "e2e": {"value": float(np.mean(walls)), "unit": "s", "h2d_bytes_per_step": 8 * n * m + 32 * (n + m),
+                    "d2h_bytes_per_step": 8 * (n + m) + 40 * len(r2.trace.rows) + 112 * len(r2.steps)},
+            "roofline": {"achieved": ach_sweep, "frac": ach_sweep / peak, "whole_op_achieved": ach_op,
+                         "whole_op_frac": ach_op / peak, "algorithmic_bytes_per_launch": alg,
+                         "traffic": static_traffic("dram_bytes_per_launch_configB"), "unit": "GB/s"},
+            "kernel_shares_ms": shares}
+
+
+def secondary_a(solver, rg, problems, args):
+    """Config A on the GPU (the CPU side of the pair is timed in cpu_baseline_leg / the reference arm)."""
+    p = problems.gen_synthetic1(1000, 1000, "iid", 2, 7, 0.01)
+    cfg = rg.SplrConfig(tol=TOL)
+    x0 = rg.DualPoint.zeros(p.n, p.m)
+    solver.set_problem(p)
+    for _ in range(3):
+        solver.run_splr(x0, cfg)
+    dev, walls = [], []
+    for _ in range(max(5, args.steps)):
+        t0 = time.perf_counter()
+        solver.set_problem(p)  # host buffers -> device inside the e2e region
+        res = solver.run_splr(x0, cfg)
+        walls.append(time.perf_counter() - t0)
+        dev.append(res.stats.device_ms)
+    last = check_converged(res, cfg, "config A")
+    return {"workload": WORKLOAD_A, "gpu_s": float(np.mean(dev)) / 1e3, "gpu_e2e_s": float(np.mean(walls)),
+            "iterations": last.iter, "marginal_error": last.marginal_error, "ls_evals": sum(s.ls_evals for s in res.steps),
+            "f": last.f}
+
+
+def cpu_baseline_leg(line, last):
+    """The reference's CPU path on this box's host cores, rank 0, N = 1: a bounded sample of config D (estimate,
+    the same pass model as the reference arm) and a MEASURED complete solve at config A."""
+    oracle, kind = load_cpu()
+    blk = d_sample_block()
+    t_grad, t_sink = cpu_sample(oracle, blk)
+    est = cpu_estimate_d(t_grad, t_sink)
+    a = cpu_measured_a(oracle)
+    sa = line["secondary"]["A"]
+    sa.update({"cpu_reference_s": a["seconds"], "cpu_iterations": a["iterations"], "cpu_ls_evals": a["ls_evals"],
+               "cpu_marginal_error": a["marginal_error"], "measured_speedup_device": a["seconds"] / sa["gpu_s"],
+               "measured_speedup_e2e": a["seconds"] / sa["gpu_e2e_s"]})
+    mine = {"ls_evals": sum(s.ls_evals for s in last.steps), "refreshes": sum(1 for s in last.steps if s.refresh),
+            "iterations": last.trace.rows[-1].iter}
+    return {"value": est, "value_kind": "estimated", "unit": "s", "cores": 1, "kind": kind,
+            "sample": (f"ESTIMATE for config D: 1 fused_gradient pass ({t_grad:.3f} s, {8e-9 * blk['n'] * blk['m'] / t_grad:.2f} GB/s) "
+                       f"+ 1 sinkhorn_step ({t_sink:.3f} s) of the reference CPU code on {CPU_SAMPLE_ROWS} of D's 50000 rows, scaled by "
+                       f"50000/{CPU_SAMPLE_ROWS} and by the pass model PASS_MODEL_D ({PASS_MODEL_D['gradient_passes']} gradient passes + "
+                       f"{PASS_MODEL_D['sinkhorn_steps']} Sinkhorn steps; this run made {mine}); lower bound (no CPU top-k / sparse "
+                       f"Cholesky at dim 99,999).  MEASURED pair: config A, complete CPU solve {a['seconds']:.2f} s "
+                       f"({a['iterations']} iterations) against {sa['gpu_s'] * 1e3:.1f} ms on the device (secondary.A)."),
+            "pass_model": PASS_MODEL_D, "this_run": mine}
 
 
 def main():
@@ -339,6 +492,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 0)
+    args.steps = max(args.steps, 1)
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))

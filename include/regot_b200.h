@@ -253,6 +253,8 @@ regot_status regot_b200_update_values(regot_ctx* ctx, regot_sparse* A, const dou
 regot_status regot_b200_matvec(regot_ctx* ctx, const regot_sparse* A, const double* v, double* y);
 /* Pattern and CSC export in the reference layout (sparsity.h:249-289):
  * alpha-column i = [diag, n+j ascending], beta-column n+j = [i ascending, diag]. */
+/* dim = n+m-1; nnz / ncoords count this context's rows; pattern_id is 0 on a row-sharded context (the id
+ * hashes the global structure). */
 regot_status regot_b200_sparse_info(const regot_sparse* A, int32_t* dim, int64_t* nnz, int64_t* ncoords,
                                     uint64_t* pattern_id);
 regot_status regot_b200_sparse_export(regot_ctx* ctx, const regot_sparse* A, int32_t* colptr, int32_t* rowidx,
@@ -325,7 +327,8 @@ regot_status regot_b200_time_kernel(regot_ctx* ctx, int which, const double* alp
                                     int iters, float* ms_out);
 /* Per-kernel device timing inside solves: when enabled every sweep / SpMV launch
  * is bracketed by CUDA events on its stream.  kind: 0 fused gradient (K1),
- * 1 row LSE (K7), 2 column LSE (K8), 3 top-k sweeps (K2), 4 SpMV (K4).
+ * 1 row LSE (K7), 2 column LSE (K8), 3 top-k sweeps (K2), 4 SpMV (K4), 5 persistent PCG solve (K5),
+ * 6 a whole pattern refresh, 7 a whole fused_gradient (K1 sweep + finalize kernels + allreduce).
  * set_profiling() also clears the recorded events. */
 regot_status regot_b200_set_profiling(regot_ctx* ctx, int enabled);
 regot_status regot_b200_get_profile(regot_ctx* ctx, int kind, int64_t* launches, double* total_ms);

@@ -442,7 +442,8 @@ regot_status regot_b200_sparse_info(const regot_sparse* A, int32_t* dim, int64_t
         if (dim) *dim = (int32_t)(A->n + A->m - 1);
         if (ncoords) *ncoords = A->nnz;
         if (nnz) *nnz = (A->n + A->m - 1) + 2 * A->nnz;
-        if (pattern_id) *pattern_id = export_csc(ctx, *A, false).pattern_id;
+        // the id hashes the GLOBAL structure (sparsity.h:160-166): a row-sharded context holds only its rows -> 0
+        if (pattern_id) *pattern_id = ctx->world == 1 ? export_csc(ctx, *A, false).pattern_id : 0;
     });
 }
 

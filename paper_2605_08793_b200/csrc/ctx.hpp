@@ -283,7 +283,8 @@ namespace rg {
 
 void ctx_require_problem(const regot_ctx* ctx);
 // kind: 0 gradient sweep (K1), 1 row LSE (K7), 2 column LSE (K8), 3 top-k sweeps (K2), 4 spmv (K4),
-// 5 persistent PCG solve (K5), 6 a whole pattern refresh (top-k sweeps + selection + structure, host gaps included)
+// 5 persistent PCG solve (K5), 6 a whole pattern refresh (top-k sweeps + selection + structure, host gaps included),
+// 7 a whole fused_gradient (K1 sweep + finalize kernels + allreduce)
 struct ProfScope {
     regot_ctx* ctx;
     cudaStream_t st;

@@ -411,6 +411,7 @@ void launch_gradient(regot_ctx* ctx, cudaStream_t st, SweepWS& ws, ncclComm* com
 {
     const DeviceProblem& pr = ctx->prob;
     out.ensure(pr.nloc, pr.m);
+    ProfScope prof_op(ctx, st, 7);  // the whole fused_gradient: sweep + both finalize kernels (+ the allreduce)
     launch_gradient_sweep_only(ctx, st, ws, alpha, beta);
 
     const int g1 = fin_grid(ctx, std::max<long>(pr.nloc, pr.m));

@@ -20,7 +20,7 @@ from typing import List, Optional, Sequence, Union
 import numpy as np
 
 from . import problems
-from .regot import (DualPoint, FormatError, IoError, ProblemInstance, RegotError, SinkhornConfig, SolverTrace,
+from .regot import (DualPoint, FormatError, IoError, ProblemInstance, RegotError, SinkhornConfig, Solver, SolverTrace,
                     SplrConfig, TraceRow, TruncationError, ValidationError, default_solver, splr_config_hash)
 
 ROTB_MAGIC = b"ROTB"

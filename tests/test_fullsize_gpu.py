@@ -53,6 +53,44 @@ def check_sinkhorn_properties(solver, a, b, x):
     return y
 
 
+def check_against_oracle(solver, oracle, p, x):
+    """One fused_gradient pass and one sinkhorn_step of the CPU oracle on the FULL matrix (a few seconds each)
+    against the device: sums, objective, gradient and the Sinkhorn update at the same point."""
+    op = dict(n=p.n, m=p.m, M=np.asfortranarray(p.M), a=p.a, b=p.b, eta=p.eta)
+    g = solver.fused_gradient(x)
+    ref = oracle.gradient(op, x.alpha, x.beta)
+    np.testing.assert_allclose(g.row_sums, ref["row"], rtol=1e-11)
+    np.testing.assert_allclose(g.col_sums, ref["col"], rtol=1e-11)
+    assert abs(g.f - ref["f"]) <= 1e-11 * (1 + abs(ref["f"]))
+    scale = max(np.abs(ref["row"]).max(), np.abs(ref["col"]).max())
+    np.testing.assert_allclose(g.grad, ref["grad"], rtol=0, atol=1e-11 * scale)
+    err = np.abs(ref["row"] - p.a).sum() + np.abs(ref["col"] - p.b).sum()
+    assert abs(g.marginal_error - err) <= 1e-11 * (1 + err)
+    y = solver.sinkhorn_step(x)
+    ra, rb = oracle.sinkhorn_step(op, x.alpha, x.beta)
+    np.testing.assert_allclose(y.alpha, ra, rtol=0, atol=1e-11)
+    np.testing.assert_allclose(y.beta, rb, rtol=0, atol=1e-11)
+    assert y.beta[-1] == 0.0 and rb[-1] == 0.0
+
+
+def test_config_b_oracle_parity_full_matrix(solver, oracle):
+    p = problems.gen_image(100, 0.001)
+    solver.set_problem(p)
+    x = rg.DualPoint.zeros(p.n, p.m)
+    for _ in range(3):
+        x = solver.sinkhorn_step(x)
+    check_against_oracle(solver, oracle, p, x)
+
+
+def test_config_c_oracle_parity_full_matrix(solver, oracle):
+    p = problems.gen_synthetic2(20000, 5000, 0.0005)
+    solver.set_problem(p)
+    x = rg.DualPoint.zeros(p.n, p.m)
+    for _ in range(2):
+        x = solver.sinkhorn_step(x)
+    check_against_oracle(solver, oracle, p, x)
+
+
 def test_config_b_full_size(solver):
     side, eta = 100, 0.001
     p = problems.gen_image(side, eta)

@@ -259,6 +259,10 @@ struct regot_ctx {
 
     // tests: run the sharded (multi-kernel + NCCL) PCG path on one GPU (REGOT_B200_MULTIKERNEL_PCG=1)
     bool force_multikernel_pcg = false;
+    // panel mat-vec of the kernel-by-kernel PCG (k4_sparse.cu): -1 auto (large patterns), 0 off, 1 always
+    // (REGOT_B200_PANEL_SPMV); panel_width > 0 caps the panel width in entries (REGOT_B200_PANEL_WIDTH, tests)
+    int panel_spmv = -1;
+    int panel_width = 0;
     // persistent PCG on one thread-block cluster when a CG iteration touches at most this many matrix entries
     // (REGOT_B200_PCG_CLUSTER = 0 | 8 | 16, REGOT_B200_PCG_CLUSTER_ENTRIES)
     int pcg_cluster_size = 0;

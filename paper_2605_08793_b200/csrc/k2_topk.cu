@@ -585,6 +585,7 @@ void pattern_from_coords(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, const in
 void finish_structure(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, regot_sparse& S)
 {
     const int nloc = (int)S.nloc, mm1 = (int)S.m - 1, nnz = (int)S.nnz;
+    ++S.structure_stamp;
     S.val.ensure((size_t)nnz + 1);
     S.cscval.ensure((size_t)nnz + 1);
     S.cscrow.ensure((size_t)nnz + 1);

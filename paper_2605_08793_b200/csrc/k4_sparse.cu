@@ -11,6 +11,8 @@
 #include "ctx.hpp"
 #include "sparse.hpp"
 
+#include <cub/cub.cuh>
+
 #include <algorithm>
 #include <cmath>
 
@@ -352,6 +354,305 @@ void sparse_matvec(regot_ctx* ctx, cudaStream_t st, ncclComm* comm, const regot_
     }
 }
 
+// ---- K4, panel form: the half mat-vecs of large patterns --------------------------------------------
+// k_spmv gathers its vector through L2: one 32-byte sector per matrix entry (44 B of L2 traffic per 12-byte
+// entry; config D: 1.1 GB per half mat-vec, 0.18 ms where the matrix itself streams from HBM in 0.05 ms).  Here the
+// gathered vector is cut into P panels of W entries (16 B each: two right-hand sides) that fit in shared memory
+// and the lines into Bk blocks per panel of equal work; CTA (p, b) copies panel p into shared memory ONCE
+// (coalesced) and processes, for the lines of its block, the entries whose index falls inside the panel -- a
+// contiguous piece of the line, since entries are sorted by index -- gathering from shared memory while the
+// matrix streams from HBM.  Each (line, panel) piece is summed by one entity in a fixed order (8 lanes, a warp
+// or the CTA, by length) into part[p][line]; k_panel_combine adds a line's P partials in panel order and
+// applies the epilogue.  No atomics on values: bitwise reproducible.
+constexpr int kPanelThreads = 1024;
+constexpr int kPanelWarps = kPanelThreads / 32;
+constexpr int kPanelMaxW = 12800;       // entries of the gathered vector per panel: 200 KB of shared memory
+constexpr int kPanelGroupMax = 256;     // pieces up to this many entries: 8 lanes
+constexpr int kPanelWarpMax = 8192;     // up to this many: one warp; longer: the whole CTA
+constexpr int kPanelDeferCap = 2048;    // deferred pieces per CTA kept in the shared-memory lists
+constexpr int kPanelLineCost = 24;      // work of a piece beyond its entries (pointer loads, reduction), in entries
+
+struct PanelArgs {
+    int P, Bk, W, nlines, ngather;
+    const int* ppt;
+    const int* blk;
+    const int* idx;     // col (row phase) or cscrow (column phase)
+    const double* val;  // val or cscval
+    const double* x;    // gathered vector, interleaved 4 doubles per index
+    double* part;       // P x nlines x 2
+};
+
+// first entry of line l whose index is >= p W, for p = 0..P (p = P: the end of the line)
+__global__ void k_panel_ptrs(int nlines, int P, int W, const int* __restrict__ ptr, const int* __restrict__ idx,
+                             int* __restrict__ ppt, int* __restrict__ cost)
+{
+    const long total = (long)nlines * (P + 1);
+    for (long q = (long)blockIdx.x * blockDim.x + threadIdx.x; q < total; q += (long)gridDim.x * blockDim.x) {
+        const int l = (int)(q / (P + 1)), p = (int)(q - (long)l * (P + 1));
+        int lo = ptr[l], hi = ptr[l + 1];
+        if (p == 0) hi = lo;
+        else if (p < P) {
+            const int key = p * W;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (idx[mid] < key) lo = mid + 1;
+                else hi = mid;
+            }
+        } else lo = hi;
+        ppt[q] = (p == 0) ? ptr[l] : lo;
+    }
+    (void)cost;
+}
+__global__ void k_panel_cost(int nlines, int P, const int* __restrict__ ppt, int* __restrict__ cost)
+{
+    const long total = (long)nlines * P;
+    for (long q = (long)blockIdx.x * blockDim.x + threadIdx.x; q < total; q += (long)gridDim.x * blockDim.x) {
+        const int p = (int)(q / nlines), l = (int)(q - (long)p * nlines);
+        const int len = ppt[(size_t)l * (P + 1) + p + 1] - ppt[(size_t)l * (P + 1) + p];
+        cost[q] = len > 0 ? len + kPanelLineCost : 1;
+    }
+}
+// block b of panel p starts at the first line whose prefix work reaches b / Bk of the panel's total
+__global__ void k_panel_blocks(int nlines, int P, int Bk, const int* __restrict__ scan, int* __restrict__ blk)
+{
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= P * (Bk + 1)) return;
+    const int p = q / (Bk + 1), b = q - p * (Bk + 1);
+    const int* s = scan + (size_t)p * nlines;
+    const long base = s[0], tot = (long)scan[(size_t)(p + 1) * nlines] - base;
+    int line = nlines;
+    if (b < Bk) {
+        const long target = base + tot * b / Bk;
+        int lo = 0, hi = nlines;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if ((long)s[mid] < target) lo = mid + 1;
+            else hi = mid;
+        }
+        line = lo;
+    }
+    blk[q] = line;
+}
+
+// lanes stride over [beg, end) with kLanes lanes and 8 entries in flight per lane; gathers from the staged panel
+template <int kLanes>
+__device__ __forceinline__ void panel_dot(int beg, int end, int gl, const int* __restrict__ idx, const double* __restrict__ val,
+                                          uint32_t vec, int col0, double& a0, double& a1)
+{
+    for (int t = beg + gl; t < end; t += kLanes * 8) {
+        int c[8];
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int tt = t + kLanes * u;
+            const bool ok = tt < end;
+            c[u] = ok ? __ldg(idx + tt) : col0;
+            v[u] = ok ? __ldg(val + tt) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const double2 g = lds_f64x2(vec + (uint32_t)(c[u] - col0) * 16u);
+            a0 = __fma_rn(v[u], g.x, a0);
+            a1 = __fma_rn(v[u], g.y, a1);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kPanelThreads, 1) k_spmv_panel(const PanelArgs a)
+{
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int p = blockIdx.x / a.Bk, b = blockIdx.x - p * a.Bk;
+    const int col0 = p * a.W, wp = min(a.W, a.ngather - col0);
+    const uint32_t vec = smem_u32(smem);
+    int* defer_w = reinterpret_cast<int*>(smem + (size_t)a.W * 16);  // pieces for a warp
+    int* defer_c = defer_w + kPanelDeferCap;                         // pieces for the CTA
+    double* wpart = reinterpret_cast<double*>(defer_c + kPanelDeferCap);  // kPanelWarps x 2
+    __shared__ int n_defer_w, n_defer_c;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) n_defer_w = n_defer_c = 0;
+    // stage the panel: entries (x[4 j], x[4 j + 1]) of the interleaved vector
+    for (int j = tid; j < wp; j += kPanelThreads) {
+        const double2 g = __ldcg(reinterpret_cast<const double2*>(a.x + (size_t)(col0 + j) * 4));
+        asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(vec + (uint32_t)j * 16u), "d"(g.x), "d"(g.y) : "memory");
+    }
+    __syncthreads();
+    const int l0 = a.blk[p * (a.Bk + 1) + b], l1 = a.blk[p * (a.Bk + 1) + b + 1];
+    const size_t pstride = (size_t)(a.P + 1);
+    double* const part = a.part + (size_t)p * a.nlines * 2;
+
+    // ---- pass 1: four lines per warp, 8 lanes each; longer pieces are deferred ----
+    const int sub = lane >> 3, gl = lane & 7;
+    for (int base = l0 + warp * 4; base < l1; base += kPanelWarps * 4) {
+        const int l = base + sub;
+        int beg = 0, end = 0;
+        if (l < l1) {
+            beg = __ldg(a.ppt + (size_t)l * pstride + p);
+            end = __ldg(a.ppt + (size_t)l * pstride + p + 1);
+        }
+        const int len = end - beg;
+        double a0 = 0.0, a1 = 0.0;
+        if (len > kPanelGroupMax) {
+            if (gl == 0) {
+                const bool cta = len > kPanelWarpMax;
+                const int slot = atomicAdd(cta ? &n_defer_c : &n_defer_w, 1);
+                if (slot < kPanelDeferCap) (cta ? defer_c : defer_w)[slot] = l;
+            }
+        } else if (len > 0) {
+            panel_dot<8>(beg, end, gl, a.idx, a.val, vec, col0, a0, a1);
+        }
+        // even lanes of a group end with the group's sum of a0, odd lanes with a1 (fixed order)
+        const bool odd = lane & 1;
+        double c = (odd ? a1 : a0) + shfl_xor_d(odd ? a0 : a1, 1);
+        c += shfl_xor_d(c, 2);
+        c += shfl_xor_d(c, 4);
+        if (l < l1 && len <= kPanelGroupMax && gl < 2) part[(size_t)l * 2 + gl] = c;
+    }
+    __syncthreads();
+    // ---- pass 2: one warp per deferred piece ----
+    const int nw_list = min(n_defer_w, kPanelDeferCap), nc_list = min(n_defer_c, kPanelDeferCap);
+    const bool overflow = n_defer_w > kPanelDeferCap || n_defer_c > kPanelDeferCap;
+    for (int q = warp; q < nw_list; q += kPanelWarps) {
+        const int l = defer_w[q];
+        const int beg = __ldg(a.ppt + (size_t)l * pstride + p), end = __ldg(a.ppt + (size_t)l * pstride + p + 1);
+        double a0 = 0.0, a1 = 0.0;
+        panel_dot<32>(beg, end, lane, a.idx, a.val, vec, col0, a0, a1);
+        a0 = warp_sum(a0);
+        a1 = warp_sum(a1);
+        if (lane == 0) {
+            part[(size_t)l * 2] = a0;
+            part[(size_t)l * 2 + 1] = a1;
+        }
+    }
+    // ---- pass 3: the whole CTA per very long piece (row 0 / column 0 of Omega*) ----
+    for (int q = 0; q < nc_list; ++q) {
+        const int l = defer_c[q];
+        const int beg = __ldg(a.ppt + (size_t)l * pstride + p), end = __ldg(a.ppt + (size_t)l * pstride + p + 1);
+        double a0 = 0.0, a1 = 0.0;
+        panel_dot<kPanelThreads>(beg, end, tid, a.idx, a.val, vec, col0, a0, a1);
+        a0 = warp_sum(a0);
+        a1 = warp_sum(a1);
+        if (lane == 0) {
+            wpart[warp * 2] = a0;
+            wpart[warp * 2 + 1] = a1;
+        }
+        __syncthreads();
+        if (tid < 2) {
+            double s = 0.0;
+            for (int w = 0; w < kPanelWarps; ++w) s += wpart[w * 2 + tid];
+            part[(size_t)l * 2 + tid] = s;
+        }
+        __syncthreads();
+    }
+    // more deferred pieces than the lists hold (never at the sizes this path is meant for): rescan, one warp each
+    if (overflow) {
+        for (int l = l0 + warp; l < l1; l += kPanelWarps) {
+            const int beg = __ldg(a.ppt + (size_t)l * pstride + p), end = __ldg(a.ppt + (size_t)l * pstride + p + 1);
+            if (end - beg <= kPanelGroupMax) continue;
+            double a0 = 0.0, a1 = 0.0;
+            panel_dot<32>(beg, end, lane, a.idx, a.val, vec, col0, a0, a1);
+            a0 = warp_sum(a0);
+            a1 = warp_sum(a1);
+            if (lane == 0) {
+                part[(size_t)l * 2] = a0;
+                part[(size_t)l * 2 + 1] = a1;
+            }
+        }
+    }
+}
+
+// y_line = sum over panels (panel order) of part[p][line], then the epilogue of the half mat-vec
+template <int kEpi>
+__global__ void k_panel_combine(int nlines, int P, const double* __restrict__ part, const double* __restrict__ diag,
+                                double* __restrict__ y)
+{
+    const int total = nlines * 2;
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < total; q += gridDim.x * blockDim.x) {
+        const int l = q >> 1, k = q & 1;
+        double s = 0.0;
+        for (int p = 0; p < P; ++p) s += part[((size_t)p * nlines + l) * 2 + k];
+        y[(size_t)l * 4 + k] = (kEpi == kEpiRowsScaled) ? s / diag[l] : s;
+    }
+}
+
+static constexpr int panel_smem(int W) { return W * 16 + 2 * kPanelDeferCap * 4 + kPanelWarps * 2 * 8; }
+
+// (re)build the plan of one half for the current pattern; everything stays on the device
+static void build_panel_plan(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, const regot_sparse& S, bool rows)
+{
+    PanelPlan& Q = rows ? S.panel_rows : S.panel_cols;
+    if (Q.stamp == S.structure_stamp && Q.P > 0) return;
+    const int nloc = (int)S.nloc, mfree = std::max((int)S.m - 1, 0);
+    Q.nlines = rows ? nloc : mfree;
+    Q.ngather = rows ? mfree : nloc;
+    const int wmax = ctx->panel_width > 0 ? std::min(ctx->panel_width, kPanelMaxW) : kPanelMaxW;
+    Q.P = std::max(1, (Q.ngather + wmax - 1) / wmax);
+    if (Q.P > ctx->sm_count) raise(REGOT_E_UNSUPPORTED, "panel mat-vec: the gathered vector needs more panels than there are SMs");
+    Q.W = ((Q.ngather + Q.P - 1) / Q.P + 31) / 32 * 32;
+    Q.Bk = std::max(1, ctx->sm_count / Q.P);
+    const size_t np = (size_t)Q.P * (size_t)Q.nlines;
+    Q.ppt.ensure((size_t)Q.nlines * (Q.P + 1) + 1);
+    Q.cost.ensure(np + 1);
+    Q.scan.ensure(np + 1);
+    Q.blk.ensure((size_t)Q.P * (Q.Bk + 1));
+    Q.part.ensure(np * 2 + 2);
+    const int* ptr = rows ? S.rowptr.p : S.cscptr.p;
+    const int* idx = rows ? S.col.p : S.cscrow.p;
+    const int g1 = (int)std::max<long>(1, std::min<long>(((long)Q.nlines * (Q.P + 1) + 255) / 256, 8L * ctx->sm_count));
+    k_panel_ptrs<<<g1, 256, 0, st>>>(Q.nlines, Q.P, Q.W, ptr, idx, Q.ppt.p, Q.cost.p);
+    k_panel_cost<<<g1, 256, 0, st>>>(Q.nlines, Q.P, Q.ppt.p, Q.cost.p);
+    RG_CUDA(cudaMemsetAsync(Q.cost.p + np, 0, sizeof(int), st));
+    size_t bytes = 0;
+    RG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, Q.cost.p, Q.scan.p, (int)(np + 1), st));
+    ws.cub_tmp.ensure(bytes);
+    RG_CUDA(cub::DeviceScan::ExclusiveSum(ws.cub_tmp.p, bytes, Q.cost.p, Q.scan.p, (int)(np + 1), st));
+    const int nb = Q.P * (Q.Bk + 1);
+    k_panel_blocks<<<(nb + 127) / 128, 128, 0, st>>>(Q.nlines, Q.P, Q.Bk, Q.scan.p, Q.blk.p);
+    RG_CUDA(cudaGetLastError());
+    ctx->launches += 5;
+    Q.stamp = S.structure_stamp;
+}
+
+// one half mat-vec in panel form: y (interleaved x4) = epilogue(B x) or epilogue(B' x) for two right-hand sides
+template <int kEpi>
+static void launch_spmv_panel(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, const regot_sparse& S, const double* x, double* y)
+{
+    constexpr bool rows = kEpi == kEpiRowsScaled;
+    build_panel_plan(ctx, st, ws, S, rows);
+    const PanelPlan& Q = rows ? S.panel_rows : S.panel_cols;
+    static bool attr_set = false;
+    if (!attr_set) {
+        RG_CUDA(cudaFuncSetAttribute(k_spmv_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, panel_smem(kPanelMaxW)));
+        attr_set = true;
+    }
+    PanelArgs a;
+    a.P = Q.P;
+    a.Bk = Q.Bk;
+    a.W = Q.W;
+    a.nlines = Q.nlines;
+    a.ngather = Q.ngather;
+    a.ppt = Q.ppt.p;
+    a.blk = Q.blk.p;
+    a.idx = rows ? S.col.p : S.cscrow.p;
+    a.val = rows ? S.val.p : S.cscval.p;
+    a.x = x;
+    a.part = Q.part.p;
+    {
+        ProfScope prof(ctx, st, 4);
+        k_spmv_panel<<<Q.P * Q.Bk, kPanelThreads, panel_smem(Q.W), st>>>(a);
+        const int g = (int)std::max<long>(1, std::min<long>(((long)Q.nlines * 2 + 255) / 256, 4L * ctx->sm_count));
+        k_panel_combine<kEpi><<<g, 256, 0, st>>>(Q.nlines, Q.P, Q.part.p, rows ? S.dA.p : nullptr, y);
+    }
+    RG_CUDA(cudaGetLastError());
+    ctx->launches += 2;
+}
+
+static bool use_panel_spmv(const regot_ctx* ctx, const regot_sparse& S, int nrhs)
+{
+    if (nrhs > 2 || ctx->panel_spmv == 0 || S.nnz == 0 || S.m < 2) return false;
+    if (ctx->panel_spmv > 0) return true;
+    return S.nnz >= (1 << 19);  // below that the gather-through-L2 kernel is not bandwidth-bound
+}
+
 // ---- K5, multi-kernel form: Jacobi-PCG on the Schur complement of the alpha block ------------------
 // Same algorithm as the persistent kernel (k5_pcg.cu) -- S x_b = r_b - B' D1^-1 r_a, S = D2 - B' D1^-1 B,
 // x_a = D1^-1 (r_a - B x_b) -- as a sequence of kernels: the path for problems whose iterated vector does
@@ -613,9 +914,16 @@ static int pcg_schur_multikernel(regot_ctx* ctx, cudaStream_t st, ncclComm* comm
     const int grid_a = (int)std::max<long>(1, std::min<long>((nloc + kCgThreads - 1) / kCgThreads, 2L * ctx->sm_count));
     const int grid_b = (int)std::max<long>(1, std::min<long>((mfree + kCgThreads - 1) / kCgThreads, 2L * ctx->sm_count));
     const double tol2 = rtol * rtol;
+    const bool panel = use_panel_spmv(ctx, S, nrhs);
+    // t = D1^-1 B x for a beta-space vector x
+    auto half_rows = [&](const double* xb) {
+        if (panel) launch_spmv_panel<kEpiRowsScaled>(ctx, st, ws, S, xb, v.ta);
+        else launch_spmv<kEpiRowsScaled>(ctx, st, S, nrhs, nullptr, xb, v.ta, nullptr, kInterleaved4, kInterleaved4);
+    };
     // u = B' t, summed over the row blocks
     auto half_cols = [&]() {
-        launch_spmv<kEpiColsPlain>(ctx, st, S, nrhs, v.ta, nullptr, nullptr, v.ub, kInterleaved4, kInterleaved4);
+        if (panel) launch_spmv_panel<kEpiColsPlain>(ctx, st, ws, S, v.ta, v.ub);
+        else launch_spmv<kEpiColsPlain>(ctx, st, S, nrhs, v.ta, nullptr, nullptr, v.ub, kInterleaved4, kInterleaved4);
         if (ctx->world > 1) allreduce_sum(ctx, comm, v.ub, 4 * (size_t)mfree, st);
     };
 
@@ -642,7 +950,7 @@ static int pcg_schur_multikernel(regot_ctx* ctx, cudaStream_t st, ncclComm* comm
     while (it < max_iter && !finished && !broke) {
         const int burst = std::min(check_every, max_iter - it);
         for (int b = 0; b < burst; ++b, ++it) {
-            launch_spmv<kEpiRowsScaled>(ctx, st, S, nrhs, nullptr, v.pb, v.ta, nullptr, kInterleaved4, kInterleaved4);  // t = D1^-1 B p
+            half_rows(v.pb);                                                                         // t = D1^-1 B p
             half_cols();                                                                            // u = B' t
             k_schur_q<<<grid_b, kCgThreads, 0, st>>>(v);
             k_schur_update<<<grid_b, kCgThreads, 0, st>>>(v, parity);
@@ -657,7 +965,7 @@ static int pcg_schur_multikernel(regot_ctx* ctx, cudaStream_t st, ncclComm* comm
     if (broke) return -1;
     it = 0;  // report the slowest system's exact count, not the burst-rounded loop count
     for (int k = 0; k < nrhs; ++k) it = std::max(it, (int)ws.h_cg[kScalIters + k]);
-    launch_spmv<kEpiRowsScaled>(ctx, st, S, nrhs, nullptr, v.xb, v.ta, nullptr, kInterleaved4, kInterleaved4);  // t = D1^-1 B x_b
+    half_rows(v.xb);  // t = D1^-1 B x_b
     k_schur_final<<<std::max(grid_a, grid_b), kCgThreads, 0, st>>>(v, d_rhs_a, d_sol_a, d_sol_b);
     RG_CUDA(cudaGetLastError());
     ++ctx->launches;

@@ -35,6 +35,20 @@ struct PcgSchedule {
 };
 }  // namespace rg
 
+namespace rg {
+// Plan of the panel mat-vec (k4_sparse.cu, k_spmv_panel): the gathered vector of one Schur half is cut into P
+// panels of W entries that fit in shared memory, the lines (rows or columns of B) of each panel into Bk blocks
+// of equal work; CTA (p, b) stages panel p once and processes the pieces of its lines that fall inside it.
+struct PanelPlan {
+    int P = 0, Bk = 0, W = 0, nlines = 0, ngather = 0;
+    unsigned long stamp = 0;  // structure_stamp of the pattern this plan was built for
+    DevBuf<int> ppt;          // nlines x (P + 1): first entry of line l at or beyond panel p
+    DevBuf<int> blk;          // P x (Bk + 1): line boundaries of the blocks
+    DevBuf<int> cost, scan;   // P x nlines (+1): work per piece and its exclusive prefix sum
+    DevBuf<double> part;      // P x nlines x 2: per-panel partial sums of every line
+};
+}  // namespace rg
+
 struct regot_sparse {
     regot_ctx* ctx = nullptr;  // owner; never dereferenced on the free path (the context may be gone by then)
     int device = 0;
@@ -61,6 +75,8 @@ struct regot_sparse {
     rg::DevBuf<int> lines_s, lines_m;
     int n_lines_s = 0, n_lines_m = 0;
     rg::PcgSchedule pcg;  // single-GPU direction solve (k5_pcg.cu)
+    unsigned long structure_stamp = 0;         // bumped by finish_structure: derived plans know when they are stale
+    mutable rg::PanelPlan panel_rows, panel_cols;  // kernel-by-kernel direction solve of large / sharded problems
 };
 
 namespace rg {

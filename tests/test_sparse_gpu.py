@@ -182,6 +182,69 @@ def multikernel_solver():
     s.close()
 
 
+@pytest.fixture(scope="module", params=[(64, "many narrow panels"), (0, "one panel")])
+def panel_solver(request):
+    """The kernel-by-kernel Schur PCG with its half mat-vecs in PANEL form (k_spmv_panel: the gathered vector
+    staged in shared memory panel by panel -- the path of config D / E and of large sharded runs), forced on
+    for small problems; a 64-entry panel width gives several panels and blocks even at n = 300."""
+    import os
+
+    os.environ["REGOT_B200_MULTIKERNEL_PCG"] = "1"
+    os.environ["REGOT_B200_PANEL_SPMV"] = "1"
+    if request.param[0]:
+        os.environ["REGOT_B200_PANEL_WIDTH"] = str(request.param[0])
+    try:
+        s = rg.Solver(0)
+    finally:
+        for k in ("REGOT_B200_MULTIKERNEL_PCG", "REGOT_B200_PANEL_SPMV", "REGOT_B200_PANEL_WIDTH"):
+            os.environ.pop(k, None)
+    yield s
+    s.close()
+
+
+@pytest.mark.parametrize("n,m,k", [(300, 257, 6000), (90, 700, 9000), (1500, 1400, 30000)])
+def test_panel_matvec_pcg_matches_oracle(panel_solver, oracle, n, m, k):
+    # long first row / column (pieces for a warp and for the whole CTA), ragged panels, two right-hand sides
+    p = oracle.gen_problem("rand", n, m, 0.1, seed=6701)
+    a0, b0 = oracle.rand_dual(n, m, 0.2, 6801)
+    coords = oracle.select_topk(oracle.plan(p, a0, b0), k)
+    x = rg.DualPoint(a0, b0)
+    dim = n + m - 1
+    s = panel_solver
+    s.set_problem(to_problem(p))
+    g = s.fused_gradient(x)
+    tau = min(1.0, g.grad_norm2)
+    A = s.assemble(x, rg.SparsityPattern(n, m - 1, coords), tau, g)
+    R = oracle.assemble(p, a0, b0, coords, tau)
+    gref = oracle.gradient(p, a0, b0)["grad"]
+    d, its = s.compute_direction(A, g.grad, cg_rtol=1e-13)
+    dr, _ = R.compute_direction(gref)
+    assert its > 0 and g.grad @ d < 0
+    assert np.linalg.norm(d - dr) <= 1e-8 * np.linalg.norm(dr)
+    # the residual through the (independent) full mat-vec kernel
+    assert np.linalg.norm(A.matvec(d) + g.grad) <= 1e-9 * np.linalg.norm(g.grad)
+
+
+def test_panel_path_solve_agrees_with_persistent_kernel(solver, panel_solver):
+    from paper_2605_08793_b200 import problems
+
+    p = problems.gen_synthetic1(300, 260, "iid", 2, 7, 0.01)
+    cfg = rg.SplrConfig(max_iter=200, tol=1e-8)
+    res = []
+    for s in (solver, panel_solver):
+        s.set_problem(p)
+        res.append(s.run_splr(rg.DualPoint.zeros(p.n, p.m), cfg))
+    a, b = res[0].trace.rows[-1], res[1].trace.rows[-1]
+    assert a.marginal_error <= 1e-8 and b.marginal_error <= 1e-8
+    for u, v in zip(res[0].steps[:15], res[1].steps[:15]):
+        assert abs(u.f_after - v.f_after) <= 1e-11 * (1 + abs(u.f_after)) and abs(u.cg_iters - v.cg_iters) <= 1
+    assert abs(a.f - b.f) <= 1e-9 * (1 + abs(a.f))
+    # and it is deterministic: the deferred-piece lists are filled in arrival order, the sums are not
+    again = panel_solver.run_splr(rg.DualPoint.zeros(p.n, p.m), cfg)
+    assert [r.f for r in again.trace.rows] == [r.f for r in res[1].trace.rows]
+    assert np.array_equal(again.x.alpha, res[1].x.alpha)
+
+
 def test_multikernel_pcg_matches_oracle_and_persistent_kernel(solver, multikernel_solver, oracle):
     p = oracle.gen_problem("rand", 300, 257, 0.1, seed=6701)
     a0, b0 = oracle.rand_dual(300, 257, 0.2, 6801)

@@ -147,6 +147,14 @@ regot_ctx* ctx_create(int device)
         // off by default: measured 11 % (config A) / 1 % (1600 x 1200) of the direction solve, slower above ~50k entries
         ctx->pcg_cluster_size = 0;
         ctx->pcg_cluster_max_entries = 50000;
+        if (const char* e = std::getenv("REGOT_B200_PCG_BLOCKS")) ctx->pcg_blocks = std::atoi(e);
+        if (const char* e = std::getenv("REGOT_B200_PCG_BLOCKS_GRID")) {
+            int bp = 0, bq = 0;
+            if (std::sscanf(e, "%dx%d", &bp, &bq) == 2 && bp >= 1 && bq >= 1 && bp <= 32 && bq <= 32) {
+                ctx->pcg_blocks_p = bp;
+                ctx->pcg_blocks_q = bq;
+            }
+        }
         if (const char* e = std::getenv("REGOT_B200_PCG_CLUSTER")) ctx->pcg_cluster_size = std::atoi(e);
         if (const char* e = std::getenv("REGOT_B200_PCG_CLUSTER_ENTRIES")) ctx->pcg_cluster_max_entries = std::atol(e);
         if (const char* e = std::getenv("REGOT_B200_EXACT_LSE")) ctx->fast_sinkhorn = e[0] != '1';

@@ -263,6 +263,10 @@ struct regot_ctx {
     // (REGOT_B200_PANEL_SPMV); panel_width > 0 caps the panel width in entries (REGOT_B200_PANEL_WIDTH, tests)
     int panel_spmv = -1;
     int panel_width = 0;
+    // block-resident PCG (k6_pcg_blocks.cu): -1 auto (whenever the pattern fits), 0 off (REGOT_B200_PCG_BLOCKS);
+    // pcg_blocks_p x pcg_blocks_q > 0 force the block grid (REGOT_B200_PCG_BLOCKS_GRID=PxQ, tests)
+    int pcg_blocks = -1;
+    int pcg_blocks_p = 0, pcg_blocks_q = 0;
     // persistent PCG on one thread-block cluster when a CG iteration touches at most this many matrix entries
     // (REGOT_B200_PCG_CLUSTER = 0 | 8 | 16, REGOT_B200_PCG_CLUSTER_ENTRIES)
     int pcg_cluster_size = 0;

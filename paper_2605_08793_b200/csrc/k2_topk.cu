@@ -618,6 +618,11 @@ void finish_structure(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, regot_spars
         k_build_csc<<<lin_grid(ctx, nnz), 256, 0, st>>>(nnz, ws.sort_v1.p, S.row.p, S.cscrow.p, S.slot.p);
         RG_CUDA(cudaGetLastError());
         ctx->launches += 4;
+        // the block plan of the resident PCG kernel is built on the device behind the CSC (sort_v1[t] = CSR position of
+        // CSC entry t); its 4-int summary travels with the pointer arrays below
+        build_pcg_blocks_plan(ctx, st, ws, S, ws.sort_v1.p);
+    } else {
+        S.blocks.fits = S.blocks.pending = false;
     }
     // Lines (rows of B, columns of B) longer than a threshold -- always row 0 and column 0 of Omega*
     // at scale -- are cut into chunks of kChunkLen entries that different warps process; the last warp
@@ -641,6 +646,7 @@ void finish_structure(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, regot_spars
     } else {
         RG_CUDA(cudaStreamSynchronize(st));
     }
+    finish_pcg_blocks_plan(ctx, ws, S);
     // The threshold grows with the problem: once a warp of the mat-vec grid has thousands of entries to
     // process anyway, a line of that length is balanced work for ONE warp, and chunking it would only
     // add the cross-warp combine (a fence and an atomic per chunk).  At config B it stays kLongLine.
@@ -712,7 +718,9 @@ void finish_structure(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, regot_spars
     if (S.n_lines_m) RG_CUDA(cudaMemcpyAsync(S.lines_m.p, hs + o_m, sizeof(int) * (size_t)S.n_lines_m, cudaMemcpyHostToDevice, st));
     if (S.n_chunks) RG_CUDA(cudaMemcpyAsync(S.chunks.p, hs + o_c, sizeof(int) * 4 * (size_t)S.n_chunks, cudaMemcpyHostToDevice, st));
     if (S.n_long) RG_CUDA(cudaMemcpyAsync(S.longlines.p, hs + o_l, sizeof(int) * 2 * (size_t)S.n_long, cudaMemcpyHostToDevice, st));
-    if (ctx->world == 1) build_pcg_schedule(ctx, st, S, rp, cp, ws.h_lines, used);
+    // the older persistent kernel (k5_pcg.cu) only where the block-resident one does not take the pattern
+    S.pcg.fits = false;
+    if (ctx->world == 1 && !S.blocks.fits) build_pcg_schedule(ctx, st, S, rp, cp, ws.h_lines, used);
     RG_CUDA(cudaStreamSynchronize(st));  // the staging is free again
 }
 

@@ -976,7 +976,10 @@ int sparse_pcg(regot_ctx* ctx, cudaStream_t st, ncclComm* comm, SparseWS& ws, co
                const DVec* const* rhs, DVec* const* sol, double rtol, int max_iter)
 {
     if (nrhs < 1 || nrhs > kMaxRhs) raise(REGOT_E_VALIDATION, "pcg: bad number of right-hand sides");
-    // one GPU and both iterated vectors fit in shared memory: the persistent kernel; else kernel by kernel
+    // one GPU: the block-resident kernel when every block of the pattern fits in shared memory, else the persistent
+    // kernel that streams the matrix (iterated vectors in shared memory), else kernel by kernel
+    if (ctx->world == 1 && !ctx->force_multikernel_pcg && S.blocks.fits)
+        return pcg_schur_blocks(ctx, st, ws, S, nrhs, rhs, sol, rtol, max_iter);
     if (ctx->world == 1 && !ctx->force_multikernel_pcg && S.pcg.fits)
         return pcg_schur_persistent(ctx, st, ws, S, nrhs, rhs, sol, rtol, max_iter);
     return pcg_schur_multikernel(ctx, st, comm, ws, S, nrhs, rhs, sol, rtol, max_iter);

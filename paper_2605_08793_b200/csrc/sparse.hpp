@@ -49,6 +49,26 @@ struct PanelPlan {
 };
 }  // namespace rg
 
+namespace rg {
+// Plan of the block-resident Schur-complement PCG kernel (k6_pcg_blocks.cu), built on the device per pattern: B
+// cut into P x Q blocks (rows dealt round-robin to block rows, columns to block columns), every block laid out
+// for one CTA's shared memory -- its rows and its columns as 32-line chunks sorted by length -- in two arenas.
+constexpr int kPcgBlocksHdrInts = 16;
+constexpr int kPcgBlocksMaxHeavy = 256;  // lines of a block too long for one thread, per copy
+struct PcgBlocksPlan {
+    bool fits = false;     // every block fits in shared memory: the solve takes this kernel
+    bool pending = false;  // built, summary not read yet
+    int P = 0, Q = 0, R = 0, C = 0, SR = 0, SC = 0, Lr = 0, Lc = 0, smem = 0;
+    unsigned long stamp = 0;
+    DevBuf<int> cnt, vpos;  // G x (R + C): line lengths per block; sorted position of every line
+    DevBuf<int> hdr;        // G x kPcgBlocksHdrInts sizes and arena offsets, then the 4-int summary
+    DevBuf<unsigned short> a16;  // per block: column index of every row-copy slot, line tables, row index and value reference of every column-copy slot
+    DevBuf<int> a32;             // per block (fixed stride): chunk and heavy-line tables
+    DevBuf<int> asrc;            // per block: CSR position of every row-copy slot (-1: padding)
+    DevBuf<unsigned short> rowslot;  // row-copy slot of every CSR entry (scratch of the construction)
+};
+}  // namespace rg
+
 struct regot_sparse {
     regot_ctx* ctx = nullptr;  // owner; never dereferenced on the free path (the context may be gone by then)
     int device = 0;
@@ -77,6 +97,7 @@ struct regot_sparse {
     rg::PcgSchedule pcg;  // single-GPU direction solve (k5_pcg.cu)
     unsigned long structure_stamp = 0;         // bumped by finish_structure: derived plans know when they are stale
     mutable rg::PanelPlan panel_rows, panel_cols;  // kernel-by-kernel direction solve of large / sharded problems
+    rg::PcgBlocksPlan blocks;                      // block-resident direction solve (k6_pcg_blocks.cu)
 };
 
 namespace rg {
@@ -113,11 +134,15 @@ struct SparseWS {
     PinnedBuf<int> h_lines;  // line lists and the PCG schedule (host -> device)
     double* h_cg = nullptr;  // pinned
     HostMailbox cg_mbox;     // iteration counts / breakdown flag of the persistent PCG kernel
+    int* h_blocks = nullptr;                 // pinned: summary of the block plan under construction
+    DevBuf<unsigned long long> blocks_xchg;  // block-resident PCG: flagged words of its five exchanges
+    unsigned int blocks_round = 0;           // next unused round number of those words
     ~SparseWS()
     {
         if (h_hist) cudaFreeHost(h_hist);
         if (h_small) cudaFreeHost(h_small);
         if (h_cg) cudaFreeHost(h_cg);
+        if (h_blocks) cudaFreeHost(h_blocks);
     }
 };
 
@@ -152,6 +177,12 @@ void build_pcg_schedule(regot_ctx* ctx, cudaStream_t st, regot_sparse& S, const 
                         PinnedBuf<int>& staging, size_t staging_used);
 int pcg_schur_persistent(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, const regot_sparse& S, int nrhs,
                          const DVec* const* rhs, DVec* const* sol, double rtol, int max_iter);
+// k6_pcg_blocks.cu -- the block-resident form: plan construction (enqueued on st; finish_* after the caller's
+// synchronisation reads the summary) and the solve
+void build_pcg_blocks_plan(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, regot_sparse& S, const int* csc2csr);
+void finish_pcg_blocks_plan(regot_ctx* ctx, SparseWS& ws, regot_sparse& S);
+int pcg_schur_blocks(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, const regot_sparse& S, int nrhs, const DVec* const* rhs,
+                     DVec* const* sol, double rtol, int max_iter);
 int sparse_pcg(regot_ctx* ctx, cudaStream_t st, ncclComm* comm, SparseWS& ws, const regot_sparse& S, int nrhs,
                const DVec* const* rhs, DVec* const* sol, double rtol, int max_iter);
 

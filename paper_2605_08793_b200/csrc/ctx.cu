@@ -148,6 +148,9 @@ regot_ctx* ctx_create(int device)
         ctx->pcg_cluster_size = 0;
         ctx->pcg_cluster_max_entries = 50000;
         if (const char* e = std::getenv("REGOT_B200_PCG_BLOCKS")) ctx->pcg_blocks = std::atoi(e);
+        if (const char* e = std::getenv("REGOT_B200_PCG_BLOCKS_CLUSTER")) ctx->pcg_blocks_cluster = std::atoi(e);
+        if (const char* e = std::getenv("REGOT_B200_PCG_BLOCKS_ONE_CLUSTER_ENTRIES")) ctx->pcg_blocks_one_cluster_entries = std::atol(e);
+        if (const char* e = std::getenv("REGOT_B200_PCG_BLOCKS_CLUSTER_ENTRIES")) ctx->pcg_blocks_cluster_entries = std::atol(e);
         if (const char* e = std::getenv("REGOT_B200_PCG_BLOCKS_GRID")) {
             int bp = 0, bq = 0;
             if (std::sscanf(e, "%dx%d", &bp, &bq) == 2 && bp >= 1 && bq >= 1 && bp <= 32 && bq <= 32) {

@@ -9,6 +9,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <ctime>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -120,8 +121,20 @@ struct HostMailbox {
     unsigned long long next() { return ++expected; }
     // block until the post with sequence number `expected` has landed (all earlier work of the posting
     // stream is then complete); a failed launch or kernel shows up through cudaStreamQuery
+    static double wall_seconds()
+    {
+        timespec ts;
+        clock_gettime(CLOCK_MONOTONIC, &ts);
+        return (double)ts.tv_sec + 1e-9 * (double)ts.tv_nsec;
+    }
+    static double timeout_seconds()
+    {
+        static const double t = std::getenv("REGOT_B200_MAILBOX_TIMEOUT_S") ? std::atof(std::getenv("REGOT_B200_MAILBOX_TIMEOUT_S")) : 300.0;
+        return t;
+    }
     void wait(cudaStream_t st) const
     {
+        const double t_start = wall_seconds();
         const volatile unsigned long long* seq = reinterpret_cast<const volatile unsigned long long*>(data) + kSlots;
         for (unsigned long spins = 0; *seq != expected; ++spins) {
             if ((spins & 0xffffUL) == 0xffffUL) {
@@ -130,6 +143,9 @@ struct HostMailbox {
                     if (e == cudaSuccess) raise(REGOT_E_CUDA, "mailbox: stream drained without the expected post (internal error)");
                     raise(REGOT_E_CUDA, std::string("mailbox: ") + cudaGetErrorString(e));
                 }
+                // a kernel that never posts (a persistent kernel waiting on itself) must not hang the caller for ever
+                if ((spins & 0xffffffUL) == 0xffffffUL && wall_seconds() - t_start > timeout_seconds())
+                    raise(REGOT_E_CUDA, "mailbox: no post within the time limit (REGOT_B200_MAILBOX_TIMEOUT_S); the device is still busy");
             }
         }
         __sync_synchronize();
@@ -267,6 +283,13 @@ struct regot_ctx {
     // pcg_blocks_p x pcg_blocks_q > 0 force the block grid (REGOT_B200_PCG_BLOCKS_GRID=PxQ, tests)
     int pcg_blocks = -1;
     int pcg_blocks_p = 0, pcg_blocks_q = 0;
+    // block rows as thread-block clusters: -1 auto, 0 off (REGOT_B200_PCG_BLOCKS_CLUSTER); patterns up to this many entries
+    // take a single cluster (REGOT_B200_PCG_BLOCKS_ONE_CLUSTER_ENTRIES); pcg_blocks_maxcl[q]: clusters of q CTAs the device holds
+    int pcg_blocks_cluster = -1;
+    long pcg_blocks_one_cluster_entries = 100000;
+    long pcg_blocks_cluster_entries = 600000;  // block rows as clusters only up to this many entries (REGOT_B200_PCG_BLOCKS_CLUSTER_ENTRIES)
+    bool pcg_blocks_probed = false;
+    int pcg_blocks_maxcl[17] = {0};
     // persistent PCG on one thread-block cluster when a CG iteration touches at most this many matrix entries
     // (REGOT_B200_PCG_CLUSTER = 0 | 8 | 16, REGOT_B200_PCG_CLUSTER_ENTRIES)
     int pcg_cluster_size = 0;

@@ -646,7 +646,7 @@ void finish_structure(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, regot_spars
     } else {
         RG_CUDA(cudaStreamSynchronize(st));
     }
-    finish_pcg_blocks_plan(ctx, ws, S);
+    finish_pcg_blocks_plan(ctx, st, ws, S, nnz > 0 ? ws.sort_v1.p : nullptr);
     // The threshold grows with the problem: once a warp of the mat-vec grid has thousands of entries to
     // process anyway, a line of that length is balanced work for ONE warp, and chunking it would only
     // add the cross-warp combine (a fence and an atomic per chunk).  At config B it stays kLongLine.

@@ -33,6 +33,8 @@
 #include "ctx.hpp"
 #include "sparse.hpp"
 
+#include <cooperative_groups.h>
+
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
@@ -87,15 +89,24 @@ __host__ __device__ __forceinline__ Lay32 lay32(int R, int C)
     return L;
 }
 
+// doubles of the owner's collection buffers: the Q x 2 SR row partial sums and the P x 2 SC column partial sums.  Through
+// L2 they are copied there one after the other (one buffer); inside a cluster the row partials are written by the
+// other CTAs at their own pace, so the two do not share
+__host__ __device__ __forceinline__ long b2_xbuf_doubles(int SR, int SC, int P, int Q, int cluster)
+{
+    const long x1 = 2L * Q * SR, x3 = 2L * P * SC;
+    return cluster ? x1 + x3 : (x1 > x3 ? x1 : x3);
+}
+
 // dynamic shared memory of the solve kernel for one block (the carve-up at the top of k_pcg_blocks)
-__host__ __device__ __forceinline__ long b2_smem_need(const int* h, int R, int C, int SR, int SC, int P, int Q)
+__host__ __device__ __forceinline__ long b2_smem_need(const int* h, int R, int C, int SR, int SC, int P, int Q, int cluster)
 {
     const int nval = h[kH_NSL_R] + h[kH_NHE_R];
     const int segcap_r = h[kH_NHE_R] / 128 + h[kH_NHV_R], segcap_c = h[kH_NHE_C] / 128 + h[kH_NHV_C];
     const int tables = 2 * h[kH_NCH_R] + 3 * h[kH_NHV_R] + 2 * h[kH_NCH_C] + 3 * h[kH_NHV_C];
     const int derived = h[kH_NV_R] + h[kH_NV_C] + 2 * (h[kH_NHV_R] + h[kH_NHV_C]) + 2 + segcap_r + segcap_c + 4;
     return (long)(((nval + 1) * 8 + 15) & ~15) + 16L * C + 16L * R + 16L * (segcap_r > segcap_c ? segcap_r : segcap_c) + 2L * lay16(h).size +
-           (long)(((tables + derived) * 4 + 15) & ~15) + 8L * (6 * 2 * SC + SC + SR) + 8L * (Q * 2 * SR > P * 2 * SC ? Q * 2 * SR : P * 2 * SC) + 8L * (8 * P * Q) + 8L * (16 + 8 * kB2Warps) + 256 + kB2Slack;
+           (long)(((tables + derived) * 4 + 15) & ~15) + 8L * (6 * 2 * SC + 2 * SC + SR) + 8L * b2_xbuf_doubles(SR, SC, P, Q, cluster) + 8L * (8 * P * Q) + 8L * (16 + 8 * kB2Warps) + 256 + 64 + 16 + kB2Slack;
 }
 
 // ---- plan construction (device; once per pattern) -----------------------------------------------------
@@ -227,7 +238,7 @@ __global__ void __launch_bounds__(256) k_b2_layout(int P, int Q, int R, int C, i
 
 // arena offsets of every block (one CTA), shared-memory need of the solve kernel per block, and the summary
 // the host reads: {largest need, any block unusable, total u16 units, total source entries}
-__global__ void k_b2_offsets(int P, int Q, int R, int C, int SR, int SC, int* __restrict__ hdr, int* __restrict__ summary)
+__global__ void k_b2_offsets(int P, int Q, int R, int C, int SR, int SC, int cluster, int* __restrict__ hdr, int* __restrict__ summary)
 {
     if (threadIdx.x != 0) return;
     const int G = P * Q;
@@ -241,7 +252,7 @@ __global__ void k_b2_offsets(int P, int Q, int R, int C, int SR, int SC, int* __
         const int nval = h[kH_NSL_R] + h[kH_NHE_R];
         off16 += L.size;
         offsrc += (nval + 3) & ~3;
-        const long need = b2_smem_need(h, R, C, SR, SC, P, Q);
+        const long need = b2_smem_need(h, R, C, SR, SC, P, Q, cluster);
         h[kH_SMEM] = need < (1L << 30) ? (int)need : (1 << 30);
         worst = max(worst, h[kH_SMEM]);
         bad |= h[kH_BAD];
@@ -360,6 +371,7 @@ struct BlocksParams {
     double* sol_b[2];
     u64 *x1, *x2, *x3, *x4, *x5;  // flagged words of the five exchanges
     unsigned int round0;          // round number of this launch's first exchange
+    int cluster;                  // CTAs of a block row form a thread-block cluster: their exchanges (X1, X2; with P == 1 all of them) go through distributed shared memory
     double* out;                  // iters[2], -, breakdown flag
     double* mbox;
     unsigned long long mseq;
@@ -377,31 +389,22 @@ __device__ __forceinline__ bool fw_try(const u64* slot, unsigned int round, doub
     v = __longlong_as_double((long long)((lo & 0xffffffffull) | (hi << 32)));
     return (unsigned int)(lo >> 32) == round && (unsigned int)(hi >> 32) == round;
 }
-// Flagged doubles -> shared memory, all threads of the CTA, 4 loads in flight per thread.  Element (o, r), o <
-// n_outer, r < n_inner, is awaited at src + 2 (o src_stride + r) and lands in dst[o n_inner + r].
-__device__ __noinline__ void fw_gather(const u64* src, double* dst, int n_inner, int n_outer, int src_stride, unsigned int round)
+// n flagged doubles at src -> dst (shared memory), all threads of the CTA, 4 loads in flight per thread
+__device__ __noinline__ void fw_gather(const u64* src, double* dst, int n, unsigned int round)
 {
-    const int n = n_inner * n_outer;
+#pragma unroll 1
     for (int i0 = threadIdx.x; i0 < n; i0 += kB2Threads * 4) {
         double v[4];
-        const u64* at[4];
         unsigned pend = 0;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int i = i0 + u * kB2Threads;
-            at[u] = src;
-            if (i < n) {
-                const int o = i / n_inner;
-                at[u] = src + 2 * ((size_t)o * src_stride + (i - o * n_inner));
-                pend |= 1u << u;
-            }
-        }
+        for (int u = 0; u < 4; ++u)
+            if (i0 + u * kB2Threads < n) pend |= 1u << u;
         const unsigned valid = pend;
         while (pend) {
 #pragma unroll
             for (int u = 0; u < 4; ++u)
                 if ((pend >> u) & 1u)
-                    if (fw_try(at[u], round, v[u])) pend &= ~(1u << u);
+                    if (fw_try(src + 2 * (size_t)(i0 + u * kB2Threads), round, v[u])) pend &= ~(1u << u);
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u)
@@ -411,29 +414,115 @@ __device__ __noinline__ void fw_gather(const u64* src, double* dst, int n_inner,
 
 constexpr int kB2Seg = 128;  // entries of a heavy line one warp sums at a time
 
-struct BlockCopy {  // one copy (rows or columns) of the CTA's block in shared memory
-    const u16* ell;     // entry -> local index into the gathered slice
-    const u16* ref;     // column copy: entry -> position in `val` (row copy: null, the entry's own position)
-    const u16* lov;     // sorted position -> local line
-    const int* off;     // sorted position -> word offset of the line's two sums in the exchange
-    const int* chunk;   // (first slot, width) per 32-line chunk
-    const int* heavy;   // (line, first entry, length) per heavy line
-    const int* hoff;    // heavy line -> word offset in the exchange
-    const int* hfirst;  // heavy line -> its first segment
-    const int* hseg;    // segment -> heavy line
+// shared-memory accesses of the mat-vec phase by 32-bit shared-window address: the phase is an out-of-line function,
+// and through generic pointers the compiler would emit generic loads (slower than ld.shared)
+__device__ __forceinline__ int lds_u16(uint32_t a)
+{
+    unsigned short v;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
+    return (int)v;
+}
+__device__ __forceinline__ int lds_s32(uint32_t a)
+{
+    int v;
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts_f64x2_b(uint32_t a, double x, double y)
+{
+    asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(x), "d"(y) : "memory");
+}
+
+// ---- exchanges inside a thread-block cluster: remote shared-memory stores that complete on the receiver's mbarrier ----
+// The receiver arms its barrier with the number of bytes a round brings (expect_tx) and waits for the phase; senders
+// write plain doubles straight into the receiver's buffer (st.async ... complete_tx): no flags, no fences, no copies.
+__device__ __forceinline__ uint32_t map_rank(uint32_t saddr, int rank)
+{
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void st_async_f64(uint32_t raddr, double v, uint32_t rmbar)
+{
+    asm volatile("st.async.weak.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(raddr),
+                 "l"(__double_as_longlong(v)), "r"(rmbar)
+                 : "memory");
+}
+__device__ __forceinline__ void st_async_f64x2(uint32_t raddr, double a, double b, uint32_t rmbar)
+{
+    asm volatile("st.async.weak.shared::cluster.mbarrier::complete_tx::bytes.v2.b64 [%0], {%1, %2}, [%3];" ::"r"(raddr),
+                 "l"(__double_as_longlong(a)), "l"(__double_as_longlong(b)), "r"(rmbar)
+                 : "memory");
+}
+// all threads of the CTA: wait until the round's `bytes` have landed (thread 0 arms the barrier; data written by
+// other CTAs of the cluster: acquire at cluster scope)
+__device__ __forceinline__ void cluster_inbox_wait(uint32_t mbar, uint32_t bytes, uint32_t& parity)
+{
+    if (threadIdx.x == 0)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes) : "memory");
+    uint32_t ok;
+    do {
+        asm volatile(
+            "{ .reg .pred p;\n"
+            "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
+            "selp.u32 %0, 1, 0, p; }"
+            : "=r"(ok)
+            : "r"(mbar), "r"(parity)
+            : "memory");
+    } while (!ok);
+    parity ^= 1u;
+}
+
+// Where the two sums of a line go.  Through L2: word offset ((owner nsrc + me) slice + r) 4 from the base of the block
+// row's (column's) exchange.  Inside a cluster: the owner's buffer has the layout [source][slice][2] doubles, so the
+// byte offset (me slice + r) 16 from the base of the buffer, in the shared memory of CTA `owner` of the cluster.
+__device__ __forceinline__ int line_offset(int owner, int r, int slice, int nsrc, int me, int dsmem)
+{
+    return dsmem ? (owner << 24) | ((me * slice + r) * 16) : ((owner * nsrc + me) * slice + r) * 4;
+}
+
+struct BlockCopy {  // one copy (rows or columns) of the CTA's block in shared memory (shared-window addresses)
+    uint32_t ell;     // u16 per entry: local index into the gathered slice
+    uint32_t ref;     // column copy: u16 per entry, position in `val` (row copy: 0, the entry's own position)
+    uint32_t lov;     // u16 per sorted position: local line
+    uint32_t off;     // int per sorted position: word offset of the line's two sums in the exchange
+    uint32_t chunk;   // int pairs (first slot, width) per 32-line chunk
+    uint32_t heavy;   // int triples (line, first entry, length) per heavy line
+    uint32_t hoff;    // int per heavy line: word offset in the exchange
+    uint32_t hfirst;  // int per heavy line: its first segment
+    uint32_t hseg;    // int per segment: heavy line
     int nv, nch, nsl, nhv, nseg;
+    int pad_lo, pad_hi, slice, nsrc, me;  // lines [pad_lo, pad_hi) exist only as padding of the last owner's slice: posted as zeros
+    int dsmem;  // the sums go to the owner's shared memory: `off` holds owner rank << 24 | byte offset into its buffer
+    uint32_t xlocal, mbar;  // that buffer and its barrier at their addresses in THIS CTA (same offsets in every CTA)
+    int self_rank;          // >= 0: every line is owned by this CTA itself (single cluster, column copy); else owner = line / slice
 };
+
+__device__ __forceinline__ void post_line(const BlockCopy& B, u64* xbase, int off, double a0, double a1, unsigned int round)
+{
+    if (B.dsmem) {
+        const int owner = (unsigned)off >> 24;
+        st_async_f64x2(map_rank(B.xlocal + (uint32_t)(off & 0xffffff), owner), a0, a1, map_rank(B.mbar, owner));
+    } else {
+        fw_post(xbase + off, a0, round);
+        fw_post(xbase + off + 2, a1, round);
+    }
+}
 
 // One mat-vec phase over the CTA's block: lines are the block's rows and `vec` the z (or x) slice of the block
 // column, or lines are its columns and `vec` the t slice of the block row.  Work items: segments of heavy lines
 // first, then the 32-line chunks by decreasing width.  Each finished line's two sums are posted as flagged words where the owner of the
-// line's slice expects them; with zvec != null (column phase) z . (B' t) is accumulated per system into dc[0..1]
-// of this thread.
-__device__ __noinline__ void block_phase(const BlockCopy* Bp, const double* __restrict__ val, int zero_slot,
-                                         const double2* __restrict__ vec, const double2* __restrict__ zvec, u64* xbase,
-                                         unsigned int round, double2* hpart, double* dc)
+// line's slice expects them; with zvec != 0 (column phase) z . (B' t) is accumulated per system into dc[0..1]
+// of this thread.  val, vec, zvec, hpart: shared-window addresses.
+__device__ __noinline__ void block_phase(uint32_t Bp, uint32_t val, int zero_slot, uint32_t vec, uint32_t zvec, u64* xbase,
+                                         unsigned int round, uint32_t hpart, double* dc)
 {
-    const BlockCopy B = *Bp;
+    BlockCopy B;
+    {
+        uint32_t* w = reinterpret_cast<uint32_t*>(&B);
+#pragma unroll
+        for (int k = 0; k < (int)(sizeof(BlockCopy) / 4); ++k) w[k] = (uint32_t)lds_s32(Bp + 4 * k);
+    }
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int total = B.nseg + B.nch;
     double dc0 = 0.0, dc1 = 0.0;
@@ -445,22 +534,24 @@ __device__ __noinline__ void block_phase(const BlockCopy* Bp, const double* __re
         if (item >= total) continue;
         double a0 = 0.0, a1 = 0.0;
         if (item < B.nseg) {
-            const int h = B.hseg[item], sidx = item - B.hfirst[h];
-            const int beg = B.nsl + B.heavy[3 * h + 1] + sidx * kB2Seg, len = min(kB2Seg, B.heavy[3 * h + 2] - sidx * kB2Seg);
+            const int h = lds_s32(B.hseg + 4 * item), sidx = item - lds_s32(B.hfirst + 4 * h);
+            const int beg = B.nsl + lds_s32(B.heavy + 12 * h + 4) + sidx * kB2Seg;
+            const int len = min(kB2Seg, lds_s32(B.heavy + 12 * h + 8) - sidx * kB2Seg);
+#pragma unroll 2
             for (int t = lane; t < len; t += 32) {
                 const int s = beg + t;
-                const double v = val[B.ref ? (int)B.ref[s] : s];
-                const double2 g = vec[B.ell[s]];
+                const double v = lds_f64(val + 8u * (uint32_t)(B.ref ? lds_u16(B.ref + 2 * s) : s));
+                const double2 g = lds_f64x2(vec + 16u * (uint32_t)lds_u16(B.ell + 2 * s));
                 a0 = __fma_rn(v, g.x, a0);
                 a1 = __fma_rn(v, g.y, a1);
             }
             a0 = warp_sum(a0);
             a1 = warp_sum(a1);
-            if (lane == 0) hpart[item] = make_double2(a0, a1);
+            if (lane == 0) sts_f64x2_b(hpart + 16u * (uint32_t)item, a0, a1);
             continue;
         }
         const int c = item - B.nseg;
-        const int base = B.chunk[2 * c] + lane, w = B.chunk[2 * c + 1];
+        const int base = lds_s32(B.chunk + 8 * c) + lane, w = lds_s32(B.chunk + 8 * c + 4);
 #pragma unroll 1
         for (int k0 = 0; k0 < w; k0 += 4) {
             int ix[4], vi[4];
@@ -468,26 +559,24 @@ __device__ __noinline__ void block_phase(const BlockCopy* Bp, const double* __re
             for (int u = 0; u < 4; ++u) {
                 const int s = base + 32 * (k0 + u);
                 const bool ok = k0 + u < w;
-                const int raw = B.ell[s];
+                const int raw = lds_u16(B.ell + 2 * s);
                 ix[u] = ok ? raw : 0;
-                const int rr = B.ref ? (int)B.ref[s] : s;
+                const int rr = B.ref ? lds_u16(B.ref + 2 * s) : s;
                 vi[u] = ok ? rr : zero_slot;
             }
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                const double v = val[vi[u]];
-                const double2 g = vec[ix[u]];
+                const double v = lds_f64(val + 8u * (uint32_t)vi[u]);
+                const double2 g = lds_f64x2(vec + 16u * (uint32_t)ix[u]);
                 a0 = __fma_rn(v, g.x, a0);
                 a1 = __fma_rn(v, g.y, a1);
             }
         }
         const int vpos = 32 * c + lane;
         if (vpos < B.nv) {
-            u64* w2 = xbase + B.off[vpos];
-            fw_post(w2, a0, round);
-            fw_post(w2 + 2, a1, round);
+            post_line(B, xbase, lds_s32(B.off + 4 * vpos), a0, a1, round);
             if (zvec) {
-                const double2 z = zvec[B.lov[vpos]];
+                const double2 z = lds_f64x2(zvec + 16u * (uint32_t)lds_u16(B.lov + 2 * vpos));
                 dc0 = __fma_rn(z.x, a0, dc0);
                 dc1 = __fma_rn(z.y, a1, dc1);
             }
@@ -495,21 +584,28 @@ __device__ __noinline__ void block_phase(const BlockCopy* Bp, const double* __re
     }
     if (B.nhv > 0) {  // uniform over the CTA
         __syncthreads();
+#pragma unroll 1
         for (int h = threadIdx.x; h < B.nhv; h += kB2Threads) {
             double a0 = 0.0, a1 = 0.0;
-            for (int sg = B.hfirst[h]; sg < B.hfirst[h + 1]; ++sg) {
-                a0 += hpart[sg].x;
-                a1 += hpart[sg].y;
+            const int sg1 = lds_s32(B.hfirst + 4 * h + 4);
+#pragma unroll 1
+            for (int sg = lds_s32(B.hfirst + 4 * h); sg < sg1; ++sg) {
+                const double2 hp = lds_f64x2(hpart + 16u * (uint32_t)sg);
+                a0 += hp.x;
+                a1 += hp.y;
             }
-            u64* w2 = xbase + B.hoff[h];
-            fw_post(w2, a0, round);
-            fw_post(w2 + 2, a1, round);
+            post_line(B, xbase, lds_s32(B.hoff + 4 * h), a0, a1, round);
             if (zvec) {
-                const double2 z = zvec[B.heavy[3 * h]];
+                const double2 z = lds_f64x2(zvec + 16u * (uint32_t)lds_s32(B.heavy + 12 * h));
                 dc0 = __fma_rn(z.x, a0, dc0);
                 dc1 = __fma_rn(z.y, a1, dc1);
             }
         }
+    }
+#pragma unroll 1
+    for (int line = B.pad_lo + threadIdx.x; line < B.pad_hi; line += kB2Threads) {
+        const int o = line / B.slice;
+        post_line(B, xbase, line_offset(B.self_rank >= 0 ? B.self_rank : o, line - o * B.slice, B.slice, B.nsrc, B.me, B.dsmem), 0.0, 0.0, round);
     }
     dc[0] = dc0;
     dc[1] = dc1;
@@ -534,7 +630,39 @@ __device__ __forceinline__ double block_sum8(const double (&v)[8], double* scrat
     return d;
 }
 static_assert(kB2Warps == 16, "block_sum8 folds 16 warps per component");
-static_assert(2 * sizeof(BlockCopy) <= 256, "descriptor area of the shared-memory plan");
+// the CTA's 8 partial dot products -> its slots of the X5 exchange; the first four (gamma, sum dB z^2) are also kept
+// in bcast[8..11]: they stay valid until the owner's next update
+__device__ __noinline__ void post_dots(const double* part, double* scratch, double* bcast, u64* x5_mine, int ndst, uint32_t stage_mine,
+                                       uint32_t mbar, unsigned int round)
+{
+    double v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = part[k];
+    const double mine = block_sum8(v, scratch);
+    const int tid = threadIdx.x;
+    if (tid < 8 * kB2Warps && (tid & (kB2Warps - 1)) == 0) {
+        const int k = tid / kB2Warps;
+        if (ndst == 0) fw_post(x5_mine + k * 2, mine, round);
+#pragma unroll 1
+        for (int dst = 0; dst < ndst; ++dst)  // single cluster: straight into everybody's staging area
+            st_async_f64(map_rank(stage_mine + 8u * (uint32_t)k, dst), mine, map_rank(mbar, dst));
+        if (k < 4) bcast[8 + k] = mine;
+    }
+}
+static_assert(2 * sizeof(BlockCopy) <= 256 && sizeof(BlockCopy) % 4 == 0, "descriptor area of the shared-memory plan");
+
+// Owners publish their slice of a beta-space vector (z, or the solution x) and every CTA collects its block
+// column's; with a single cluster (P == 1) the owner of the block column is this CTA and the slice is simply copied.
+__device__ __forceinline__ void publish_slice(bool local, u64* column, int first, const double* src, int n_mine, double* dst,
+                                              int n_all, unsigned int round)
+{
+    if (local) {
+        for (int item = threadIdx.x; item < n_mine; item += kB2Threads) dst[item] = src[item];
+        return;
+    }
+    for (int item = threadIdx.x; item < n_mine; item += kB2Threads) fw_post(column + 2 * (size_t)(first + item), src[item], round);
+    fw_gather(column, dst, n_all, round);
+}
 
 // Why a single buffer per exchange is enough (a word is awaited by exact round number, so a writer must
 // not get a round ahead of a reader): round r + 1 writes of X4 follow the owner's update, which needs every
@@ -565,13 +693,27 @@ __global__ void __launch_bounds__(kB2Threads, 1) k_pcg_blocks(const __grid_const
     const int segcap_r = h[kH_NHE_R] / kB2Seg + Br.nhv, segcap_c = h[kH_NHE_C] / kB2Seg + Bc.nhv;
 
     // ---- shared-memory carve-up (b2_smem_need) ----
+    // What other CTAs of the cluster write into comes first: its offsets depend on the grid only, so a remote CTA
+    // finds it at the same place in my shared memory as in its own.  Everything sized by this block follows.
+    const bool cl = A.cluster != 0, one = cl && P == 1;
     unsigned char* sp = smem;
-    double* val = reinterpret_cast<double*>(sp);
-    sp += ((nval + 1) * 8 + 15) & ~15;
-    double2* vecz = reinterpret_cast<double2*>(sp);
-    sp += 16 * (size_t)A.C;
+    // barriers of the exchanges that stay inside the cluster: row partial sums -> xbuf1, t -> vect, (single cluster:)
+    // column partial sums -> xbuf3, dot products -> stage
+    uint64_t* mbars = reinterpret_cast<uint64_t*>(sp);
+    sp += 64;
+    const uint32_t mb1 = smem_u32(mbars), mb2 = mb1 + 8, mb3 = mb1 + 16, mb5 = mb1 + 24;
+    uint32_t ph1 = 0, ph2 = 0, ph3 = 0, ph5 = 0;
     double2* vect = reinterpret_cast<double2*>(sp);
     sp += 16 * (size_t)A.R;
+    double* xbuf1 = reinterpret_cast<double*>(sp);  // partial sums collected by the owner: Q x 2 SR of its rows ...
+    double* xbuf3 = xbuf1 + (cl ? 2 * Q * SR : 0);  // ... and P x 2 SC of its columns (one buffer when both come through L2)
+    sp += 8 * (size_t)b2_xbuf_doubles(SR, SC, P, Q, A.cluster);
+    double* stage = reinterpret_cast<double*>(sp);  // 8 G: everybody's partial dot products
+    sp += 8 * (size_t)(8 * G);
+    double2* vecz = reinterpret_cast<double2*>(sp);
+    sp += 16 * (size_t)A.C;
+    double* val = reinterpret_cast<double*>(sp);
+    sp += ((nval + 1) * 8 + 15) & ~15;
     double2* hpart = reinterpret_cast<double2*>(sp);
     sp += 16 * (size_t)max(segcap_r, segcap_c);
     u16* s16 = reinterpret_cast<u16*>(sp);
@@ -581,41 +723,42 @@ __global__ void __launch_bounds__(kB2Threads, 1) k_pcg_blocks(const __grid_const
     const int n_derived = Br.nv + Bc.nv + 2 * (Br.nhv + Bc.nhv) + 2 + segcap_r + segcap_c + 4;
     sp += ((n_tables + n_derived) * 4 + 15) & ~15;
     double* own = reinterpret_cast<double*>(sp);  // z p s x r w of the owned column slice (x2), 1/dB of it, 1/dA of the owned row slice
-    sp += 8 * (size_t)(6 * 2 * SC + SC + SR);
-    double* xbuf = reinterpret_cast<double*>(sp);  // partial sums collected by the owner: Q x 2 SR or P x 2 SC
-    sp += 8 * (size_t)max(Q * 2 * SR, P * 2 * SC);
-    double* stage = reinterpret_cast<double*>(sp);  // 8 G: everybody's partial dot products
-    sp += 8 * (size_t)(8 * G);
+    sp += 8 * (size_t)(6 * 2 * SC + 2 * SC + SR);
     double* bcast = reinterpret_cast<double*>(sp);  // 8 totals, my own 4 partials, then block_sum scratch
     double* scratch = bcast + 16;
     BlockCopy* s_copy = reinterpret_cast<BlockCopy*>(scratch + 8 * kB2Warps);  // the two copies' descriptors, read by block_phase
     double *oz = own, *op = own + 2 * SC, *os = own + 4 * SC, *ox = own + 6 * SC, *orr = own + 8 * SC, *ow = own + 10 * SC,
-           *oib = own + 12 * SC, *oia = own + 13 * SC;
+           *oib = own + 12 * SC, *odb = own + 13 * SC, *oia = own + 14 * SC;
     int* tb = s32;
-    Br.chunk = tb;
+    int* const chunk_r = tb;
     tb += 2 * Br.nch;
-    Br.heavy = tb;
+    int* const heavy_r = tb;
     tb += 3 * Br.nhv;
-    Bc.chunk = tb;
+    int* const chunk_c = tb;
     tb += 2 * Bc.nch;
-    Bc.heavy = tb;
+    int* const heavy_c = tb;
     tb += 3 * Bc.nhv;
     int *off_r = tb, *off_c = off_r + Br.nv, *hoff_r = off_c + Bc.nv, *hoff_c = hoff_r + Br.nhv, *hfirst_r = hoff_c + Bc.nhv,
         *hfirst_c = hfirst_r + Br.nhv + 1, *hseg_r = hfirst_c + Bc.nhv + 1, *hseg_c = hseg_r + segcap_r;
-    Br.ell = s16 + L16.ell_r;
-    Br.ref = nullptr;
-    Br.lov = s16 + L16.lov_r;
-    Br.off = off_r;
-    Br.hoff = hoff_r;
-    Br.hfirst = hfirst_r;
-    Br.hseg = hseg_r;
-    Bc.ell = s16 + L16.ell_c;
-    Bc.ref = s16 + L16.ref_c;
-    Bc.lov = s16 + L16.lov_c;
-    Bc.off = off_c;
-    Bc.hoff = hoff_c;
-    Bc.hfirst = hfirst_c;
-    Bc.hseg = hseg_c;
+    const u16 *lov_r = s16 + L16.lov_r, *lov_c = s16 + L16.lov_c;
+    Br.ell = smem_u32(s16 + L16.ell_r);
+    Br.ref = 0;
+    Br.lov = smem_u32(lov_r);
+    Br.off = smem_u32(off_r);
+    Br.chunk = smem_u32(chunk_r);
+    Br.heavy = smem_u32(heavy_r);
+    Br.hoff = smem_u32(hoff_r);
+    Br.hfirst = smem_u32(hfirst_r);
+    Br.hseg = smem_u32(hseg_r);
+    Bc.ell = smem_u32(s16 + L16.ell_c);
+    Bc.ref = smem_u32(s16 + L16.ref_c);
+    Bc.lov = smem_u32(lov_c);
+    Bc.off = smem_u32(off_c);
+    Bc.chunk = smem_u32(chunk_c);
+    Bc.heavy = smem_u32(heavy_c);
+    Bc.hoff = smem_u32(hoff_c);
+    Bc.hfirst = smem_u32(hfirst_c);
+    Bc.hseg = smem_u32(hseg_c);
 
     // ---- the block: structure from the arenas, values from the CSR of B ----
     {
@@ -641,50 +784,76 @@ __global__ void __launch_bounds__(kB2Threads, 1) k_pcg_blocks(const __grid_const
     __syncthreads();
     // where each line's sums go: rows -> [owner = line / SR][source q][line % SR][2], columns likewise with P, SC
     for (int v = tid; v < Br.nv; v += kB2Threads) {
-        const int line = Br.lov[v], o = line / SR;
-        off_r[v] = ((o * Q + q) * SR + (line - o * SR)) * 4;
+        const int line = lov_r[v], o = line / SR;
+        off_r[v] = line_offset(o, line - o * SR, SR, Q, q, cl);
     }
     for (int v = tid; v < Bc.nv; v += kB2Threads) {
-        const int line = Bc.lov[v], o = line / SC;
-        off_c[v] = ((o * P + p) * SC + (line - o * SC)) * 4;
+        const int line = lov_c[v], o = line / SC;
+        off_c[v] = line_offset(one ? q : o, line - o * SC, SC, P, p, one);
     }
     for (int hh = tid; hh < Br.nhv; hh += kB2Threads) {
-        const int line = Br.heavy[3 * hh], o = line / SR;
-        hoff_r[hh] = ((o * Q + q) * SR + (line - o * SR)) * 4;
+        const int line = heavy_r[3 * hh], o = line / SR;
+        hoff_r[hh] = line_offset(o, line - o * SR, SR, Q, q, cl);
     }
     for (int hh = tid; hh < Bc.nhv; hh += kB2Threads) {
-        const int line = Bc.heavy[3 * hh], o = line / SC;
-        hoff_c[hh] = ((o * P + p) * SC + (line - o * SC)) * 4;
+        const int line = heavy_c[3 * hh], o = line / SC;
+        hoff_c[hh] = line_offset(one ? q : o, line - o * SC, SC, P, p, one);
     }
     if (tid < 2) {  // segments of the heavy lines: thread 0 the rows', thread 1 the columns'
-        const BlockCopy& B = tid == 0 ? Br : Bc;
+        const int nhv = tid == 0 ? Br.nhv : Bc.nhv;
+        const int* hv = tid == 0 ? heavy_r : heavy_c;
         int* hf = tid == 0 ? hfirst_r : hfirst_c;
         int* hs = tid == 0 ? hseg_r : hseg_c;
         int n = 0;
-        for (int hh = 0; hh < B.nhv; ++hh) {
+        for (int hh = 0; hh < nhv; ++hh) {
             hf[hh] = n;
-            const int cnt = (B.heavy[3 * hh + 2] + kB2Seg - 1) / kB2Seg;
+            const int cnt = (hv[3 * hh + 2] + kB2Seg - 1) / kB2Seg;
             for (int k = 0; k < cnt; ++k) hs[n++] = hh;
         }
-        hf[B.nhv] = n;
+        hf[nhv] = n;
     }
     __syncthreads();
     if (tid == 0) {
         Br.nseg = hfirst_r[Br.nhv];
         Bc.nseg = hfirst_c[Bc.nhv];
+        Br.pad_lo = Rp;
+        Br.pad_hi = Q * SR;
+        Br.slice = SR;
+        Br.nsrc = Q;
+        Br.me = q;
+        Br.dsmem = cl;
+        Br.xlocal = smem_u32(xbuf1);
+        Br.mbar = mb1;
+        Br.self_rank = -1;
+        Bc.dsmem = one;  // a single cluster has P == 1: the owner of my columns is this CTA itself
+        Bc.xlocal = smem_u32(xbuf3);
+        Bc.mbar = mb3;
+        Bc.self_rank = one ? q : -1;
+        Bc.pad_lo = Cq;
+        Bc.pad_hi = P * SC;
+        Bc.slice = SC;
+        Bc.nsrc = P;
+        Bc.me = p;
         s_copy[0] = Br;
         s_copy[1] = Bc;
+    }
+
+    if (cl && tid == 0) {
+        for (int k = 0; k < 4; ++k) mbar_init(mbars + k, 1);
+        fence_mbar_init();
     }
 
     // owned slices: local rows [r_lo, r_hi) of block row p, local columns [c_lo, c_hi) of block column q
     const int r_lo = min(q * SR, Rp), r_hi = min(r_lo + SR, Rp), c_lo = min(p * SC, Cq), c_hi = min(c_lo + SC, Cq);
     const int n_own_r = r_hi - r_lo, n_own_c = c_hi - c_lo;
-    u64* const x1_mine = A.x1 + (size_t)(p * Q) * Q * SR * 4;          // block row p: [owner][source q][SR][2] doubles
-    u64* const x1_own = x1_mine + (size_t)q * Q * SR * 4;               // what I sum as owner q
-    u64* const x2_row = A.x2 + (size_t)p * A.R * 4;                     // t of block row p: [R][2]
-    u64* const x3_mine = A.x3 + (size_t)(q * P) * P * SC * 4;          // block column q: [owner][source p][SC][2]
+    // through L2: block row p of X1 is [owner][source q][SR][2] doubles, X2 [R][2]; block column q of X3 is
+    // [owner][source p][SC][2], X4 [C][2]
+    u64* const x1_mine = A.x1 + (size_t)(p * Q) * Q * SR * 4;
+    u64* const x1_own = x1_mine + (size_t)q * Q * SR * 4;  // what I sum as owner q
+    u64* const x2_row = A.x2 + (size_t)p * A.R * 4;
+    u64* const x3_mine = A.x3 + (size_t)(q * P) * P * SC * 4;
     u64* const x3_own = x3_mine + (size_t)p * P * SC * 4;
-    u64* const x4_col = A.x4 + (size_t)q * A.C * 4;                     // z of block column q: [C][2]
+    u64* const x4_col = A.x4 + (size_t)q * A.C * 4;
 
     // ---- t = D1^-1 r_a on my block row; the alpha part of r' D^-1 r over my row slice ----
     double part[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};  // gamma[2], sum dB z^2 [2], z.(B't) [2], r'D^-1 r [2]
@@ -700,8 +869,13 @@ __global__ void __launch_bounds__(kB2Threads, 1) k_pcg_blocks(const __grid_const
         }
         vect[li] = make_double2(t0, t1);
     }
-    for (int c = tid; c < n_own_c; c += kB2Threads) oib[c] = 1.0 / __ldg(A.dB + q + (c_lo + c) * Q);
+    for (int c = tid; c < n_own_c; c += kB2Threads) {
+        const double d = __ldg(A.dB + q + (c_lo + c) * Q);
+        odb[c] = d;
+        oib[c] = 1.0 / d;
+    }
     __syncthreads();
+    if (cl) cooperative_groups::this_cluster().sync();  // every inbox of the cluster is cleared before the first post
 
 #ifdef REGOT_PCG_TIMING  // per-section cycle counts per CTA (experiments only)
     long long tsec[8] = {0, 0, 0, 0, 0, 0, 0, 0}, tprev = clock64();
@@ -715,46 +889,60 @@ __global__ void __launch_bounds__(kB2Threads, 1) k_pcg_blocks(const __grid_const
 #else
 #define B2_TICK(i)
 #endif
-    double gamma[2] = {0.0, 0.0}, gamma0[2] = {0.0, 0.0}, gamma_old[2] = {1.0, 1.0}, alpha_old[2] = {1.0, 1.0};
-    bool done[2] = {false, false}, broke = false;
-    int iters[2] = {0, 0}, it = 0;
+    // every thread keeps the CG scalars of ONE system, k = tid & 1 (the parity of the items it owns); flags are
+    // exchanged inside the lane pair, so control flow is uniform and each division is compiled once
+    const int myk = tid & 1;
+    double gam = 0.0, gam0 = 0.0, gam_old = 1.0, al_old = 1.0;
+    bool done_mine = false, done_other = false, broke = false;
+    int it_mine = 0, it = 0;
     bool init = true;
     unsigned int round = A.round0;
 #pragma unroll 1
     for (;; ++round) {
         if (!init) {
             // owners publish z of their column slice; everybody collects its block column's
-            for (int item = tid; item < 2 * n_own_c; item += kB2Threads) fw_post(x4_col + ((size_t)c_lo * 2 + item) * 2, oz[item], round);
-            fw_gather(x4_col, reinterpret_cast<double*>(vecz), 2 * Cq, 1, 0, round);
+            publish_slice(one, x4_col, 2 * c_lo, oz, 2 * n_own_c, reinterpret_cast<double*>(vecz), 2 * Cq, round);
             __syncthreads();
             B2_TICK(0)
-            block_phase(&s_copy[0], val, nval, vecz, nullptr, x1_mine, round, hpart, bcast + 12);
+            block_phase(smem_u32(&s_copy[0]), smem_u32(val), nval, smem_u32(vecz), 0u, x1_mine, round, smem_u32(hpart), bcast + 12);
             B2_TICK(1)
             // owner: the Q partials of my rows, summed in block order; t = D1^-1 sum goes to the block row
-            fw_gather(x1_own, xbuf, 2 * n_own_r, Q, 2 * SR, round);
+            if (cl) cluster_inbox_wait(mb1, 16u * (uint32_t)(Q * SR), ph1);
+            else fw_gather(x1_own, xbuf1, Q * 2 * SR, round);
             __syncthreads();
             for (int item = tid; item < 2 * n_own_r; item += kB2Threads) {
                 double s = 0.0;
-                for (int src = 0; src < Q; ++src) s += xbuf[src * 2 * n_own_r + item];
-                fw_post(x2_row + ((size_t)r_lo * 2 + item) * 2, s * oia[item >> 1], round);
+#pragma unroll 1
+                for (int src = 0; src < Q; ++src) s += xbuf1[src * 2 * SR + item];
+                const double tv = s * oia[item >> 1];
+                if (!cl) fw_post(x2_row + ((size_t)r_lo * 2 + item) * 2, tv, round);
+#pragma unroll 1
+                for (int dst = 0; dst < (cl ? Q : 0); ++dst)  // straight into the t slice of every CTA of the block row
+                    st_async_f64(map_rank(smem_u32(vect) + 8u * (uint32_t)(r_lo * 2 + item), dst), tv, map_rank(mb2, dst));
             }
             B2_TICK(2)
-            fw_gather(x2_row, reinterpret_cast<double*>(vect), 2 * Rp, 1, 0, round);
+            if (cl) cluster_inbox_wait(mb2, 16u * (uint32_t)Rp, ph2);
+            else fw_gather(x2_row, reinterpret_cast<double*>(vect), 2 * Rp, round);
             __syncthreads();
             B2_TICK(3)
         }
         // column phase: partial B' t of my block; z . (B' t) rides along
-        block_phase(&s_copy[1], val, nval, vect, vecz, x3_mine, round, hpart, part + 4);
+        block_phase(smem_u32(&s_copy[1]), smem_u32(val), nval, smem_u32(vect), smem_u32(vecz), x3_mine, round, smem_u32(hpart), part + 4);
         if (init) part[4] = part[5] = 0.0;
         B2_TICK(4)
+        // everybody's partial dot products are known here (except in the set-up pass): their exchange overlaps the
+        // exchange of the column partial sums
+        if (!init) post_dots(part, scratch, bcast, A.x5 + (size_t)b * 16, one ? Q : 0, smem_u32(stage + 8 * b), mb5, round);
         // owner: u = sum of the P partials of my columns, then the new r/z (set-up) or w = D2 z - u
-        fw_gather(x3_own, xbuf, 2 * n_own_c, P, 2 * SC, round);
+        if (one) cluster_inbox_wait(mb3, 16u * (uint32_t)(P * SC), ph3);
+        else fw_gather(x3_own, xbuf3, P * 2 * SC, round);
         __syncthreads();
         for (int item = tid; item < 2 * n_own_c; item += kB2Threads) {
             const int c = item >> 1, k = item & 1;
             double u = 0.0;
-            for (int src = 0; src < P; ++src) u += xbuf[src * 2 * n_own_c + item];
-            const double inv = oib[c], d = __ldg(A.dB + q + (c_lo + c) * Q);
+            #pragma unroll 1
+            for (int src = 0; src < P; ++src) u += xbuf3[src * 2 * SC + item];
+            const double inv = oib[c], d = odb[c];
             if (init) {
                 const double rb = k < nrhs ? __ldg((k ? A.rhs_b[1] : A.rhs_b[0]) + q + (c_lo + c) * Q) : 0.0;
                 const double r = rb - u, z = r * inv;  // Schur right-hand side
@@ -778,18 +966,13 @@ __global__ void __launch_bounds__(kB2Threads, 1) k_pcg_blocks(const __grid_const
             }
         }
         B2_TICK(5)
-        // everybody's partial dot products, summed in CTA order
-        {
-            const double mine = block_sum8(part, scratch);
-            if (tid < 8 * kB2Warps && (tid & (kB2Warps - 1)) == 0) {
-                fw_post(A.x5 + ((size_t)b * 8 + tid / kB2Warps) * 2, mine, round);
-                if (tid < 4 * kB2Warps) bcast[8 + tid / kB2Warps] = mine;  // my partials of gamma and sum dB z^2 stay valid until my next update
-            }
-        }
-        fw_gather(A.x5, stage, 8 * G, 1, 0, round);
+        if (init) post_dots(part, scratch, bcast, A.x5 + (size_t)b * 16, one ? Q : 0, smem_u32(stage + 8 * b), mb5, round);
+        if (one) cluster_inbox_wait(mb5, 64u * (uint32_t)G, ph5);
+        else fw_gather(A.x5, stage, 8 * G, round);
         __syncthreads();
         if (warp < 8) {
             double s = 0.0;
+#pragma unroll 1
             for (int c = lane; c < G; c += 32) s += stage[c * 8 + warp];
             s = warp_sum(s);
             if (lane == 0) bcast[warp] = s;
@@ -804,54 +987,53 @@ __global__ void __launch_bounds__(kB2Threads, 1) k_pcg_blocks(const __grid_const
         B2_TICK(6)
 
         if (init) {
-#pragma unroll
-            for (int k = 0; k < 2; ++k) {
-                gamma[k] = tot[k];
-                gamma0[k] = tot[6 + k];
-                done[k] = (k >= nrhs) || gamma0[k] == 0.0 || !(gamma[k] > A.tol2 * gamma0[k]);
-                if (A.fixed_iters > 0 && k < nrhs) done[k] = false;
-            }
+            gam = myk ? tot[1] : tot[0];
+            gam0 = myk ? tot[7] : tot[6];
+            done_mine = (myk >= nrhs) || gam0 == 0.0 || !(gam > A.tol2 * gam0);
+            if (A.fixed_iters > 0 && myk < nrhs) done_mine = false;
+            done_other = __shfl_xor_sync(0xffffffffu, done_mine, 1);
             if (tid == 0) {
 #pragma unroll
                 for (int k = 0; k < 4; ++k) part[k] = bcast[8 + k];
             }
             init = false;
         } else {
-            double al[2], be[2];
-#pragma unroll
-            for (int k = 0; k < 2; ++k) {
-                al[k] = be[k] = 0.0;
-                if (done[k]) continue;
-                gamma[k] = tot[k];
-                if (it > 0 && !(gamma[k] > A.tol2 * gamma0[k]) && A.fixed_iters == 0) {
-                    done[k] = true;
-                    continue;
+            double al = 0.0, be = 0.0;
+            bool brk = false;
+            if (!done_mine) {
+                gam = myk ? tot[1] : tot[0];
+                if (it > 0 && !(gam > A.tol2 * gam0) && A.fixed_iters == 0) {
+                    done_mine = true;
+                } else {
+                    const double delta = (myk ? tot[3] : tot[2]) - (myk ? tot[5] : tot[4]);  // z'D2 z - z'B'D1^-1 B z
+                    // beta = gamma / gamma_old; p'Sp = delta - beta gamma / alpha_old, with the two quotients independent
+                    const double g_over_a = gam / al_old;
+                    be = (it == 0) ? 0.0 : gam / gam_old;
+                    const double denom = delta - be * g_over_a;
+                    if (!(denom > 0.0) && A.fixed_iters == 0) brk = true;     // not positive definite (or NaN)
+                    al = gam / denom;
+                    gam_old = gam;
+                    al_old = al;
+                    ++it_mine;
                 }
-                const double delta = tot[2 + k] - tot[4 + k];  // z'D2 z - z'B'D1^-1 B z
-                be[k] = (it == 0) ? 0.0 : gamma[k] / gamma_old[k];
-                const double denom = delta - be[k] * gamma[k] / alpha_old[k];  // = p'Sp
-                if (!(denom > 0.0) && A.fixed_iters == 0) broke = true;        // not positive definite (or NaN)
-                al[k] = gamma[k] / denom;
-                gamma_old[k] = gamma[k];
-                alpha_old[k] = al[k];
-                ++iters[k];
             }
             ++it;
-            if (!broke && !(done[0] && done[1])) {
-                // p = z + beta p, s = w + beta s, x += alpha p, r -= alpha s, z = D2^-1 r on the owned slice
+            done_other = __shfl_xor_sync(0xffffffffu, done_mine, 1);
+            broke = brk || __shfl_xor_sync(0xffffffffu, brk, 1);
+            if (!broke && !done_mine) {
+                // p = z + beta p, s = w + beta s, x += alpha p, r -= alpha s, z = D2^-1 r on the owned slice (a finished
+                // system is frozen; its partials are not used any more)
+#pragma unroll 1
                 for (int item = tid; item < 2 * n_own_c; item += kB2Threads) {
-                    const int k = item & 1;
-                    if (k ? done[1] : done[0]) continue;  // a finished system is frozen; its partials are not used any more
-                    const double bek = k ? be[1] : be[0], alk = k ? al[1] : al[0];
-                    const double inv = oib[item >> 1], d = __ldg(A.dB + q + (c_lo + (item >> 1)) * Q);
-                    const double pn = oz[item] + bek * op[item], sn = ow[item] + bek * os[item];
-                    const double xn = ox[item] + alk * pn, rn = orr[item] - alk * sn, zn = rn * inv;
+                    const double inv = oib[item >> 1], d = odb[item >> 1];
+                    const double pn = oz[item] + be * op[item], sn = ow[item] + be * os[item];
+                    const double xn = ox[item] + al * pn, rn = orr[item] - al * sn, zn = rn * inv;
                     op[item] = pn;
                     os[item] = sn;
                     ox[item] = xn;
                     orr[item] = rn;
                     oz[item] = zn;
-                    if (k) {
+                    if (myk) {
                         part[1] += rn * zn;
                         part[3] += d * zn * zn;
                     } else {
@@ -862,7 +1044,7 @@ __global__ void __launch_bounds__(kB2Threads, 1) k_pcg_blocks(const __grid_const
             }
         }
         B2_TICK(7)
-        bool all_done = done[0] && done[1];
+        bool all_done = done_mine && done_other;
         if (A.fixed_iters > 0) all_done = it >= A.fixed_iters;
         if (all_done || broke || it >= A.max_iter) break;
     }
@@ -875,21 +1057,25 @@ __global__ void __launch_bounds__(kB2Threads, 1) k_pcg_blocks(const __grid_const
     ++round;
     for (int item = tid; item < 2 * n_own_c; item += kB2Threads) {
         const int k = item & 1;
-        fw_post(x4_col + ((size_t)c_lo * 2 + item) * 2, ox[item], round);
         if (k < nrhs) (k ? A.sol_b[1] : A.sol_b[0])[q + (c_lo + (item >> 1)) * Q] = ox[item];
     }
-    fw_gather(x4_col, reinterpret_cast<double*>(vecz), 2 * Cq, 1, 0, round);
+    publish_slice(one, x4_col, 2 * c_lo, ox, 2 * n_own_c, reinterpret_cast<double*>(vecz), 2 * Cq, round);
     __syncthreads();
-    block_phase(&s_copy[0], val, nval, vecz, nullptr, x1_mine, round, hpart, bcast + 12);
-    fw_gather(x1_own, xbuf, 2 * n_own_r, Q, 2 * SR, round);
+    block_phase(smem_u32(&s_copy[0]), smem_u32(val), nval, smem_u32(vecz), 0u, x1_mine, round, smem_u32(hpart), bcast + 12);
+    if (cl) cluster_inbox_wait(mb1, 16u * (uint32_t)(Q * SR), ph1);
+    else fw_gather(x1_own, xbuf1, Q * 2 * SR, round);
     __syncthreads();
     for (int item = tid; item < 2 * n_own_r; item += kB2Threads) {
         const int k = item & 1, gi = p + (r_lo + (item >> 1)) * P;
         double s = 0.0;
-        for (int src = 0; src < Q; ++src) s += xbuf[src * 2 * n_own_r + item];
+        #pragma unroll 1
+                for (int src = 0; src < Q; ++src) s += xbuf1[src * 2 * SR + item];
         if (k < nrhs) (k ? A.sol_a[1] : A.sol_a[0])[gi] = (__ldg((k ? A.rhs_a[1] : A.rhs_a[0]) + gi) - s) / __ldg(A.dA + gi);
     }
+    if (cl) cooperative_groups::this_cluster().sync();  // nobody leaves while its shared memory may still be written or read
+    const int it_other = __shfl_xor_sync(0xffffffffu, it_mine, 1);
     if (b == 0 && tid == 0) {
+        const int iters[2] = {it_mine, it_other};
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
             if (k < nrhs) A.sol_b[k][A.mfree] = 0.0;
@@ -907,30 +1093,127 @@ __global__ void __launch_bounds__(kB2Threads, 1) k_pcg_blocks(const __grid_const
 // ---- host ---------------------------------------------------------------------------------------------------
 static int gcd_int(int a, int b) { return b ? gcd_int(b, a % b) : a; }
 
-// largest coprime P x Q <= sm_count with 8 <= Q <= 16 (block rows exchange among Q CTAs, block columns among P)
-static void pick_grid(const regot_ctx* ctx, int& P, int& Q)
+// How many clusters of `size` CTAs (one per SM, full shared-memory budget) the device can hold at once; 0: none
+static int max_clusters_of(int size)
 {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)size);
+    cfg.blockDim = dim3(kB2Threads);
+    cfg.dynamicSmemBytes = kPcgSmemBudget;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)size;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, (const void*)k_pcg_blocks, &cfg) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+static void set_kernel_attributes()
+{
+    static bool attr_set = false;
+    if (attr_set) return;
+    RG_CUDA(cudaFuncSetAttribute(k_pcg_blocks, cudaFuncAttributeMaxDynamicSharedMemorySize, kPcgSmemBudget));
+    RG_CUDA(cudaFuncSetAttribute(k_pcg_blocks, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    attr_set = true;
+}
+
+// host-side estimate of the shared-memory plan of one block (entries spread evenly, 8 % padding); the exact need is
+// only known once the plan is built
+static long estimate_smem(long nnz, long nloc, long mfree, int P, int Q, int cluster)
+{
+    const long G = (long)P * Q, R = (nloc + P - 1) / P, C = (mfree + Q - 1) / Q, SR = (R + Q - 1) / Q, SC = (C + P - 1) / P;
+    return (long)(1.08 * 14.0 * (double)nnz / (double)G) + 22 * (R + C) + 8 * b2_xbuf_doubles((int)SR, (int)SC, P, Q, cluster) +
+           8 * (14 * SC + SR) + 64 * G + 6144;
+}
+
+// The block grid: coprime P x Q <= sm_count.  Through L2: among the grids that use at least 93 % of the SMs the one
+// with the smallest plan (a tall pattern wants more block rows: slices of n / P rows and m / Q columns sit in every
+// CTA).  With clusters a block row is one cluster of Q CTAs (its exchanges stay in distributed shared memory), so P
+// is bounded by the number of clusters of that size the device holds at once (GPC by GPC); small patterns take ONE
+// cluster (P = 1): every exchange is then inside it.  Clusters only where the estimate says the plan fits.
+static void pick_grid(regot_ctx* ctx, long nnz, long nloc, long mfree, bool allow_cluster, int& P, int& Q, int& cluster)
+{
+    cluster = 0;
+    if (ctx->pcg_blocks_cluster != 0 && !ctx->pcg_blocks_probed) {
+        set_kernel_attributes();
+        for (int q = 2; q <= 16; ++q) ctx->pcg_blocks_maxcl[q] = max_clusters_of(q);
+        ctx->pcg_blocks_probed = true;
+        if (std::getenv("REGOT_B200_PCG_BLOCKS_INFO")) {
+            std::fprintf(stderr, "pcg blocks: clusters the device holds at once, by size 2..16:");
+            for (int q = 2; q <= 16; ++q) std::fprintf(stderr, " %d", ctx->pcg_blocks_maxcl[q]);
+            std::fprintf(stderr, "\n");
+        }
+    }
+    allow_cluster = allow_cluster && ctx->pcg_blocks_cluster != 0;
     if (ctx->pcg_blocks_p > 0 && ctx->pcg_blocks_q > 0) {
         P = ctx->pcg_blocks_p;
         Q = ctx->pcg_blocks_q;
+        cluster = allow_cluster && Q >= 2 && Q <= 16 && ctx->pcg_blocks_maxcl[Q] >= P;
         return;
     }
-    int best = 0;
+    const long budget = kPcgSmemBudget - kPcgSmemBudget / 16;  // the estimate must leave some room
+    int most = 0;
+    for (int q = 4; q <= 32; ++q)
+        for (int p = 4; p <= 32; ++p)
+            if (p * q <= ctx->sm_count && gcd_int(p, q) == 1) most = std::max(most, p * q);
     P = Q = 1;
-    for (int q = 8; q <= 16; ++q) {
-        int p = ctx->sm_count / q;
-        while (p > 1 && gcd_int(p, q) != 1) --p;
-        if (p * q >= best && p >= 1) {
-            best = p * q;
-            P = p;
-            Q = q;
+    long best = -1;
+    for (int q = 4; q <= 32; ++q)
+        for (int p = 4; p <= 32; ++p) {
+            if (p * q > ctx->sm_count || gcd_int(p, q) != 1 || p * q * 100 < most * 93) continue;
+            const long est = estimate_smem(nnz, nloc, mfree, p, q, 0);
+            if (best < 0 || est < best) {
+                best = est;
+                P = p;
+                Q = q;
+            }
         }
+    if (best < 0) {  // a device with very few SMs
+        P = 1;
+        Q = std::max(1, std::min(ctx->sm_count, 16));
+        return;
+    }
+    if (!allow_cluster) return;
+    if (nnz <= ctx->pcg_blocks_one_cluster_entries && ctx->pcg_blocks_maxcl[16] >= 1 && estimate_smem(nnz, nloc, mfree, 1, 16, 1) <= budget) {
+        P = 1;
+        Q = 16;
+        cluster = 1;
+        return;
+    }
+    // larger patterns are bound by their mat-vec phases, not by the exchanges: there the grid with more CTAs wins
+    if (nnz > ctx->pcg_blocks_cluster_entries) return;
+    int cg = 0, cp = 0, cq = 0;
+    long cest = 0;
+    for (int q = 4; q <= 16; ++q) {
+        int p = std::min(std::min(ctx->pcg_blocks_maxcl[q], ctx->sm_count / q), 32);
+        while (p > 1 && gcd_int(p, q) != 1) --p;
+        if (p < 2) continue;
+        const long est = estimate_smem(nnz, nloc, mfree, p, q, 1);
+        if (est > budget) continue;
+        if (p * q > cg || (p * q == cg && est < cest)) {
+            cg = p * q;
+            cp = p;
+            cq = q;
+            cest = est;
+        }
+    }
+    if (cg * 10 >= P * Q * 8) {  // a cluster grid that keeps at least 80 % as many SMs busy
+        P = cp;
+        Q = cq;
+        cluster = 1;
     }
 }
 
 // Build the block plan of the current pattern; everything is enqueued on st, the summary lands in pinned memory
 // (valid after the caller's next synchronisation with st).  csc2csr[t] = CSR position of CSC entry t.
-void build_pcg_blocks_plan(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, regot_sparse& S, const int* csc2csr)
+void build_pcg_blocks_plan(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, regot_sparse& S, const int* csc2csr, bool allow_cluster)
 {
     PcgBlocksPlan& Q2 = S.blocks;
     Q2.fits = false;
@@ -939,9 +1222,10 @@ void build_pcg_blocks_plan(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, regot_
     if (ctx->pcg_blocks == 0 || ctx->world != 1 || nnz < 1 || nloc < 64 || mfree < 64) return;
     // far too large for shared memory: do not even try (12 B per entry and copy at the very least)
     if ((long)nnz * 12 > (long)ctx->sm_count * kPcgSmemBudget) return;
-    int P, Q;
-    pick_grid(ctx, P, Q);
+    int P, Q, cluster;
+    pick_grid(ctx, nnz, nloc, mfree, allow_cluster, P, Q, cluster);
     if (P * Q > ctx->sm_count || gcd_int(P, Q) != 1) raise(REGOT_E_VALIDATION, "pcg blocks: grid must be coprime and fit the device");
+    Q2.cluster = cluster;
     const int G = P * Q, R = (nloc + P - 1) / P, C = (mfree + Q - 1) / Q;
     if (R > 32000 || C > 32000) return;
     Q2.P = P;
@@ -976,7 +1260,7 @@ void build_pcg_blocks_plan(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, regot_
     const int g1 = (int)std::max<long>(1, std::min<long>(((long)nnz + 255) / 256, 8L * ctx->sm_count));
     k_b2_count<<<g1, 256, 0, st>>>(nnz, P, Q, R, C, S.row.p, S.col.p, cnt_r, cnt_c);
     k_b2_layout<<<G, 256, 0, st>>>(P, Q, R, C, nloc, mfree, Q2.Lr, Q2.Lc, cnt_r, cnt_c, vpos_r, vpos_c, Q2.a32.p, Q2.hdr.p);
-    k_b2_offsets<<<1, 32, 0, st>>>(P, Q, R, C, Q2.SR, Q2.SC, Q2.hdr.p, summary);
+    k_b2_offsets<<<1, 32, 0, st>>>(P, Q, R, C, Q2.SR, Q2.SC, cluster, Q2.hdr.p, summary);
     k_b2_fill<<<G, 256, 0, st>>>(P, Q, R, C, nloc, mfree, Q2.hdr.p, vpos_r, vpos_c, Q2.a16.p, Q2.asrc.p);
     const int gr = (int)std::max<long>(1, std::min<long>(((long)nloc + 7) / 8, 16L * ctx->sm_count));
     const int gc = (int)std::max<long>(1, std::min<long>(((long)mfree + 7) / 8, 16L * ctx->sm_count));
@@ -993,18 +1277,22 @@ void build_pcg_blocks_plan(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, regot_
 }
 
 // after the stream has been synchronised: does the plan fit?
-void finish_pcg_blocks_plan(regot_ctx* ctx, SparseWS& ws, regot_sparse& S)
+void finish_pcg_blocks_plan(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, regot_sparse& S, const int* csc2csr)
 {
     PcgBlocksPlan& Q2 = S.blocks;
-    if (!Q2.pending) return;
-    Q2.pending = false;
-    Q2.smem = ws.h_blocks[0];
-    Q2.fits = ws.h_blocks[1] == 0 && Q2.smem <= kPcgSmemBudget;
     static const bool show = std::getenv("REGOT_B200_PCG_BLOCKS_INFO") != nullptr;
-    if (show)
-        std::fprintf(stderr, "pcg blocks: %d x %d blocks, slices %d x %d, L %d/%d, smem %d B, %s\n", Q2.P, Q2.Q, Q2.R, Q2.C, Q2.Lr, Q2.Lc,
-                     Q2.smem, Q2.fits ? "fits" : "does not fit");
-    (void)ctx;
+    for (int attempt = 0; attempt < 2 && Q2.pending; ++attempt) {
+        Q2.pending = false;
+        Q2.smem = ws.h_blocks[0];
+        Q2.fits = ws.h_blocks[1] == 0 && Q2.smem <= kPcgSmemBudget;
+        if (show)
+            std::fprintf(stderr, "pcg blocks: %d x %d blocks%s, slices %d x %d, L %d/%d, smem %d B, %s\n", Q2.P, Q2.Q,
+                         Q2.cluster ? " (block row = cluster)" : "", Q2.R, Q2.C, Q2.Lr, Q2.Lc, Q2.smem, Q2.fits ? "fits" : "does not fit");
+        if (Q2.fits || !Q2.cluster || csc2csr == nullptr) break;
+        // the cluster grid (fewer, larger blocks) was too optimistic for this pattern: once more through L2
+        build_pcg_blocks_plan(ctx, st, ws, S, csc2csr, false);
+        RG_CUDA(cudaStreamSynchronize(st));
+    }
 }
 
 static int pcg_blocks_launch(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, const regot_sparse& S, int nrhs,
@@ -1012,11 +1300,7 @@ static int pcg_blocks_launch(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, cons
 {
     const PcgBlocksPlan& Q2 = S.blocks;
     const int nloc = (int)S.nloc, mfree = std::max((int)S.m - 1, 0), G = Q2.P * Q2.Q;
-    static bool attr_set = false;
-    if (!attr_set) {
-        RG_CUDA(cudaFuncSetAttribute(k_pcg_blocks, cudaFuncAttributeMaxDynamicSharedMemorySize, kPcgSmemBudget));
-        attr_set = true;
-    }
+    set_kernel_attributes();
     BlocksParams A;
     std::memset(&A, 0, sizeof(A));
     A.nloc = nloc;
@@ -1064,6 +1348,7 @@ static int pcg_blocks_launch(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, cons
     A.x4 = A.x3 + n3;
     A.x5 = A.x4 + n4;
     A.round0 = ws.blocks_round;
+    A.cluster = Q2.cluster;
     ws.blocks_round += rounds;
     ws.cg_scal.ensure(16 + (size_t)G * 8);
     if (!ws.h_cg) RG_CUDA(cudaMallocHost((void**)&ws.h_cg, sizeof(double) * 4096));
@@ -1074,7 +1359,25 @@ static int pcg_blocks_launch(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, cons
     void* args[] = {&A};
     {
         ProfScope prof(ctx, st, 5);
-        RG_CUDA(cudaLaunchCooperativeKernel((const void*)k_pcg_blocks, dim3(G), dim3(kB2Threads), args, (size_t)Q2.smem, st));
+        if (Q2.cluster) {
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(G);
+            cfg.blockDim = dim3(kB2Threads);
+            cfg.dynamicSmemBytes = (size_t)Q2.smem;
+            cfg.stream = st;
+            cudaLaunchAttribute attr[2];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = (unsigned)Q2.Q;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            attr[1].id = cudaLaunchAttributeCooperative;  // all clusters resident at once, or the launch fails
+            attr[1].val.cooperative = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 2;
+            RG_CUDA(cudaLaunchKernelExC(&cfg, (const void*)k_pcg_blocks, args));
+        } else {
+            RG_CUDA(cudaLaunchCooperativeKernel((const void*)k_pcg_blocks, dim3(G), dim3(kB2Threads), args, (size_t)Q2.smem, st));
+        }
     }
     ++ctx->launches;
     ws.cg_mbox.wait(st);

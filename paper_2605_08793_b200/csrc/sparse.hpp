@@ -59,6 +59,7 @@ struct PcgBlocksPlan {
     bool fits = false;     // every block fits in shared memory: the solve takes this kernel
     bool pending = false;  // built, summary not read yet
     int P = 0, Q = 0, R = 0, C = 0, SR = 0, SC = 0, Lr = 0, Lc = 0, smem = 0;
+    int cluster = 0;  // the CTAs of a block row form a thread-block cluster (exchanges in distributed shared memory)
     unsigned long stamp = 0;
     DevBuf<int> cnt, vpos;  // G x (R + C): line lengths per block; sorted position of every line
     DevBuf<int> hdr;        // G x kPcgBlocksHdrInts sizes and arena offsets, then the 4-int summary
@@ -179,8 +180,8 @@ int pcg_schur_persistent(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, const re
                          const DVec* const* rhs, DVec* const* sol, double rtol, int max_iter);
 // k6_pcg_blocks.cu -- the block-resident form: plan construction (enqueued on st; finish_* after the caller's
 // synchronisation reads the summary) and the solve
-void build_pcg_blocks_plan(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, regot_sparse& S, const int* csc2csr);
-void finish_pcg_blocks_plan(regot_ctx* ctx, SparseWS& ws, regot_sparse& S);
+void build_pcg_blocks_plan(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, regot_sparse& S, const int* csc2csr, bool allow_cluster = true);
+void finish_pcg_blocks_plan(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, regot_sparse& S, const int* csc2csr);
 int pcg_schur_blocks(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, const regot_sparse& S, int nrhs, const DVec* const* rhs,
                      DVec* const* sol, double rtol, int max_iter);
 int sparse_pcg(regot_ctx* ctx, cudaStream_t st, ncclComm* comm, SparseWS& ws, const regot_sparse& S, int nrhs,

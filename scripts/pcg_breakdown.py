@@ -1,4 +1,4 @@
-"""Time of the direction solve (config B pattern after 20 Sinkhorn steps): the persistent Schur-complement
+"""Time of the direction solve (pattern of config B, or of PROBLEM=kind:n:m:eta, after 20 Sinkhorn steps): the persistent Schur-complement
 PCG kernel to convergence and for a fixed 1000 iterations (REGOT_B200_PCG_FIXED_ITERS), and the former
 full-system kernel (REGOT_B200_PCG_FULL=1 in the environment) for comparison.
 Usage: python scripts/pcg_breakdown.py [nrhs=3]"""
@@ -12,7 +12,12 @@ import paper_2605_08793_b200 as rg  # noqa: E402
 from paper_2605_08793_b200 import problems  # noqa: E402
 
 nrhs = int(sys.argv[1]) if len(sys.argv) > 1 else 3
-p = problems.gen_image(100, 0.001)
+spec = os.environ.get("PROBLEM", "")  # kind:n:m:eta (d = 2, seed = 7); default: config B
+if spec:
+    kind, n_, m_, eta_ = spec.split(":")
+    p = problems.make_problem(kind, int(n_), int(m_), float(eta_), 2, 7)
+else:
+    p = problems.gen_image(100, 0.001)
 s = rg.Solver(0)
 s.set_problem(p)
 x = rg.DualPoint.zeros(p.n, p.m)

@@ -97,6 +97,15 @@ __host__ __device__ __forceinline__ long b2_xbuf_doubles(int SR, int SC, int P, 
     const long x1 = 2L * Q * SR, x3 = 2L * P * SC;
     return cluster ? x1 + x3 : (x1 > x3 ? x1 : x3);
 }
+// doubles of the staging the mat-vec phases write their sums to before they are shipped: through L2 the collection
+// buffer itself serves (it is filled after the sums have left); inside a cluster other CTAs write into that buffer at
+// their own pace, so the row sums (and, in a single cluster, the column sums) get their own staging, plus the t slice
+// an owner sends to its block row
+__host__ __device__ __forceinline__ long b2_staging_doubles(int SR, int SC, int P, int Q, int cluster)
+{
+    if (!cluster) return 0;
+    return 2L * Q * SR + (P == 1 ? 2L * P * SC : 0L) + 2L * SR;
+}
 
 // dynamic shared memory of the solve kernel for one block (the carve-up at the top of k_pcg_blocks)
 __host__ __device__ __forceinline__ long b2_smem_need(const int* h, int R, int C, int SR, int SC, int P, int Q, int cluster)
@@ -104,9 +113,9 @@ __host__ __device__ __forceinline__ long b2_smem_need(const int* h, int R, int C
     const int nval = h[kH_NSL_R] + h[kH_NHE_R];
     const int segcap_r = h[kH_NHE_R] / 128 + h[kH_NHV_R], segcap_c = h[kH_NHE_C] / 128 + h[kH_NHV_C];
     const int tables = 2 * h[kH_NCH_R] + 3 * h[kH_NHV_R] + 2 * h[kH_NCH_C] + 3 * h[kH_NHV_C];
-    const int derived = h[kH_NV_R] + h[kH_NV_C] + 2 * (h[kH_NHV_R] + h[kH_NHV_C]) + 2 + segcap_r + segcap_c + 4;
+    const int derived = (h[kH_NHV_R] + h[kH_NHV_C]) + 2 + segcap_r + segcap_c + 4;
     return (long)(((nval + 1) * 8 + 15) & ~15) + 16L * C + 16L * R + 16L * (segcap_r > segcap_c ? segcap_r : segcap_c) + 2L * lay16(h).size +
-           (long)(((tables + derived) * 4 + 15) & ~15) + 8L * (6 * 2 * SC + 2 * SC + SR) + 8L * b2_xbuf_doubles(SR, SC, P, Q, cluster) + 8L * (8 * P * Q) + 8L * (16 + 8 * kB2Warps) + 256 + 64 + 16 + kB2Slack;
+           (long)(((tables + derived) * 4 + 15) & ~15) + 8L * (6 * 2 * SC + 2 * SC + SR) + 8L * (b2_xbuf_doubles(SR, SC, P, Q, cluster) + b2_staging_doubles(SR, SC, P, Q, cluster)) + 8L * (8 * P * Q) + 8L * (16 + 8 * kB2Warps) + 256 + 64 + 16 + kB2Slack;
 }
 
 // ---- plan construction (device; once per pattern) -----------------------------------------------------
@@ -473,49 +482,25 @@ __device__ __forceinline__ void cluster_inbox_wait(uint32_t mbar, uint32_t bytes
     parity ^= 1u;
 }
 
-// Where the two sums of a line go.  Through L2: word offset ((owner nsrc + me) slice + r) 4 from the base of the block
-// row's (column's) exchange.  Inside a cluster: the owner's buffer has the layout [source][slice][2] doubles, so the
-// byte offset (me slice + r) 16 from the base of the buffer, in the shared memory of CTA `owner` of the cluster.
-__device__ __forceinline__ int line_offset(int owner, int r, int slice, int nsrc, int me, int dsmem)
-{
-    return dsmem ? (owner << 24) | ((me * slice + r) * 16) : ((owner * nsrc + me) * slice + r) * 4;
-}
-
 struct BlockCopy {  // one copy (rows or columns) of the CTA's block in shared memory (shared-window addresses)
     uint32_t ell;     // u16 per entry: local index into the gathered slice
     uint32_t ref;     // column copy: u16 per entry, position in `val` (row copy: 0, the entry's own position)
     uint32_t lov;     // u16 per sorted position: local line
-    uint32_t off;     // int per sorted position: word offset of the line's two sums in the exchange
     uint32_t chunk;   // int pairs (first slot, width) per 32-line chunk
     uint32_t heavy;   // int triples (line, first entry, length) per heavy line
-    uint32_t hoff;    // int per heavy line: word offset in the exchange
     uint32_t hfirst;  // int per heavy line: its first segment
     uint32_t hseg;    // int per segment: heavy line
     int nv, nch, nsl, nhv, nseg;
-    int pad_lo, pad_hi, slice, nsrc, me;  // lines [pad_lo, pad_hi) exist only as padding of the last owner's slice: posted as zeros
-    int dsmem;  // the sums go to the owner's shared memory: `off` holds owner rank << 24 | byte offset into its buffer
-    uint32_t xlocal, mbar;  // that buffer and its barrier at their addresses in THIS CTA (same offsets in every CTA)
-    int self_rank;          // >= 0: every line is owned by this CTA itself (single cluster, column copy); else owner = line / slice
 };
-
-__device__ __forceinline__ void post_line(const BlockCopy& B, u64* xbase, int off, double a0, double a1, unsigned int round)
-{
-    if (B.dsmem) {
-        const int owner = (unsigned)off >> 24;
-        st_async_f64x2(map_rank(B.xlocal + (uint32_t)(off & 0xffffff), owner), a0, a1, map_rank(B.mbar, owner));
-    } else {
-        fw_post(xbase + off, a0, round);
-        fw_post(xbase + off + 2, a1, round);
-    }
-}
 
 // One mat-vec phase over the CTA's block: lines are the block's rows and `vec` the z (or x) slice of the block
 // column, or lines are its columns and `vec` the t slice of the block row.  Work items: segments of heavy lines
-// first, then the 32-line chunks by decreasing width.  Each finished line's two sums are posted as flagged words where the owner of the
-// line's slice expects them; with zvec != 0 (column phase) z . (B' t) is accumulated per system into dc[0..1]
-// of this thread.  val, vec, zvec, hpart: shared-window addresses.
-__device__ __noinline__ void block_phase(uint32_t Bp, uint32_t val, int zero_slot, uint32_t vec, uint32_t zvec, u64* xbase,
-                                         unsigned int round, uint32_t hpart, double* dc)
+// first, then the 32-line chunks by decreasing width.  The two sums of line l land in out[l] (shared memory, 16 B per
+// line, line order = owner order: the caller ships each owner's slice in one piece); with zvec != 0 (column phase)
+// z . (B' t) is accumulated per system into dc[0..1] of this thread.  val, vec, zvec, out, hpart: shared-window
+// addresses.  Ends with a CTA barrier: out is complete.
+__device__ __noinline__ void block_phase(uint32_t Bp, uint32_t val, int zero_slot, uint32_t vec, uint32_t zvec, uint32_t out,
+                                         uint32_t hpart, double* dc)
 {
     BlockCopy B;
     {
@@ -574,9 +559,10 @@ __device__ __noinline__ void block_phase(uint32_t Bp, uint32_t val, int zero_slo
         }
         const int vpos = 32 * c + lane;
         if (vpos < B.nv) {
-            post_line(B, xbase, lds_s32(B.off + 4 * vpos), a0, a1, round);
+            const uint32_t line = (uint32_t)lds_u16(B.lov + 2 * vpos);
+            sts_f64x2_b(out + 16u * line, a0, a1);
             if (zvec) {
-                const double2 z = lds_f64x2(zvec + 16u * (uint32_t)lds_u16(B.lov + 2 * vpos));
+                const double2 z = lds_f64x2(zvec + 16u * line);
                 dc0 = __fma_rn(z.x, a0, dc0);
                 dc1 = __fma_rn(z.y, a1, dc1);
             }
@@ -594,21 +580,45 @@ __device__ __noinline__ void block_phase(uint32_t Bp, uint32_t val, int zero_slo
                 a0 += hp.x;
                 a1 += hp.y;
             }
-            post_line(B, xbase, lds_s32(B.hoff + 4 * h), a0, a1, round);
+            const uint32_t line = (uint32_t)lds_s32(B.heavy + 12 * h);
+            sts_f64x2_b(out + 16u * line, a0, a1);
             if (zvec) {
-                const double2 z = lds_f64x2(zvec + 16u * (uint32_t)lds_s32(B.heavy + 12 * h));
+                const double2 z = lds_f64x2(zvec + 16u * line);
                 dc0 = __fma_rn(z.x, a0, dc0);
                 dc1 = __fma_rn(z.y, a1, dc1);
             }
         }
     }
-#pragma unroll 1
-    for (int line = B.pad_lo + threadIdx.x; line < B.pad_hi; line += kB2Threads) {
-        const int o = line / B.slice;
-        post_line(B, xbase, line_offset(B.self_rank >= 0 ? B.self_rank : o, line - o * B.slice, B.slice, B.nsrc, B.me, B.dsmem), 0.0, 0.0, round);
-    }
     dc[0] = dc0;
     dc[1] = dc1;
+    __syncthreads();
+}
+
+// Ship the staged sums (out of block_phase: [owner][slice][2] doubles) to their owners.  Through L2: flagged words,
+// written by all threads in address order (whole lines of the owner's region instead of one 16-byte piece per
+// line).  Inside a cluster: one bulk copy per owner into its collection buffer, completing on its barrier.
+__device__ __forceinline__ void ship_sums(bool dsmem, const double* staged, int nowner, int slice, int me, int nsrc, u64* xbase,
+                                          uint32_t xlocal, uint32_t mbar, int only_rank, unsigned int round)
+{
+    if (dsmem) {
+        fence_proxy_async();  // the sums were written through the generic proxy, the copy engine reads them
+        __syncthreads();
+        if ((int)threadIdx.x < nowner) {
+            const int o = threadIdx.x, dst_rank = only_rank >= 0 ? only_rank : o;
+            const uint32_t bytes = 16u * (uint32_t)slice;
+            asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                             map_rank(xlocal + (uint32_t)me * bytes, dst_rank)),
+                         "r"(smem_u32(staged) + (uint32_t)o * bytes), "r"(bytes), "r"(map_rank(mbar, dst_rank))
+                         : "memory");
+        }
+        return;
+    }
+    const int per = 2 * slice, n = nowner * per;
+#pragma unroll 1
+    for (int i = threadIdx.x; i < n; i += kB2Threads) {
+        const int o = i / per;
+        fw_post(xbase + 2 * ((size_t)(o * nsrc + me) * per + (i - o * per)), staged[i], round);
+    }
 }
 
 // Sum of 8 per-thread values over the CTA in a fixed order (transposing butterfly in the warp, then the 16 warps in
@@ -708,6 +718,11 @@ __global__ void __launch_bounds__(kB2Threads, 1) k_pcg_blocks(const __grid_const
     double* xbuf1 = reinterpret_cast<double*>(sp);  // partial sums collected by the owner: Q x 2 SR of its rows ...
     double* xbuf3 = xbuf1 + (cl ? 2 * Q * SR : 0);  // ... and P x 2 SC of its columns (one buffer when both come through L2)
     sp += 8 * (size_t)b2_xbuf_doubles(SR, SC, P, Q, A.cluster);
+    // where the phases put their sums before they are shipped ([owner][slice][2]; lines beyond the last real one stay 0)
+    double* stg_r = cl ? reinterpret_cast<double*>(sp) : xbuf1;
+    double* stg_c = one ? stg_r + 2 * Q * SR : xbuf3;
+    double* tloc = stg_r + 2 * Q * SR + (one ? 2 * P * SC : 0);  // cluster: the t slice I own, as it goes out
+    sp += 8 * (size_t)b2_staging_doubles(SR, SC, P, Q, A.cluster);
     double* stage = reinterpret_cast<double*>(sp);  // 8 G: everybody's partial dot products
     sp += 8 * (size_t)(8 * G);
     double2* vecz = reinterpret_cast<double2*>(sp);
@@ -720,7 +735,7 @@ __global__ void __launch_bounds__(kB2Threads, 1) k_pcg_blocks(const __grid_const
     sp += 2 * (size_t)L16.size;
     int* s32 = reinterpret_cast<int*>(sp);
     const int n_tables = 2 * Br.nch + 3 * Br.nhv + 2 * Bc.nch + 3 * Bc.nhv;
-    const int n_derived = Br.nv + Bc.nv + 2 * (Br.nhv + Bc.nhv) + 2 + segcap_r + segcap_c + 4;
+    const int n_derived = (Br.nhv + Bc.nhv) + 2 + segcap_r + segcap_c + 4;
     sp += ((n_tables + n_derived) * 4 + 15) & ~15;
     double* own = reinterpret_cast<double*>(sp);  // z p s x r w of the owned column slice (x2), 1/dB of it, 1/dA of the owned row slice
     sp += 8 * (size_t)(6 * 2 * SC + 2 * SC + SR);
@@ -738,25 +753,20 @@ __global__ void __launch_bounds__(kB2Threads, 1) k_pcg_blocks(const __grid_const
     tb += 2 * Bc.nch;
     int* const heavy_c = tb;
     tb += 3 * Bc.nhv;
-    int *off_r = tb, *off_c = off_r + Br.nv, *hoff_r = off_c + Bc.nv, *hoff_c = hoff_r + Br.nhv, *hfirst_r = hoff_c + Bc.nhv,
-        *hfirst_c = hfirst_r + Br.nhv + 1, *hseg_r = hfirst_c + Bc.nhv + 1, *hseg_c = hseg_r + segcap_r;
+    int *hfirst_r = tb, *hfirst_c = hfirst_r + Br.nhv + 1, *hseg_r = hfirst_c + Bc.nhv + 1, *hseg_c = hseg_r + segcap_r;
     const u16 *lov_r = s16 + L16.lov_r, *lov_c = s16 + L16.lov_c;
     Br.ell = smem_u32(s16 + L16.ell_r);
     Br.ref = 0;
     Br.lov = smem_u32(lov_r);
-    Br.off = smem_u32(off_r);
     Br.chunk = smem_u32(chunk_r);
     Br.heavy = smem_u32(heavy_r);
-    Br.hoff = smem_u32(hoff_r);
     Br.hfirst = smem_u32(hfirst_r);
     Br.hseg = smem_u32(hseg_r);
     Bc.ell = smem_u32(s16 + L16.ell_c);
     Bc.ref = smem_u32(s16 + L16.ref_c);
     Bc.lov = smem_u32(lov_c);
-    Bc.off = smem_u32(off_c);
     Bc.chunk = smem_u32(chunk_c);
     Bc.heavy = smem_u32(heavy_c);
-    Bc.hoff = smem_u32(hoff_c);
     Bc.hfirst = smem_u32(hfirst_c);
     Bc.hseg = smem_u32(hseg_c);
 
@@ -782,23 +792,9 @@ __global__ void __launch_bounds__(kB2Threads, 1) k_pcg_blocks(const __grid_const
         if (tid == 0) val[nval] = 0.0;
     }
     __syncthreads();
-    // where each line's sums go: rows -> [owner = line / SR][source q][line % SR][2], columns likewise with P, SC
-    for (int v = tid; v < Br.nv; v += kB2Threads) {
-        const int line = lov_r[v], o = line / SR;
-        off_r[v] = line_offset(o, line - o * SR, SR, Q, q, cl);
-    }
-    for (int v = tid; v < Bc.nv; v += kB2Threads) {
-        const int line = lov_c[v], o = line / SC;
-        off_c[v] = line_offset(one ? q : o, line - o * SC, SC, P, p, one);
-    }
-    for (int hh = tid; hh < Br.nhv; hh += kB2Threads) {
-        const int line = heavy_r[3 * hh], o = line / SR;
-        hoff_r[hh] = line_offset(o, line - o * SR, SR, Q, q, cl);
-    }
-    for (int hh = tid; hh < Bc.nhv; hh += kB2Threads) {
-        const int line = heavy_c[3 * hh], o = line / SC;
-        hoff_c[hh] = line_offset(one ? q : o, line - o * SC, SC, P, p, one);
-    }
+    // staging of the sums: the padding lines of the last owner's slice are shipped as zeros (never written again)
+    for (int i = tid; i < 2 * Q * SR; i += kB2Threads) stg_r[i] = 0.0;
+    for (int i = tid; i < 2 * P * SC; i += kB2Threads) stg_c[i] = 0.0;
     if (tid < 2) {  // segments of the heavy lines: thread 0 the rows', thread 1 the columns'
         const int nhv = tid == 0 ? Br.nhv : Bc.nhv;
         const int* hv = tid == 0 ? heavy_r : heavy_c;
@@ -816,24 +812,6 @@ __global__ void __launch_bounds__(kB2Threads, 1) k_pcg_blocks(const __grid_const
     if (tid == 0) {
         Br.nseg = hfirst_r[Br.nhv];
         Bc.nseg = hfirst_c[Bc.nhv];
-        Br.pad_lo = Rp;
-        Br.pad_hi = Q * SR;
-        Br.slice = SR;
-        Br.nsrc = Q;
-        Br.me = q;
-        Br.dsmem = cl;
-        Br.xlocal = smem_u32(xbuf1);
-        Br.mbar = mb1;
-        Br.self_rank = -1;
-        Bc.dsmem = one;  // a single cluster has P == 1: the owner of my columns is this CTA itself
-        Bc.xlocal = smem_u32(xbuf3);
-        Bc.mbar = mb3;
-        Bc.self_rank = one ? q : -1;
-        Bc.pad_lo = Cq;
-        Bc.pad_hi = P * SC;
-        Bc.slice = SC;
-        Bc.nsrc = P;
-        Bc.me = p;
         s_copy[0] = Br;
         s_copy[1] = Bc;
     }
@@ -904,21 +882,33 @@ __global__ void __launch_bounds__(kB2Threads, 1) k_pcg_blocks(const __grid_const
             publish_slice(one, x4_col, 2 * c_lo, oz, 2 * n_own_c, reinterpret_cast<double*>(vecz), 2 * Cq, round);
             __syncthreads();
             B2_TICK(0)
-            block_phase(smem_u32(&s_copy[0]), smem_u32(val), nval, smem_u32(vecz), 0u, x1_mine, round, smem_u32(hpart), bcast + 12);
+            block_phase(smem_u32(&s_copy[0]), smem_u32(val), nval, smem_u32(vecz), 0u, smem_u32(stg_r), smem_u32(hpart), bcast + 12);
+            ship_sums(cl, stg_r, Q, SR, q, Q, x1_mine, smem_u32(xbuf1), mb1, -1, round);
             B2_TICK(1)
             // owner: the Q partials of my rows, summed in block order; t = D1^-1 sum goes to the block row
-            if (cl) cluster_inbox_wait(mb1, 16u * (uint32_t)(Q * SR), ph1);
-            else fw_gather(x1_own, xbuf1, Q * 2 * SR, round);
+            if (cl) {
+                cluster_inbox_wait(mb1, 16u * (uint32_t)(Q * SR), ph1);
+            } else {
+                __syncthreads();  // the staged sums (in xbuf1) have left
+                fw_gather(x1_own, xbuf1, Q * 2 * SR, round);
+            }
             __syncthreads();
             for (int item = tid; item < 2 * n_own_r; item += kB2Threads) {
                 double s = 0.0;
 #pragma unroll 1
                 for (int src = 0; src < Q; ++src) s += xbuf1[src * 2 * SR + item];
                 const double tv = s * oia[item >> 1];
-                if (!cl) fw_post(x2_row + ((size_t)r_lo * 2 + item) * 2, tv, round);
-#pragma unroll 1
-                for (int dst = 0; dst < (cl ? Q : 0); ++dst)  // straight into the t slice of every CTA of the block row
-                    st_async_f64(map_rank(smem_u32(vect) + 8u * (uint32_t)(r_lo * 2 + item), dst), tv, map_rank(mb2, dst));
+                if (cl) tloc[item] = tv;
+                else fw_post(x2_row + ((size_t)r_lo * 2 + item) * 2, tv, round);
+            }
+            if (cl) {  // my t slice straight into the t vector of every CTA of the block row: one bulk copy each
+                fence_proxy_async();
+                __syncthreads();
+                if (tid < Q && n_own_r > 0)
+                    asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                                     map_rank(smem_u32(vect) + 16u * (uint32_t)r_lo, tid)),
+                                 "r"(smem_u32(tloc)), "r"(16u * (uint32_t)n_own_r), "r"(map_rank(mb2, tid))
+                                 : "memory");
             }
             B2_TICK(2)
             if (cl) cluster_inbox_wait(mb2, 16u * (uint32_t)Rp, ph2);
@@ -927,15 +917,20 @@ __global__ void __launch_bounds__(kB2Threads, 1) k_pcg_blocks(const __grid_const
             B2_TICK(3)
         }
         // column phase: partial B' t of my block; z . (B' t) rides along
-        block_phase(smem_u32(&s_copy[1]), smem_u32(val), nval, smem_u32(vect), smem_u32(vecz), x3_mine, round, smem_u32(hpart), part + 4);
+        block_phase(smem_u32(&s_copy[1]), smem_u32(val), nval, smem_u32(vect), smem_u32(vecz), smem_u32(stg_c), smem_u32(hpart), part + 4);
         if (init) part[4] = part[5] = 0.0;
+        ship_sums(one, stg_c, P, SC, p, P, x3_mine, smem_u32(xbuf3), mb3, one ? q : -1, round);
         B2_TICK(4)
         // everybody's partial dot products are known here (except in the set-up pass): their exchange overlaps the
         // exchange of the column partial sums
         if (!init) post_dots(part, scratch, bcast, A.x5 + (size_t)b * 16, one ? Q : 0, smem_u32(stage + 8 * b), mb5, round);
         // owner: u = sum of the P partials of my columns, then the new r/z (set-up) or w = D2 z - u
-        if (one) cluster_inbox_wait(mb3, 16u * (uint32_t)(P * SC), ph3);
-        else fw_gather(x3_own, xbuf3, P * 2 * SC, round);
+        if (one) {
+            cluster_inbox_wait(mb3, 16u * (uint32_t)(P * SC), ph3);
+        } else {
+            __syncthreads();  // the staged sums (in xbuf3) have left
+            fw_gather(x3_own, xbuf3, P * 2 * SC, round);
+        }
         __syncthreads();
         for (int item = tid; item < 2 * n_own_c; item += kB2Threads) {
             const int c = item >> 1, k = item & 1;
@@ -1061,9 +1056,14 @@ __global__ void __launch_bounds__(kB2Threads, 1) k_pcg_blocks(const __grid_const
     }
     publish_slice(one, x4_col, 2 * c_lo, ox, 2 * n_own_c, reinterpret_cast<double*>(vecz), 2 * Cq, round);
     __syncthreads();
-    block_phase(smem_u32(&s_copy[0]), smem_u32(val), nval, smem_u32(vecz), 0u, x1_mine, round, smem_u32(hpart), bcast + 12);
-    if (cl) cluster_inbox_wait(mb1, 16u * (uint32_t)(Q * SR), ph1);
-    else fw_gather(x1_own, xbuf1, Q * 2 * SR, round);
+    block_phase(smem_u32(&s_copy[0]), smem_u32(val), nval, smem_u32(vecz), 0u, smem_u32(stg_r), smem_u32(hpart), bcast + 12);
+    ship_sums(cl, stg_r, Q, SR, q, Q, x1_mine, smem_u32(xbuf1), mb1, -1, round);
+    if (cl) {
+        cluster_inbox_wait(mb1, 16u * (uint32_t)(Q * SR), ph1);
+    } else {
+        __syncthreads();
+        fw_gather(x1_own, xbuf1, Q * 2 * SR, round);
+    }
     __syncthreads();
     for (int item = tid; item < 2 * n_own_r; item += kB2Threads) {
         const int k = item & 1, gi = p + (r_lo + (item >> 1)) * P;
@@ -1129,7 +1129,8 @@ static void set_kernel_attributes()
 static long estimate_smem(long nnz, long nloc, long mfree, int P, int Q, int cluster)
 {
     const long G = (long)P * Q, R = (nloc + P - 1) / P, C = (mfree + Q - 1) / Q, SR = (R + Q - 1) / Q, SC = (C + P - 1) / P;
-    return (long)(1.08 * 14.0 * (double)nnz / (double)G) + 22 * (R + C) + 8 * b2_xbuf_doubles((int)SR, (int)SC, P, Q, cluster) +
+    return (long)(1.08 * 14.0 * (double)nnz / (double)G) + 18 * (R + C) +
+           8 * (b2_xbuf_doubles((int)SR, (int)SC, P, Q, cluster) + b2_staging_doubles((int)SR, (int)SC, P, Q, cluster)) +
            8 * (14 * SC + SR) + 64 * G + 6144;
 }
 

@@ -1014,7 +1014,8 @@ __global__ void __launch_bounds__(kB2Threads, 1) k_pcg_blocks(const __grid_const
             }
             ++it;
             done_other = __shfl_xor_sync(0xffffffffu, done_mine, 1);
-            broke = brk || __shfl_xor_sync(0xffffffffu, brk, 1);
+            const bool brk_other = __shfl_xor_sync(0xffffffffu, brk, 1);  // every lane takes part: no short-circuit around a shuffle
+            broke = brk || brk_other;
             if (!broke && !done_mine) {
                 // p = z + beta p, s = w + beta s, x += alpha p, r -= alpha s, z = D2^-1 r on the owned slice (a finished
                 // system is frozen; its partials are not used any more)

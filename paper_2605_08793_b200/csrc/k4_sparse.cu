@@ -274,6 +274,7 @@ __device__ __forceinline__ void spmv_warp(const SpmvMat& A, const LineRanges R, 
 }
 
 struct SpmvParams {
+    const double* skip = nullptr;  // != null and *skip != 0: nothing to do (an iteration past the end of a PCG solve)
     SpmvMat A;
     LineRanges R;
     int nrhs;
@@ -287,6 +288,7 @@ struct SpmvParams {
 template <int kEpi>
 __global__ void __launch_bounds__(kSpmvThreads, 4) k_spmv(const SpmvParams p)
 {
+    if (p.skip != nullptr && *p.skip != 0.0) return;
     const int wpb = kSpmvThreads / 32;
     spmv_warp<kEpi>(p.A, p.R, p.nrhs, p.va, p.vb, p.sa, p.sb, p.ya, p.yb, blockIdx.x * wpb + (threadIdx.x >> 5),
                     gridDim.x * wpb, threadIdx.x & 31);
@@ -321,9 +323,10 @@ static SpmvMat mat_view(const regot_ctx* ctx, const regot_sparse& S)
 // one (part of a) mat-vec: kEpiFull over all lines, or one of the two halves of the Schur mat-vec
 template <int kEpi>
 static void launch_spmv(regot_ctx* ctx, cudaStream_t st, const regot_sparse& S, int nrhs, const double* va,
-                        const double* vb, double* ya, double* yb, long sa, long sb)
+                        const double* vb, double* ya, double* yb, long sa, long sb, const double* skip = nullptr)
 {
     SpmvParams p;
+    p.skip = skip;
     p.A = mat_view(ctx, S);
     if (kEpi == kEpiFull) p.R = LineRanges{0, S.n_chunks, 0, S.n_lines_m, 0, S.n_lines_s};
     else if (kEpi == kEpiRowsScaled) p.R = LineRanges{0, S.n_chunks_rows, 0, S.n_lines_m_rows, 0, S.n_lines_s_rows};
@@ -373,6 +376,7 @@ constexpr int kPanelDeferCap = 2048;    // deferred pieces per CTA kept in the s
 constexpr int kPanelLineCost = 24;      // work of a piece beyond its entries (pointer loads, reduction), in entries
 
 struct PanelArgs {
+    const double* skip;  // != null and *skip != 0: nothing to do
     int P, Bk, W, nlines, ngather;
     const int* ppt;
     const int* blk;
@@ -461,6 +465,7 @@ __device__ __forceinline__ void panel_dot(int beg, int end, int gl, const int* _
 __global__ void __launch_bounds__(kPanelThreads, 1) k_spmv_panel(const PanelArgs a)
 {
     extern __shared__ __align__(16) unsigned char smem[];
+    if (a.skip != nullptr && *a.skip != 0.0) return;
     const int p = blockIdx.x / a.Bk, b = blockIdx.x - p * a.Bk;
     const int col0 = p * a.W, wp = min(a.W, a.ngather - col0);
     const uint32_t vec = smem_u32(smem);
@@ -563,8 +568,9 @@ __global__ void __launch_bounds__(kPanelThreads, 1) k_spmv_panel(const PanelArgs
 // y_line = sum over panels (panel order) of part[p][line], then the epilogue of the half mat-vec
 template <int kEpi>
 __global__ void k_panel_combine(int nlines, int P, const double* __restrict__ part, const double* __restrict__ diag,
-                                double* __restrict__ y)
+                                double* __restrict__ y, const double* skip)
 {
+    if (skip != nullptr && *skip != 0.0) return;
     const int total = nlines * 2;
     for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < total; q += gridDim.x * blockDim.x) {
         const int l = q >> 1, k = q & 1;
@@ -614,7 +620,8 @@ static void build_panel_plan(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, cons
 
 // one half mat-vec in panel form: y (interleaved x4) = epilogue(B x) or epilogue(B' x) for two right-hand sides
 template <int kEpi>
-static void launch_spmv_panel(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, const regot_sparse& S, const double* x, double* y)
+static void launch_spmv_panel(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, const regot_sparse& S, const double* x, double* y,
+                              const double* skip = nullptr, bool combine = true)
 {
     constexpr bool rows = kEpi == kEpiRowsScaled;
     build_panel_plan(ctx, st, ws, S, rows);
@@ -625,6 +632,7 @@ static void launch_spmv_panel(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, con
         attr_set = true;
     }
     PanelArgs a;
+    a.skip = skip;
     a.P = Q.P;
     a.Bk = Q.Bk;
     a.W = Q.W;
@@ -639,11 +647,13 @@ static void launch_spmv_panel(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, con
     {
         ProfScope prof(ctx, st, 4);
         k_spmv_panel<<<Q.P * Q.Bk, kPanelThreads, panel_smem(Q.W), st>>>(a);
-        const int g = (int)std::max<long>(1, std::min<long>(((long)Q.nlines * 2 + 255) / 256, 4L * ctx->sm_count));
-        k_panel_combine<kEpi><<<g, 256, 0, st>>>(Q.nlines, Q.P, Q.part.p, rows ? S.dA.p : nullptr, y);
+        if (combine) {  // else the consumer adds the per-panel partials itself (one kernel and one pass over the vector less)
+            const int g = (int)std::max<long>(1, std::min<long>(((long)Q.nlines * 2 + 255) / 256, 4L * ctx->sm_count));
+            k_panel_combine<kEpi><<<g, 256, 0, st>>>(Q.nlines, Q.P, Q.part.p, rows ? S.dA.p : nullptr, y, skip);
+        }
     }
     RG_CUDA(cudaGetLastError());
-    ctx->launches += 2;
+    ctx->launches += combine ? 2 : 1;
 }
 
 static bool use_panel_spmv(const regot_ctx* ctx, const regot_sparse& S, int nrhs)
@@ -660,33 +670,48 @@ static bool use_panel_spmv(const regot_ctx* ctx, const regot_sparse& S, int nrhs
 // gather wants at that size) and for row-sharded runs: alpha-space quantities and the rows of B are
 // local, beta-space vectors are replicated, so the only collective per iteration is ONE allreduce of
 // the m-1 partial sums B' t (every rank then takes identical decisions from identical dot products).
-// scalars (device), per rhs k: rz[2][k] (double-buffered by iteration parity), pAp[k], rz0[k] (the FULL
-// system's r' D^-1 r: the meaning of rtol is unchanged), done[k], breakdown flag, iterations[k], g0a[k]
-constexpr int kScalRz = 0;                   // 2 * kMaxRhs
-constexpr int kScalPap = 2 * kMaxRhs;        // kMaxRhs
-constexpr int kScalRz0 = 3 * kMaxRhs;        // kMaxRhs
-constexpr int kScalDone = 4 * kMaxRhs;       // kMaxRhs (0/1)
-constexpr int kScalBreak = 5 * kMaxRhs;      // 1: breakdown flag
-constexpr int kScalIters = 5 * kMaxRhs + 1;  // kMaxRhs: iterations taken by each system
-constexpr int kScalG0a = 6 * kMaxRhs + 1;    // kMaxRhs: alpha-block part of rz0 (summed over ranks)
-constexpr int kScalG0b = 7 * kMaxRhs + 1;    // kMaxRhs: beta-block part of rz0
-constexpr int kScalCount = 8 * kMaxRhs + 4;
+// Single-reduction recurrences (Chronopoulos-Gear), as in the persistent kernels: z = D2^-1 r, w = S z,
+// gamma = r'z, delta = z'w; beta = gamma / gamma_old, alpha = gamma / (delta - beta gamma / alpha_old);
+// p = z + beta p, s = w + beta s, x += alpha p, r -= alpha s.  One iteration = rows half (t = D1^-1 B z) | columns
+// half (u = B' t, all-reduced over row blocks) | k_schur_w (w = D2 z - u, the two dot products; the last CTA to finish
+// turns them into alpha, beta and the convergence flags) | k_schur_step (the five vector updates).  Every kernel
+// returns at once when the all-done flag is set, so the host enqueues iterations in bursts and looks at the flags
+// only between bursts: an iteration past convergence costs five empty launches, not a pass over the matrix.
+// scalars (device), per system k: gamma_old, alpha_old, gamma0 (the FULL system's r' D^-1 r: the meaning of rtol is
+// unchanged), alpha, beta, done, iterations, g0a / g0b (the two halves of gamma0), then the global flags
+constexpr int kScalGammaOld = 0 * kMaxRhs;
+constexpr int kScalAlphaOld = 1 * kMaxRhs;
+constexpr int kScalGamma0 = 2 * kMaxRhs;
+constexpr int kScalAlpha = 3 * kMaxRhs;
+constexpr int kScalBeta = 4 * kMaxRhs;
+constexpr int kScalDone = 5 * kMaxRhs;   // 0 / 1
+constexpr int kScalIters = 6 * kMaxRhs;  // iterations taken by each system
+constexpr int kScalG0a = 7 * kMaxRhs;    // alpha-block part of gamma0 (summed over ranks)
+constexpr int kScalG0b = 8 * kMaxRhs;    // beta-block part of gamma0
+constexpr int kScalDots = 9 * kMaxRhs;   // 2 kMaxRhs: gamma, delta of the current iteration
+constexpr int kScalBreak = 11 * kMaxRhs;      // breakdown flag
+constexpr int kScalAllDone = 11 * kMaxRhs + 1;  // every system done, or breakdown, or the iteration limit: nothing left to do
+constexpr int kScalIt = 11 * kMaxRhs + 2;       // iterations started
+constexpr int kScalStepIt = 11 * kMaxRhs + 3;   // the iteration whose alpha / beta are waiting for their step (0: none)
+constexpr int kScalCount = 11 * kMaxRhs + 4;
 constexpr int kCgThreads = 256;
 
 struct CgVecs {
-    int nloc, mfree, nrhs;
+    int nloc, mfree, nrhs, max_iter, n_parts;
+    double tol2;
     // all interleaved 4 doubles per index (entry 3 is padding)
-    double *ta;                      // alpha space: t = D1^-1 (...)
-    double *ub, *xb, *rb, *pb, *qb;  // beta space: u = B' t, x, r, p, q = S p
+    double *ta;                           // alpha space: t = D1^-1 (...)
+    double *ub, *xb, *rb, *pb, *sb, *zb;  // beta space: u = B' t, x, r, p, s = S p, z = D2^-1 r
+    const double* part;                   // panel mat-vec on one GPU: u = sum of n_parts per-panel partials (mfree x 2 each); else null
     const double *dA, *dB;
     double* scal;
     double* partials;
     unsigned int* ticket;
 };
 
+// block partials -> global partials; the last CTA to arrive sums them in CTA order into out[0..NV) and returns true
 template <int NV>
-__device__ __forceinline__ void two_stage_store(double (&acc)[NV], double* scratch, double* partials,
-                                                unsigned int* ticket, double* out)
+__device__ __forceinline__ bool two_stage_sum(double (&acc)[NV], double* scratch, double* partials, unsigned int* ticket, double* out)
 {
     block_sum<NV>(acc, scratch);
     if (threadIdx.x == 0)
@@ -696,18 +721,19 @@ __device__ __forceinline__ void two_stage_store(double (&acc)[NV], double* scrat
     __syncthreads();
     if (threadIdx.x == 0) is_last = (atomicAdd(ticket, 1u) == gridDim.x - 1);
     __syncthreads();
-    if (is_last) {
-        __threadfence();
-        if (threadIdx.x < 32) {
-            for (int k = 0; k < NV; ++k) {
-                double s = 0.0;
-                for (int b = threadIdx.x; b < (int)gridDim.x; b += 32) s += partials[(size_t)b * NV + k];
-                s = warp_sum(s);
-                if (threadIdx.x == 0) out[k] = s;
-            }
-            if (threadIdx.x == 0) *ticket = 0u;
+    if (!is_last) return false;
+    __threadfence();
+    if (threadIdx.x < 32) {
+        for (int k = 0; k < NV; ++k) {
+            double s = 0.0;
+            for (int b = threadIdx.x; b < (int)gridDim.x; b += 32) s += partials[(size_t)b * NV + k];
+            s = warp_sum(s);
+            if (threadIdx.x == 0) out[k] = s;
         }
+        if (threadIdx.x == 0) *ticket = 0u;
     }
+    __syncthreads();
+    return true;
 }
 
 // t = D1^-1 r_a and the alpha-block part of r' D^-1 r
@@ -722,10 +748,20 @@ __global__ void __launch_bounds__(kCgThreads) k_schur_init_a(const CgVecs v, con
             v.ta[(size_t)i * 4 + k] = t;
             acc[k] += r * t;
         }
-    two_stage_store<kMaxRhs>(acc, scratch, v.partials, v.ticket, v.scal + kScalG0a);
+    two_stage_sum<kMaxRhs>(acc, scratch, v.partials, v.ticket, v.scal + kScalG0a);
 }
 
-// c = r_b - u (u = B' t summed over ranks): r = c, z = D2^-1 c, p = z, x = 0; rz = r'z; beta part of rz0
+// u of system k at column j: the all-reduced vector, or (panel mat-vec on one GPU) the sum of the per-panel partials
+__device__ __forceinline__ double schur_u(const CgVecs& v, int j, int k)
+{
+    if (v.part == nullptr || k >= 2) return v.ub[(size_t)j * 4 + k];
+    double s = 0.0;
+    for (int p = 0; p < v.n_parts; ++p) s += v.part[((size_t)p * v.mfree + j) * 2 + k];
+    return s;
+}
+
+// set-up: c = r_b - u (u = B' t summed over ranks): r = c, z = D2^-1 c, x = p = s = 0; gamma = r'z; beta part of
+// gamma0; the last CTA decides which systems need iterations at all
 __global__ void __launch_bounds__(kCgThreads) k_schur_init_b(const CgVecs v, const double* const* rhs_b)
 {
     __shared__ double scratch[2 * kMaxRhs * (kCgThreads / 32)];
@@ -734,115 +770,101 @@ __global__ void __launch_bounds__(kCgThreads) k_schur_init_b(const CgVecs v, con
     for (int k = 0; k < v.nrhs; ++k)
         for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < v.mfree; j += stride) {
             const double d = v.dB[j], rb = rhs_b[k][j];
-            const double c = rb - v.ub[(size_t)j * 4 + k], z = c / d;
-            v.rb[(size_t)j * 4 + k] = c;
-            v.pb[(size_t)j * 4 + k] = z;
-            v.xb[(size_t)j * 4 + k] = 0.0;
+            const double c = rb - schur_u(v, j, k), z = c / d;
+            const size_t o = (size_t)j * 4 + k;
+            v.rb[o] = c;
+            v.zb[o] = z;
+            v.xb[o] = 0.0;
+            v.pb[o] = 0.0;
+            v.sb[o] = 0.0;
             acc[k] += c * z;
             acc[kMaxRhs + k] += rb * (rb / d);
         }
-    // rz[0][k] and g0b[k] are not adjacent: two stores through a small staging area
     __shared__ double out6[2 * kMaxRhs];
-    block_sum<2 * kMaxRhs>(acc, scratch);
-    if (threadIdx.x == 0)
-        for (int k = 0; k < 2 * kMaxRhs; ++k) v.partials[(size_t)blockIdx.x * 2 * kMaxRhs + k] = acc[k];
-    __shared__ bool is_last;
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) is_last = (atomicAdd(v.ticket, 1u) == gridDim.x - 1);
-    __syncthreads();
-    if (is_last) {
-        __threadfence();
-        if (threadIdx.x < 32) {
-            for (int k = 0; k < 2 * kMaxRhs; ++k) {
-                double s = 0.0;
-                for (int b = threadIdx.x; b < (int)gridDim.x; b += 32) s += v.partials[(size_t)b * 2 * kMaxRhs + k];
-                s = warp_sum(s);
-                if (threadIdx.x == 0) out6[k] = s;
-            }
-            if (threadIdx.x == 0) {
-                for (int k = 0; k < kMaxRhs; ++k) {
-                    v.scal[kScalRz + k] = out6[k];
-                    v.scal[kScalG0b + k] = out6[kMaxRhs + k];
-                }
-                *v.ticket = 0u;
-            }
+    if (!two_stage_sum<2 * kMaxRhs>(acc, scratch, v.partials, v.ticket, out6)) return;
+    if (threadIdx.x == 0) {
+        bool all = true;
+        for (int k = 0; k < kMaxRhs; ++k) {
+            const double gamma = out6[k], gamma0 = v.scal[kScalG0a + k] + out6[kMaxRhs + k];
+            v.scal[kScalG0b + k] = out6[kMaxRhs + k];
+            v.scal[kScalGamma0 + k] = gamma0;
+            v.scal[kScalGammaOld + k] = 1.0;
+            v.scal[kScalAlphaOld + k] = 1.0;
+            const bool done = k >= v.nrhs || gamma0 == 0.0 || !(gamma > v.tol2 * gamma0);
+            v.scal[kScalDone + k] = done ? 1.0 : 0.0;
+            all = all && done;
         }
+        v.scal[kScalAllDone] = all ? 1.0 : 0.0;
     }
 }
 
-// q = D2 p - u, pAp[k] = p_k . q_k
-__global__ void __launch_bounds__(kCgThreads) k_schur_q(const CgVecs v)
+// w = D2 z - u, gamma = r'z, delta = z'w; the last CTA turns the dot products into this iteration's alpha and beta
+// and the flags (a system is done when gamma <= tol^2 gamma0; p'Sp <= 0 is a breakdown: not positive definite)
+__global__ void __launch_bounds__(kCgThreads) k_schur_w(const CgVecs v)
 {
-    __shared__ double scratch[kMaxRhs * (kCgThreads / 32)];
-    double acc[kMaxRhs] = {0.0, 0.0, 0.0};
-    const int stride = gridDim.x * blockDim.x;
-    for (int k = 0; k < v.nrhs; ++k)
-        for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < v.mfree; j += stride) {
-            const double p = v.pb[(size_t)j * 4 + k];
-            const double q = v.dB[j] * p - v.ub[(size_t)j * 4 + k];
-            v.qb[(size_t)j * 4 + k] = q;
-            acc[k] += p * q;
-        }
-    two_stage_store<kMaxRhs>(acc, scratch, v.partials, v.ticket, v.scal + kScalPap);
-}
-
-// x += a p, r -= a q, rz_new = r . D2^-1 r ; a = rz / pAp (0 once the system is done)
-__global__ void __launch_bounds__(kCgThreads) k_schur_update(const CgVecs v, int parity)
-{
-    __shared__ double scratch[kMaxRhs * (kCgThreads / 32)];
-    double acc[kMaxRhs] = {0.0, 0.0, 0.0};
+    if (v.scal[kScalAllDone] != 0.0) return;
+    __shared__ double scratch[2 * kMaxRhs * (kCgThreads / 32)];
+    double acc[2 * kMaxRhs] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
     const int stride = gridDim.x * blockDim.x;
     for (int k = 0; k < v.nrhs; ++k) {
-        const double pap = v.scal[kScalPap + k];
-        const bool live = v.scal[kScalDone + k] == 0.0 && pap > 0.0;
-        const double a = live ? v.scal[kScalRz + parity * kMaxRhs + k] / pap : 0.0;
+        if (v.scal[kScalDone + k] != 0.0) continue;
         for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < v.mfree; j += stride) {
-            v.xb[(size_t)j * 4 + k] += a * v.pb[(size_t)j * 4 + k];
-            const double r = v.rb[(size_t)j * 4 + k] - a * v.qb[(size_t)j * 4 + k];
-            v.rb[(size_t)j * 4 + k] = r;
-            acc[k] += r * (r / v.dB[j]);
+            const size_t o = (size_t)j * 4 + k;
+            const double z = v.zb[o], w = v.dB[j] * z - schur_u(v, j, k);
+            v.ub[o] = w;  // u is not needed any more: w takes its place
+            acc[k] += v.rb[o] * z;
+            acc[kMaxRhs + k] += z * w;
         }
     }
-    two_stage_store<kMaxRhs>(acc, scratch, v.partials, v.ticket, v.scal + kScalRz + (parity ^ 1) * kMaxRhs);
+    if (!two_stage_sum<2 * kMaxRhs>(acc, scratch, v.partials, v.ticket, v.scal + kScalDots)) return;
+    if (threadIdx.x == 0) {
+        const int it = (int)v.scal[kScalIt];
+        bool all = true, broke = false;
+        for (int k = 0; k < v.nrhs; ++k) {
+            v.scal[kScalAlpha + k] = v.scal[kScalBeta + k] = 0.0;
+            if (v.scal[kScalDone + k] != 0.0) continue;
+            const double gamma = v.scal[kScalDots + k], delta = v.scal[kScalDots + kMaxRhs + k];
+            if (it > 0 && !(gamma > v.tol2 * v.scal[kScalGamma0 + k])) {
+                v.scal[kScalDone + k] = 1.0;
+                continue;
+            }
+            const double beta = it == 0 ? 0.0 : gamma / v.scal[kScalGammaOld + k];
+            const double denom = delta - beta * gamma / v.scal[kScalAlphaOld + k];  // = p'Sp
+            if (!(denom > 0.0)) broke = true;
+            const double alpha = gamma / denom;
+            v.scal[kScalAlpha + k] = alpha;
+            v.scal[kScalBeta + k] = beta;
+            v.scal[kScalGammaOld + k] = gamma;
+            v.scal[kScalAlphaOld + k] = alpha;
+            v.scal[kScalIters + k] += 1.0;
+            all = false;
+        }
+        v.scal[kScalIt] = (double)(it + 1);
+        if (broke) v.scal[kScalBreak] = 1.0;
+        if (all || broke || it + 1 >= v.max_iter) v.scal[kScalAllDone] = 1.0;
+        // the step below runs for the systems that got an alpha in this very iteration, unless it broke down
+        v.scal[kScalStepIt] = (all || broke) ? 0.0 : (double)(it + 1);
+    }
 }
 
-// p = z + b p with b = rz_new / rz
-__global__ void __launch_bounds__(kCgThreads) k_schur_direction(const CgVecs v, int parity)
+// p = z + beta p, s = w + beta s, x += alpha p, r -= alpha s, z = D2^-1 r (a finished system is frozen)
+__global__ void __launch_bounds__(kCgThreads) k_schur_step(const CgVecs v, int iteration)
 {
+    if (v.scal[kScalStepIt] != (double)iteration) return;  // this iteration was skipped (the solve had ended) or broke down
     const int stride = gridDim.x * blockDim.x;
     for (int k = 0; k < v.nrhs; ++k) {
-        const double rz = v.scal[kScalRz + parity * kMaxRhs + k];
-        const double rzn = v.scal[kScalRz + (parity ^ 1) * kMaxRhs + k];
-        const bool done = v.scal[kScalDone + k] != 0.0;
-        const double b = (!done && rz > 0.0) ? rzn / rz : 0.0;
-        if (!done)
-            for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < v.mfree; j += stride)
-                v.pb[(size_t)j * 4 + k] = v.rb[(size_t)j * 4 + k] / v.dB[j] + b * v.pb[(size_t)j * 4 + k];
-    }
-}
-
-// single thread: bookkeeping between iterations (runs after k_schur_update)
-__global__ void k_cg_flags(double* scal, int nrhs, int parity, double tol2, int first)
-{
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    for (int k = 0; k < nrhs; ++k) {
-        if (first) {
-            const double rz0 = scal[kScalG0a + k] + scal[kScalG0b + k];
-            scal[kScalRz0 + k] = rz0;
-            scal[kScalDone + k] = (rz0 == 0.0 || !(scal[kScalRz + k] > tol2 * rz0)) ? 1.0 : 0.0;
-            continue;
+        const double al = v.scal[kScalAlpha + k], be = v.scal[kScalBeta + k];
+        if (v.scal[kScalDone + k] != 0.0 || al == 0.0) continue;
+        for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < v.mfree; j += stride) {
+            const size_t o = (size_t)j * 4 + k;
+            const double pn = v.zb[o] + be * v.pb[o], sn = v.ub[o] + be * v.sb[o];
+            const double rn = v.rb[o] - al * sn;
+            v.pb[o] = pn;
+            v.sb[o] = sn;
+            v.xb[o] += al * pn;
+            v.rb[o] = rn;
+            v.zb[o] = rn / v.dB[j];
         }
-        if (scal[kScalDone + k] != 0.0) {
-            // keep the buffered rz equal so a finished system stays finished
-            scal[kScalRz + (parity ^ 1) * kMaxRhs + k] = scal[kScalRz + parity * kMaxRhs + k];
-            continue;
-        }
-        const double pap = scal[kScalPap + k];
-        if (!(pap > 0.0)) scal[kScalBreak] = 1.0;  // not positive definite (or NaN)
-        scal[kScalIters + k] += 1.0;
-        const double rzn = scal[kScalRz + (parity ^ 1) * kMaxRhs + k];
-        if (!(rzn > tol2 * scal[kScalRz0 + k])) scal[kScalDone + k] = 1.0;
     }
 }
 
@@ -864,8 +886,8 @@ static int pcg_schur_multikernel(regot_ctx* ctx, cudaStream_t st, ncclComm* comm
 {
     const int nloc = (int)S.nloc, mfree = std::max((int)S.m - 1, 0);
     const size_t la = 4 * (size_t)std::max(nloc, 1), lb = 4 * (size_t)std::max(mfree, 1);
-    // layout of ws.cg: t | u | x | r | p | q, interleaved x4
-    ws.cg.ensure(la + 5 * lb + 16);
+    // layout of ws.cg: t | u (then w) | x | r | p | s | z, interleaved x4
+    ws.cg.ensure(la + 6 * lb + 16);
     ws.cg_scal.ensure(kScalCount + 8 * kMaxRhs);
     ws.cg_partials.ensure((size_t)(2 * ctx->sm_count + 8) * 2 * kMaxRhs);
     if (!ws.cg_ticket.p) {
@@ -875,24 +897,30 @@ static int pcg_schur_multikernel(regot_ctx* ctx, cudaStream_t st, ncclComm* comm
     if (!ws.h_cg) RG_CUDA(cudaMallocHost((void**)&ws.h_cg, sizeof(double) * 4096));
     RG_CUDA(cudaMemsetAsync(ws.cg_scal.p, 0, sizeof(double) * (kScalCount + 8 * kMaxRhs), st));
 
+    const bool panel = use_panel_spmv(ctx, S, nrhs);
     CgVecs v;
     v.nloc = nloc;
     v.mfree = mfree;
     v.nrhs = nrhs;
+    v.max_iter = max_iter;
+    v.tol2 = rtol * rtol;
     double* base = ws.cg.p;
     v.ta = base;
     v.ub = base + la;
     v.xb = v.ub + lb;
     v.rb = v.xb + lb;
     v.pb = v.rb + lb;
-    v.qb = v.pb + lb;
+    v.sb = v.pb + lb;
+    v.zb = v.sb + lb;
     // the padding entries are gathered (and multiplied into an unused accumulator): keep them finite
-    RG_CUDA(cudaMemsetAsync(base, 0, sizeof(double) * (la + 5 * lb), st));
+    RG_CUDA(cudaMemsetAsync(base, 0, sizeof(double) * (la + 6 * lb), st));
     v.dA = S.dA.p;
     v.dB = S.dB.p;
     v.scal = ws.cg_scal.p;
     v.partials = ws.cg_partials.p;
     v.ticket = ws.cg_ticket.p;
+    v.part = nullptr;
+    v.n_parts = 0;
 
     // pointer tables (rhs_a | rhs_b | sol_a | sol_b) live behind the scalars on the device
     for (int k = 0; k < nrhs; ++k) sol[k]->ensure(S.nloc, S.m);
@@ -913,63 +941,64 @@ static int pcg_schur_multikernel(regot_ctx* ctx, cudaStream_t st, ncclComm* comm
 
     const int grid_a = (int)std::max<long>(1, std::min<long>((nloc + kCgThreads - 1) / kCgThreads, 2L * ctx->sm_count));
     const int grid_b = (int)std::max<long>(1, std::min<long>((mfree + kCgThreads - 1) / kCgThreads, 2L * ctx->sm_count));
-    const double tol2 = rtol * rtol;
-    const bool panel = use_panel_spmv(ctx, S, nrhs);
+    const double* skip = ws.cg_scal.p + kScalAllDone;
     // t = D1^-1 B x for a beta-space vector x
-    auto half_rows = [&](const double* xb) {
-        if (panel) launch_spmv_panel<kEpiRowsScaled>(ctx, st, ws, S, xb, v.ta);
-        else launch_spmv<kEpiRowsScaled>(ctx, st, S, nrhs, nullptr, xb, v.ta, nullptr, kInterleaved4, kInterleaved4);
+    auto half_rows = [&](const double* xb, const double* skip_flag) {
+        if (panel) launch_spmv_panel<kEpiRowsScaled>(ctx, st, ws, S, xb, v.ta, skip_flag, true);
+        else launch_spmv<kEpiRowsScaled>(ctx, st, S, nrhs, nullptr, xb, v.ta, nullptr, kInterleaved4, kInterleaved4, skip_flag);
     };
-    // u = B' t, summed over the row blocks
-    auto half_cols = [&]() {
-        if (panel) launch_spmv_panel<kEpiColsPlain>(ctx, st, ws, S, v.ta, v.ub);
-        else launch_spmv<kEpiColsPlain>(ctx, st, S, nrhs, v.ta, nullptr, nullptr, v.ub, kInterleaved4, kInterleaved4);
+    // u = B' t, summed over the row blocks; on one GPU the panel form leaves its per-panel partials for the consumer
+    auto half_cols = [&](const double* skip_flag) {
+        if (panel) launch_spmv_panel<kEpiColsPlain>(ctx, st, ws, S, v.ta, v.ub, skip_flag, ctx->world > 1);
+        else launch_spmv<kEpiColsPlain>(ctx, st, S, nrhs, v.ta, nullptr, nullptr, v.ub, kInterleaved4, kInterleaved4, skip_flag);
         if (ctx->world > 1) allreduce_sum(ctx, comm, v.ub, 4 * (size_t)mfree, st);
     };
+    if (panel && ctx->world == 1) {
+        build_panel_plan(ctx, st, ws, S, false);
+        v.part = S.panel_cols.part.p;
+        v.n_parts = S.panel_cols.P;
+    }
 
     k_schur_init_a<<<grid_a, kCgThreads, 0, st>>>(v, d_rhs_a);
     RG_CUDA(cudaGetLastError());
     if (ctx->world > 1) allreduce_sum(ctx, comm, ws.cg_scal.p + kScalG0a, kMaxRhs, st);
-    half_cols();
+    half_cols(nullptr);
     k_schur_init_b<<<grid_b, kCgThreads, 0, st>>>(v, d_rhs_b);
-    k_cg_flags<<<1, 32, 0, st>>>(ws.cg_scal.p, nrhs, 0, tol2, 1);
     RG_CUDA(cudaGetLastError());
-    ctx->launches += 3;
+    ctx->launches += 2;
 
-    const int check_every = 8;
-    int it = 0, parity = 0;
     bool finished = false, broke = false;
     auto poll = [&]() {
         RG_CUDA(cudaMemcpyAsync(ws.h_cg, ws.cg_scal.p, sizeof(double) * kScalCount, cudaMemcpyDeviceToHost, st));
         RG_CUDA(cudaStreamSynchronize(st));
         broke = ws.h_cg[kScalBreak] != 0.0;
-        finished = true;
-        for (int k = 0; k < nrhs; ++k) finished &= ws.h_cg[kScalDone + k] != 0.0;
+        finished = ws.h_cg[kScalAllDone] != 0.0;
     };
     poll();  // a right-hand side that is already solved takes no iteration
-    while (it < max_iter && !finished && !broke) {
-        const int burst = std::min(check_every, max_iter - it);
-        for (int b = 0; b < burst; ++b, ++it) {
-            half_rows(v.pb);                                                                         // t = D1^-1 B p
-            half_cols();                                                                            // u = B' t
-            k_schur_q<<<grid_b, kCgThreads, 0, st>>>(v);
-            k_schur_update<<<grid_b, kCgThreads, 0, st>>>(v, parity);
-            k_cg_flags<<<1, 32, 0, st>>>(ws.cg_scal.p, nrhs, parity, tol2, 0);
-            k_schur_direction<<<grid_b, kCgThreads, 0, st>>>(v, parity);
+    // sharded runs enqueue a collective per iteration, which no rank may skip on its own: there the flags are identical on
+    // every rank (replicated beta-space arithmetic), so skipping is consistent, but the collective itself is always issued
+    int burst = 8;
+    for (int it = 0; it < max_iter && !finished && !broke;) {
+        const int n = std::min(burst, max_iter - it);
+        for (int b = 0; b < n; ++b, ++it) {
+            half_rows(v.zb, skip);  // t = D1^-1 B z
+            half_cols(skip);        // u = B' t
+            k_schur_w<<<grid_b, kCgThreads, 0, st>>>(v);
+            k_schur_step<<<grid_b, kCgThreads, 0, st>>>(v, it + 1);
             RG_CUDA(cudaGetLastError());
-            ctx->launches += 4;
-            parity ^= 1;
+            ctx->launches += 2;
         }
         poll();
+        burst = std::min(32, burst * 2);  // long solves look at the flags less often
     }
     if (broke) return -1;
-    it = 0;  // report the slowest system's exact count, not the burst-rounded loop count
-    for (int k = 0; k < nrhs; ++k) it = std::max(it, (int)ws.h_cg[kScalIters + k]);
-    half_rows(v.xb);  // t = D1^-1 B x_b
+    int iters = 0;  // report the slowest system's exact count
+    for (int k = 0; k < nrhs; ++k) iters = std::max(iters, (int)ws.h_cg[kScalIters + k]);
+    half_rows(v.xb, nullptr);  // t = D1^-1 B x_b
     k_schur_final<<<std::max(grid_a, grid_b), kCgThreads, 0, st>>>(v, d_rhs_a, d_sol_a, d_sol_b);
     RG_CUDA(cudaGetLastError());
     ++ctx->launches;
-    return it;
+    return iters;
 }
 
 int sparse_pcg(regot_ctx* ctx, cudaStream_t st, ncclComm* comm, SparseWS& ws, const regot_sparse& S, int nrhs,

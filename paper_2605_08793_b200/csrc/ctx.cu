@@ -147,6 +147,7 @@ regot_ctx* ctx_create(int device)
         // off by default: measured 11 % (config A) / 1 % (1600 x 1200) of the direction solve, slower above ~50k entries
         ctx->pcg_cluster_size = 0;
         ctx->pcg_cluster_max_entries = 50000;
+        if (const char* e = std::getenv("REGOT_B200_FUSED_FINALIZE")) ctx->fused_finalize = e[0] != '0';
         if (const char* e = std::getenv("REGOT_B200_PCG_BLOCKS")) ctx->pcg_blocks = std::atoi(e);
         if (const char* e = std::getenv("REGOT_B200_PCG_BLOCKS_CLUSTER")) ctx->pcg_blocks_cluster = std::atoi(e);
         if (const char* e = std::getenv("REGOT_B200_PCG_BLOCKS_ONE_CLUSTER_ENTRIES")) ctx->pcg_blocks_one_cluster_entries = std::atol(e);
@@ -161,6 +162,7 @@ regot_ctx* ctx_create(int device)
         if (const char* e = std::getenv("REGOT_B200_PCG_CLUSTER")) ctx->pcg_cluster_size = std::atoi(e);
         if (const char* e = std::getenv("REGOT_B200_PCG_CLUSTER_ENTRIES")) ctx->pcg_cluster_max_entries = std::atol(e);
         if (const char* e = std::getenv("REGOT_B200_EXACT_LSE")) ctx->fast_sinkhorn = e[0] != '1';
+        if (const char* e = std::getenv("REGOT_B200_LSE_FAST_SHIFT")) ctx->lse_fast_shift = e[0] == '1';
         if (const char* e = std::getenv("REGOT_B200_FAST_CHAIN")) ctx->fast_sinkhorn_chain = e[0] == '1';
         RG_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
         RG_CUDA(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
@@ -278,7 +280,7 @@ void ensure_sweep_ws(regot_ctx* ctx, SweepWS& ws)
     ws.colpart2.ensure((size_t)pl.n_segments * kTC);
     ws.pack.ensure((size_t)pr.m + 16);
     ws.pack2.ensure(2 * (size_t)pr.m + 32);
-    ws.partials.ensure((size_t)(2 * ctx->sm_count + 8) * 8);
+    ws.partials.ensure((size_t)(2 * ctx->sm_count + 8) * 12);  // 8 per CTA for the two-kernel finalize, 12 for the fused one
     if (!ws.ticket.p) {
         ws.ticket.ensure(8);
         RG_CUDA(cudaMemset(ws.ticket.p, 0, 8 * sizeof(unsigned int)));

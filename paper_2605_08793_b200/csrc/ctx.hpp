@@ -279,6 +279,8 @@ struct regot_ctx {
     // (REGOT_B200_PANEL_SPMV); panel_width > 0 caps the panel width in entries (REGOT_B200_PANEL_WIDTH, tests)
     int panel_spmv = -1;
     int panel_width = 0;
+    // one GPU: the two finalize kernels of a gradient pass as one (REGOT_B200_FUSED_FINALIZE=0: two kernels, as sharded runs)
+    bool fused_finalize = true;
     // block-resident PCG (k6_pcg_blocks.cu): -1 auto (whenever the pattern fits), 0 off (REGOT_B200_PCG_BLOCKS);
     // pcg_blocks_p x pcg_blocks_q > 0 force the block grid (REGOT_B200_PCG_BLOCKS_GRID=PxQ, tests)
     int pcg_blocks = -1;
@@ -299,6 +301,9 @@ struct regot_ctx {
     // candidate chain of run_splr only with REGOT_B200_FAST_CHAIN=1 (see solver.cu); the stand-alone entry
     // points always use the log-sum-exp kernels
     bool fast_sinkhorn = true;
+    // row log-sum-exp kernel: shift by the warp's approximate maximum (one redux instead of five shuffle rounds; same
+    // value up to rounding) -- REGOT_B200_LSE_FAST_SHIFT=1; default: the exact maximum, the reference's arithmetic
+    bool lse_fast_shift = false;
     bool fast_sinkhorn_chain = false;
 
     // optional per-kernel timing (regot_b200_set_profiling): event pairs around the sweep kernels

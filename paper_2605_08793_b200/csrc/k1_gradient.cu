@@ -361,6 +361,97 @@ __global__ void k_plan(int nloc, int m, const CostViewDev cost, const double* __
 }
 
 // ---- host side ------------------------------------------------------------------------
+// ---- both epilogues in one kernel (one GPU: no allreduce between them) -----------------------------------
+// Same loops and the same per-thread summation order as k_gradient_fin1 followed by k_gradient_fin2 on the same
+// grid (so a square problem gets bit-identical scalars); one launch and one grid-wide hand-over less per evaluation.
+struct Fin12Params {
+    Fin1Params r;
+    Fin2Params c;
+};
+constexpr int kNScal12 = 12;
+__global__ void __launch_bounds__(kFinThreads) k_gradient_fin12(const Fin12Params q)
+{
+    const Fin1Params& p = q.r;
+    const Fin2Params& f = q.c;
+    __shared__ double scratch[kNScal12 * (kFinThreads / 32)];
+    // 0..5 as in k_gradient_fin1; 6 beta.b (free part) 7 sum|c-b| (all m) 8 beta.(c-b) 9 |c-b|^2 (free part) 10 (c-b).d_beta (free part)
+    double acc[11] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    const int stride = gridDim.x * blockDim.x;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < p.nloc; i += stride) {
+        double r = 0.0;
+        for (int P0 = 0; P0 < p.n_panels; P0 += 8) {
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = (P0 + u < p.n_panels) ? p.rowpart[(size_t)(P0 + u) * p.nloc + i] : 0.0;
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (P0 + u < p.n_panels) r += v[u];
+        }
+        const double al = p.alpha[i], ai = p.a[i];
+        const double ga = r - ai;
+        p.row_sums[i] = r;
+        p.g_alpha[i] = ga;
+        acc[0] += r;
+        acc[1] += al * ai;
+        acc[2] += fabs(ga);
+        acc[3] += al * ga;
+        acc[4] += ga * ga;
+        if (p.dir_a) acc[5] += ga * p.dir_a[i];
+    }
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < p.m; j += stride) {
+        const int P = j / kTC, off = j - P * kTC;
+        double c = 0.0;
+        const int s1 = p.panel_seg0[P + 1];
+        for (int sg = p.panel_seg0[P]; sg < s1; sg += 8) {
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = (sg + u < s1) ? p.colpart[(size_t)(sg + u) * kTC + off] : 0.0;
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (sg + u < s1) c += v[u];
+        }
+        const double bj = f.b[j], be = f.beta[j];
+        const double gb = c - bj;
+        f.col_sums[j] = c;
+        f.g_beta[j] = gb;
+        acc[7] += fabs(gb);
+        acc[8] += be * gb;
+        if (j < p.m - 1) {
+            acc[6] += be * bj;
+            acc[9] += gb * gb;
+            if (f.dir_b) acc[10] += gb * f.dir_b[j];
+        }
+    }
+    block_sum<11>(acc, scratch);
+    if (threadIdx.x == 0)
+        for (int k = 0; k < 11; ++k) p.partials[(size_t)blockIdx.x * kNScal12 + k] = acc[k];
+    if (last_block_done(p.ticket)) {
+        if (threadIdx.x < 32) {
+            double t[11];
+            for (int k = 0; k < 11; ++k) {
+                double s = 0.0;
+                for (int b = threadIdx.x; b < (int)gridDim.x; b += 32) s += p.partials[(size_t)b * kNScal12 + k];
+                t[k] = warp_sum(s);
+            }
+            if (threadIdx.x == 0) {
+                GradScalars o;
+                o.total_mass = t[0];
+                o.f = f.eta * t[0] - t[1] - t[6];  // dual.h:157-158
+                o.row_abs = t[2];
+                o.col_abs = t[7];
+                o.marginal_error = t[2] + t[7];  // dual.h:219-222
+                o.duality_gap = t[3] + t[8];     // dual.h:225-229
+                o.grad_sqnorm = t[4] + t[9];
+                o.g_dot_d = t[5] + t[10];
+                o.lse_flag = (double)*f.sk_flag;
+                *f.out = o;
+                *p.ticket = 0u;
+                mailbox_post(f.mbox, reinterpret_cast<const double*>(&o), 9, f.seq);
+            }
+        }
+    }
+}
+
 static int fin_grid(const regot_ctx* ctx, long work)
 {
     long g = (work + kFinThreads - 1) / kFinThreads;
@@ -430,9 +521,12 @@ void launch_gradient(regot_ctx* ctx, cudaStream_t st, SweepWS& ws, ncclComm* com
     f1.pack = ws.pack.p;
     f1.partials = ws.partials.p;
     f1.ticket = ws.ticket.p;
-    k_gradient_fin1<<<g1, kFinThreads, 0, st>>>(f1);
-    RG_CUDA(cudaGetLastError());
-    ++ctx->launches;
+    const bool fused = ctx->world == 1 && ctx->fused_finalize;
+    if (!fused) {
+        k_gradient_fin1<<<g1, kFinThreads, 0, st>>>(f1);
+        RG_CUDA(cudaGetLastError());
+        ++ctx->launches;
+    }
 
     if (ctx->world > 1) allreduce_sum(ctx, comm, ws.pack.p, (size_t)pr.m + kNScal, st);
 
@@ -452,7 +546,14 @@ void launch_gradient(regot_ctx* ctx, cudaStream_t st, SweepWS& ws, ncclComm* com
     f2.mbox = ws.mbox.data;
     f2.seq = ws.mbox.next();
     f2.sk_flag = ws.sk_flag.p;
-    k_gradient_fin2<<<g2, kFinThreads, 0, st>>>(f2);
+    if (fused) {
+        Fin12Params f12;
+        f12.r = f1;
+        f12.c = f2;
+        k_gradient_fin12<<<g1, kFinThreads, 0, st>>>(f12);
+    } else {
+        k_gradient_fin2<<<g2, kFinThreads, 0, st>>>(f2);
+    }
     RG_CUDA(cudaGetLastError());
     ++ctx->launches;
 }

@@ -26,16 +26,30 @@ struct LseParams {
     const double* exp_table;
     double* part_sum;  // row: n_panels x nloc ; column: n_segments x kTC
     double* part_max;
+    int fast_shift;  // row LSE: shift by the warp's approximate maximum (warp_shift) instead of the exact one
 };
 
 __device__ __forceinline__ double dmax(double a, double b) { return a > b ? a : b; }
+
+// (opt-in, REGOT_B200_LSE_FAST_SHIFT=1; the default subtracts the exact maximum like sinkhorn.h:57-68)
+// The shift of a log-sum-exp need not be the exact maximum: any value within a few hundred of it keeps every
+// exponential in range, and lse = shift + log(sum exp(v - shift)) holds for all of them.  The warp's shift is the
+// maximum of the HIGH WORDS of the lanes' maxima (one redux.sync on an order-preserving integer key instead of five
+// 64-bit shuffle + compare rounds), i.e. the true maximum with its low 32 bits cleared: within 2^-20 relative of it.
+__device__ __forceinline__ double warp_shift(double lane_max)
+{
+    const int hi = __double2hiint(lane_max);
+    int key = hi >= 0 ? hi : (hi ^ 0x7fffffff);  // sign-magnitude -> two's complement order
+    key = __reduce_max_sync(0xffffffffu, key);
+    return __hiloint2double(key >= 0 ? key : (key ^ 0x7fffffff), 0);
+}
 
 // ---- K7: row LSE sweep ---------------------------------------------------------------
 // v_ij = (beta_j - M_ij) / eta.  Warp w owns row w of each tile: lane max ->
 // warp max (shuffles) -> sum of exp(v - max) -> staged transposing flush.
 template <bool kRagged>
 __device__ __forceinline__ void row_lse_row(const double2 (&mv)[4], const double (&bj)[kEPL], unsigned cmask,
-                                            double inv_eta, uint32_t tbl_lane, double& wmax, double& lsum)
+                                            double inv_eta, uint32_t tbl_lane, bool fast_shift, double& wmax, double& lsum)
 {
     double v[kEPL];
 #pragma unroll
@@ -48,12 +62,12 @@ __device__ __forceinline__ void row_lse_row(const double2 (&mv)[4], const double
         for (int k = 0; k < kEPL; ++k) v[k] = (cmask >> k) & 1u ? v[k] : -INFINITY;
     }
     double mx = dmax(dmax(dmax(v[0], v[1]), dmax(v[2], v[3])), dmax(dmax(v[4], v[5]), dmax(v[6], v[7])));
-    mx = warp_max(mx);
+    mx = fast_shift ? warp_shift(mx) : warp_max(mx);
     double sacc[kEPL];
     unsigned amax = 0;
 #pragma unroll
     for (int k = 0; k < kEPL; ++k) {
-        sacc[k] = v[k] - mx;  // <= 0, -inf for masked columns
+        sacc[k] = v[k] - mx;  // <= |mx| 2^-20, -inf for masked columns
         amax = max(amax, abs_hi(sacc[k]));
     }
     if (amax >= kHi700) {
@@ -131,8 +145,8 @@ k_row_lse_sweep(const __grid_constant__ CUtensorMap tmap, const LseParams p)
 #pragma unroll
                         for (int q = 0; q < 4; ++q) mv[q] = trow[q * 32 + lane];
                     }
-                    if (ragged) row_lse_row<true>(mv, bj, cmask, inv_eta, tbl_lane, wmax, lsum);
-                    else row_lse_row<false>(mv, bj, cmask, inv_eta, tbl_lane, wmax, lsum);
+                    if (ragged) row_lse_row<true>(mv, bj, cmask, inv_eta, tbl_lane, p.fast_shift != 0, wmax, lsum);
+                    else row_lse_row<false>(mv, bj, cmask, inv_eta, tbl_lane, p.fast_shift != 0, wmax, lsum);
                 }
                 if (!kCloud) {
                     __syncwarp();
@@ -401,6 +415,7 @@ static LseParams make_lse_params(regot_ctx* ctx, const double* vec, double* psum
     p.inv_eta = 1.0 / ctx->prob.eta;
     p.exp_table = ctx->exp_table.p;
     p.part_sum = psum;
+    p.fast_shift = ctx->lse_fast_shift ? 1 : 0;
     p.part_max = pmax;
     return p;
 }

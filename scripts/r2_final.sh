@@ -1,0 +1,28 @@
+#!/bin/bash
+# round-2 evidence: smoke, GPU suite, both bench arms, launch list of one config-D solve, ncu --set full captures of the
+# direction-solve kernels, per-iteration and end-to-end tables.  Outputs under gpurun_out/ (copied into profiles/ by hand).
+mkdir -p gpurun_out
+export REGOT_B200_MAILBOX_TIMEOUT_S=300
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.txt 2>&1; tail -2 gpurun_out/smoke.txt
+timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu_full.txt 2>&1; tail -5 gpurun_out/pytest_gpu_full.txt | tee gpurun_out/pytest_gpu.txt
+timeout 1200 python bench.py --gpus 1 --steps 5 --warmup 3 2>&1 | tail -1 > gpurun_out/bench.txt; cut -c1-400 gpurun_out/bench.txt
+timeout 900 python bench.py --impl reference --gpus 1 --steps 2 --warmup 1 2>&1 | tail -1 > gpurun_out/bench_ref.txt; cut -c1-300 gpurun_out/bench_ref.txt
+# launch list of one config-D solve (second solve of the process would double it: REPS=1)
+timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none -c 80000 --csv --log-file gpurun_out/r02_launches_D.csv \
+    python scripts/solve_cloud.py D 0 > gpurun_out/r02_launches_D.log 2>&1
+python scripts/launch_summary.py gpurun_out/r02_launches_D.csv gpurun_out/r02_launches_D_summary.csv | head -24
+rm -f gpurun_out/r02_launches_D.csv.tmp
+# the direction-solve kernels under ncu --set full
+REGOT_B200_PCG_FIXED_ITERS=200 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_pcg_blocks -c 1 \
+    -o gpurun_out/r02_pcg_blocks_B -f python scripts/pcg_breakdown.py 1 > gpurun_out/r02_ncu_pcg_B.log 2>&1; tail -1 gpurun_out/r02_ncu_pcg_B.log
+PROBLEM=synth1-iid:1600:1200:0.001 REGOT_B200_PCG_FIXED_ITERS=200 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_pcg_blocks -c 1 \
+    -o gpurun_out/r02_pcg_blocks_small -f python scripts/pcg_breakdown.py 1 > gpurun_out/r02_ncu_pcg_small.log 2>&1; tail -1 gpurun_out/r02_ncu_pcg_small.log
+MAXIT=2 timeout 900 ncu --set full --clock-control none --import-source on -k "regex:k_spmv_panel|k_schur_w|k_schur_step|k_gradient_fin12" -s 20 -c 8 \
+    -o gpurun_out/r02_mk_D -f python scripts/solve_cloud.py D 0 > gpurun_out/r02_ncu_mk_D.log 2>&1; tail -1 gpurun_out/r02_ncu_mk_D.log
+# tables
+bash scripts/r2_blocks_iter.sh > /dev/null 2>&1
+bash scripts/r2_e2e.sh > /dev/null 2>&1
+REPS=2 timeout 900 python scripts/solve_cloud.py E 1 2>&1 | tail -10 > gpurun_out/e2e_E.txt
+REPS=2 timeout 900 python scripts/solve_cloud.py D 0 2>&1 | tail -10 > gpurun_out/e2e_D.txt
+bash scripts/r2_host.sh > /dev/null 2>&1
+ls -la gpurun_out | head -50

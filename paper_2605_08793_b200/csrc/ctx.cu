@@ -148,6 +148,7 @@ regot_ctx* ctx_create(int device)
         ctx->pcg_cluster_size = 0;
         ctx->pcg_cluster_max_entries = 50000;
         if (const char* e = std::getenv("REGOT_B200_FUSED_FINALIZE")) ctx->fused_finalize = e[0] != '0';
+        if (const char* e = std::getenv("REGOT_B200_EXTENDED_F")) ctx->extended_f = e[0] != '0';
         if (const char* e = std::getenv("REGOT_B200_PCG_BLOCKS")) ctx->pcg_blocks = std::atoi(e);
         if (const char* e = std::getenv("REGOT_B200_PCG_BLOCKS_CLUSTER")) ctx->pcg_blocks_cluster = std::atoi(e);
         if (const char* e = std::getenv("REGOT_B200_PCG_BLOCKS_ONE_CLUSTER_ENTRIES")) ctx->pcg_blocks_one_cluster_entries = std::atol(e);
@@ -280,7 +281,7 @@ void ensure_sweep_ws(regot_ctx* ctx, SweepWS& ws)
     ws.colpart2.ensure((size_t)pl.n_segments * kTC);
     ws.pack.ensure((size_t)pr.m + 16);
     ws.pack2.ensure(2 * (size_t)pr.m + 32);
-    ws.partials.ensure((size_t)(2 * ctx->sm_count + 8) * 12);  // 8 per CTA for the two-kernel finalize, 12 for the fused one
+    ws.partials.ensure((size_t)(2 * ctx->sm_count + 8) * (12 * 2 + 6));  // per CTA: 8 (two-kernel finalize) or 12 (fused) scalars, + 3 double-doubles behind 2 x grid of them
     if (!ws.ticket.p) {
         ws.ticket.ensure(8);
         RG_CUDA(cudaMemset(ws.ticket.p, 0, 8 * sizeof(unsigned int)));

@@ -173,6 +173,7 @@ struct GradScalars {
     double f, marginal_error, duality_gap, grad_sqnorm, total_mass, g_dot_d;
     double row_abs, col_abs;  // the two halves of the marginal error
     double lse_flag;          // != 0: a fast Sinkhorn update on this stream left its safe range since the last check
+    double f_lo;              // f = f + f_lo to about twice the working precision (one GPU; 0 where the plain sum is used)
 };
 
 // Per-stream scratch of one sweep (gradient or LSE) so the main stream and the
@@ -281,6 +282,10 @@ struct regot_ctx {
     int panel_width = 0;
     // one GPU: the two finalize kernels of a gradient pass as one (REGOT_B200_FUSED_FINALIZE=0: two kernels, as sharded runs)
     bool fused_finalize = true;
+    // the objective's three sums accumulated in double-double and the line search comparing objectives as (hi, lo) pairs, so
+    // that decreases below one ulp of f still register near the tolerance (REGOT_B200_EXTENDED_F=0: plain doubles, like the
+    // reference); one GPU with the fused finalize kernel only
+    bool extended_f = true;
     // block-resident PCG (k6_pcg_blocks.cu): -1 auto (whenever the pattern fits), 0 off (REGOT_B200_PCG_BLOCKS);
     // pcg_blocks_p x pcg_blocks_q > 0 force the block grid (REGOT_B200_PCG_BLOCKS_GRID=PxQ, tests)
     int pcg_blocks = -1;

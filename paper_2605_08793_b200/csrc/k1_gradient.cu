@@ -335,10 +335,11 @@ __global__ void __launch_bounds__(kFinThreads) k_gradient_fin2(const Fin2Params 
                 o.grad_sqnorm = S[4] + c[3];
                 o.g_dot_d = S[5] + c[4];
                 o.lse_flag = (double)*p.sk_flag;
+                o.f_lo = 0.0;
                 *p.out = o;
                 *p.ticket = 0u;
-                static_assert(sizeof(GradScalars) == 9 * sizeof(double), "GradScalars is 9 doubles");
-                mailbox_post(p.mbox, reinterpret_cast<const double*>(&o), 9, p.seq);
+                static_assert(sizeof(GradScalars) == 10 * sizeof(double), "GradScalars is 10 doubles");
+                mailbox_post(p.mbox, reinterpret_cast<const double*>(&o), 10, p.seq);
             }
         }
     }
@@ -367,7 +368,73 @@ __global__ void k_plan(int nloc, int m, const CostViewDev cost, const double* __
 struct Fin12Params {
     Fin1Params r;
     Fin2Params c;
+    int extended;  // the three sums of the objective in double-double
 };
+// double-double: an unevaluated sum hi + lo with |lo| <= ulp(hi) / 2
+struct dd {
+    double hi, lo;
+};
+__device__ __forceinline__ dd dd_add(dd a, dd b)
+{
+    const double s = a.hi + b.hi, bb = s - a.hi;
+    const double e = ((a.hi - (s - bb)) + (b.hi - bb)) + (a.lo + b.lo);
+    dd r;
+    r.hi = s + e;
+    r.lo = e - (r.hi - s);
+    return r;
+}
+__device__ __forceinline__ dd dd_add_d(dd a, double b)  // b exact
+{
+    const double s = a.hi + b, bb = s - a.hi;
+    const double e = ((a.hi - (s - bb)) + (b - bb)) + a.lo;
+    dd r;
+    r.hi = s + e;
+    r.lo = e - (r.hi - s);
+    return r;
+}
+__device__ __forceinline__ dd dd_add_prod(dd a, double x, double y)  // a + x y with the product's rounding error kept
+{
+    const double p = __dmul_rn(x, y), pe = __fma_rn(x, y, -p);  // no contraction of the product into the sums below
+    dd r = dd_add_d(a, p);
+    r.lo += pe;
+    return r;
+}
+__device__ __forceinline__ dd dd_shfl_xor(dd a, int mask)
+{
+    dd r;
+    r.hi = shfl_xor_d(a.hi, mask);
+    r.lo = shfl_xor_d(a.lo, mask);
+    return r;
+}
+// CTA-wide sum of three double-doubles in a fixed order; valid in thread 0.  scratch: 6 x (kFinThreads / 32) doubles.
+__device__ __forceinline__ void dd_block_sum3(dd (&v)[3], double* scratch)
+{
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = kFinThreads / 32;
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v[k] = dd_add(v[k], dd_shfl_xor(v[k], o));
+    if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            scratch[(2 * k) * nwarp + warp] = v[k].hi;
+            scratch[(2 * k + 1) * nwarp + warp] = v[k].lo;
+        }
+    }
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            dd t;
+            t.hi = lane < nwarp ? scratch[(2 * k) * nwarp + lane] : 0.0;
+            t.lo = lane < nwarp ? scratch[(2 * k + 1) * nwarp + lane] : 0.0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) t = dd_add(t, dd_shfl_xor(t, o));
+            v[k] = t;
+        }
+    }
+    __syncthreads();
+}
 constexpr int kNScal12 = 12;
 __global__ void __launch_bounds__(kFinThreads) k_gradient_fin12(const Fin12Params q)
 {
@@ -376,6 +443,7 @@ __global__ void __launch_bounds__(kFinThreads) k_gradient_fin12(const Fin12Param
     __shared__ double scratch[kNScal12 * (kFinThreads / 32)];
     // 0..5 as in k_gradient_fin1; 6 beta.b (free part) 7 sum|c-b| (all m) 8 beta.(c-b) 9 |c-b|^2 (free part) 10 (c-b).d_beta (free part)
     double acc[11] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    dd ex[3] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};  // extended: sum r, alpha.a, beta.b (free part)
     const int stride = gridDim.x * blockDim.x;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < p.nloc; i += stride) {
         double r = 0.0;
@@ -397,6 +465,10 @@ __global__ void __launch_bounds__(kFinThreads) k_gradient_fin12(const Fin12Param
         acc[3] += al * ga;
         acc[4] += ga * ga;
         if (p.dir_a) acc[5] += ga * p.dir_a[i];
+        if (q.extended) {
+            ex[0] = dd_add_d(ex[0], r);
+            ex[1] = dd_add_prod(ex[1], al, ai);
+        }
     }
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < p.m; j += stride) {
         const int P = j / kTC, off = j - P * kTC;
@@ -411,6 +483,7 @@ __global__ void __launch_bounds__(kFinThreads) k_gradient_fin12(const Fin12Param
                 if (sg + u < s1) c += v[u];
         }
         const double bj = f.b[j], be = f.beta[j];
+        if (q.extended && j < p.m - 1) ex[2] = dd_add_prod(ex[2], be, bj);
         const double gb = c - bj;
         f.col_sums[j] = c;
         f.g_beta[j] = gb;
@@ -425,6 +498,14 @@ __global__ void __launch_bounds__(kFinThreads) k_gradient_fin12(const Fin12Param
     block_sum<11>(acc, scratch);
     if (threadIdx.x == 0)
         for (int k = 0; k < 11; ++k) p.partials[(size_t)blockIdx.x * kNScal12 + k] = acc[k];
+    if (q.extended) {
+        dd_block_sum3(ex, scratch);
+        if (threadIdx.x == 0)
+            for (int k = 0; k < 3; ++k) {
+                p.partials[(size_t)(2 * gridDim.x) * kNScal12 + (size_t)blockIdx.x * 6 + 2 * k] = ex[k].hi;
+                p.partials[(size_t)(2 * gridDim.x) * kNScal12 + (size_t)blockIdx.x * 6 + 2 * k + 1] = ex[k].lo;
+            }
+    }
     if (last_block_done(p.ticket)) {
         if (threadIdx.x < 32) {
             double t[11];
@@ -444,9 +525,37 @@ __global__ void __launch_bounds__(kFinThreads) k_gradient_fin12(const Fin12Param
                 o.grad_sqnorm = t[4] + t[9];
                 o.g_dot_d = t[5] + t[10];
                 o.lse_flag = (double)*f.sk_flag;
+                o.f_lo = 0.0;
                 *f.out = o;
+            }
+            if (q.extended) {
+                // f = eta sum r - alpha.a - beta.b with the three sums in double-double (CTA order, then lanes)
+                dd tx[3];
+                for (int k = 0; k < 3; ++k) {
+                    dd t = {0.0, 0.0};
+                    for (int b = threadIdx.x; b < (int)gridDim.x; b += 32) {
+                        const double* src = p.partials + (size_t)(2 * gridDim.x) * kNScal12 + (size_t)b * 6 + 2 * k;
+                        dd u = {src[0], src[1]};
+                        t = dd_add(t, u);
+                    }
+                    for (int o2 = 16; o2 > 0; o2 >>= 1) t = dd_add(t, dd_shfl_xor(t, o2));
+                    tx[k] = t;
+                }
+                if (threadIdx.x == 0) {
+                    // eta * (hi + lo): product of the high parts with its error, the low part's product in plain doubles
+                    const double ph = __dmul_rn(f.eta, tx[0].hi), pe = __fma_rn(f.eta, tx[0].hi, -ph) + f.eta * tx[0].lo;
+                    dd fx = {ph, pe};
+                    dd neg1 = {-tx[1].hi, -tx[1].lo}, neg2 = {-tx[2].hi, -tx[2].lo};
+                    fx = dd_add(fx, neg1);
+                    fx = dd_add(fx, neg2);
+                    f.out->f = fx.hi;
+                    f.out->f_lo = fx.lo;
+                }
+            }
+            if (threadIdx.x == 0) {
+                GradScalars o = *f.out;
                 *p.ticket = 0u;
-                mailbox_post(f.mbox, reinterpret_cast<const double*>(&o), 9, f.seq);
+                mailbox_post(f.mbox, reinterpret_cast<const double*>(&o), 10, f.seq);
             }
         }
     }
@@ -550,6 +659,7 @@ void launch_gradient(regot_ctx* ctx, cudaStream_t st, SweepWS& ws, ncclComm* com
         Fin12Params f12;
         f12.r = f1;
         f12.c = f2;
+        f12.extended = ctx->extended_f ? 1 : 0;
         k_gradient_fin12<<<g1, kFinThreads, 0, st>>>(f12);
     } else {
         k_gradient_fin2<<<g2, kFinThreads, 0, st>>>(f2);

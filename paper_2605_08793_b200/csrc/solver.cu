@@ -299,16 +299,21 @@ struct LineSearch {
         raise(REGOT_E_CUDA, "line_search: out of trial slots (internal error)");
     }
 
-    LsOut run(const DVec& x0, const DVec& d, double f0, double dphi0, const regot_splr_config& cfg)
+    // Objectives are compared as (hi, lo) pairs: a - b = (a.hi - b.hi) + (a.lo - b.lo), exact in the first term whenever the
+    // two are within a factor two of each other.  With lo == 0 (sharded runs, REGOT_B200_EXTENDED_F=0) every comparison is
+    // the reference's comparison of doubles (splr.h:185-290); with the extended objective of the one-GPU finalize kernel a
+    // decrease below one ulp of f still registers, which is what the Armijo test needs near the tolerance.
+    LsOut run(const DVec& x0, const DVec& d, double f0, double f0_lo, double dphi0, const regot_splr_config& cfg)
     {
         if (!(dphi0 < 0.0)) raise(REGOT_E_VALIDATION, "line_search: g'd must be negative");
         const double c1 = cfg.c1, c2 = cfg.c2;
         int evals = 0, best = -1;
-        double best_f = 0.0, best_gamma = 0.0, best_dphi = 0.0;
+        double best_f = 0.0, best_f_lo = 0.0, best_gamma = 0.0, best_dphi = 0.0;
         struct Trial {
-            double gamma, f, dphi;
+            double gamma, f, f_lo, dphi;
             int slot;
         };
+        auto minus = [](double a, double a_lo, double b, double b_lo) { return (a - b) + (a_lo - b_lo); };
         auto probe = [&](double gamma) {
             Trial e;
             e.gamma = gamma;
@@ -316,17 +321,23 @@ struct LineSearch {
             vec_axpy(ctx, ctx->stream, gamma, x0, d, S.tx[e.slot]);
             gradient_sync(ctx, ctx->stream, ctx->ws_main, ctx->comm, S.tx[e.slot], &d, S.tg[e.slot], stats);
             e.f = S.tg[e.slot].sc.f;
+            e.f_lo = S.tg[e.slot].sc.f_lo;
             e.dphi = S.tg[e.slot].sc.g_dot_d;
             ++evals;
             return e;
         };
-        auto armijo = [&](const Trial& e) { return std::isfinite(e.f) && e.f <= f0 + c1 * e.gamma * dphi0; };
+        auto armijo = [&](const Trial& e) {
+            if (!std::isfinite(e.f)) return false;
+            if (e.f_lo == 0.0 && f0_lo == 0.0) return e.f <= f0 + c1 * e.gamma * dphi0;  // the reference's test, bit for bit
+            return minus(e.f, e.f_lo, f0, f0_lo) <= c1 * e.gamma * dphi0;
+        };
         auto drop = [&](const Trial& e) { used[e.slot] = false; };
         auto remember = [&](const Trial& e) {
-            if (best < 0 || e.f < best_f) {
+            if (best < 0 || minus(e.f, e.f_lo, best_f, best_f_lo) < 0.0) {
                 if (best >= 0) used[best] = false;
                 best = e.slot;
                 best_f = e.f;
+                best_f_lo = e.f_lo;
                 best_gamma = e.gamma;
                 best_dphi = e.dphi;
             } else {
@@ -356,37 +367,39 @@ struct LineSearch {
             r.slot = best;
             return r;
         };
-        auto zoom = [&](double lo, double f_lo, double hi) {
+        auto zoom = [&](double lo, double f_lo, double f_lo_lo, double hi) {
             while (evals < cfg.max_ls_trials) {
                 const double mid = 0.5 * (lo + hi);
                 if (mid == lo || mid == hi) break;
                 Trial e = probe(mid);
-                if (!armijo(e) || e.f >= f_lo) {
+                if (!armijo(e) || minus(e.f, e.f_lo, f_lo, f_lo_lo) >= 0.0) {
                     hi = mid;
                     drop(e);
                     continue;
                 }
                 if (e.dphi >= c2 * dphi0) return accept(e);
-                const double dphi = e.dphi, ef = e.f;
+                const double dphi = e.dphi, ef = e.f, ef_lo = e.f_lo;
                 remember(e);
                 if (dphi * (hi - lo) >= 0.0) hi = lo;
                 lo = mid;
                 f_lo = ef;
+                f_lo_lo = ef_lo;
             }
             return fallback();
         };
-        double g_prev = 0.0, f_prev = f0, gamma = 1.0;
+        double g_prev = 0.0, f_prev = f0, f_prev_lo = f0_lo, gamma = 1.0;
         while (evals < cfg.max_ls_trials) {
             Trial e = probe(gamma);
-            if (!armijo(e) || (g_prev > 0.0 && e.f >= f_prev)) {
+            if (!armijo(e) || (g_prev > 0.0 && minus(e.f, e.f_lo, f_prev, f_prev_lo) >= 0.0)) {
                 drop(e);
-                return zoom(g_prev, f_prev, gamma);
+                return zoom(g_prev, f_prev, f_prev_lo, gamma);
             }
             if (e.dphi >= c2 * dphi0) return accept(e);
-            const double ef = e.f;
+            const double ef = e.f, ef_lo = e.f_lo;
             remember(e);
             g_prev = gamma;
             f_prev = ef;
+            f_prev_lo = ef_lo;
             gamma *= 2.0;
         }
         return fallback();
@@ -546,7 +559,7 @@ void splr_step_state(regot_ctx* ctx, SplrStateDev& S, const regot_splr_config& c
     bool ls_failed = false;
     LineSearch ls_engine{ctx, S, &out};
     try {
-        ls = ls_engine.run(S.x, S.d, S.cur.sc.f, g_dot_d, cfg);
+        ls = ls_engine.run(S.x, S.d, S.cur.sc.f, S.cur.sc.f_lo, g_dot_d, cfg);
     } catch (const Error& e) {
         if (e.code != REGOT_E_LINE_SEARCH) {
             if (have_s && cfg.overlap) cudaStreamSynchronize(ctx->side);
@@ -561,11 +574,12 @@ void splr_step_state(regot_ctx* ctx, SplrStateDev& S, const regot_splr_config& c
         ls.slot = -1;
     }
     const double f_qn = ls_failed ? S.cur.sc.f : S.tg[ls.slot].sc.f;
+    const double f_qn_lo = ls_failed ? S.cur.sc.f_lo : S.tg[ls.slot].sc.f_lo;
     sect.tick(5);
 
     if (have_s && cfg.overlap) join_chain();  // join the side stream, then read its scalars
     // hybrid selection, ties to the Sinkhorn candidate (splr.h:442-443)
-    const bool pick_s = have_s && std::isfinite(S.cand.sc.f) && (ls_failed || S.cand.sc.f <= f_qn);
+    const bool pick_s = have_s && std::isfinite(S.cand.sc.f) && (ls_failed || (S.cand.sc.f - f_qn) + (S.cand.sc.f_lo - f_qn_lo) <= 0.0);
 
     rec.iter = k;
     rec.refresh = refresh;

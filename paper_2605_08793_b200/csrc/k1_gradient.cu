@@ -187,189 +187,6 @@ k_gradient_sweep(const __grid_constant__ CUtensorMap tmap, const GradParams p)
 constexpr int kNScal = 8;
 constexpr int kFinThreads = 256;
 
-struct Fin1Params {
-    int nloc, m, n_panels;
-    const double* rowpart;
-    const double* colpart;
-    const int* panel_seg0;
-    const double* alpha;
-    const double* a;
-    const double* dir_a;  // nullable
-    double* row_sums;
-    double* g_alpha;
-    double* pack;
-    double* partials;  // gridDim.x * kNScal
-    unsigned int* ticket;
-};
-
-__device__ __forceinline__ bool last_block_done(unsigned int* ticket)
-{
-    __shared__ bool is_last;
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        const unsigned int prev = atomicAdd(ticket, 1u);
-        is_last = (prev == gridDim.x - 1);
-    }
-    __syncthreads();
-    if (is_last) __threadfence();
-    return is_last;
-}
-
-// sum of per-block partials in block order; valid in every lane of warp 0
-__device__ __forceinline__ double ordered_partial_sum(const double* partials, int k, int nblocks, int lane)
-{
-    double s = 0.0;
-    for (int b = lane; b < nblocks; b += 32) s += partials[(size_t)b * kNScal + k];
-    return warp_sum(s);
-}
-
-__global__ void __launch_bounds__(kFinThreads) k_gradient_fin1(const Fin1Params p)
-{
-    __shared__ double scratch[kNScal * (kFinThreads / 32)];
-    double acc[6] = {0, 0, 0, 0, 0, 0};
-    const int stride = gridDim.x * blockDim.x;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < p.nloc; i += stride) {
-        // panel order (fixed), 8 loads in flight
-        double r = 0.0;
-        for (int P0 = 0; P0 < p.n_panels; P0 += 8) {
-            double v[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) v[u] = (P0 + u < p.n_panels) ? p.rowpart[(size_t)(P0 + u) * p.nloc + i] : 0.0;
-#pragma unroll
-            for (int u = 0; u < 8; ++u)
-                if (P0 + u < p.n_panels) r += v[u];
-        }
-        const double al = p.alpha[i], ai = p.a[i];
-        const double ga = r - ai;
-        p.row_sums[i] = r;
-        p.g_alpha[i] = ga;
-        acc[0] += r;
-        acc[1] += al * ai;
-        acc[2] += fabs(ga);
-        acc[3] += al * ga;
-        acc[4] += ga * ga;
-        if (p.dir_a) acc[5] += ga * p.dir_a[i];
-    }
-    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < p.m; j += stride) {
-        const int P = j / kTC, off = j - P * kTC;
-        double c = 0.0;
-        const int s1 = p.panel_seg0[P + 1];
-        for (int sg = p.panel_seg0[P]; sg < s1; sg += 8) {  // segment order (fixed), 8 loads in flight
-            double v[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) v[u] = (sg + u < s1) ? p.colpart[(size_t)(sg + u) * kTC + off] : 0.0;
-#pragma unroll
-            for (int u = 0; u < 8; ++u)
-                if (sg + u < s1) c += v[u];
-        }
-        p.pack[j] = c;
-    }
-    block_sum<6>(acc, scratch);
-    if (threadIdx.x == 0)
-        for (int k = 0; k < 6; ++k) p.partials[(size_t)blockIdx.x * kNScal + k] = acc[k];
-    if (last_block_done(p.ticket)) {
-        if (threadIdx.x < 32) {
-            for (int k = 0; k < 6; ++k) {
-                const double v = ordered_partial_sum(p.partials, k, gridDim.x, threadIdx.x);
-                if (threadIdx.x == 0) p.pack[p.m + k] = v;
-            }
-            if (threadIdx.x == 0) *p.ticket = 0u;
-        }
-    }
-}
-
-// ---- epilogue 2 (after the allreduce of pack): column-side scalars, objective -------
-struct Fin2Params {
-    int m;
-    double eta;
-    const double* pack;  // m column sums + row-side scalars (global after allreduce)
-    const double* beta;
-    const double* b;
-    const double* dir_b;  // nullable
-    double* col_sums;
-    double* g_beta;
-    double* partials;
-    unsigned int* ticket;
-    GradScalars* out;
-    double* mbox;  // host mailbox: the scalars go straight to pinned host memory
-    unsigned long long seq;
-    const unsigned int* sk_flag;
-};
-
-__global__ void __launch_bounds__(kFinThreads) k_gradient_fin2(const Fin2Params p)
-{
-    __shared__ double scratch[kNScal * (kFinThreads / 32)];
-    // 0 beta.b (free part) 1 sum|c-b| (all m) 2 beta.(c-b) 3 |c-b|^2 (free part) 4 (c-b).d_beta (free part)
-    double acc[5] = {0, 0, 0, 0, 0};
-    const int stride = gridDim.x * blockDim.x;
-    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < p.m; j += stride) {
-        const double c = p.pack[j], bj = p.b[j], be = p.beta[j];
-        const double gb = c - bj;
-        p.col_sums[j] = c;
-        p.g_beta[j] = gb;
-        acc[1] += fabs(gb);
-        acc[2] += be * gb;
-        if (j < p.m - 1) {
-            acc[0] += be * bj;
-            acc[3] += gb * gb;
-            if (p.dir_b) acc[4] += gb * p.dir_b[j];
-        }
-    }
-    block_sum<5>(acc, scratch);
-    if (threadIdx.x == 0)
-        for (int k = 0; k < 5; ++k) p.partials[(size_t)blockIdx.x * kNScal + k] = acc[k];
-    if (last_block_done(p.ticket)) {
-        if (threadIdx.x < 32) {
-            double c[5];
-            for (int k = 0; k < 5; ++k) c[k] = ordered_partial_sum(p.partials, k, gridDim.x, threadIdx.x);
-            if (threadIdx.x == 0) {
-                const double* S = p.pack + p.m;
-                GradScalars o;
-                o.total_mass = S[0];
-                o.f = p.eta * S[0] - S[1] - c[0];  // dual.h:157-158
-                o.row_abs = S[2];
-                o.col_abs = c[1];
-                o.marginal_error = S[2] + c[1];  // dual.h:219-222
-                o.duality_gap = S[3] + c[2];     // dual.h:225-229
-                o.grad_sqnorm = S[4] + c[3];
-                o.g_dot_d = S[5] + c[4];
-                o.lse_flag = (double)*p.sk_flag;
-                o.f_lo = 0.0;
-                *p.out = o;
-                *p.ticket = 0u;
-                static_assert(sizeof(GradScalars) == 10 * sizeof(double), "GradScalars is 10 doubles");
-                mailbox_post(p.mbox, reinterpret_cast<const double*>(&o), 10, p.seq);
-            }
-        }
-    }
-}
-
-// ---- dense plan (tests / diagnostics; dual.h:83-94) ---------------------------------
-__global__ void k_plan(int nloc, int m, const CostViewDev cost, const double* __restrict__ alpha,
-                       const double* __restrict__ beta, const ExpScale E, const double* __restrict__ exp_table,
-                       double* __restrict__ T)
-{
-    __shared__ double tbl[kExpN * kExpCopies];
-    exp_table_fill(tbl, exp_table, threadIdx.x, blockDim.x);
-    __syncthreads();
-    const uint32_t tbl_lane = smem_u32(tbl) + (uint32_t)(threadIdx.x & 15) * 8u;
-    const long total = (long)nloc * m;
-    for (long q = (long)blockIdx.x * blockDim.x + threadIdx.x; q < total; q += (long)gridDim.x * blockDim.x) {
-        const int i = (int)(q / m), j = (int)(q % m);
-        T[q] = plan_entry_dev((alpha[i] + beta[j]) - cost_at(cost, i, j), E, tbl_lane);
-    }
-}
-
-// ---- host side ------------------------------------------------------------------------
-// ---- both epilogues in one kernel (one GPU: no allreduce between them) -----------------------------------
-// Same loops and the same per-thread summation order as k_gradient_fin1 followed by k_gradient_fin2 on the same
-// grid (so a square problem gets bit-identical scalars); one launch and one grid-wide hand-over less per evaluation.
-struct Fin12Params {
-    Fin1Params r;
-    Fin2Params c;
-    int extended;  // the three sums of the objective in double-double
-};
 // double-double: an unevaluated sum hi + lo with |lo| <= ulp(hi) / 2
 struct dd {
     double hi, lo;
@@ -435,6 +252,264 @@ __device__ __forceinline__ void dd_block_sum3(dd (&v)[3], double* scratch)
     }
     __syncthreads();
 }
+// the high part of a double-double cut into 30 + 23 significant bits (Veltkamp): sums of a few such 30-bit pieces over
+// the ranks of an allreduce are exact in any order, the 23-bit remainders and the low parts sum with errors far below
+// what the objective needs
+__device__ __forceinline__ void split30(double hi, double& h1, double& h2)
+{
+    const double c = 8388609.0 * hi;  // 2^23 + 1
+    h1 = c - (c - hi);
+    h2 = hi - h1;
+}
+constexpr int kNScalPack = 12;  // row-side scalars behind the m column sums of the allreduce payload: 6 plain + 2 x 3 pieces
+
+struct Fin1Params {
+    int nloc, m, n_panels;
+    const double* rowpart;
+    const double* colpart;
+    const int* panel_seg0;
+    const double* alpha;
+    const double* a;
+    const double* dir_a;  // nullable
+    double* row_sums;
+    double* g_alpha;
+    double* pack;
+    double* partials;  // gridDim.x * kNScal
+    unsigned int* ticket;
+    int extended;      // also sum r and alpha.a in double-double -> pack[m + 6 .. m + 12) as (30-bit, 23-bit, low) pieces
+};
+
+__device__ __forceinline__ bool last_block_done(unsigned int* ticket)
+{
+    __shared__ bool is_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned int prev = atomicAdd(ticket, 1u);
+        is_last = (prev == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (is_last) __threadfence();
+    return is_last;
+}
+
+// sum of per-block partials in block order; valid in every lane of warp 0
+__device__ __forceinline__ double ordered_partial_sum(const double* partials, int k, int nblocks, int lane)
+{
+    double s = 0.0;
+    for (int b = lane; b < nblocks; b += 32) s += partials[(size_t)b * kNScal + k];
+    return warp_sum(s);
+}
+
+__global__ void __launch_bounds__(kFinThreads) k_gradient_fin1(const Fin1Params p)
+{
+    __shared__ double scratch[kNScal * (kFinThreads / 32)];
+    double acc[6] = {0, 0, 0, 0, 0, 0};
+    dd ex[3] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+    const int stride = gridDim.x * blockDim.x;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < p.nloc; i += stride) {
+        // panel order (fixed), 8 loads in flight
+        double r = 0.0;
+        for (int P0 = 0; P0 < p.n_panels; P0 += 8) {
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = (P0 + u < p.n_panels) ? p.rowpart[(size_t)(P0 + u) * p.nloc + i] : 0.0;
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (P0 + u < p.n_panels) r += v[u];
+        }
+        const double al = p.alpha[i], ai = p.a[i];
+        const double ga = r - ai;
+        p.row_sums[i] = r;
+        p.g_alpha[i] = ga;
+        acc[0] += r;
+        acc[1] += al * ai;
+        acc[2] += fabs(ga);
+        acc[3] += al * ga;
+        acc[4] += ga * ga;
+        if (p.dir_a) acc[5] += ga * p.dir_a[i];
+        if (p.extended) {
+            ex[0] = dd_add_d(ex[0], r);
+            ex[1] = dd_add_prod(ex[1], al, ai);
+        }
+    }
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < p.m; j += stride) {
+        const int P = j / kTC, off = j - P * kTC;
+        double c = 0.0;
+        const int s1 = p.panel_seg0[P + 1];
+        for (int sg = p.panel_seg0[P]; sg < s1; sg += 8) {  // segment order (fixed), 8 loads in flight
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = (sg + u < s1) ? p.colpart[(size_t)(sg + u) * kTC + off] : 0.0;
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (sg + u < s1) c += v[u];
+        }
+        p.pack[j] = c;
+    }
+    block_sum<6>(acc, scratch);
+    if (threadIdx.x == 0)
+        for (int k = 0; k < 6; ++k) p.partials[(size_t)blockIdx.x * kNScal + k] = acc[k];
+    double* const ddpart = p.partials + (size_t)(2 * gridDim.x) * 12;  // behind the plain partials of either finalize form
+    if (p.extended) {
+        dd_block_sum3(ex, scratch);
+        if (threadIdx.x == 0)
+            for (int k = 0; k < 2; ++k) {
+                ddpart[(size_t)blockIdx.x * 6 + 2 * k] = ex[k].hi;
+                ddpart[(size_t)blockIdx.x * 6 + 2 * k + 1] = ex[k].lo;
+            }
+    }
+    if (last_block_done(p.ticket)) {
+        if (threadIdx.x < 32) {
+            for (int k = 0; k < 6; ++k) {
+                const double v = ordered_partial_sum(p.partials, k, gridDim.x, threadIdx.x);
+                if (threadIdx.x == 0) p.pack[p.m + k] = v;
+            }
+            for (int k = 0; k < 2; ++k) {
+                dd t = {0.0, 0.0};
+                if (p.extended) {
+                    for (int b = threadIdx.x; b < (int)gridDim.x; b += 32) {
+                        dd u = {ddpart[(size_t)b * 6 + 2 * k], ddpart[(size_t)b * 6 + 2 * k + 1]};
+                        t = dd_add(t, u);
+                    }
+                    for (int o = 16; o > 0; o >>= 1) t = dd_add(t, dd_shfl_xor(t, o));
+                }
+                if (threadIdx.x == 0) {
+                    double h1, h2;
+                    split30(t.hi, h1, h2);
+                    p.pack[p.m + 6 + 3 * k] = h1;
+                    p.pack[p.m + 7 + 3 * k] = h2;
+                    p.pack[p.m + 8 + 3 * k] = t.lo;
+                }
+            }
+            if (threadIdx.x == 0) *p.ticket = 0u;
+        }
+    }
+}
+
+// ---- epilogue 2 (after the allreduce of pack): column-side scalars, objective -------
+struct Fin2Params {
+    int m;
+    double eta;
+    const double* pack;  // m column sums + row-side scalars (global after allreduce)
+    const double* beta;
+    const double* b;
+    const double* dir_b;  // nullable
+    double* col_sums;
+    double* g_beta;
+    double* partials;
+    unsigned int* ticket;
+    GradScalars* out;
+    double* mbox;  // host mailbox: the scalars go straight to pinned host memory
+    unsigned long long seq;
+    const unsigned int* sk_flag;
+    int extended;  // objective in double-double from the pieces in pack[m + 6 ..) and beta.b summed here
+};
+
+__global__ void __launch_bounds__(kFinThreads) k_gradient_fin2(const Fin2Params p)
+{
+    __shared__ double scratch[kNScal * (kFinThreads / 32)];
+    // 0 beta.b (free part) 1 sum|c-b| (all m) 2 beta.(c-b) 3 |c-b|^2 (free part) 4 (c-b).d_beta (free part)
+    double acc[5] = {0, 0, 0, 0, 0};
+    dd ex[3] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+    const int stride = gridDim.x * blockDim.x;
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < p.m; j += stride) {
+        const double c = p.pack[j], bj = p.b[j], be = p.beta[j];
+        const double gb = c - bj;
+        if (p.extended && j < p.m - 1) ex[0] = dd_add_prod(ex[0], be, bj);
+        p.col_sums[j] = c;
+        p.g_beta[j] = gb;
+        acc[1] += fabs(gb);
+        acc[2] += be * gb;
+        if (j < p.m - 1) {
+            acc[0] += be * bj;
+            acc[3] += gb * gb;
+            if (p.dir_b) acc[4] += gb * p.dir_b[j];
+        }
+    }
+    block_sum<5>(acc, scratch);
+    if (threadIdx.x == 0)
+        for (int k = 0; k < 5; ++k) p.partials[(size_t)blockIdx.x * kNScal + k] = acc[k];
+    double* const ddpart = p.partials + (size_t)(2 * gridDim.x) * 12;
+    if (p.extended) {
+        dd_block_sum3(ex, scratch);
+        if (threadIdx.x == 0) {
+            ddpart[(size_t)blockIdx.x * 6] = ex[0].hi;
+            ddpart[(size_t)blockIdx.x * 6 + 1] = ex[0].lo;
+        }
+    }
+    if (last_block_done(p.ticket)) {
+        if (threadIdx.x < 32) {
+            double c[5];
+            for (int k = 0; k < 5; ++k) c[k] = ordered_partial_sum(p.partials, k, gridDim.x, threadIdx.x);
+            dd bb = {0.0, 0.0};
+            if (p.extended) {
+                for (int b = threadIdx.x; b < (int)gridDim.x; b += 32) {
+                    dd u = {ddpart[(size_t)b * 6], ddpart[(size_t)b * 6 + 1]};
+                    bb = dd_add(bb, u);
+                }
+                for (int o = 16; o > 0; o >>= 1) bb = dd_add(bb, dd_shfl_xor(bb, o));
+            }
+            if (threadIdx.x == 0) {
+                const double* S = p.pack + p.m;
+                GradScalars o;
+                o.total_mass = S[0];
+                o.f = p.eta * S[0] - S[1] - c[0];  // dual.h:157-158
+                o.row_abs = S[2];
+                o.col_abs = c[1];
+                o.marginal_error = S[2] + c[1];  // dual.h:219-222
+                o.duality_gap = S[3] + c[2];     // dual.h:225-229
+                o.grad_sqnorm = S[4] + c[3];
+                o.g_dot_d = S[5] + c[4];
+                o.lse_flag = (double)*p.sk_flag;
+                o.f_lo = 0.0;
+                if (p.extended) {
+                    // sum r and alpha.a arrive as (30-bit, 23-bit, low) pieces summed over the ranks
+                    dd sr = {S[6], 0.0}, aa = {S[9], 0.0};
+                    sr = dd_add_d(dd_add_d(sr, S[7]), S[8]);
+                    aa = dd_add_d(dd_add_d(aa, S[10]), S[11]);
+                    const double ph = __dmul_rn(p.eta, sr.hi), pe = __fma_rn(p.eta, sr.hi, -ph) + p.eta * sr.lo;
+                    dd fx = {ph, pe};
+                    dd neg1 = {-aa.hi, -aa.lo}, neg2 = {-bb.hi, -bb.lo};
+                    fx = dd_add(fx, neg1);
+                    fx = dd_add(fx, neg2);
+                    o.f = fx.hi;
+                    o.f_lo = fx.lo;
+                }
+                *p.out = o;
+                *p.ticket = 0u;
+                static_assert(sizeof(GradScalars) == 10 * sizeof(double), "GradScalars is 10 doubles");
+                mailbox_post(p.mbox, reinterpret_cast<const double*>(&o), 10, p.seq);
+            }
+        }
+    }
+}
+
+// ---- dense plan (tests / diagnostics; dual.h:83-94) ---------------------------------
+__global__ void k_plan(int nloc, int m, const CostViewDev cost, const double* __restrict__ alpha,
+                       const double* __restrict__ beta, const ExpScale E, const double* __restrict__ exp_table,
+                       double* __restrict__ T)
+{
+    __shared__ double tbl[kExpN * kExpCopies];
+    exp_table_fill(tbl, exp_table, threadIdx.x, blockDim.x);
+    __syncthreads();
+    const uint32_t tbl_lane = smem_u32(tbl) + (uint32_t)(threadIdx.x & 15) * 8u;
+    const long total = (long)nloc * m;
+    for (long q = (long)blockIdx.x * blockDim.x + threadIdx.x; q < total; q += (long)gridDim.x * blockDim.x) {
+        const int i = (int)(q / m), j = (int)(q % m);
+        T[q] = plan_entry_dev((alpha[i] + beta[j]) - cost_at(cost, i, j), E, tbl_lane);
+    }
+}
+
+// ---- host side ------------------------------------------------------------------------
+// ---- both epilogues in one kernel (one GPU: no allreduce between them) -----------------------------------
+// Same loops and the same per-thread summation order as k_gradient_fin1 followed by k_gradient_fin2 on the same
+// grid (so a square problem gets bit-identical scalars); one launch and one grid-wide hand-over less per evaluation.
+struct Fin12Params {
+    Fin1Params r;
+    Fin2Params c;
+    int extended;  // the three sums of the objective in double-double
+};
 constexpr int kNScal12 = 12;
 __global__ void __launch_bounds__(kFinThreads) k_gradient_fin12(const Fin12Params q)
 {
@@ -630,6 +705,7 @@ void launch_gradient(regot_ctx* ctx, cudaStream_t st, SweepWS& ws, ncclComm* com
     f1.pack = ws.pack.p;
     f1.partials = ws.partials.p;
     f1.ticket = ws.ticket.p;
+    f1.extended = ctx->extended_f ? 1 : 0;
     const bool fused = ctx->world == 1 && ctx->fused_finalize;
     if (!fused) {
         k_gradient_fin1<<<g1, kFinThreads, 0, st>>>(f1);
@@ -637,7 +713,7 @@ void launch_gradient(regot_ctx* ctx, cudaStream_t st, SweepWS& ws, ncclComm* com
         ++ctx->launches;
     }
 
-    if (ctx->world > 1) allreduce_sum(ctx, comm, ws.pack.p, (size_t)pr.m + kNScal, st);
+    if (ctx->world > 1) allreduce_sum(ctx, comm, ws.pack.p, (size_t)pr.m + kNScalPack, st);
 
     const int g2 = fin_grid(ctx, pr.m);
     Fin2Params f2;
@@ -655,6 +731,7 @@ void launch_gradient(regot_ctx* ctx, cudaStream_t st, SweepWS& ws, ncclComm* com
     f2.mbox = ws.mbox.data;
     f2.seq = ws.mbox.next();
     f2.sk_flag = ws.sk_flag.p;
+    f2.extended = ctx->extended_f ? 1 : 0;
     if (fused) {
         Fin12Params f12;
         f12.r = f1;

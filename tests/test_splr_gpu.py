@@ -203,3 +203,48 @@ def test_step_error_and_validation(solver, oracle):
     x.beta[5] = 0.5
     with pytest.raises(rg.ValidationError, match="gauge"):
         solver.run_splr(x, rg.SplrConfig())
+
+
+def test_extended_objective_keeps_line_searches_alive_near_the_tolerance():
+    """The one-GPU finalize kernel sums the objective in double-double and the line search compares (hi, lo) pairs
+    (csrc/k1_gradient.cu, csrc/solver.cu): a decrease below one ulp of f still registers, so no line search fails on
+    rounding noise near the tolerance.  With REGOT_B200_EXTENDED_F=0 the comparisons are the reference's (plain doubles,
+    splr.h:185-290) and the plateau of failing 30-evaluation searches is back.  Both take the same iterates while the
+    objective still moves in its leading digits."""
+    import os
+
+    from paper_2605_08793_b200 import problems
+
+    p = problems.gen_synthetic2(256, 256, 0.001)
+    cfg = rg.SplrConfig(max_iter=1000, tol=1e-8)
+    x0 = rg.DualPoint.zeros(p.n, p.m)
+    runs = {}
+    for ext in ("1", "0"):
+        os.environ["REGOT_B200_EXTENDED_F"] = ext
+        try:
+            s = rg.Solver(0)
+        finally:
+            del os.environ["REGOT_B200_EXTENDED_F"]
+        s.set_problem(p)
+        runs[ext] = s.run_splr(x0, cfg)
+        s.close()
+    on, off = runs["1"], runs["0"]
+    assert on.trace.rows[-1].marginal_error <= 1e-8 and off.trace.rows[-1].marginal_error <= 1e-8
+    failed_on, failed_off = sum(st.ls_failed for st in on.steps), sum(st.ls_failed for st in off.steps)
+    evals_on, evals_off = sum(st.ls_evals for st in on.steps), sum(st.ls_evals for st in off.steps)
+    print(f"extended: {on.trace.rows[-1].iter} iterations, {evals_on} evaluations, {failed_on} failed searches; "
+          f"plain: {off.trace.rows[-1].iter}, {evals_off}, {failed_off}")
+    # measured: 211 iterations / 306 evaluations / 1 failed search against 251 / 1825 / 47 with plain doubles
+    assert failed_on <= 2 and failed_off >= 10 * max(failed_on, 1)
+    assert 2 * evals_on <= evals_off
+    assert on.trace.rows[-1].iter <= off.trace.rows[-1].iter
+    # same iterates before the plateau (the reported f is the correctly rounded extended sum: equal to rounding)
+    rows_off = {r.iter: r for r in off.trace.rows}
+    checked = 0
+    for r in on.trace.rows:
+        q = rows_off.get(r.iter)
+        if q is None or min(r.marginal_error, q.marginal_error) < 1e-5:
+            continue
+        assert abs(r.f - q.f) <= 1e-12 * (1 + abs(q.f)), (r.iter, r.f, q.f)
+        checked += 1
+    assert checked >= 10

@@ -163,8 +163,8 @@ regot_ctx* ctx_create(int device)
         if (const char* e = std::getenv("REGOT_B200_PCG_CLUSTER")) ctx->pcg_cluster_size = std::atoi(e);
         if (const char* e = std::getenv("REGOT_B200_PCG_CLUSTER_ENTRIES")) ctx->pcg_cluster_max_entries = std::atol(e);
         if (const char* e = std::getenv("REGOT_B200_EXACT_LSE")) ctx->fast_sinkhorn = e[0] != '1';
-        if (const char* e = std::getenv("REGOT_B200_LSE_FAST_SHIFT")) ctx->lse_fast_shift = e[0] == '1';
-        if (const char* e = std::getenv("REGOT_B200_FAST_CHAIN")) ctx->fast_sinkhorn_chain = e[0] == '1';
+        if (const char* e = std::getenv("REGOT_B200_LSE_FAST_SHIFT")) ctx->lse_fast_shift = e[0] != '0';
+        if (const char* e = std::getenv("REGOT_B200_FAST_CHAIN")) ctx->fast_sinkhorn_chain = e[0] != '0';
         RG_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
         RG_CUDA(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
         RG_CUDA(cudaEventCreate(&ctx->ev_a));

@@ -302,14 +302,15 @@ struct regot_ctx {
     int pcg_cluster_size = 0;
     bool pcg_cluster_probed = false;
     long pcg_cluster_max_entries = 0;
-    // run_sinkhorn's updates take the gradient-sweep form (k7_lse.cu) unless REGOT_B200_EXACT_LSE=1; the
-    // candidate chain of run_splr only with REGOT_B200_FAST_CHAIN=1 (see solver.cu); the stand-alone entry
-    // points always use the log-sum-exp kernels
+    // Sinkhorn updates take the gradient-sweep form (k7_lse.cu: alpha_i += eta (log a_i - log r_i) from K1-speed sweeps,
+    // with an exact redo through the log-sum-exp kernels whenever a sum leaves [e^-600, e^600]) in run_sinkhorn
+    // (REGOT_B200_EXACT_LSE=1: always the log-sum-exp kernels) and in the candidate chain of run_splr
+    // (REGOT_B200_FAST_CHAIN=0: log-sum-exp kernels there); the stand-alone entry points always use the log-sum-exp kernels
     bool fast_sinkhorn = true;
+    bool fast_sinkhorn_chain = true;
     // row log-sum-exp kernel: shift by the warp's approximate maximum (one redux instead of five shuffle rounds; same
-    // value up to rounding) -- REGOT_B200_LSE_FAST_SHIFT=1; default: the exact maximum, the reference's arithmetic
-    bool lse_fast_shift = false;
-    bool fast_sinkhorn_chain = false;
+    // value up to rounding) -- REGOT_B200_LSE_FAST_SHIFT=0: the exact maximum, the reference's arithmetic
+    bool lse_fast_shift = true;
 
     // optional per-kernel timing (regot_b200_set_profiling): event pairs around the sweep kernels
     bool profiling = false;

@@ -31,7 +31,7 @@ struct LseParams {
 
 __device__ __forceinline__ double dmax(double a, double b) { return a > b ? a : b; }
 
-// (opt-in, REGOT_B200_LSE_FAST_SHIFT=1; the default subtracts the exact maximum like sinkhorn.h:57-68)
+// (default; REGOT_B200_LSE_FAST_SHIFT=0 subtracts the exact maximum like sinkhorn.h:57-68)
 // The shift of a log-sum-exp need not be the exact maximum: any value within a few hundred of it keeps every
 // exponential in range, and lse = shift + log(sum exp(v - shift)) holds for all of them.  The warp's shift is the
 // maximum of the HIGH WORDS of the lanes' maxima (one redux.sync on an order-preserving integer key instead of five

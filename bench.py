@@ -49,11 +49,11 @@ WORKLOAD_A = "A: n=m=1000 Gaussian clouds in R^2 (gen_synthetic1 iid, seed 7), e
 # ONE pass-count model for every CPU estimate of config D (both arms use these constants): the reference's CPU
 # code cannot run D (dense T 20 GB + 40 GB of top-k scratch + Cholesky fill), so its time-to-tolerance is
 # ESTIMATED as passes x measured time per pass.  Counts of the device solve at D recorded on a B200
-# (profiles/r02_configs.txt): 62 iterations, 122 line-search evaluations, 7 refreshes.  In the reference
-# (splr.h:348-478) that is 1 + 122 gradient passes + per refresh one plan() pass and one candidate gradient
+# (profiles/r02_configs.txt): 62 iterations, 93 line-search evaluations, 7 refreshes.  In the reference
+# (splr.h:348-478) that is 1 + 93 gradient passes + per refresh one plan() pass and one candidate gradient
 # pass, and J = 5 Sinkhorn steps per refresh.
-PASS_MODEL_D = {"iterations": 62, "ls_evals": 122, "refreshes": 7,
-                "gradient_passes": 1 + 122 + 2 * 7, "sinkhorn_steps": 5 * 7}
+PASS_MODEL_D = {"iterations": 62, "ls_evals": 93, "refreshes": 7,
+                "gradient_passes": 1 + 93 + 2 * 7, "sinkhorn_steps": 5 * 7}
 CPU_SAMPLE_ROWS = 2000  # rows of config D's cost matrix the CPU legs time (2000 x 50000 = 1e8 entries = config B's size)
 
 

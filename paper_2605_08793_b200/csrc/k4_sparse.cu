@@ -380,7 +380,7 @@ struct PanelArgs {
     int P, Bk, W, nlines, ngather;
     const int* ppt;
     const int* blk;
-    const int* idx;     // col (row phase) or cscrow (column phase)
+    const unsigned short* idx;  // per entry: its index minus the first index of its panel (the panel is given by the piece)
     const double* val;  // val or cscval
     const double* x;    // gathered vector, interleaved 4 doubles per index
     double* part;       // P x nlines x 2
@@ -416,6 +416,12 @@ __global__ void k_panel_cost(int nlines, int P, const int* __restrict__ ppt, int
         cost[q] = len > 0 ? len + kPanelLineCost : 1;
     }
 }
+// 16-bit panel-relative indices (10 bytes per streamed entry instead of 12)
+__global__ void k_panel_idx16(int nnz, int W, const int* __restrict__ idx, unsigned short* __restrict__ out)
+{
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < nnz; e += gridDim.x * blockDim.x) out[e] = (unsigned short)(idx[e] % W);
+}
+
 // block b of panel p starts at the first line whose prefix work reaches b / Bk of the panel's total
 __global__ void k_panel_blocks(int nlines, int P, int Bk, const int* __restrict__ scan, int* __restrict__ blk)
 {
@@ -440,22 +446,22 @@ __global__ void k_panel_blocks(int nlines, int P, int Bk, const int* __restrict_
 
 // lanes stride over [beg, end) with kLanes lanes and 8 entries in flight per lane; gathers from the staged panel
 template <int kLanes>
-__device__ __forceinline__ void panel_dot(int beg, int end, int gl, const int* __restrict__ idx, const double* __restrict__ val,
-                                          uint32_t vec, int col0, double& a0, double& a1)
+__device__ __forceinline__ void panel_dot(int beg, int end, int gl, const unsigned short* __restrict__ idx,
+                                          const double* __restrict__ val, uint32_t vec, double& a0, double& a1)
 {
     for (int t = beg + gl; t < end; t += kLanes * 8) {
-        int c[8];
+        unsigned c[8];
         double v[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
             const int tt = t + kLanes * u;
             const bool ok = tt < end;
-            c[u] = ok ? __ldg(idx + tt) : col0;
+            c[u] = ok ? (unsigned)__ldg(idx + tt) : 0u;
             v[u] = ok ? __ldg(val + tt) : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-            const double2 g = lds_f64x2(vec + (uint32_t)(c[u] - col0) * 16u);
+            const double2 g = lds_f64x2(vec + c[u] * 16u);
             a0 = __fma_rn(v[u], g.x, a0);
             a1 = __fma_rn(v[u], g.y, a1);
         }
@@ -503,7 +509,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1) k_spmv_panel(const PanelArgs
                 if (slot < kPanelDeferCap) (cta ? defer_c : defer_w)[slot] = l;
             }
         } else if (len > 0) {
-            panel_dot<8>(beg, end, gl, a.idx, a.val, vec, col0, a0, a1);
+            panel_dot<8>(beg, end, gl, a.idx, a.val, vec, a0, a1);
         }
         // even lanes of a group end with the group's sum of a0, odd lanes with a1 (fixed order)
         const bool odd = lane & 1;
@@ -520,7 +526,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1) k_spmv_panel(const PanelArgs
         const int l = defer_w[q];
         const int beg = __ldg(a.ppt + (size_t)l * pstride + p), end = __ldg(a.ppt + (size_t)l * pstride + p + 1);
         double a0 = 0.0, a1 = 0.0;
-        panel_dot<32>(beg, end, lane, a.idx, a.val, vec, col0, a0, a1);
+        panel_dot<32>(beg, end, lane, a.idx, a.val, vec, a0, a1);
         a0 = warp_sum(a0);
         a1 = warp_sum(a1);
         if (lane == 0) {
@@ -533,7 +539,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1) k_spmv_panel(const PanelArgs
         const int l = defer_c[q];
         const int beg = __ldg(a.ppt + (size_t)l * pstride + p), end = __ldg(a.ppt + (size_t)l * pstride + p + 1);
         double a0 = 0.0, a1 = 0.0;
-        panel_dot<kPanelThreads>(beg, end, tid, a.idx, a.val, vec, col0, a0, a1);
+        panel_dot<kPanelThreads>(beg, end, tid, a.idx, a.val, vec, a0, a1);
         a0 = warp_sum(a0);
         a1 = warp_sum(a1);
         if (lane == 0) {
@@ -554,7 +560,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1) k_spmv_panel(const PanelArgs
             const int beg = __ldg(a.ppt + (size_t)l * pstride + p), end = __ldg(a.ppt + (size_t)l * pstride + p + 1);
             if (end - beg <= kPanelGroupMax) continue;
             double a0 = 0.0, a1 = 0.0;
-            panel_dot<32>(beg, end, lane, a.idx, a.val, vec, col0, a0, a1);
+            panel_dot<32>(beg, end, lane, a.idx, a.val, vec, a0, a1);
             a0 = warp_sum(a0);
             a1 = warp_sum(a1);
             if (lane == 0) {
@@ -601,8 +607,11 @@ static void build_panel_plan(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, cons
     Q.scan.ensure(np + 1);
     Q.blk.ensure((size_t)Q.P * (Q.Bk + 1));
     Q.part.ensure(np * 2 + 2);
+    Q.idx16.ensure((size_t)S.nnz + 8);
     const int* ptr = rows ? S.rowptr.p : S.cscptr.p;
     const int* idx = rows ? S.col.p : S.cscrow.p;
+    k_panel_idx16<<<(int)std::max<long>(1, std::min<long>(((long)S.nnz + 255) / 256, 8L * ctx->sm_count)), 256, 0, st>>>((int)S.nnz, Q.W, idx,
+                                                                                                                    Q.idx16.p);
     const int g1 = (int)std::max<long>(1, std::min<long>(((long)Q.nlines * (Q.P + 1) + 255) / 256, 8L * ctx->sm_count));
     k_panel_ptrs<<<g1, 256, 0, st>>>(Q.nlines, Q.P, Q.W, ptr, idx, Q.ppt.p, Q.cost.p);
     k_panel_cost<<<g1, 256, 0, st>>>(Q.nlines, Q.P, Q.ppt.p, Q.cost.p);
@@ -640,7 +649,7 @@ static void launch_spmv_panel(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, con
     a.ngather = Q.ngather;
     a.ppt = Q.ppt.p;
     a.blk = Q.blk.p;
-    a.idx = rows ? S.col.p : S.cscrow.p;
+    a.idx = Q.idx16.p;
     a.val = rows ? S.val.p : S.cscval.p;
     a.x = x;
     a.part = Q.part.p;

@@ -44,6 +44,7 @@ struct PanelPlan {
     unsigned long stamp = 0;  // structure_stamp of the pattern this plan was built for
     DevBuf<int> ppt;          // nlines x (P + 1): first entry of line l at or beyond panel p
     DevBuf<int> blk;          // P x (Bk + 1): line boundaries of the blocks
+    DevBuf<unsigned short> idx16;  // per entry of the half's matrix copy: index relative to its panel
     DevBuf<int> cost, scan;   // P x nlines (+1): work per piece and its exclusive prefix sum
     DevBuf<double> part;      // P x nlines x 2: per-panel partial sums of every line
 };

@@ -493,12 +493,31 @@ __global__ void __launch_bounds__(kPanelThreads, 1) k_spmv_panel(const PanelArgs
 
     // ---- pass 1: four lines per warp, 8 lanes each; longer pieces are deferred ----
     const int sub = lane >> 3, gl = lane & 7;
+    // The pointers of a group of lines are loaded two trips ahead and the piece they delimit is prefetched into L2 one
+    // trip ahead (with pointers that arrived a trip ago: the prefetch does not wait for a load): the demand loads of the
+    // next trip then pay an L2 latency instead of an HBM one.  The kernel is bound by loads in flight, and prefetches
+    // hold no registers.
+    auto piece = [&](int l, int& pb, int& pe) {
+        pb = pe = 0;
+        if (l < l1) {
+            pb = __ldg(a.ppt + (size_t)l * pstride + p);
+            pe = __ldg(a.ppt + (size_t)l * pstride + p + 1);
+        }
+    };
+    int nbeg, nend, n2beg, n2end;
+    piece(l0 + warp * 4 + sub, nbeg, nend);
+    piece(l0 + warp * 4 + sub + kPanelWarps * 4, n2beg, n2end);
     for (int base = l0 + warp * 4; base < l1; base += kPanelWarps * 4) {
         const int l = base + sub;
-        int beg = 0, end = 0;
-        if (l < l1) {
-            beg = __ldg(a.ppt + (size_t)l * pstride + p);
-            end = __ldg(a.ppt + (size_t)l * pstride + p + 1);
+        const int beg = nbeg, end = nend;
+        nbeg = n2beg;
+        nend = n2end;
+        piece(l + 2 * kPanelWarps * 4, n2beg, n2end);
+        {
+            const int plen = min(nend - nbeg, kPanelGroupMax);
+            // 16 values or 64 indices per 128-byte line
+            for (int t = gl * 16; t < plen; t += 8 * 16) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.val + nbeg + t));
+            for (int t = gl * 64; t < plen; t += 8 * 64) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.idx + nbeg + t));
         }
         const int len = end - beg;
         double a0 = 0.0, a1 = 0.0;

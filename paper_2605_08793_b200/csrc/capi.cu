@@ -128,7 +128,7 @@ regot_status regot_b200_set_problem(regot_ctx* ctx, int64_t n, int64_t m, const 
                                     const double* a, const double* b, double eta)
 {
     return guard(ctx, [&] {
-        if (ctx->world != 1) raise(REGOT_E_VALIDATION, "set_problem: use set_problem_rows on a sharded context");
+        if (ctx->sharded) raise(REGOT_E_VALIDATION, "set_problem: use set_problem_rows on a sharded context");
         set_problem_host(ctx, n, m, 0, n, M, layout, ld, a, b, eta);
     });
 }
@@ -154,7 +154,7 @@ regot_status regot_b200_set_pointcloud(regot_ctx* ctx, int64_t n, int64_t m, int
                                        const double* a, const double* b, double eta, int32_t on_the_fly)
 {
     return guard(ctx, [&] {
-        if (ctx->world != 1) raise(REGOT_E_VALIDATION, "set_pointcloud: use set_pointcloud_rows on a sharded context");
+        if (ctx->sharded) raise(REGOT_E_VALIDATION, "set_pointcloud: use set_pointcloud_rows on a sharded context");
         set_pointcloud(ctx, n, m, 0, n, d, X, Y, a, b, eta, on_the_fly != 0);
     });
 }

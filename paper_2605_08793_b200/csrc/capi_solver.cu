@@ -91,7 +91,7 @@ struct HostCsc {
 
 HostCsc export_csc(regot_ctx* ctx, const regot_sparse& S, bool with_values)
 {
-    if (ctx->world != 1) raise(REGOT_E_UNSUPPORTED, "sparse export: only on an unsharded context");
+    if (ctx->sharded) raise(REGOT_E_UNSUPPORTED, "sparse export: only on an unsharded context");
     const int n = (int)S.nloc, mm1 = (int)S.m - 1, nnz = (int)S.nnz, dim = n + mm1;
     std::vector<int> rowptr((size_t)n + 1), col((size_t)nnz), cscptr((size_t)mm1 + 1), cscrow((size_t)nnz);
     std::vector<double> val((size_t)nnz), cscval((size_t)nnz), dA((size_t)n), dB((size_t)std::max(mm1, 0));
@@ -443,7 +443,7 @@ regot_status regot_b200_sparse_info(const regot_sparse* A, int32_t* dim, int64_t
         if (ncoords) *ncoords = A->nnz;
         if (nnz) *nnz = (A->n + A->m - 1) + 2 * A->nnz;
         // the id hashes the GLOBAL structure (sparsity.h:160-166): a row-sharded context holds only its rows -> 0
-        if (pattern_id) *pattern_id = ctx->world == 1 ? export_csc(ctx, *A, false).pattern_id : 0;
+        if (pattern_id) *pattern_id = !ctx->sharded ? export_csc(ctx, *A, false).pattern_id : 0;
     });
 }
 

@@ -79,6 +79,10 @@ void comm_init(regot_ctx* ctx, int rank, int world, const void* id128)
     if (world < 1 || rank < 0 || rank >= world) raise(REGOT_E_VALIDATION, "comm_init: bad rank/world");
     ctx->rank = rank;
     ctx->world = world;
+    // REGOT_B200_SHARDED_SINGLE: a one-rank communicator takes the sharded path (row-block upload, every collective
+    // issued) -- how the tests run the real libnccl on one GPU
+    const char* single = std::getenv("REGOT_B200_SHARDED_SINGLE");
+    ctx->sharded = world > 1 || (id128 != nullptr && single && single[0] == '1');
     if (world == 1 && id128 == nullptr) return;
     if (!nccl().lib) raise(REGOT_E_NCCL, "NCCL unavailable: " + nccl().why);
     // two communicators from two ids packed back to back (2 x 128 bytes): the
@@ -99,20 +103,20 @@ void comm_destroy(regot_ctx* ctx)
 
 void allreduce_sum(regot_ctx* ctx, ncclComm* comm, double* buf, size_t count, cudaStream_t st)
 {
-    if (ctx->world == 1) return;
+    if (!ctx->sharded) return;
     if (!comm) raise(REGOT_E_NCCL, "allreduce: communicator not initialised (regot_b200_comm_init)");
     nccl_check(nccl().AllReduce(buf, buf, count, ncclDouble, ncclSum, comm, st), "ncclAllReduce(sum)");
 }
 void allreduce_max(regot_ctx* ctx, ncclComm* comm, double* buf, size_t count, cudaStream_t st)
 {
-    if (ctx->world == 1) return;
+    if (!ctx->sharded) return;
     if (!comm) raise(REGOT_E_NCCL, "allreduce: communicator not initialised (regot_b200_comm_init)");
     nccl_check(nccl().AllReduce(buf, buf, count, ncclDouble, ncclMax, comm, st), "ncclAllReduce(max)");
 }
 
 void allreduce_sum_u64(regot_ctx* ctx, ncclComm* comm, unsigned long long* buf, size_t count, cudaStream_t st)
 {
-    if (ctx->world == 1) return;
+    if (!ctx->sharded) return;
     if (!comm) raise(REGOT_E_NCCL, "allreduce: communicator not initialised (regot_b200_comm_init)");
     nccl_check(nccl().AllReduce(buf, buf, count, ncclUint64, ncclSum, comm, st), "ncclAllReduce(u64)");
 }
@@ -511,7 +515,7 @@ void set_pointcloud(regot_ctx* ctx, int64_t n, int64_t m, int64_t row_begin, int
     RG_CUDA(cudaStreamSynchronize(st));
     double cmax = 0.0;
     for (double v : hb) cmax = std::max(cmax, v);
-    if (ctx->world > 1) {
+    if (ctx->sharded) {
         RG_CUDA(cudaMemcpyAsync(bm.p, &cmax, sizeof(double), cudaMemcpyHostToDevice, st));
         allreduce_max(ctx, ctx->comm, bm.p, 1, st);
         RG_CUDA(cudaMemcpyAsync(&cmax, bm.p, sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -629,7 +633,7 @@ void validate_problem_device(regot_ctx* ctx)
     if (!fin) raise(REGOT_E_VALIDATION, "problem: non-finite entries");
     if (!(mina > 0.0)) raise(REGOT_E_VALIDATION, "problem: a must be elementwise positive");
     if (!(minb > 0.0)) raise(REGOT_E_VALIDATION, "problem: b must be elementwise positive");
-    if (ctx->world > 1) {
+    if (ctx->sharded) {
         // the row block only holds part of a: sum the pieces
         DevBuf<double> s;
         s.ensure(1);

@@ -260,6 +260,7 @@ struct regot_ctx {
 
     // multi-GPU
     int rank = 0, world = 1;
+    bool sharded = false;  // world > 1, or a one-rank communicator driven through the sharded path (REGOT_B200_SHARDED_SINGLE: tests)
     ncclComm* comm = nullptr;       // main-stream collectives
     ncclComm* comm_side = nullptr;  // side-stream collectives (own communicator: no cross-stream ordering hazards)
 

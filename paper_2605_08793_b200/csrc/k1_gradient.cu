@@ -706,14 +706,14 @@ void launch_gradient(regot_ctx* ctx, cudaStream_t st, SweepWS& ws, ncclComm* com
     f1.partials = ws.partials.p;
     f1.ticket = ws.ticket.p;
     f1.extended = ctx->extended_f ? 1 : 0;
-    const bool fused = ctx->world == 1 && ctx->fused_finalize;
+    const bool fused = !ctx->sharded && ctx->fused_finalize;
     if (!fused) {
         k_gradient_fin1<<<g1, kFinThreads, 0, st>>>(f1);
         RG_CUDA(cudaGetLastError());
         ++ctx->launches;
     }
 
-    if (ctx->world > 1) allreduce_sum(ctx, comm, ws.pack.p, (size_t)pr.m + kNScalPack, st);
+    if (ctx->sharded) allreduce_sum(ctx, comm, ws.pack.p, (size_t)pr.m + kNScalPack, st);
 
     const int g2 = fin_grid(ctx, pr.m);
     Fin2Params f2;

@@ -349,7 +349,7 @@ void allreduce_sum_u64(regot_ctx* ctx, ncclComm* comm, unsigned long long* buf, 
 static void fetch_hist(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, size_t bins)
 {
     if (!ws.h_hist) RG_CUDA(cudaMallocHost((void**)&ws.h_hist, sizeof(unsigned long long) * kFineBins));
-    if (ctx->world > 1) allreduce_sum_u64(ctx, ctx->comm, ws.hist.p, bins, st);
+    if (ctx->sharded) allreduce_sum_u64(ctx, ctx->comm, ws.hist.p, bins, st);
     RG_CUDA(cudaMemcpyAsync(ws.h_hist, ws.hist.p, sizeof(unsigned long long) * bins, cudaMemcpyDeviceToHost, st));
     RG_CUDA(cudaStreamSynchronize(st));
 }
@@ -498,7 +498,7 @@ void topk_build_pattern(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, TopkSourc
     if (take > 0) {
         exclusive_scan(ctx, st, ws, ws.tie.p, ws.scan_a.p, nc);
         long tie_offset = 0;
-        if (ctx->world > 1) {
+        if (ctx->sharded) {
             // ties are taken in global row-major order: ranks before this one go first
             ws.hist.ensure(kFineBins);
             RG_CUDA(cudaMemsetAsync(ws.hist.p, 0, sizeof(unsigned long long) * (size_t)ctx->world, st));
@@ -720,7 +720,7 @@ void finish_structure(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, regot_spars
     if (S.n_long) RG_CUDA(cudaMemcpyAsync(S.longlines.p, hs + o_l, sizeof(int) * 2 * (size_t)S.n_long, cudaMemcpyHostToDevice, st));
     // the older persistent kernel (k5_pcg.cu) only where the block-resident one does not take the pattern
     S.pcg.fits = false;
-    if (ctx->world == 1 && !S.blocks.fits) build_pcg_schedule(ctx, st, S, rp, cp, ws.h_lines, used);
+    if (!ctx->sharded && !S.blocks.fits) build_pcg_schedule(ctx, st, S, rp, cp, ws.h_lines, used);
     RG_CUDA(cudaStreamSynchronize(st));  // the staging is free again
 }
 

@@ -316,7 +316,7 @@ static SpmvMat mat_view(const regot_ctx* ctx, const regot_sparse& S)
     A.n_lines_m = S.n_lines_m;
     A.chunk_part = S.chunk_part.p;
     A.chunk_cnt = S.chunk_cnt.p;
-    A.add_diag_b = (ctx->world == 1 || ctx->rank == 0) ? 1 : 0;
+    A.add_diag_b = (!ctx->sharded || ctx->rank == 0) ? 1 : 0;
     return A;
 }
 
@@ -352,7 +352,7 @@ void sparse_matvec(regot_ctx* ctx, cudaStream_t st, ncclComm* comm, const regot_
     if (nrhs < 1 || nrhs > kMaxRhs) raise(REGOT_E_VALIDATION, "matvec: bad number of right-hand sides");
     launch_spmv<kEpiFull>(ctx, st, S, nrhs, va, vb, ya, yb, stride_a, stride_b);
     // column results are partial sums over the row blocks
-    if (ctx->world > 1) {
+    if (ctx->sharded) {
         for (int k = 0; k < nrhs; ++k) allreduce_sum(ctx, comm, yb + (size_t)k * stride_b, (size_t)S.m - 1, st);
     }
 }
@@ -977,11 +977,11 @@ static int pcg_schur_multikernel(regot_ctx* ctx, cudaStream_t st, ncclComm* comm
     };
     // u = B' t, summed over the row blocks; on one GPU the panel form leaves its per-panel partials for the consumer
     auto half_cols = [&](const double* skip_flag) {
-        if (panel) launch_spmv_panel<kEpiColsPlain>(ctx, st, ws, S, v.ta, v.ub, skip_flag, ctx->world > 1);
+        if (panel) launch_spmv_panel<kEpiColsPlain>(ctx, st, ws, S, v.ta, v.ub, skip_flag, ctx->sharded);
         else launch_spmv<kEpiColsPlain>(ctx, st, S, nrhs, v.ta, nullptr, nullptr, v.ub, kInterleaved4, kInterleaved4, skip_flag);
-        if (ctx->world > 1) allreduce_sum(ctx, comm, v.ub, 4 * (size_t)mfree, st);
+        if (ctx->sharded) allreduce_sum(ctx, comm, v.ub, 4 * (size_t)mfree, st);
     };
-    if (panel && ctx->world == 1) {
+    if (panel && !ctx->sharded) {
         build_panel_plan(ctx, st, ws, S, false);
         v.part = S.panel_cols.part.p;
         v.n_parts = S.panel_cols.P;
@@ -989,7 +989,7 @@ static int pcg_schur_multikernel(regot_ctx* ctx, cudaStream_t st, ncclComm* comm
 
     k_schur_init_a<<<grid_a, kCgThreads, 0, st>>>(v, d_rhs_a);
     RG_CUDA(cudaGetLastError());
-    if (ctx->world > 1) allreduce_sum(ctx, comm, ws.cg_scal.p + kScalG0a, kMaxRhs, st);
+    if (ctx->sharded) allreduce_sum(ctx, comm, ws.cg_scal.p + kScalG0a, kMaxRhs, st);
     half_cols(nullptr);
     k_schur_init_b<<<grid_b, kCgThreads, 0, st>>>(v, d_rhs_b);
     RG_CUDA(cudaGetLastError());
@@ -1035,9 +1035,9 @@ int sparse_pcg(regot_ctx* ctx, cudaStream_t st, ncclComm* comm, SparseWS& ws, co
     if (nrhs < 1 || nrhs > kMaxRhs) raise(REGOT_E_VALIDATION, "pcg: bad number of right-hand sides");
     // one GPU: the block-resident kernel when every block of the pattern fits in shared memory, else the persistent
     // kernel that streams the matrix (iterated vectors in shared memory), else kernel by kernel
-    if (ctx->world == 1 && !ctx->force_multikernel_pcg && S.blocks.fits)
+    if (!ctx->sharded && !ctx->force_multikernel_pcg && S.blocks.fits)
         return pcg_schur_blocks(ctx, st, ws, S, nrhs, rhs, sol, rtol, max_iter);
-    if (ctx->world == 1 && !ctx->force_multikernel_pcg && S.pcg.fits)
+    if (!ctx->sharded && !ctx->force_multikernel_pcg && S.pcg.fits)
         return pcg_schur_persistent(ctx, st, ws, S, nrhs, rhs, sol, rtol, max_iter);
     return pcg_schur_multikernel(ctx, st, comm, ws, S, nrhs, rhs, sol, rtol, max_iter);
 }

@@ -1221,7 +1221,7 @@ void build_pcg_blocks_plan(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, regot_
     Q2.fits = false;
     Q2.pending = false;
     const int nloc = (int)S.nloc, mfree = std::max((int)S.m - 1, 0), nnz = (int)S.nnz;
-    if (ctx->pcg_blocks == 0 || ctx->world != 1 || nnz < 1 || nloc < 64 || mfree < 64) return;
+    if (ctx->pcg_blocks == 0 || ctx->sharded || nnz < 1 || nloc < 64 || mfree < 64) return;
     // far too large for shared memory: do not even try (12 B per entry and copy at the very least)
     if ((long)nnz * 12 > (long)ctx->sm_count * kPcgSmemBudget) return;
     int P, Q, cluster;

@@ -483,7 +483,7 @@ void launch_optimal_beta(regot_ctx* ctx, cudaStream_t st, SweepWS& ws, ncclComm*
                                                       ws.pack.p);
     RG_CUDA(cudaGetLastError());
     ++ctx->launches;
-    if (ctx->world > 1) {
+    if (ctx->sharded) {
         glob_max = ws.pack2.p + (size_t)m + 16;
         RG_CUDA(cudaMemcpyAsync(glob_max, loc_max, sizeof(double) * (size_t)m, cudaMemcpyDeviceToDevice, st));
         allreduce_max(ctx, comm, glob_max, (size_t)m, st);
@@ -587,7 +587,7 @@ void launch_sinkhorn_step_fast(regot_ctx* ctx, cudaStream_t st, SweepWS& ws, ncc
     launch_gradient_sweep_only(ctx, st, ws, alpha_io, beta_io);
     k_sk_cols<<<vec_grid(ctx, m), 256, 0, st>>>(m, ctx->plan.d_panel_seg0.p, ws.colpart.p, ws.pack.p);
     RG_CUDA(cudaGetLastError());
-    if (ctx->world > 1) allreduce_sum(ctx, comm, ws.pack.p, (size_t)m, st);
+    if (ctx->sharded) allreduce_sum(ctx, comm, ws.pack.p, (size_t)m, st);
     k_sk_beta_fin<<<vec_grid(ctx, std::max(nloc, m)), 256, 0, st>>>(nloc, m, pr.eta, ws.pack.p, pr.b, beta_io, alpha_io,
                                                                     ws.sk_flag.p);
     k_sk_gauge_zero<<<1, 32, 0, st>>>(beta_io, m);

@@ -60,7 +60,7 @@ void download_point(regot_ctx* ctx, const DVec& x, std::vector<double>& alpha, s
     const DeviceProblem& pr = ctx->prob;
     alpha.assign((size_t)pr.n, 0.0);
     beta.assign((size_t)pr.m, 0.0);
-    if (ctx->world > 1) {
+    if (ctx->sharded) {
         DevBuf<double> full;
         full.ensure((size_t)pr.n);
         RG_CUDA(cudaMemsetAsync(full.p, 0, sizeof(double) * (size_t)pr.n, ctx->stream));

@@ -180,7 +180,7 @@ void vec_dots(regot_ctx* ctx, cudaStream_t st, ncclComm* comm, DotScratch& ws, i
     job.partials = ws.partials.p;
     job.out = ws.out.p;
     job.ticket = ws.ticket.p;
-    const bool post = ctx->world == 1;  // sharded: the alpha parts are summed over ranks first
+    const bool post = !ctx->sharded;  // sharded: the alpha parts are summed over ranks first
     ws.mbox.ensure();
     job.mbox = post ? ws.mbox.data : nullptr;
     job.seq = post ? ws.mbox.next() : 0ULL;

@@ -148,6 +148,8 @@ regot_ctx* ctx_create(int device)
         if (const char* e = std::getenv("REGOT_B200_MULTIKERNEL_PCG")) ctx->force_multikernel_pcg = e[0] == '1';
         if (const char* e = std::getenv("REGOT_B200_PANEL_SPMV")) ctx->panel_spmv = std::atoi(e);
         if (const char* e = std::getenv("REGOT_B200_PANEL_WIDTH")) ctx->panel_width = std::atoi(e);
+        if (const char* e = std::getenv("REGOT_B200_PANEL_ELL")) ctx->panel_ell = std::atoi(e);
+        if (const char* e = std::getenv("REGOT_B200_PANEL_AHEAD")) ctx->panel_ahead = std::max(0, std::atoi(e));
         // off by default: measured 11 % (config A) / 1 % (1600 x 1200) of the direction solve, slower above ~50k entries
         ctx->pcg_cluster_size = 0;
         ctx->pcg_cluster_max_entries = 50000;

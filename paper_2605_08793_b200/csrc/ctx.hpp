@@ -281,6 +281,8 @@ struct regot_ctx {
     // (REGOT_B200_PANEL_SPMV); panel_width > 0 caps the panel width in entries (REGOT_B200_PANEL_WIDTH, tests)
     int panel_spmv = -1;
     int panel_width = 0;
+    int panel_ahead = 0;  // REGOT_B200_PANEL_AHEAD: prefetch distance of the ELL stream in rows of 32 entries (0: off)
+    int panel_ell = 1;  // REGOT_B200_PANEL_ELL=0: pieces straight from the CSR / CSC copy (the form before the ELL stream)
     // one GPU: the two finalize kernels of a gradient pass as one (REGOT_B200_FUSED_FINALIZE=0: two kernels, as sharded runs)
     bool fused_finalize = true;
     // the objective's three sums accumulated in double-double and the line search comparing objectives as (hi, lo) pairs, so

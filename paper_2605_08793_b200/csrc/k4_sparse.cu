@@ -374,6 +374,10 @@ constexpr int kPanelGroupMax = 256;     // pieces up to this many entries: 8 lan
 constexpr int kPanelWarpMax = 8192;     // up to this many: one warp; longer: the whole CTA
 constexpr int kPanelDeferCap = 2048;    // deferred pieces per CTA kept in the shared-memory lists
 constexpr int kPanelLineCost = 24;      // work of a piece beyond its entries (pointer loads, reduction), in entries
+constexpr int kEllPieces = 8;           // ELL stream: pieces per chunk ...
+constexpr int kEllPhases = 4;           // ... and lanes per piece (entry k of a piece belongs to lane group k % 4)
+constexpr int kEllBatch = 4;            // rows per batch: a lane's values of a batch are 2 x 16 bytes, its indices 8 bytes
+constexpr int kEllKeyBits = 9;          // cap - length fits in 9 bits (kPanelGroupMax = 256)
 
 struct PanelArgs {
     const double* skip;  // != null and *skip != 0: nothing to do
@@ -384,6 +388,18 @@ struct PanelArgs {
     const double* val;  // val or cscval
     const double* x;    // gathered vector, interleaved 4 doubles per index
     double* part;       // P x nlines x 2
+    // ELL stream (null eval: pieces are read from the CSR / CSC copy)
+    const int* itembase;  // per piece q = p nlines + l: its first item (np + 1 entries)
+    const int* elen;      // per sorted item: entries, ...
+    const int* eout;      // ... and where its two sums go (index into part, in pairs)
+    const int* chrows;
+    const int* choff;
+    const unsigned short* eidx;
+    const double* eval;
+    int ahead;  // rows of the stream between a trip and the rows it prefetches into L2 (0: no prefetch)
+#ifdef REGOT_PANEL_TIMING
+    int fake;
+#endif
 };
 
 // first entry of line l whose index is >= p W, for p = 0..P (p = P: the end of the line)
@@ -444,6 +460,126 @@ __global__ void k_panel_blocks(int nlines, int P, int Bk, const int* __restrict_
     blk[q] = line;
 }
 
+// ---- ELL stream: the pieces of a (panel, block) CTA as one contiguous, coalesced stream ------------------------------
+// Reading the pieces where they lie in the CSR / CSC copy costs pointer loads per piece, half-empty trips (a piece of 125
+// entries on 8 lanes x 8 in flight) and shuffles per piece; measured 0.085 ms per half at config D = 0.45 of the HBM roof.
+// Here the pieces of a CTA up to kPanelGroupMax entries are sorted by length (stable), taken 8 to a chunk, and laid out so
+// that a warp reads whole 256-byte rows: entry k of piece j of a chunk sits at row k / 4, lane (k % 4) * 8 + j.  Four
+// lanes sum a piece, each its k % 4 class in order, then a fixed two-step butterfly: bitwise reproducible, and independent
+// of which warp takes which chunk (chunks are handed out longest first through a counter).  Indices are laid out once per
+// pattern; the values are copied into the layout once per solve (k_ell_values).
+// items of piece q = p * nlines + l: its segments of up to kPanelGroupMax entries (an empty piece is one empty item)
+__global__ void k_ell_count(int nlines, int P, const int* __restrict__ ppt, int* __restrict__ nseg)
+{
+    const long total = (long)nlines * P;
+    for (long q = (long)blockIdx.x * blockDim.x + threadIdx.x; q <= total; q += (long)gridDim.x * blockDim.x) {
+        int ns = 0;
+        if (q < total) {
+            const int p = (int)(q / nlines), l = (int)(q - (long)p * nlines);
+            const int len = ppt[(size_t)l * (P + 1) + p + 1] - ppt[(size_t)l * (P + 1) + p];
+            ns = max(1, (len + kPanelGroupMax - 1) / kPanelGroupMax);
+        }
+        nseg[q] = ns;
+    }
+}
+__global__ void k_ell_fill_u32(long n, unsigned v, unsigned* __restrict__ out)
+{
+    for (long q = (long)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += (long)gridDim.x * blockDim.x) out[q] = v;
+}
+__global__ void k_ell_keys(int nlines, int P, int Bk, const int* __restrict__ ppt, const int* __restrict__ blk,
+                           const int* __restrict__ itembase, unsigned* __restrict__ key, int* __restrict__ id0, int* __restrict__ item_q)
+{
+    const long total = (long)nlines * P;
+    for (long q = (long)blockIdx.x * blockDim.x + threadIdx.x; q < total; q += (long)gridDim.x * blockDim.x) {
+        const int p = (int)(q / nlines), l = (int)(q - (long)p * nlines);
+        const int len = ppt[(size_t)l * (P + 1) + p + 1] - ppt[(size_t)l * (P + 1) + p];
+        // the block of line l in panel p: the last b with blk[p][b] <= l (blocks may be empty)
+        const int* bl = blk + (size_t)p * (Bk + 1);
+        int lo = 0, hi = Bk;  // invariant: bl[lo] <= l, answer in [lo, hi)
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (bl[mid] <= l) lo = mid;
+            else hi = mid;
+        }
+        const unsigned cta = (unsigned)(p * Bk + lo) << kEllKeyBits;
+        const int b0 = itembase[q], ns = itembase[q + 1] - b0;
+        for (int sg = 0; sg < ns; ++sg) {
+            const int seglen = min(kPanelGroupMax, len - sg * kPanelGroupMax);
+            key[b0 + sg] = cta | (unsigned)(kPanelGroupMax - seglen);
+            id0[b0 + sg] = b0 + sg;
+            item_q[b0 + sg] = (int)q;
+        }
+    }
+}
+// per sorted item: length, first entry, where its sum goes (part[q] for a piece of one item, else part[np + item]); per
+// chunk its rows (from its first = longest item)
+__global__ void k_ell_chunks(int nlines, int P, int Bk, const int* __restrict__ ppt, const int* __restrict__ blk,
+                             const int* __restrict__ itembase, const unsigned* __restrict__ key, const int* __restrict__ id,
+                             const int* __restrict__ item_q, int* __restrict__ elen, int* __restrict__ ebeg,
+                             int* __restrict__ eout, int* __restrict__ chrows)
+{
+    const long np = (long)nlines * P;
+    const long total = itembase[np];
+    for (long r = (long)blockIdx.x * blockDim.x + threadIdx.x; r < total; r += (long)gridDim.x * blockDim.x) {
+        const int it = id[r], q = item_q[it];
+        const int p = q / nlines, l = q - p * nlines;
+        const int b0 = itembase[q], ns = itembase[q + 1] - b0, sg = it - b0;
+        const int beg = ppt[(size_t)l * (P + 1) + p], len = ppt[(size_t)l * (P + 1) + p + 1] - beg;
+        const int seglen = min(kPanelGroupMax, len - sg * kPanelGroupMax);
+        elen[r] = seglen;
+        ebeg[r] = beg + sg * kPanelGroupMax;
+        eout[r] = ns == 1 ? q : (int)np + it;
+        const int cta = (int)(key[r] >> kEllKeyBits);
+        const int first = itembase[(size_t)p * nlines + blk[(size_t)p * (Bk + 1) + (cta - p * Bk)]];
+        const int pos = (int)(r - first);
+        // rows in whole batches of kEllBatch (the loads are vectors over 2 / 4 consecutive rows)
+        if (pos % kEllPieces == 0)
+            chrows[first / kEllPieces + cta + pos / kEllPieces] = (seglen + kEllPhases * kEllBatch - 1) / (kEllPhases * kEllBatch) * kEllBatch;
+    }
+}
+// indices and the slot -> entry map of every chunk: one warp per chunk, CTA c of the grid = CTA c of the mat-vec
+__global__ void k_ell_fill(int nlines, int P, int Bk, const int* __restrict__ blk, const int* __restrict__ itembase,
+                           const int* __restrict__ elen, const int* __restrict__ ebeg, const int* __restrict__ chrows,
+                           const int* __restrict__ choff, const unsigned short* __restrict__ idx16,
+                           int* __restrict__ emap, unsigned short* __restrict__ eidx)
+{
+    const int cta = blockIdx.x, p = cta / Bk, b = cta - p * Bk;
+    const int l0 = blk[(size_t)p * (Bk + 1) + b], l1 = blk[(size_t)p * (Bk + 1) + b + 1];
+    const int first = itembase[(size_t)p * nlines + l0], cnt = itembase[(size_t)p * nlines + l1] - first;
+    const int nch = (cnt + kEllPieces - 1) / kEllPieces;
+    const int cb = first / kEllPieces + cta;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const int g = lane >> 3, j = lane & 7;
+    for (int ci = warp; ci < nch; ci += nwarps) {
+        const int rows = chrows[cb + ci];
+        const size_t off = (size_t)choff[cb + ci] * 32;
+        const bool valid = ci * kEllPieces + j < cnt;
+        int beg = 0, eff = 0;
+        if (valid) {
+            const int r = first + ci * kEllPieces + j;
+            eff = elen[r];
+            beg = ebeg[r];
+        }
+        for (int t = 0; t < rows; ++t) {
+            const int k = t * kEllPhases + g;
+            const bool ok = k < eff;
+            // values: rows in pairs, a lane's two values adjacent; indices: rows in fours, a lane's four adjacent
+            emap[off + (size_t)(t >> 1) * 64 + lane * 2 + (t & 1)] = ok ? beg + k : -1;
+            eidx[off + (size_t)(t >> 2) * 128 + lane * 4 + (t & 3)] = ok ? idx16[beg + k] : (unsigned short)0;
+        }
+    }
+}
+// the values into the layout, once per solve; the slot count comes from the scan (device memory)
+__global__ void k_ell_values(const int* __restrict__ total_rows, const int* __restrict__ emap, const double* __restrict__ val,
+                             double* __restrict__ eval)
+{
+    const long total = (long)(*total_rows) * 32;
+    for (long q = (long)blockIdx.x * blockDim.x + threadIdx.x; q < total; q += (long)gridDim.x * blockDim.x) {
+        const int e = emap[q];
+        eval[q] = e >= 0 ? __ldg(val + e) : 0.0;
+    }
+}
+
 // lanes stride over [beg, end) with kLanes lanes and 8 entries in flight per lane; gathers from the staged panel
 template <int kLanes>
 __device__ __forceinline__ void panel_dot(int beg, int end, int gl, const unsigned short* __restrict__ idx,
@@ -478,66 +614,180 @@ __global__ void __launch_bounds__(kPanelThreads, 1) k_spmv_panel(const PanelArgs
     int* defer_w = reinterpret_cast<int*>(smem + (size_t)a.W * 16);  // pieces for a warp
     int* defer_c = defer_w + kPanelDeferCap;                         // pieces for the CTA
     double* wpart = reinterpret_cast<double*>(defer_c + kPanelDeferCap);  // kPanelWarps x 2
-    __shared__ int n_defer_w, n_defer_c;
+    __shared__ int n_defer_w, n_defer_c, next_chunk;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) n_defer_w = n_defer_c = 0;
+    if (tid == 0) n_defer_w = n_defer_c = next_chunk = 0;
+#ifdef REGOT_PANEL_TIMING
+    __shared__ long long t_warp[kPanelWarps];
+    const long long t_0 = clock64();
+#endif
     // stage the panel: entries (x[4 j], x[4 j + 1]) of the interleaved vector
     for (int j = tid; j < wp; j += kPanelThreads) {
         const double2 g = __ldcg(reinterpret_cast<const double2*>(a.x + (size_t)(col0 + j) * 4));
         asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(vec + (uint32_t)j * 16u), "d"(g.x), "d"(g.y) : "memory");
     }
     __syncthreads();
+#ifdef REGOT_PANEL_TIMING
+    const long long t_1 = clock64();
+#endif
     const int l0 = a.blk[p * (a.Bk + 1) + b], l1 = a.blk[p * (a.Bk + 1) + b + 1];
     const size_t pstride = (size_t)(a.P + 1);
     double* const part = a.part + (size_t)p * a.nlines * 2;
 
-    // ---- pass 1: four lines per warp, 8 lanes each; longer pieces are deferred ----
-    const int sub = lane >> 3, gl = lane & 7;
-    // The pointers of a group of lines are loaded two trips ahead and the piece they delimit is prefetched into L2 one
-    // trip ahead (with pointers that arrived a trip ago: the prefetch does not wait for a load): the demand loads of the
-    // next trip then pay an L2 latency instead of an HBM one.  The kernel is bound by loads in flight, and prefetches
-    // hold no registers.
-    auto piece = [&](int l, int& pb, int& pe) {
-        pb = pe = 0;
-        if (l < l1) {
-            pb = __ldg(a.ppt + (size_t)l * pstride + p);
-            pe = __ldg(a.ppt + (size_t)l * pstride + p + 1);
-        }
-    };
-    int nbeg, nend, n2beg, n2end;
-    piece(l0 + warp * 4 + sub, nbeg, nend);
-    piece(l0 + warp * 4 + sub + kPanelWarps * 4, n2beg, n2end);
-    for (int base = l0 + warp * 4; base < l1; base += kPanelWarps * 4) {
-        const int l = base + sub;
-        const int beg = nbeg, end = nend;
-        nbeg = n2beg;
-        nend = n2end;
-        piece(l + 2 * kPanelWarps * 4, n2beg, n2end);
-        {
-            const int plen = min(nend - nbeg, kPanelGroupMax);
-            // 16 values or 64 indices per 128-byte line
-            for (int t = gl * 16; t < plen; t += 8 * 16) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.val + nbeg + t));
-            for (int t = gl * 64; t < plen; t += 8 * 64) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.idx + nbeg + t));
-        }
-        const int len = end - beg;
-        double a0 = 0.0, a1 = 0.0;
-        if (len > kPanelGroupMax) {
-            if (gl == 0) {
-                const bool cta = len > kPanelWarpMax;
-                const int slot = atomicAdd(cta ? &n_defer_c : &n_defer_w, 1);
-                if (slot < kPanelDeferCap) (cta ? defer_c : defer_w)[slot] = l;
+    if (a.eval != nullptr) {
+        // ---- pass 1, ELL stream: chunks of 8 pieces handed out longest first; 4 lanes per piece ----
+        const int g = lane >> 3, j = lane & 7;
+        const int first = __ldg(a.itembase + (size_t)p * a.nlines + l0);
+        const int cnt = __ldg(a.itembase + (size_t)p * a.nlines + l1) - first, nch = (cnt + kEllPieces - 1) / kEllPieces;
+        const int cb = first / kEllPieces + blockIdx.x;
+        // the CTA's stream is contiguous (chunk after chunk); every trip asks L2 for the 8 rows kEllAhead rows further
+        // down the stream -- for whichever warp gets there: prefetches hold no registers, and the demand loads of a
+        // trip then pay an L2 latency
+        const int end_row = __ldg(a.choff + cb + nch);
+        if (a.ahead > 0 && lane < 2) {  // the head of the stream, which no trip asks for
+            const int begin_row = __ldg(a.choff + cb);
+            for (int r = begin_row + warp * 8; r < min(begin_row + a.ahead, end_row - 8); r += kPanelWarps * 8) {
+                if (lane == 0)
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.eval + (size_t)r * 32), "r"(8 * 32 * 8) : "memory");
+                else
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.eidx + (size_t)r * 32), "r"(8 * 32 * 2) : "memory");
             }
-        } else if (len > 0) {
-            panel_dot<8>(beg, end, gl, a.idx, a.val, vec, a0, a1);
         }
-        // even lanes of a group end with the group's sum of a0, odd lanes with a1 (fixed order)
-        const bool odd = lane & 1;
-        double c = (odd ? a1 : a0) + shfl_xor_d(odd ? a0 : a1, 1);
-        c += shfl_xor_d(c, 2);
-        c += shfl_xor_d(c, 4);
-        if (l < l1 && len <= kPanelGroupMax && gl < 2) part[(size_t)l * 2 + gl] = c;
+        for (;;) {
+            int ci = 0;
+            if (lane == 0) ci = atomicAdd(&next_chunk, 1);
+            ci = __shfl_sync(0xffffffffu, ci, 0);
+            if (ci >= nch) break;
+            const int rows = __ldg(a.chrows + cb + ci);
+            const int row0 = __ldg(a.choff + cb + ci);
+            const bool valid = ci * kEllPieces + j < cnt;
+            int dest = 0, eff = 0;
+            if (valid) {
+                eff = __ldg(a.elen + first + ci * kEllPieces + j);
+                dest = __ldg(a.eout + first + ci * kEllPieces + j);
+            }
+            const double* vp = a.eval + (size_t)row0 * 32 + lane * 2;          // + (t / 2) * 64: rows t, t + 1
+            const unsigned short* ip = a.eidx + (size_t)row0 * 32 + lane * 4;  // + (t / 4) * 128: rows t .. t + 3
+            double a0 = 0.0, a1 = 0.0;
+            // A batch is 4 rows: per lane two 16-byte loads of values and one 8-byte load of indices (the LSU takes a
+            // request per instruction whatever its width: 16 scalar loads per 8 rows kept its queue full -- lg_throttle --
+            // at 13 B/clk per SM).  Two batches in registers: one is loaded while the other is consumed.  L1::no_allocate:
+            // the stream is read once, and with the panel in shared memory L1 is too small to hold the lines in flight.
+            // Vectors wholly past the item's end are not loaded; padding inside a vector is (value 0, index 0).
+            struct Batch {
+                double2 v01, v23;
+                uint2 c;
+            };
+            auto load4 = [&](int t, Batch& B) {
+                B.v01 = B.v23 = make_double2(0.0, 0.0);
+                B.c = make_uint2(0u, 0u);
+                if (t * kEllPhases + g < eff) {
+                    asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0, %1}, [%2];" : "=r"(B.c.x), "=r"(B.c.y) : "l"(ip + (size_t)(t >> 2) * 128));
+                    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(B.v01.x), "=d"(B.v01.y) : "l"(vp + (size_t)(t >> 1) * 64));
+                }
+                if ((t + 2) * kEllPhases + g < eff)
+                    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(B.v23.x), "=d"(B.v23.y) : "l"(vp + (size_t)((t >> 1) + 1) * 64));
+            };
+            auto use1 = [&](unsigned c, double v) {
+#ifdef REGOT_PANEL_TIMING
+                if (a.fake == 1) c = lane;  // (experiment) conflict-free gather
+                if (a.fake == 2) {          // (experiment) the stream alone: no gather
+                    a0 = __fma_rn(v, (double)c, a0);
+                    return;
+                }
+#endif
+                const double2 gv = lds_f64x2(vec + c * 16u);
+                a0 = __fma_rn(v, gv.x, a0);
+                a1 = __fma_rn(v, gv.y, a1);
+            };
+            auto use4 = [&](const Batch& B) {
+                use1(B.c.x & 0xffffu, B.v01.x);
+                use1(B.c.x >> 16, B.v01.y);
+                use1(B.c.y & 0xffffu, B.v23.x);
+                use1(B.c.y >> 16, B.v23.y);
+            };
+            Batch bA, bB;
+            load4(0, bA);
+            for (int t = 0; t < rows; t += 8) {
+                if (a.ahead > 0) {
+                    const int prow = row0 + t + a.ahead;
+                    if (prow + 8 <= end_row) {
+                        // one bulk request per array: 8 rows of values (2 KB) and of indices (512 B)
+                        if (lane == 0)
+                            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.eval + (size_t)prow * 32), "r"(8 * 32 * 8) : "memory");
+                        else if (lane == 1)
+                            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.eidx + (size_t)prow * 32), "r"(8 * 32 * 2) : "memory");
+                    }
+                }
+                load4(t + 4, bB);
+                use4(bA);
+                load4(t + 8, bA);
+                use4(bB);
+            }
+            // lane groups 0 / 2 end with the piece's sum of a0, groups 1 / 3 with a1; then the pairs (fixed order)
+            const bool odd = g & 1;
+            double c2 = (odd ? a1 : a0) + shfl_xor_d(odd ? a0 : a1, 8);
+            c2 += shfl_xor_d(c2, 16);
+            if (valid && g < 2) a.part[(size_t)dest * 2 + g] = c2;
+        }
+#ifndef REGOT_PANEL_TIMING
+        return;  // every piece went through the stream: no deferred pieces
+#endif
+    } else {
+        // ---- pass 1: four lines per warp, 8 lanes each; longer pieces are deferred ----
+        const int sub = lane >> 3, gl = lane & 7;
+        // The pointers of a group of lines are loaded two trips ahead and the piece they delimit is prefetched into L2 one
+        // trip ahead (with pointers that arrived a trip ago: the prefetch does not wait for a load): the demand loads of the
+        // next trip then pay an L2 latency instead of an HBM one.  The kernel is bound by loads in flight, and prefetches
+        // hold no registers.
+        auto piece = [&](int l, int& pb, int& pe) {
+            pb = pe = 0;
+            if (l < l1) {
+                pb = __ldg(a.ppt + (size_t)l * pstride + p);
+                pe = __ldg(a.ppt + (size_t)l * pstride + p + 1);
+            }
+        };
+        int nbeg, nend, n2beg, n2end;
+        piece(l0 + warp * 4 + sub, nbeg, nend);
+        piece(l0 + warp * 4 + sub + kPanelWarps * 4, n2beg, n2end);
+        for (int base = l0 + warp * 4; base < l1; base += kPanelWarps * 4) {
+            const int l = base + sub;
+            const int beg = nbeg, end = nend;
+            nbeg = n2beg;
+            nend = n2end;
+            piece(l + 2 * kPanelWarps * 4, n2beg, n2end);
+            {
+                const int plen = min(nend - nbeg, kPanelGroupMax);
+                // 16 values or 64 indices per 128-byte line
+                for (int t = gl * 16; t < plen; t += 8 * 16) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.val + nbeg + t));
+                for (int t = gl * 64; t < plen; t += 8 * 64) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.idx + nbeg + t));
+            }
+            const int len = end - beg;
+            double a0 = 0.0, a1 = 0.0;
+            if (len > kPanelGroupMax) {
+                if (gl == 0) {
+                    const bool cta = len > kPanelWarpMax;
+                    const int slot = atomicAdd(cta ? &n_defer_c : &n_defer_w, 1);
+                    if (slot < kPanelDeferCap) (cta ? defer_c : defer_w)[slot] = l;
+                }
+            } else if (len > 0) {
+                panel_dot<8>(beg, end, gl, a.idx, a.val, vec, a0, a1);
+            }
+            // even lanes of a group end with the group's sum of a0, odd lanes with a1 (fixed order)
+            const bool odd = lane & 1;
+            double c = (odd ? a1 : a0) + shfl_xor_d(odd ? a0 : a1, 1);
+            c += shfl_xor_d(c, 2);
+            c += shfl_xor_d(c, 4);
+            if (l < l1 && len <= kPanelGroupMax && gl < 2) part[(size_t)l * 2 + gl] = c;
+        }
     }
+#ifdef REGOT_PANEL_TIMING
+    if (lane == 0) t_warp[warp] = clock64();
+#endif
     __syncthreads();
+#ifdef REGOT_PANEL_TIMING
+    const long long t_2 = clock64();
+#endif
     // ---- pass 2: one warp per deferred piece ----
     const int nw_list = min(n_defer_w, kPanelDeferCap), nc_list = min(n_defer_c, kPanelDeferCap);
     const bool overflow = n_defer_w > kPanelDeferCap || n_defer_c > kPanelDeferCap;
@@ -573,6 +823,19 @@ __global__ void __launch_bounds__(kPanelThreads, 1) k_spmv_panel(const PanelArgs
         }
         __syncthreads();
     }
+#ifdef REGOT_PANEL_TIMING
+    __syncthreads();
+    if (tid == 0 && a.ahead == 7777) {
+        long long lo = t_warp[0], hi = t_warp[0], sum = 0;
+        for (int w = 0; w < kPanelWarps; ++w) {
+            lo = min(lo, t_warp[w]);
+            hi = max(hi, t_warp[w]);
+            sum += t_warp[w] - t_1;
+        }
+        printf("panel cta %3d p %d b %2d lines %5d stage %6lld pass1 first %6lld mean %6lld last %6lld pass23 %6lld defer %d %d\n", (int)blockIdx.x,
+               p, b, l1 - l0, t_1 - t_0, lo - t_1, sum / kPanelWarps, hi - t_1, clock64() - t_2, n_defer_w, n_defer_c);
+    }
+#endif
     // more deferred pieces than the lists hold (never at the sizes this path is meant for): rescan, one warp each
     if (overflow) {
         for (int l = l0 + warp; l < l1; l += kPanelWarps) {
@@ -590,22 +853,46 @@ __global__ void __launch_bounds__(kPanelThreads, 1) k_spmv_panel(const PanelArgs
     }
 }
 
+// sum of line l's per-panel partials in panel order; a piece the ELL stream cut into several items is summed in item
+// order first (its items' sums sit behind the P x nlines piece slots)
+__device__ __forceinline__ double panel_line_sum(const double* __restrict__ part, const int* __restrict__ itembase, int nlines, int P,
+                                                 int l, int k)
+{
+    double s = 0.0;
+    if (itembase == nullptr) {
+        for (int p = 0; p < P; ++p) s += part[((size_t)p * nlines + l) * 2 + k];
+        return s;
+    }
+    const size_t np = (size_t)nlines * P;
+    for (int p = 0; p < P; ++p) {
+        const size_t q = (size_t)p * nlines + l;
+        const int b0 = itembase[q], ns = itembase[q + 1] - b0;
+        if (ns == 1) {
+            s += part[q * 2 + k];
+        } else {
+            double t = 0.0;
+            for (int sg = 0; sg < ns; ++sg) t += part[(np + (size_t)(b0 + sg)) * 2 + k];
+            s += t;
+        }
+    }
+    return s;
+}
+
 // y_line = sum over panels (panel order) of part[p][line], then the epilogue of the half mat-vec
 template <int kEpi>
-__global__ void k_panel_combine(int nlines, int P, const double* __restrict__ part, const double* __restrict__ diag,
-                                double* __restrict__ y, const double* skip)
+__global__ void k_panel_combine(int nlines, int P, const double* __restrict__ part, const int* __restrict__ itembase,
+                                const double* __restrict__ diag, double* __restrict__ y, const double* skip)
 {
     if (skip != nullptr && *skip != 0.0) return;
     const int total = nlines * 2;
     for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < total; q += gridDim.x * blockDim.x) {
         const int l = q >> 1, k = q & 1;
-        double s = 0.0;
-        for (int p = 0; p < P; ++p) s += part[((size_t)p * nlines + l) * 2 + k];
+        const double s = panel_line_sum(part, itembase, nlines, P, l, k);
         y[(size_t)l * 4 + k] = (kEpi == kEpiRowsScaled) ? s / diag[l] : s;
     }
 }
 
-static constexpr int panel_smem(int W) { return W * 16 + 2 * kPanelDeferCap * 4 + kPanelWarps * 2 * 8; }
+static constexpr int panel_smem(int W, bool ell = false) { return W * 16 + (ell ? 0 : 2 * kPanelDeferCap * 4 + kPanelWarps * 2 * 8); }
 
 // (re)build the plan of one half for the current pattern; everything stays on the device
 static void build_panel_plan(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, const regot_sparse& S, bool rows)
@@ -643,7 +930,67 @@ static void build_panel_plan(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, cons
     k_panel_blocks<<<(nb + 127) / 128, 128, 0, st>>>(Q.nlines, Q.P, Q.Bk, Q.scan.p, Q.blk.p);
     RG_CUDA(cudaGetLastError());
     ctx->launches += 5;
+    if (ctx->panel_ell) {
+        // ELL stream: every piece cut into items of up to kPanelGroupMax entries, the items of a CTA sorted by length
+        // (stable), chunk tables, indices.  Item and slot counts stay on the device; the buffers take their bounds.
+        const int ncta = Q.P * Q.Bk;
+        Q.item_cap = np + (size_t)S.nnz / kPanelGroupMax + 1;
+        Q.nchunk_slots = (int)(Q.item_cap / kEllPieces) + ncta + 1;
+        Q.ell_cap = (size_t)S.nnz + (size_t)ncta * 2 * kEllPieces * kPanelGroupMax + (size_t)Q.nchunk_slots * 32 * kEllBatch + 64;
+        Q.nseg.ensure(np + 2);
+        Q.itembase.ensure(np + 2);
+        Q.ekey.ensure(Q.item_cap);
+        Q.ekey2.ensure(Q.item_cap);
+        Q.eid0.ensure(Q.item_cap);
+        Q.eid.ensure(Q.item_cap);
+        Q.item_q.ensure(Q.item_cap);
+        Q.elen.ensure(Q.item_cap);
+        Q.ebeg.ensure(Q.item_cap);
+        Q.eout.ensure(Q.item_cap);
+        Q.chrows.ensure((size_t)Q.nchunk_slots + 1);
+        Q.choff.ensure((size_t)Q.nchunk_slots + 1);
+        Q.emap.ensure(Q.ell_cap);
+        Q.eidx.ensure(Q.ell_cap);
+        Q.eval.ensure(Q.ell_cap);
+        Q.part.ensure((np + Q.item_cap) * 2 + 2);
+        const int gi = (int)std::max<long>(1, std::min<long>(((long)np + 255) / 256, 8L * ctx->sm_count));
+        const int gk = (int)std::max<long>(1, std::min<long>(((long)Q.item_cap + 255) / 256, 8L * ctx->sm_count));
+        int cta_bits = 1;
+        while ((1 << cta_bits) < ncta) ++cta_bits;
+        const int key_bits = kEllKeyBits + cta_bits + 1;  // the top bit marks the unused tail of the item arrays
+        size_t sbytes = 0;
+        k_ell_count<<<gi, 256, 0, st>>>(Q.nlines, Q.P, Q.ppt.p, Q.nseg.p);
+        RG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, sbytes, Q.nseg.p, Q.itembase.p, (int)np + 1, st));
+        ws.cub_tmp.ensure(sbytes);
+        RG_CUDA(cub::DeviceScan::ExclusiveSum(ws.cub_tmp.p, sbytes, Q.nseg.p, Q.itembase.p, (int)np + 1, st));
+        k_ell_fill_u32<<<gk, 256, 0, st>>>((long)Q.item_cap, 1u << (kEllKeyBits + cta_bits), Q.ekey.p);
+        k_ell_keys<<<gi, 256, 0, st>>>(Q.nlines, Q.P, Q.Bk, Q.ppt.p, Q.blk.p, Q.itembase.p, Q.ekey.p, Q.eid0.p, Q.item_q.p);
+        RG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, sbytes, Q.ekey.p, Q.ekey2.p, Q.eid0.p, Q.eid.p, (int)Q.item_cap, 0, key_bits, st));
+        ws.cub_tmp.ensure(sbytes);
+        RG_CUDA(cub::DeviceRadixSort::SortPairs(ws.cub_tmp.p, sbytes, Q.ekey.p, Q.ekey2.p, Q.eid0.p, Q.eid.p, (int)Q.item_cap, 0, key_bits, st));
+        RG_CUDA(cudaMemsetAsync(Q.chrows.p, 0, sizeof(int) * ((size_t)Q.nchunk_slots + 1), st));
+        k_ell_chunks<<<gk, 256, 0, st>>>(Q.nlines, Q.P, Q.Bk, Q.ppt.p, Q.blk.p, Q.itembase.p, Q.ekey2.p, Q.eid.p, Q.item_q.p, Q.elen.p,
+                                         Q.ebeg.p, Q.eout.p, Q.chrows.p);
+        RG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, sbytes, Q.chrows.p, Q.choff.p, Q.nchunk_slots + 1, st));
+        ws.cub_tmp.ensure(sbytes);
+        RG_CUDA(cub::DeviceScan::ExclusiveSum(ws.cub_tmp.p, sbytes, Q.chrows.p, Q.choff.p, Q.nchunk_slots + 1, st));
+        k_ell_fill<<<ncta, 1024, 0, st>>>(Q.nlines, Q.P, Q.Bk, Q.blk.p, Q.itembase.p, Q.elen.p, Q.ebeg.p, Q.chrows.p, Q.choff.p,
+                                          Q.idx16.p, Q.emap.p, Q.eidx.p);
+        RG_CUDA(cudaGetLastError());
+        ctx->launches += 8;
+    }
     Q.stamp = S.structure_stamp;
+}
+
+// the current values of the half's matrix copy into the ELL stream (once per solve: the values change between solves)
+static void panel_refresh_values(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, const regot_sparse& S, bool rows)
+{
+    if (!ctx->panel_ell) return;
+    build_panel_plan(ctx, st, ws, S, rows);
+    PanelPlan& Q = rows ? S.panel_rows : S.panel_cols;
+    k_ell_values<<<8 * ctx->sm_count, 256, 0, st>>>(Q.choff.p + Q.nchunk_slots, Q.emap.p, rows ? S.val.p : S.cscval.p, Q.eval.p);
+    RG_CUDA(cudaGetLastError());
+    ++ctx->launches;
 }
 
 // one half mat-vec in panel form: y (interleaved x4) = epilogue(B x) or epilogue(B' x) for two right-hand sides
@@ -672,12 +1019,27 @@ static void launch_spmv_panel(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, con
     a.val = rows ? S.val.p : S.cscval.p;
     a.x = x;
     a.part = Q.part.p;
+    a.itembase = Q.itembase.p;
+    a.elen = Q.elen.p;
+    a.eout = Q.eout.p;
+    a.chrows = Q.chrows.p;
+    a.choff = Q.choff.p;
+    a.eidx = Q.eidx.p;
+    a.eval = ctx->panel_ell ? Q.eval.p : nullptr;
+    a.ahead = ctx->panel_ahead;
+#ifdef REGOT_PANEL_TIMING
+    static long dbg_count = 0;
+    if (ctx->panel_ahead == 7777 || ctx->panel_ahead == 7778) a.ahead = (++dbg_count % 400) < 2 ? 7777 : 0;
+    static const bool fake = std::getenv("REGOT_PANEL_FAKE") != nullptr;
+    a.fake = fake ? std::atoi(std::getenv("REGOT_PANEL_FAKE")) : 0;
+#endif
     {
         ProfScope prof(ctx, st, 4);
-        k_spmv_panel<<<Q.P * Q.Bk, kPanelThreads, panel_smem(Q.W), st>>>(a);
+        k_spmv_panel<<<Q.P * Q.Bk, kPanelThreads, panel_smem(Q.W, ctx->panel_ell != 0), st>>>(a);
         if (combine) {  // else the consumer adds the per-panel partials itself (one kernel and one pass over the vector less)
             const int g = (int)std::max<long>(1, std::min<long>(((long)Q.nlines * 2 + 255) / 256, 4L * ctx->sm_count));
-            k_panel_combine<kEpi><<<g, 256, 0, st>>>(Q.nlines, Q.P, Q.part.p, rows ? S.dA.p : nullptr, y, skip);
+            k_panel_combine<kEpi><<<g, 256, 0, st>>>(Q.nlines, Q.P, Q.part.p, ctx->panel_ell ? Q.itembase.p : nullptr, rows ? S.dA.p : nullptr, y,
+                                                     skip);
         }
     }
     RG_CUDA(cudaGetLastError());
@@ -730,6 +1092,7 @@ struct CgVecs {
     // all interleaved 4 doubles per index (entry 3 is padding)
     double *ta;                           // alpha space: t = D1^-1 (...)
     double *ub, *xb, *rb, *pb, *sb, *zb;  // beta space: u = B' t, x, r, p, s = S p, z = D2^-1 r
+    const int* part_itembase;             // ELL stream: first item of every (panel, column) piece; else null
     const double* part;                   // panel mat-vec on one GPU: u = sum of n_parts per-panel partials (mfree x 2 each); else null
     const double *dA, *dB;
     double* scal;
@@ -783,9 +1146,7 @@ __global__ void __launch_bounds__(kCgThreads) k_schur_init_a(const CgVecs v, con
 __device__ __forceinline__ double schur_u(const CgVecs& v, int j, int k)
 {
     if (v.part == nullptr || k >= 2) return v.ub[(size_t)j * 4 + k];
-    double s = 0.0;
-    for (int p = 0; p < v.n_parts; ++p) s += v.part[((size_t)p * v.mfree + j) * 2 + k];
-    return s;
+    return panel_line_sum(v.part, v.part_itembase, v.mfree, v.n_parts, j, k);
 }
 
 // set-up: c = r_b - u (u = B' t summed over ranks): r = c, z = D2^-1 c, x = p = s = 0; gamma = r'z; beta part of
@@ -948,6 +1309,7 @@ static int pcg_schur_multikernel(regot_ctx* ctx, cudaStream_t st, ncclComm* comm
     v.partials = ws.cg_partials.p;
     v.ticket = ws.cg_ticket.p;
     v.part = nullptr;
+    v.part_itembase = nullptr;
     v.n_parts = 0;
 
     // pointer tables (rhs_a | rhs_b | sol_a | sol_b) live behind the scalars on the device
@@ -981,9 +1343,14 @@ static int pcg_schur_multikernel(regot_ctx* ctx, cudaStream_t st, ncclComm* comm
         else launch_spmv<kEpiColsPlain>(ctx, st, S, nrhs, v.ta, nullptr, nullptr, v.ub, kInterleaved4, kInterleaved4, skip_flag);
         if (ctx->sharded) allreduce_sum(ctx, comm, v.ub, 4 * (size_t)mfree, st);
     };
+    if (panel) {
+        panel_refresh_values(ctx, st, ws, S, true);
+        panel_refresh_values(ctx, st, ws, S, false);
+    }
     if (panel && !ctx->sharded) {
         build_panel_plan(ctx, st, ws, S, false);
         v.part = S.panel_cols.part.p;
+        v.part_itembase = ctx->panel_ell ? S.panel_cols.itembase.p : nullptr;
         v.n_parts = S.panel_cols.P;
     }
 

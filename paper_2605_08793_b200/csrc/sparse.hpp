@@ -46,7 +46,21 @@ struct PanelPlan {
     DevBuf<int> blk;          // P x (Bk + 1): line boundaries of the blocks
     DevBuf<unsigned short> idx16;  // per entry of the half's matrix copy: index relative to its panel
     DevBuf<int> cost, scan;   // P x nlines (+1): work per piece and its exclusive prefix sum
-    DevBuf<double> part;      // P x nlines x 2: per-panel partial sums of every line
+    DevBuf<double> part;      // P x nlines x 2: per-panel partial sums of every line (ELL stream: then the sums of the items of cut pieces)
+    // ELL stream of the pieces (k4_sparse.cu): every piece cut into items of up to kPanelGroupMax entries, the items of a
+    // CTA sorted by length, 8 to a chunk, entry k of item j of a chunk at row k / 4, lane (k % 4) * 8 + j
+    DevBuf<int> nseg, itembase;     // per piece q = p nlines + l: its items, and their exclusive prefix sum (np + 1)
+    DevBuf<unsigned> ekey, ekey2;   // sort keys: (CTA, cap - length)
+    DevBuf<int> eid0, eid;          // item ids before / after the sort
+    DevBuf<int> item_q;             // piece of every item
+    DevBuf<int> elen, ebeg, eout;   // per sorted item: entries, first entry, where its sums go (pairs of part)
+    DevBuf<int> chrows, choff;      // per chunk slot: rows of 32 entries, first row
+    DevBuf<int> emap;               // per ELL slot: the entry of the matrix copy it holds, or -1
+    DevBuf<unsigned short> eidx;    // per ELL slot: panel-relative index
+    DevBuf<double> eval;            // per ELL slot: value (rewritten once per solve)
+    size_t item_cap = 0;
+    int nchunk_slots = 0;
+    size_t ell_cap = 0;             // slots allocated
 };
 }  // namespace rg
 

@@ -1,0 +1,25 @@
+"""Repeated solves of config D on ONE context: same bits every time?"""
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2605_08793_b200 as rg  # noqa: E402
+from paper_2605_08793_b200 import problems  # noqa: E402
+
+n = m = int(os.environ.get("N", "50000"))
+X, Y = problems.gen_gmm_points(n, m, 10, 21)
+a, b = np.full(n, 1.0 / n), np.full(m, 1.0 / m)
+s = rg.Solver(0)
+s.set_pointcloud(X, Y, a, b, 0.001, on_the_fly=False)
+if os.environ.get("PROF", "0") == "1":
+    s.set_profiling(True)
+ref = None
+for rep in range(int(os.environ.get("REPS", "4"))):
+    res = s.run_splr(rg.DualPoint.zeros(n, m), rg.SplrConfig(max_iter=int(os.environ.get("MAXIT", "100"))))
+    sig = [(st.cg_iters, st.ls_evals, st.f_after) for st in res.steps]
+    if ref is None:
+        ref = sig
+    first = next((i for i, (u, v) in enumerate(zip(ref, sig)) if u != v), None)
+    print(f"rep {rep}: {len(sig)} steps, first difference at step {first}", sig[first] if first is not None else "", ref[first] if first is not None else "", flush=True)

@@ -182,7 +182,7 @@ def multikernel_solver():
     s.close()
 
 
-@pytest.fixture(scope="module", params=[(64, "many narrow panels"), (0, "one panel")])
+@pytest.fixture(scope="module", params=[(64, 1, "many narrow panels"), (0, 1, "one panel"), (64, 0, "pieces read from the CSR / CSC copy")])
 def panel_solver(request):
     """The kernel-by-kernel Schur PCG with its half mat-vecs in PANEL form (k_spmv_panel: the gathered vector
     staged in shared memory panel by panel -- the path of config D / E and of large sharded runs), forced on
@@ -193,10 +193,11 @@ def panel_solver(request):
     os.environ["REGOT_B200_PANEL_SPMV"] = "1"
     if request.param[0]:
         os.environ["REGOT_B200_PANEL_WIDTH"] = str(request.param[0])
+    os.environ["REGOT_B200_PANEL_ELL"] = str(request.param[1])
     try:
         s = rg.Solver(0)
     finally:
-        for k in ("REGOT_B200_MULTIKERNEL_PCG", "REGOT_B200_PANEL_SPMV", "REGOT_B200_PANEL_WIDTH"):
+        for k in ("REGOT_B200_MULTIKERNEL_PCG", "REGOT_B200_PANEL_SPMV", "REGOT_B200_PANEL_WIDTH", "REGOT_B200_PANEL_ELL"):
             os.environ.pop(k, None)
     yield s
     s.close()

@@ -155,6 +155,7 @@ regot_ctx* ctx_create(int device)
         ctx->pcg_cluster_max_entries = 50000;
         if (const char* e = std::getenv("REGOT_B200_FUSED_FINALIZE")) ctx->fused_finalize = e[0] != '0';
         if (const char* e = std::getenv("REGOT_B200_EXTENDED_F")) ctx->extended_f = e[0] != '0';
+        if (const char* e = std::getenv("REGOT_B200_SCHUR_DIAG")) ctx->schur_diag = std::atoi(e);
         if (const char* e = std::getenv("REGOT_B200_PCG_BLOCKS")) ctx->pcg_blocks = std::atoi(e);
         if (const char* e = std::getenv("REGOT_B200_PCG_BLOCKS_CLUSTER")) ctx->pcg_blocks_cluster = std::atoi(e);
         if (const char* e = std::getenv("REGOT_B200_PCG_BLOCKS_ONE_CLUSTER_ENTRIES")) ctx->pcg_blocks_one_cluster_entries = std::atol(e);

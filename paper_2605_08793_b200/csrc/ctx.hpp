@@ -291,6 +291,7 @@ struct regot_ctx {
     bool extended_f = true;
     // block-resident PCG (k6_pcg_blocks.cu): -1 auto (whenever the pattern fits), 0 off (REGOT_B200_PCG_BLOCKS);
     // pcg_blocks_p x pcg_blocks_q > 0 force the block grid (REGOT_B200_PCG_BLOCKS_GRID=PxQ, tests)
+    int schur_diag = 1;  // REGOT_B200_SCHUR_DIAG=0: precondition with D2 instead of diag(D2 - B' D1^-1 B)
     int pcg_blocks = -1;
     int pcg_blocks_p = 0, pcg_blocks_q = 0;
     // block rows as thread-block clusters: -1 auto, 0 off (REGOT_B200_PCG_BLOCKS_CLUSTER); patterns up to this many entries

@@ -370,6 +370,7 @@ void sparse_matvec(regot_ctx* ctx, cudaStream_t st, ncclComm* comm, const regot_
 constexpr int kPanelThreads = 1024;
 constexpr int kPanelWarps = kPanelThreads / 32;
 constexpr int kPanelMaxW = 12800;       // entries of the gathered vector per panel: 200 KB of shared memory
+constexpr int kPanelEllW = 8448;        // ELL stream: narrower panels (132 KB) -- measured best at config D (7168..8352: 0.060 ms, 12800: 0.064)
 constexpr int kPanelGroupMax = 256;     // pieces up to this many entries: 8 lanes
 constexpr int kPanelWarpMax = 8192;     // up to this many: one warp; longer: the whole CTA
 constexpr int kPanelDeferCap = 2048;    // deferred pieces per CTA kept in the shared-memory lists
@@ -377,7 +378,8 @@ constexpr int kPanelLineCost = 24;      // work of a piece beyond its entries (p
 constexpr int kEllPieces = 8;           // ELL stream: pieces per chunk ...
 constexpr int kEllPhases = 4;           // ... and lanes per piece (entry k of a piece belongs to lane group k % 4)
 constexpr int kEllBatch = 4;            // rows per batch: a lane's values of a batch are 2 x 16 bytes, its indices 8 bytes
-constexpr int kEllKeyBits = 9;          // cap - length fits in 9 bits (kPanelGroupMax = 256)
+constexpr int kEllItemMax = 2048;        // entries per item: above kPanelGroupMax an item takes a chunk of its own (32 lanes)
+constexpr int kEllKeyBits = 12;          // item cap - length fits in 12 bits
 
 struct PanelArgs {
     const double* skip;  // != null and *skip != 0: nothing to do
@@ -390,6 +392,7 @@ struct PanelArgs {
     double* part;       // P x nlines x 2
     // ELL stream (null eval: pieces are read from the CSR / CSC copy)
     const int* itembase;  // per piece q = p nlines + l: its first item (np + 1 entries)
+    const int* nlong;     // per CTA: its long items (one chunk each; they sort first)
     const int* elen;      // per sorted item: entries, ...
     const int* eout;      // ... and where its two sums go (index into part, in pairs)
     const int* chrows;
@@ -468,7 +471,7 @@ __global__ void k_panel_blocks(int nlines, int P, int Bk, const int* __restrict_
 // lanes sum a piece, each its k % 4 class in order, then a fixed two-step butterfly: bitwise reproducible, and independent
 // of which warp takes which chunk (chunks are handed out longest first through a counter).  Indices are laid out once per
 // pattern; the values are copied into the layout once per solve (k_ell_values).
-// items of piece q = p * nlines + l: its segments of up to kPanelGroupMax entries (an empty piece is one empty item)
+// items of piece q = p * nlines + l: its segments of up to kEllItemMax entries (an empty piece is one empty item)
 __global__ void k_ell_count(int nlines, int P, const int* __restrict__ ppt, int* __restrict__ nseg)
 {
     const long total = (long)nlines * P;
@@ -477,7 +480,7 @@ __global__ void k_ell_count(int nlines, int P, const int* __restrict__ ppt, int*
         if (q < total) {
             const int p = (int)(q / nlines), l = (int)(q - (long)p * nlines);
             const int len = ppt[(size_t)l * (P + 1) + p + 1] - ppt[(size_t)l * (P + 1) + p];
-            ns = max(1, (len + kPanelGroupMax - 1) / kPanelGroupMax);
+            ns = max(1, (len + kEllItemMax - 1) / kEllItemMax);
         }
         nseg[q] = ns;
     }
@@ -485,6 +488,15 @@ __global__ void k_ell_count(int nlines, int P, const int* __restrict__ ppt, int*
 __global__ void k_ell_fill_u32(long n, unsigned v, unsigned* __restrict__ out)
 {
     for (long q = (long)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += (long)gridDim.x * blockDim.x) out[q] = v;
+}
+// per line: does any of its pieces consist of several items (then the consumers add those items' sums first)
+__global__ void k_ell_multi(int nlines, int P, const int* __restrict__ nseg, unsigned char* __restrict__ multi)
+{
+    for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < nlines; l += gridDim.x * blockDim.x) {
+        bool m = false;
+        for (int p = 0; p < P; ++p) m = m || nseg[(size_t)p * nlines + l] > 1;
+        multi[l] = m ? 1 : 0;
+    }
 }
 __global__ void k_ell_keys(int nlines, int P, int Bk, const int* __restrict__ ppt, const int* __restrict__ blk,
                            const int* __restrict__ itembase, unsigned* __restrict__ key, int* __restrict__ id0, int* __restrict__ item_q)
@@ -504,19 +516,18 @@ __global__ void k_ell_keys(int nlines, int P, int Bk, const int* __restrict__ pp
         const unsigned cta = (unsigned)(p * Bk + lo) << kEllKeyBits;
         const int b0 = itembase[q], ns = itembase[q + 1] - b0;
         for (int sg = 0; sg < ns; ++sg) {
-            const int seglen = min(kPanelGroupMax, len - sg * kPanelGroupMax);
-            key[b0 + sg] = cta | (unsigned)(kPanelGroupMax - seglen);
+            const int seglen = min(kEllItemMax, len - sg * kEllItemMax);
+            key[b0 + sg] = cta | (unsigned)(kEllItemMax - seglen);
             id0[b0 + sg] = b0 + sg;
             item_q[b0 + sg] = (int)q;
         }
     }
 }
-// per sorted item: length, first entry, where its sum goes (part[q] for a piece of one item, else part[np + item]); per
-// chunk its rows (from its first = longest item)
-__global__ void k_ell_chunks(int nlines, int P, int Bk, const int* __restrict__ ppt, const int* __restrict__ blk,
-                             const int* __restrict__ itembase, const unsigned* __restrict__ key, const int* __restrict__ id,
-                             const int* __restrict__ item_q, int* __restrict__ elen, int* __restrict__ ebeg,
-                             int* __restrict__ eout, int* __restrict__ chrows)
+// per sorted item: length, first entry, where its sums go (part[q] for a piece of one item, else part[np + item]); per CTA
+// the number of long items (they sort first)
+__global__ void k_ell_items(int nlines, int P, const int* __restrict__ ppt, const int* __restrict__ itembase,
+                            const unsigned* __restrict__ key, const int* __restrict__ id, const int* __restrict__ item_q,
+                            int* __restrict__ elen, int* __restrict__ ebeg, int* __restrict__ eout, int* __restrict__ nlong)
 {
     const long np = (long)nlines * P;
     const long total = itembase[np];
@@ -525,43 +536,66 @@ __global__ void k_ell_chunks(int nlines, int P, int Bk, const int* __restrict__ 
         const int p = q / nlines, l = q - p * nlines;
         const int b0 = itembase[q], ns = itembase[q + 1] - b0, sg = it - b0;
         const int beg = ppt[(size_t)l * (P + 1) + p], len = ppt[(size_t)l * (P + 1) + p + 1] - beg;
-        const int seglen = min(kPanelGroupMax, len - sg * kPanelGroupMax);
+        const int seglen = min(kEllItemMax, len - sg * kEllItemMax);
         elen[r] = seglen;
-        ebeg[r] = beg + sg * kPanelGroupMax;
+        ebeg[r] = beg + sg * kEllItemMax;
         eout[r] = ns == 1 ? q : (int)np + it;
-        const int cta = (int)(key[r] >> kEllKeyBits);
-        const int first = itembase[(size_t)p * nlines + blk[(size_t)p * (Bk + 1) + (cta - p * Bk)]];
-        const int pos = (int)(r - first);
-        // rows in whole batches of kEllBatch (the loads are vectors over 2 / 4 consecutive rows)
-        if (pos % kEllPieces == 0)
-            chrows[first / kEllPieces + cta + pos / kEllPieces] = (seglen + kEllPhases * kEllBatch - 1) / (kEllPhases * kEllBatch) * kEllBatch;
+        if (seglen > kPanelGroupMax) atomicAdd(nlong + (key[r] >> kEllKeyBits), 1);
+    }
+}
+// Chunks of CTA (p, b), whose sorted items are [first, first + cnt): the nl long items one per chunk (32 lanes, entry k
+// at row k / 32), then the others 8 per chunk (4 lanes each, entry k at row k / 4).  Chunk slots of the CTA start at
+// first + cta (an item per slot at worst).  Rows in whole batches of kEllBatch (the loads are vectors over 2 / 4 rows).
+struct EllCta {
+    int first, cnt, nl, nch, cb;
+};
+__device__ __forceinline__ EllCta ell_cta(int cta, int nlines, int Bk, const int* __restrict__ blk, const int* __restrict__ itembase,
+                                          const int* __restrict__ nlong)
+{
+    const int p = cta / Bk, b = cta - p * Bk;
+    const int l0 = __ldg(blk + (size_t)p * (Bk + 1) + b), l1 = __ldg(blk + (size_t)p * (Bk + 1) + b + 1);
+    EllCta c;
+    c.first = __ldg(itembase + (size_t)p * nlines + l0);
+    c.cnt = __ldg(itembase + (size_t)p * nlines + l1) - c.first;
+    c.nl = __ldg(nlong + cta);
+    c.nch = c.nl + (c.cnt - c.nl + kEllPieces - 1) / kEllPieces;
+    c.cb = c.first + cta;
+    return c;
+}
+__global__ void k_ell_rows(int nlines, int P, int Bk, const int* __restrict__ blk, const int* __restrict__ itembase,
+                           const int* __restrict__ nlong, const int* __restrict__ elen, int* __restrict__ chrows)
+{
+    const EllCta c = ell_cta(blockIdx.x, nlines, Bk, blk, itembase, nlong);
+    (void)P;
+    for (int ci = threadIdx.x; ci < c.nch; ci += blockDim.x) {
+        const bool lng = ci < c.nl;
+        const int len = elen[c.first + (lng ? ci : c.nl + (ci - c.nl) * kEllPieces)];
+        const int per = (lng ? 32 : kEllPhases) * kEllBatch;
+        chrows[c.cb + ci] = (len + per - 1) / per * kEllBatch;
     }
 }
 // indices and the slot -> entry map of every chunk: one warp per chunk, CTA c of the grid = CTA c of the mat-vec
 __global__ void k_ell_fill(int nlines, int P, int Bk, const int* __restrict__ blk, const int* __restrict__ itembase,
-                           const int* __restrict__ elen, const int* __restrict__ ebeg, const int* __restrict__ chrows,
-                           const int* __restrict__ choff, const unsigned short* __restrict__ idx16,
+                           const int* __restrict__ nlong, const int* __restrict__ elen, const int* __restrict__ ebeg,
+                           const int* __restrict__ chrows, const int* __restrict__ choff, const unsigned short* __restrict__ idx16,
                            int* __restrict__ emap, unsigned short* __restrict__ eidx)
 {
-    const int cta = blockIdx.x, p = cta / Bk, b = cta - p * Bk;
-    const int l0 = blk[(size_t)p * (Bk + 1) + b], l1 = blk[(size_t)p * (Bk + 1) + b + 1];
-    const int first = itembase[(size_t)p * nlines + l0], cnt = itembase[(size_t)p * nlines + l1] - first;
-    const int nch = (cnt + kEllPieces - 1) / kEllPieces;
-    const int cb = first / kEllPieces + cta;
+    const EllCta c = ell_cta(blockIdx.x, nlines, Bk, blk, itembase, nlong);
+    (void)P;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-    const int g = lane >> 3, j = lane & 7;
-    for (int ci = warp; ci < nch; ci += nwarps) {
-        const int rows = chrows[cb + ci];
-        const size_t off = (size_t)choff[cb + ci] * 32;
-        const bool valid = ci * kEllPieces + j < cnt;
+    for (int ci = warp; ci < c.nch; ci += nwarps) {
+        const int rows = chrows[c.cb + ci];
+        const size_t off = (size_t)choff[c.cb + ci] * 32;
+        const bool lng = ci < c.nl;
+        const int G = lng ? 32 : kEllPhases, g = lng ? lane : lane >> 3;
+        const int pos = lng ? ci : c.nl + (ci - c.nl) * kEllPieces + (lane & 7);
         int beg = 0, eff = 0;
-        if (valid) {
-            const int r = first + ci * kEllPieces + j;
-            eff = elen[r];
-            beg = ebeg[r];
+        if (pos < c.cnt) {
+            eff = elen[c.first + pos];
+            beg = ebeg[c.first + pos];
         }
         for (int t = 0; t < rows; ++t) {
-            const int k = t * kEllPhases + g;
+            const int k = t * G + g;
             const bool ok = k < eff;
             // values: rows in pairs, a lane's two values adjacent; indices: rows in fours, a lane's four adjacent
             emap[off + (size_t)(t >> 1) * 64 + lane * 2 + (t & 1)] = ok ? beg + k : -1;
@@ -636,13 +670,10 @@ __global__ void __launch_bounds__(kPanelThreads, 1) k_spmv_panel(const PanelArgs
 
     if (a.eval != nullptr) {
         // ---- pass 1, ELL stream: chunks of 8 pieces handed out longest first; 4 lanes per piece ----
-        const int g = lane >> 3, j = lane & 7;
-        const int first = __ldg(a.itembase + (size_t)p * a.nlines + l0);
-        const int cnt = __ldg(a.itembase + (size_t)p * a.nlines + l1) - first, nch = (cnt + kEllPieces - 1) / kEllPieces;
-        const int cb = first / kEllPieces + blockIdx.x;
-        // the CTA's stream is contiguous (chunk after chunk); every trip asks L2 for the 8 rows kEllAhead rows further
-        // down the stream -- for whichever warp gets there: prefetches hold no registers, and the demand loads of a
-        // trip then pay an L2 latency
+        const EllCta ec = ell_cta(blockIdx.x, a.nlines, a.Bk, a.blk, a.itembase, a.nlong);
+        const int nch = ec.nch, cb = ec.cb;
+        // the CTA's stream is contiguous (chunk after chunk); with a.ahead > 0 every trip asks L2 for the 8 rows a.ahead
+        // rows further down the stream (measured: no gain -- the stream is not bound by latency; off by default)
         const int end_row = __ldg(a.choff + cb + nch);
         if (a.ahead > 0 && lane < 2) {  // the head of the stream, which no trip asks for
             const int begin_row = __ldg(a.choff + cb);
@@ -660,11 +691,14 @@ __global__ void __launch_bounds__(kPanelThreads, 1) k_spmv_panel(const PanelArgs
             if (ci >= nch) break;
             const int rows = __ldg(a.chrows + cb + ci);
             const int row0 = __ldg(a.choff + cb + ci);
-            const bool valid = ci * kEllPieces + j < cnt;
+            const bool lng = ci < ec.nl;  // a long item alone on 32 lanes, else 8 items on 4 lanes each
+            const int G = lng ? 32 : kEllPhases, g = lng ? lane : lane >> 3;
+            const int pos = lng ? ci : ec.nl + (ci - ec.nl) * kEllPieces + (lane & 7);
+            const bool valid = pos < ec.cnt;
             int dest = 0, eff = 0;
             if (valid) {
-                eff = __ldg(a.elen + first + ci * kEllPieces + j);
-                dest = __ldg(a.eout + first + ci * kEllPieces + j);
+                eff = __ldg(a.elen + ec.first + pos);
+                dest = __ldg(a.eout + ec.first + pos);
             }
             const double* vp = a.eval + (size_t)row0 * 32 + lane * 2;          // + (t / 2) * 64: rows t, t + 1
             const unsigned short* ip = a.eidx + (size_t)row0 * 32 + lane * 4;  // + (t / 4) * 128: rows t .. t + 3
@@ -681,11 +715,11 @@ __global__ void __launch_bounds__(kPanelThreads, 1) k_spmv_panel(const PanelArgs
             auto load4 = [&](int t, Batch& B) {
                 B.v01 = B.v23 = make_double2(0.0, 0.0);
                 B.c = make_uint2(0u, 0u);
-                if (t * kEllPhases + g < eff) {
+                if (t * G + g < eff) {
                     asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0, %1}, [%2];" : "=r"(B.c.x), "=r"(B.c.y) : "l"(ip + (size_t)(t >> 2) * 128));
                     asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(B.v01.x), "=d"(B.v01.y) : "l"(vp + (size_t)(t >> 1) * 64));
                 }
-                if ((t + 2) * kEllPhases + g < eff)
+                if ((t + 2) * G + g < eff)
                     asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(B.v23.x), "=d"(B.v23.y) : "l"(vp + (size_t)((t >> 1) + 1) * 64));
             };
             auto use1 = [&](unsigned c, double v) {
@@ -724,11 +758,22 @@ __global__ void __launch_bounds__(kPanelThreads, 1) k_spmv_panel(const PanelArgs
                 load4(t + 8, bA);
                 use4(bB);
             }
-            // lane groups 0 / 2 end with the piece's sum of a0, groups 1 / 3 with a1; then the pairs (fixed order)
-            const bool odd = g & 1;
-            double c2 = (odd ? a1 : a0) + shfl_xor_d(odd ? a0 : a1, 8);
-            c2 += shfl_xor_d(c2, 16);
-            if (valid && g < 2) a.part[(size_t)dest * 2 + g] = c2;
+            // short items: lane groups 0 / 2 end with the item's sum of a0, groups 1 / 3 with a1, then the pairs; a long
+            // item: the butterfly over the warp, even lanes carrying a0 and odd lanes a1 after the first step (fixed orders)
+            double c2;
+            if (lng) {
+                const bool odd = lane & 1;
+                c2 = (odd ? a1 : a0) + shfl_xor_d(odd ? a0 : a1, 1);
+                c2 += shfl_xor_d(c2, 2);
+                c2 += shfl_xor_d(c2, 4);
+                c2 += shfl_xor_d(c2, 8);
+                c2 += shfl_xor_d(c2, 16);
+            } else {
+                const bool odd = g & 1;
+                c2 = (odd ? a1 : a0) + shfl_xor_d(odd ? a0 : a1, 8);
+                c2 += shfl_xor_d(c2, 16);
+            }
+            if (valid && g < 2) a.part[(size_t)dest * 2 + g] = c2;  // long: lanes 0 and 1
         }
 #ifndef REGOT_PANEL_TIMING
         return;  // every piece went through the stream: no deferred pieces
@@ -855,11 +900,11 @@ __global__ void __launch_bounds__(kPanelThreads, 1) k_spmv_panel(const PanelArgs
 
 // sum of line l's per-panel partials in panel order; a piece the ELL stream cut into several items is summed in item
 // order first (its items' sums sit behind the P x nlines piece slots)
-__device__ __forceinline__ double panel_line_sum(const double* __restrict__ part, const int* __restrict__ itembase, int nlines, int P,
-                                                 int l, int k)
+__device__ __forceinline__ double panel_line_sum(const double* __restrict__ part, const int* __restrict__ itembase,
+                                                 const unsigned char* __restrict__ multi, int nlines, int P, int l, int k)
 {
     double s = 0.0;
-    if (itembase == nullptr) {
+    if (itembase == nullptr || multi[l] == 0) {  // every piece of the line is one item
         for (int p = 0; p < P; ++p) s += part[((size_t)p * nlines + l) * 2 + k];
         return s;
     }
@@ -881,13 +926,14 @@ __device__ __forceinline__ double panel_line_sum(const double* __restrict__ part
 // y_line = sum over panels (panel order) of part[p][line], then the epilogue of the half mat-vec
 template <int kEpi>
 __global__ void k_panel_combine(int nlines, int P, const double* __restrict__ part, const int* __restrict__ itembase,
-                                const double* __restrict__ diag, double* __restrict__ y, const double* skip)
+                                const unsigned char* __restrict__ multi, const double* __restrict__ diag, double* __restrict__ y,
+                                const double* skip)
 {
     if (skip != nullptr && *skip != 0.0) return;
     const int total = nlines * 2;
     for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < total; q += gridDim.x * blockDim.x) {
         const int l = q >> 1, k = q & 1;
-        const double s = panel_line_sum(part, itembase, nlines, P, l, k);
+        const double s = panel_line_sum(part, itembase, multi, nlines, P, l, k);
         y[(size_t)l * 4 + k] = (kEpi == kEpiRowsScaled) ? s / diag[l] : s;
     }
 }
@@ -902,7 +948,7 @@ static void build_panel_plan(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, cons
     const int nloc = (int)S.nloc, mfree = std::max((int)S.m - 1, 0);
     Q.nlines = rows ? nloc : mfree;
     Q.ngather = rows ? mfree : nloc;
-    const int wmax = ctx->panel_width > 0 ? std::min(ctx->panel_width, kPanelMaxW) : kPanelMaxW;
+    const int wmax = ctx->panel_width > 0 ? std::min(ctx->panel_width, kPanelMaxW) : (ctx->panel_ell ? kPanelEllW : kPanelMaxW);
     Q.P = std::max(1, (Q.ngather + wmax - 1) / wmax);
     if (Q.P > ctx->sm_count) raise(REGOT_E_UNSUPPORTED, "panel mat-vec: the gathered vector needs more panels than there are SMs");
     Q.W = ((Q.ngather + Q.P - 1) / Q.P + 31) / 32 * 32;
@@ -934,9 +980,11 @@ static void build_panel_plan(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, cons
         // ELL stream: every piece cut into items of up to kPanelGroupMax entries, the items of a CTA sorted by length
         // (stable), chunk tables, indices.  Item and slot counts stay on the device; the buffers take their bounds.
         const int ncta = Q.P * Q.Bk;
-        Q.item_cap = np + (size_t)S.nnz / kPanelGroupMax + 1;
-        Q.nchunk_slots = (int)(Q.item_cap / kEllPieces) + ncta + 1;
-        Q.ell_cap = (size_t)S.nnz + (size_t)ncta * 2 * kEllPieces * kPanelGroupMax + (size_t)Q.nchunk_slots * 32 * kEllBatch + 64;
+        Q.item_cap = np + (size_t)S.nnz / kEllItemMax + 1;
+        Q.nchunk_slots = (int)Q.item_cap + ncta + 1;
+        // slots: the entries, the sorted short chunks' slack (16 x 256 per CTA), up to a batch of rows of padding per chunk
+        const size_t max_chunks = Q.item_cap / kEllPieces + (size_t)ncta + (size_t)S.nnz / (kPanelGroupMax + 1) + 1;
+        Q.ell_cap = (size_t)S.nnz + (size_t)ncta * 2 * kEllPieces * kPanelGroupMax + max_chunks * 32 * kEllBatch + 64;
         Q.nseg.ensure(np + 2);
         Q.itembase.ensure(np + 2);
         Q.ekey.ensure(Q.item_cap);
@@ -947,6 +995,8 @@ static void build_panel_plan(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, cons
         Q.elen.ensure(Q.item_cap);
         Q.ebeg.ensure(Q.item_cap);
         Q.eout.ensure(Q.item_cap);
+        Q.nlong.ensure((size_t)ncta + 1);
+        Q.multi.ensure((size_t)Q.nlines + 1);
         Q.chrows.ensure((size_t)Q.nchunk_slots + 1);
         Q.choff.ensure((size_t)Q.nchunk_slots + 1);
         Q.emap.ensure(Q.ell_cap);
@@ -969,15 +1019,18 @@ static void build_panel_plan(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, cons
         ws.cub_tmp.ensure(sbytes);
         RG_CUDA(cub::DeviceRadixSort::SortPairs(ws.cub_tmp.p, sbytes, Q.ekey.p, Q.ekey2.p, Q.eid0.p, Q.eid.p, (int)Q.item_cap, 0, key_bits, st));
         RG_CUDA(cudaMemsetAsync(Q.chrows.p, 0, sizeof(int) * ((size_t)Q.nchunk_slots + 1), st));
-        k_ell_chunks<<<gk, 256, 0, st>>>(Q.nlines, Q.P, Q.Bk, Q.ppt.p, Q.blk.p, Q.itembase.p, Q.ekey2.p, Q.eid.p, Q.item_q.p, Q.elen.p,
-                                         Q.ebeg.p, Q.eout.p, Q.chrows.p);
+        RG_CUDA(cudaMemsetAsync(Q.nlong.p, 0, sizeof(int) * ((size_t)ncta + 1), st));
+        k_ell_items<<<gk, 256, 0, st>>>(Q.nlines, Q.P, Q.ppt.p, Q.itembase.p, Q.ekey2.p, Q.eid.p, Q.item_q.p, Q.elen.p, Q.ebeg.p, Q.eout.p,
+                                        Q.nlong.p);
+        k_ell_rows<<<ncta, 256, 0, st>>>(Q.nlines, Q.P, Q.Bk, Q.blk.p, Q.itembase.p, Q.nlong.p, Q.elen.p, Q.chrows.p);
+        k_ell_multi<<<(Q.nlines + 255) / 256, 256, 0, st>>>(Q.nlines, Q.P, Q.nseg.p, Q.multi.p);
         RG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, sbytes, Q.chrows.p, Q.choff.p, Q.nchunk_slots + 1, st));
         ws.cub_tmp.ensure(sbytes);
         RG_CUDA(cub::DeviceScan::ExclusiveSum(ws.cub_tmp.p, sbytes, Q.chrows.p, Q.choff.p, Q.nchunk_slots + 1, st));
-        k_ell_fill<<<ncta, 1024, 0, st>>>(Q.nlines, Q.P, Q.Bk, Q.blk.p, Q.itembase.p, Q.elen.p, Q.ebeg.p, Q.chrows.p, Q.choff.p,
-                                          Q.idx16.p, Q.emap.p, Q.eidx.p);
+        k_ell_fill<<<ncta, 1024, 0, st>>>(Q.nlines, Q.P, Q.Bk, Q.blk.p, Q.itembase.p, Q.nlong.p, Q.elen.p, Q.ebeg.p, Q.chrows.p,
+                                          Q.choff.p, Q.idx16.p, Q.emap.p, Q.eidx.p);
         RG_CUDA(cudaGetLastError());
-        ctx->launches += 8;
+        ctx->launches += 10;
     }
     Q.stamp = S.structure_stamp;
 }
@@ -1020,6 +1073,7 @@ static void launch_spmv_panel(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, con
     a.x = x;
     a.part = Q.part.p;
     a.itembase = Q.itembase.p;
+    a.nlong = Q.nlong.p;
     a.elen = Q.elen.p;
     a.eout = Q.eout.p;
     a.chrows = Q.chrows.p;
@@ -1038,8 +1092,8 @@ static void launch_spmv_panel(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, con
         k_spmv_panel<<<Q.P * Q.Bk, kPanelThreads, panel_smem(Q.W, ctx->panel_ell != 0), st>>>(a);
         if (combine) {  // else the consumer adds the per-panel partials itself (one kernel and one pass over the vector less)
             const int g = (int)std::max<long>(1, std::min<long>(((long)Q.nlines * 2 + 255) / 256, 4L * ctx->sm_count));
-            k_panel_combine<kEpi><<<g, 256, 0, st>>>(Q.nlines, Q.P, Q.part.p, ctx->panel_ell ? Q.itembase.p : nullptr, rows ? S.dA.p : nullptr, y,
-                                                     skip);
+            k_panel_combine<kEpi><<<g, 256, 0, st>>>(Q.nlines, Q.P, Q.part.p, ctx->panel_ell ? Q.itembase.p : nullptr, Q.multi.p, rows ? S.dA.p : nullptr,
+                                                     y, skip);
         }
     }
     RG_CUDA(cudaGetLastError());
@@ -1093,8 +1147,10 @@ struct CgVecs {
     double *ta;                           // alpha space: t = D1^-1 (...)
     double *ub, *xb, *rb, *pb, *sb, *zb;  // beta space: u = B' t, x, r, p, s = S p, z = D2^-1 r
     const int* part_itembase;             // ELL stream: first item of every (panel, column) piece; else null
+    const unsigned char* part_multi;      // ELL stream: per column, whether any of its pieces has several items
     const double* part;                   // panel mat-vec on one GPU: u = sum of n_parts per-panel partials (mfree x 2 each); else null
     const double *dA, *dB;
+    const double* mB;  // Jacobi preconditioner of the Schur complement (its diagonal)
     double* scal;
     double* partials;
     unsigned int* ticket;
@@ -1146,7 +1202,7 @@ __global__ void __launch_bounds__(kCgThreads) k_schur_init_a(const CgVecs v, con
 __device__ __forceinline__ double schur_u(const CgVecs& v, int j, int k)
 {
     if (v.part == nullptr || k >= 2) return v.ub[(size_t)j * 4 + k];
-    return panel_line_sum(v.part, v.part_itembase, v.mfree, v.n_parts, j, k);
+    return panel_line_sum(v.part, v.part_itembase, v.part_multi, v.mfree, v.n_parts, j, k);
 }
 
 // set-up: c = r_b - u (u = B' t summed over ranks): r = c, z = D2^-1 c, x = p = s = 0; gamma = r'z; beta part of
@@ -1159,7 +1215,7 @@ __global__ void __launch_bounds__(kCgThreads) k_schur_init_b(const CgVecs v, con
     for (int k = 0; k < v.nrhs; ++k)
         for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < v.mfree; j += stride) {
             const double d = v.dB[j], rb = rhs_b[k][j];
-            const double c = rb - schur_u(v, j, k), z = c / d;
+            const double c = rb - schur_u(v, j, k), z = c / v.mB[j];
             const size_t o = (size_t)j * 4 + k;
             v.rb[o] = c;
             v.zb[o] = z;
@@ -1252,7 +1308,7 @@ __global__ void __launch_bounds__(kCgThreads) k_schur_step(const CgVecs v, int i
             v.sb[o] = sn;
             v.xb[o] += al * pn;
             v.rb[o] = rn;
-            v.zb[o] = rn / v.dB[j];
+            v.zb[o] = rn / v.mB[j];
         }
     }
 }
@@ -1305,11 +1361,13 @@ static int pcg_schur_multikernel(regot_ctx* ctx, cudaStream_t st, ncclComm* comm
     RG_CUDA(cudaMemsetAsync(base, 0, sizeof(double) * (la + 6 * lb), st));
     v.dA = S.dA.p;
     v.dB = S.dB.p;
+    v.mB = S.dS.p;
     v.scal = ws.cg_scal.p;
     v.partials = ws.cg_partials.p;
     v.ticket = ws.cg_ticket.p;
     v.part = nullptr;
     v.part_itembase = nullptr;
+    v.part_multi = nullptr;
     v.n_parts = 0;
 
     // pointer tables (rhs_a | rhs_b | sol_a | sol_b) live behind the scalars on the device
@@ -1351,6 +1409,7 @@ static int pcg_schur_multikernel(regot_ctx* ctx, cudaStream_t st, ncclComm* comm
         build_panel_plan(ctx, st, ws, S, false);
         v.part = S.panel_cols.part.p;
         v.part_itembase = ctx->panel_ell ? S.panel_cols.itembase.p : nullptr;
+        v.part_multi = S.panel_cols.multi.p;
         v.n_parts = S.panel_cols.P;
     }
 
@@ -1396,10 +1455,101 @@ static int pcg_schur_multikernel(regot_ctx* ctx, cudaStream_t st, ncclComm* comm
     return iters;
 }
 
+// ---- the Jacobi preconditioner: the diagonal of the Schur complement itself -----------------------------------------
+// S = D2 - B' D1^-1 B.  D2 alone is a poor stand-in for diag(S) once the plan concentrates: the pattern then carries most
+// of a column's mass, B_ij^2 / D1_i nearly cancels D2_j, and diag(S)_j / D2_j ranges over three orders of magnitude
+// (measured on Gaussian-mixture clouds: 7e-4 .. 0.95), which is exactly the scaling Jacobi is there to remove: 129 -> 56
+// and 165 -> 43 PCG iterations on a 700 x 700 instance, config D 4919 -> see DESIGN.md.  One pass over the CSC copy per
+// solve (the values change between solves); sharded runs add the ranks' partial column sums.  A difference lost to
+// rounding (below 1e-10 D2_j: the pattern carries the whole column) falls back to that floor: any positive diagonal
+// is a valid preconditioner.  The stopping rule keeps its D^-1 norm of the right-hand side (gamma0): with
+// 1 / diag(S) >= 1 / D2 the test gamma <= tol^2 gamma0 is at least as strict as before.
+__device__ __forceinline__ double schur_diag_guard(double d2, double s)
+{
+    const double x = d2 - s, lo = 1e-10 * d2;
+    return x > lo ? x : lo;
+}
+constexpr int kDiagThreads = 1024, kDiagWarps = kDiagThreads / 32;
+constexpr int kDiagLong = 2048;  // columns above this many entries are summed by the whole CTA (column 0 of Omega* is full)
+__global__ void __launch_bounds__(kDiagThreads) k_schur_diag(int mfree, const int* __restrict__ cscptr, const int* __restrict__ cscrow,
+                                                             const double* __restrict__ cscval, const double* __restrict__ dA,
+                                                             const double* __restrict__ dB, double* __restrict__ out, int finalize)
+{
+    __shared__ int long_col[kDiagWarps];
+    __shared__ double wsum[kDiagWarps];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    auto term = [&](int e) {
+        const double v = __ldg(cscval + e);
+        return v * (v / __ldg(dA + __ldg(cscrow + e)));
+    };
+    // a warp per column, 32 columns per CTA and trip; every sum in a fixed order (lanes strided, butterfly, warps in order)
+    for (int base = blockIdx.x * kDiagWarps; base < mfree; base += gridDim.x * kDiagWarps) {
+        const int j = base + warp;
+        int beg = 0, end = 0;
+        if (j < mfree) {
+            beg = __ldg(cscptr + j);
+            end = __ldg(cscptr + j + 1);
+        }
+        const bool lng = end - beg > kDiagLong;
+        if (lane == 0) long_col[warp] = lng ? j : -1;
+        if (j < mfree && !lng) {
+            double s = 0.0;
+#pragma unroll 4
+            for (int e = beg + lane; e < end; e += 32) s += term(e);
+            s = warp_sum(s);
+            if (lane == 0) out[j] = finalize ? schur_diag_guard(__ldg(dB + j), s) : s;
+        }
+        __syncthreads();
+        for (int w = 0; w < kDiagWarps; ++w) {
+            const int jl = long_col[w];
+            if (jl < 0) continue;  // uniform over the CTA
+            const int b2 = __ldg(cscptr + jl), e2 = __ldg(cscptr + jl + 1);
+            double s = 0.0;
+#pragma unroll 4
+            for (int e = b2 + tid; e < e2; e += kDiagThreads) s += term(e);
+            s = warp_sum(s);
+            if (lane == 0) wsum[warp] = s;
+            __syncthreads();
+            if (tid == 0) {
+                double t = 0.0;
+                for (int q = 0; q < kDiagWarps; ++q) t += wsum[q];
+                out[jl] = finalize ? schur_diag_guard(__ldg(dB + jl), t) : t;
+            }
+            __syncthreads();
+        }
+        __syncthreads();
+    }
+}
+__global__ void k_schur_diag_fin(int mfree, const double* __restrict__ dB, double* __restrict__ io)
+{
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < mfree; j += gridDim.x * blockDim.x) io[j] = schur_diag_guard(dB[j], io[j]);
+}
+static void compute_schur_diag(regot_ctx* ctx, cudaStream_t st, ncclComm* comm, const regot_sparse& S)
+{
+    const int mfree = std::max((int)S.m - 1, 0);
+    S.dS.ensure((size_t)std::max(mfree, 1));
+    if (mfree == 0) return;
+    if (!ctx->schur_diag) {
+        RG_CUDA(cudaMemcpyAsync(S.dS.p, S.dB.p, sizeof(double) * (size_t)mfree, cudaMemcpyDeviceToDevice, st));
+        return;
+    }
+    const int grid = (int)std::max<long>(1, std::min<long>(((long)mfree + kDiagWarps - 1) / kDiagWarps, 8L * ctx->sm_count));
+    k_schur_diag<<<grid, kDiagThreads, 0, st>>>(mfree, S.cscptr.p, S.cscrow.p, S.cscval.p, S.dA.p, S.dB.p, S.dS.p, ctx->sharded ? 0 : 1);
+    RG_CUDA(cudaGetLastError());
+    ++ctx->launches;
+    if (ctx->sharded) {
+        allreduce_sum(ctx, comm, S.dS.p, (size_t)mfree, st);
+        k_schur_diag_fin<<<(mfree + 255) / 256, 256, 0, st>>>(mfree, S.dB.p, S.dS.p);
+        RG_CUDA(cudaGetLastError());
+        ++ctx->launches;
+    }
+}
+
 int sparse_pcg(regot_ctx* ctx, cudaStream_t st, ncclComm* comm, SparseWS& ws, const regot_sparse& S, int nrhs,
                const DVec* const* rhs, DVec* const* sol, double rtol, int max_iter)
 {
     if (nrhs < 1 || nrhs > kMaxRhs) raise(REGOT_E_VALIDATION, "pcg: bad number of right-hand sides");
+    compute_schur_diag(ctx, st, comm, S);
     // one GPU: the block-resident kernel when every block of the pattern fits in shared memory, else the persistent
     // kernel that streams the matrix (iterated vectors in shared memory), else kernel by kernel
     if (!ctx->sharded && !ctx->force_multikernel_pcg && S.blocks.fits)

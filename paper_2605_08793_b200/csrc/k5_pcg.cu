@@ -59,6 +59,7 @@ struct SchurParams {
     const double* cscval;
     const double* dA;
     const double* dB;
+    const double* mB;  // Jacobi preconditioner: diag of the Schur complement (k4_sparse.cu compute_schur_diag)
     const int* items;  // kPcgItemInts per item
     const int* wptr;   // 2 x (nw + 1)
     double* chunk_part;  // n_chunks x 2
@@ -371,7 +372,7 @@ __device__ __forceinline__ void run_phase(const SchurParams& P, int mode, const 
                 if (mode == kColInit) {
                     const double* rb = kk ? P.rhs_b[1] : P.rhs_b[0];
                     const double c = (kk < P.nrhs ? rb[line] : 0.0) - sum;  // Schur right-hand side
-                    const double z = c / diag;
+                    const double z = c / __ldg(P.mB + line);
                     P.rb[o] = c;
                     P.zb[o] = z;
                     P.xb[o] = 0.0;
@@ -553,7 +554,7 @@ __global__ void __launch_bounds__(kSchurThreads, 1) k_pcg_schur(const __grid_con
                     const size_t o = (size_t)j * 2;
                     const double2 z2 = ldcg_x2(P.zb + o), p2 = ldcg_x2(P.pb + o), w2 = ldcg_x2(P.wb + o);
                     const double2 s2 = ldcg_x2(P.sb + o), x2 = ldcg_x2(P.xb + o), r2 = ldcg_x2(P.rb + o);
-                    const double dj = __ldg(P.dB + j);
+                    const double dj = __ldg(P.mB + j);
                     const double zv[2] = {z2.x, z2.y}, pv[2] = {p2.x, p2.y}, wv[2] = {w2.x, w2.y};
                     const double sv[2] = {s2.x, s2.y}, xv[2] = {x2.x, x2.y}, rv[2] = {r2.x, r2.y};
                     double pn[2], sn[2], xn[2], rn[2], zn[2];
@@ -871,6 +872,7 @@ static int pcg_schur_launch(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, const
     P.cscval = S.cscval.p;
     P.dA = S.dA.p;
     P.dB = S.dB.p;
+    P.mB = S.dS.p;
     P.items = Q.items.p;
     P.wptr = Q.wptr.p;
     P.chunk_part = Q.chunk_part.p;

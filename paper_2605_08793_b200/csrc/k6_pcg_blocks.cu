@@ -374,6 +374,7 @@ struct BlocksParams {
     const double* val;  // CSR values of B (regot_sparse::val)
     const double* dA;
     const double* dB;
+    const double* mB;  // Jacobi preconditioner: diag of the Schur complement (k4_sparse.cu compute_schur_diag)
     const double* rhs_a[2];
     const double* rhs_b[2];
     double* sol_a[2];
@@ -850,7 +851,7 @@ __global__ void __launch_bounds__(kB2Threads, 1) k_pcg_blocks(const __grid_const
     for (int c = tid; c < n_own_c; c += kB2Threads) {
         const double d = __ldg(A.dB + q + (c_lo + c) * Q);
         odb[c] = d;
-        oib[c] = 1.0 / d;
+        oib[c] = 1.0 / __ldg(A.mB + q + (c_lo + c) * Q);
     }
     __syncthreads();
     if (cl) cooperative_groups::this_cluster().sync();  // every inbox of the cluster is cleared before the first post
@@ -946,7 +947,7 @@ __global__ void __launch_bounds__(kB2Threads, 1) k_pcg_blocks(const __grid_const
                 ox[item] = 0.0;
                 op[item] = 0.0;
                 os[item] = 0.0;
-                const double g0 = rb * (rb * inv);
+                const double g0 = rb * (rb / d);  // the stopping rule's norm keeps D2
                 if (k) {
                     part[1] += r * z;
                     part[3] += d * z * z;
@@ -1325,6 +1326,7 @@ static int pcg_blocks_launch(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, cons
     A.val = S.val.p;
     A.dA = S.dA.p;
     A.dB = S.dB.p;
+    A.mB = S.dS.p;
     for (int k = 0; k < 2; ++k) {
         const int kk = k < nrhs ? k : 0;
         A.rhs_a[k] = rhs[kk]->a.p;

@@ -47,12 +47,15 @@ struct PanelPlan {
     DevBuf<unsigned short> idx16;  // per entry of the half's matrix copy: index relative to its panel
     DevBuf<int> cost, scan;   // P x nlines (+1): work per piece and its exclusive prefix sum
     DevBuf<double> part;      // P x nlines x 2: per-panel partial sums of every line (ELL stream: then the sums of the items of cut pieces)
-    // ELL stream of the pieces (k4_sparse.cu): every piece cut into items of up to kPanelGroupMax entries, the items of a
-    // CTA sorted by length, 8 to a chunk, entry k of item j of a chunk at row k / 4, lane (k % 4) * 8 + j
+    // ELL stream of the pieces (k4_sparse.cu): every piece cut into items of up to kEllItemMax entries, the items of a
+    // CTA sorted by length; a long item is a chunk (entry k at row k / 32, lane k % 32), the others go 8 to a chunk (entry k
+    // of item j at row k / 4, lane (k % 4) * 8 + j)
     DevBuf<int> nseg, itembase;     // per piece q = p nlines + l: its items, and their exclusive prefix sum (np + 1)
     DevBuf<unsigned> ekey, ekey2;   // sort keys: (CTA, cap - length)
     DevBuf<int> eid0, eid;          // item ids before / after the sort
     DevBuf<int> item_q;             // piece of every item
+    DevBuf<int> nlong;              // per CTA: items above kPanelGroupMax entries (a chunk each)
+    DevBuf<unsigned char> multi;    // per line: any piece of several items
     DevBuf<int> elen, ebeg, eout;   // per sorted item: entries, first entry, where its sums go (pairs of part)
     DevBuf<int> chrows, choff;      // per chunk slot: rows of 32 entries, first row
     DevBuf<int> emap;               // per ELL slot: the entry of the matrix copy it holds, or -1
@@ -112,6 +115,7 @@ struct regot_sparse {
     int n_lines_s = 0, n_lines_m = 0;
     rg::PcgSchedule pcg;  // single-GPU direction solve (k5_pcg.cu)
     unsigned long structure_stamp = 0;         // bumped by finish_structure: derived plans know when they are stale
+    mutable rg::DevBuf<double> dS;  // diagonal of the Schur complement D2 - B' D1^-1 B: the Jacobi preconditioner of the PCG (per solve)
     mutable rg::PanelPlan panel_rows, panel_cols;  // kernel-by-kernel direction solve of large / sharded problems
     rg::PcgBlocksPlan blocks;                      // block-resident direction solve (k6_pcg_blocks.cu)
 };

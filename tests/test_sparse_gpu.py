@@ -203,9 +203,10 @@ def panel_solver(request):
     s.close()
 
 
-@pytest.mark.parametrize("n,m,k", [(300, 257, 6000), (90, 700, 9000), (1500, 1400, 30000)])
+@pytest.mark.parametrize("n,m,k", [(300, 257, 6000), (90, 700, 9000), (1500, 1400, 30000), (260, 2600, 14000)])
 def test_panel_matvec_pcg_matches_oracle(panel_solver, oracle, n, m, k):
-    # long first row / column (pieces for a warp and for the whole CTA), ragged panels, two right-hand sides
+    # long first row / column (items of a chunk of their own; with one panel the 2599-entry row is cut into two items,
+    # whose sums the consumers add), ragged panels, two right-hand sides
     p = oracle.gen_problem("rand", n, m, 0.1, seed=6701)
     a0, b0 = oracle.rand_dual(n, m, 0.2, 6801)
     coords = oracle.select_topk(oracle.plan(p, a0, b0), k)

@@ -898,27 +898,40 @@ __global__ void __launch_bounds__(kPanelThreads, 1) k_spmv_panel(const PanelArgs
     }
 }
 
-// sum of line l's per-panel partials in panel order; a piece the ELL stream cut into several items is summed in item
-// order first (its items' sums sit behind the P x nlines piece slots)
-__device__ __forceinline__ double panel_line_sum(const double* __restrict__ part, const int* __restrict__ itembase,
-                                                 const unsigned char* __restrict__ multi, int nlines, int P, int l, int k)
+// sums (both right-hand sides) of line l's per-panel partials in panel order; a piece the ELL stream cut into several items
+// is summed in item order first (its items' sums sit behind the P x nlines piece slots).  The loads of the common case
+// are independent 16-byte loads.
+__device__ __forceinline__ double2 panel_line_sum2(const double* __restrict__ part, const int* __restrict__ itembase,
+                                                   const unsigned char* __restrict__ multi, int nlines, int P, int l)
 {
-    double s = 0.0;
-    if (itembase == nullptr || multi[l] == 0) {  // every piece of the line is one item
-        for (int p = 0; p < P; ++p) s += part[((size_t)p * nlines + l) * 2 + k];
-        return s;
+    const double2* part2 = reinterpret_cast<const double2*>(part);
+    // the common case first and unconditionally (its loads do not wait for the flag): every piece of the line is one item
+    const bool cut = itembase != nullptr && multi[l] != 0;
+    double2 s = make_double2(0.0, 0.0);
+#pragma unroll 4
+    for (int p = 0; p < P; ++p) {
+        const double2 t = part2[(size_t)p * nlines + l];
+        s.x += t.x;
+        s.y += t.y;
     }
+    if (!cut) return s;
+    s = make_double2(0.0, 0.0);
     const size_t np = (size_t)nlines * P;
     for (int p = 0; p < P; ++p) {
         const size_t q = (size_t)p * nlines + l;
         const int b0 = itembase[q], ns = itembase[q + 1] - b0;
+        double2 t = make_double2(0.0, 0.0);
         if (ns == 1) {
-            s += part[q * 2 + k];
+            t = part2[q];
         } else {
-            double t = 0.0;
-            for (int sg = 0; sg < ns; ++sg) t += part[(np + (size_t)(b0 + sg)) * 2 + k];
-            s += t;
+            for (int sg = 0; sg < ns; ++sg) {
+                const double2 c = part2[np + (size_t)(b0 + sg)];
+                t.x += c.x;
+                t.y += c.y;
+            }
         }
+        s.x += t.x;
+        s.y += t.y;
     }
     return s;
 }
@@ -930,11 +943,14 @@ __global__ void k_panel_combine(int nlines, int P, const double* __restrict__ pa
                                 const double* skip)
 {
     if (skip != nullptr && *skip != 0.0) return;
-    const int total = nlines * 2;
-    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < total; q += gridDim.x * blockDim.x) {
-        const int l = q >> 1, k = q & 1;
-        const double s = panel_line_sum(part, itembase, multi, nlines, P, l, k);
-        y[(size_t)l * 4 + k] = (kEpi == kEpiRowsScaled) ? s / diag[l] : s;
+    for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < nlines; l += gridDim.x * blockDim.x) {
+        double2 sm = panel_line_sum2(part, itembase, multi, nlines, P, l);
+        if (kEpi == kEpiRowsScaled) {
+            const double d = diag[l];
+            sm.x = sm.x / d;
+            sm.y = sm.y / d;
+        }
+        *reinterpret_cast<double2*>(y + (size_t)l * 4) = sm;
     }
 }
 
@@ -1091,8 +1107,8 @@ static void launch_spmv_panel(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, con
         ProfScope prof(ctx, st, 4);
         k_spmv_panel<<<Q.P * Q.Bk, kPanelThreads, panel_smem(Q.W, ctx->panel_ell != 0), st>>>(a);
         if (combine) {  // else the consumer adds the per-panel partials itself (one kernel and one pass over the vector less)
-            const int g = (int)std::max<long>(1, std::min<long>(((long)Q.nlines * 2 + 255) / 256, 4L * ctx->sm_count));
-            k_panel_combine<kEpi><<<g, 256, 0, st>>>(Q.nlines, Q.P, Q.part.p, ctx->panel_ell ? Q.itembase.p : nullptr, Q.multi.p, rows ? S.dA.p : nullptr,
+            const int g = (int)std::max<long>(1, std::min<long>(((long)Q.nlines + 127) / 128, 8L * ctx->sm_count));
+            k_panel_combine<kEpi><<<g, 128, 0, st>>>(Q.nlines, Q.P, Q.part.p, ctx->panel_ell ? Q.itembase.p : nullptr, Q.multi.p, rows ? S.dA.p : nullptr,
                                                      y, skip);
         }
     }
@@ -1202,7 +1218,8 @@ __global__ void __launch_bounds__(kCgThreads) k_schur_init_a(const CgVecs v, con
 __device__ __forceinline__ double schur_u(const CgVecs& v, int j, int k)
 {
     if (v.part == nullptr || k >= 2) return v.ub[(size_t)j * 4 + k];
-    return panel_line_sum(v.part, v.part_itembase, v.part_multi, v.mfree, v.n_parts, j, k);
+    const double2 u2 = panel_line_sum2(v.part, v.part_itembase, v.part_multi, v.mfree, v.n_parts, j);
+    return k ? u2.y : u2.x;
 }
 
 // set-up: c = r_b - u (u = B' t summed over ranks): r = c, z = D2^-1 c, x = p = s = 0; gamma = r'z; beta part of
@@ -1251,14 +1268,39 @@ __global__ void __launch_bounds__(kCgThreads) k_schur_w(const CgVecs v)
     __shared__ double scratch[2 * kMaxRhs * (kCgThreads / 32)];
     double acc[2 * kMaxRhs] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
     const int stride = gridDim.x * blockDim.x;
-    for (int k = 0; k < v.nrhs; ++k) {
-        if (v.scal[kScalDone + k] != 0.0) continue;
-        for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < v.mfree; j += stride) {
-            const size_t o = (size_t)j * 4 + k;
-            const double z = v.zb[o], w = v.dB[j] * z - schur_u(v, j, k);
-            v.ub[o] = w;  // u is not needed any more: w takes its place
-            acc[k] += v.rb[o] * z;
-            acc[kMaxRhs + k] += z * w;
+    bool live[kMaxRhs];
+    for (int k = 0; k < kMaxRhs; ++k) live[k] = k < v.nrhs && v.scal[kScalDone + k] == 0.0;
+    // one column per thread and trip, all systems at once: 16-byte loads, the per-panel partials of both systems in one
+    // go; every accumulator still adds its columns in ascending order
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < v.mfree; j += stride) {
+        const size_t o = (size_t)j * 4;
+        double u[kMaxRhs], z[kMaxRhs], r[kMaxRhs];
+        if (v.part != nullptr) {
+            const double2 u2 = panel_line_sum2(v.part, v.part_itembase, v.part_multi, v.mfree, v.n_parts, j);
+            u[0] = u2.x;
+            u[1] = u2.y;
+            u[2] = live[2] ? v.ub[o + 2] : 0.0;
+        } else {
+            const double2 u2 = *reinterpret_cast<const double2*>(v.ub + o);
+            u[0] = u2.x;
+            u[1] = u2.y;
+            u[2] = live[2] ? v.ub[o + 2] : 0.0;
+        }
+        const double2 z2 = *reinterpret_cast<const double2*>(v.zb + o), r2 = *reinterpret_cast<const double2*>(v.rb + o);
+        z[0] = z2.x;
+        z[1] = z2.y;
+        z[2] = live[2] ? v.zb[o + 2] : 0.0;
+        r[0] = r2.x;
+        r[1] = r2.y;
+        r[2] = live[2] ? v.rb[o + 2] : 0.0;
+        const double d = v.dB[j];
+#pragma unroll
+        for (int k = 0; k < kMaxRhs; ++k) {
+            if (!live[k]) continue;
+            const double w = d * z[k] - u[k];
+            v.ub[o + k] = w;  // u is not needed any more: w takes its place
+            acc[k] += r[k] * z[k];
+            acc[kMaxRhs + k] += z[k] * w;
         }
     }
     if (!two_stage_sum<2 * kMaxRhs>(acc, scratch, v.partials, v.ticket, v.scal + kScalDots)) return;
@@ -1297,18 +1339,50 @@ __global__ void __launch_bounds__(kCgThreads) k_schur_step(const CgVecs v, int i
 {
     if (v.scal[kScalStepIt] != (double)iteration) return;  // this iteration was skipped (the solve had ended) or broke down
     const int stride = gridDim.x * blockDim.x;
-    for (int k = 0; k < v.nrhs; ++k) {
-        const double al = v.scal[kScalAlpha + k], be = v.scal[kScalBeta + k];
-        if (v.scal[kScalDone + k] != 0.0 || al == 0.0) continue;
-        for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < v.mfree; j += stride) {
-            const size_t o = (size_t)j * 4 + k;
-            const double pn = v.zb[o] + be * v.pb[o], sn = v.ub[o] + be * v.sb[o];
-            const double rn = v.rb[o] - al * sn;
-            v.pb[o] = pn;
-            v.sb[o] = sn;
-            v.xb[o] += al * pn;
-            v.rb[o] = rn;
-            v.zb[o] = rn / v.mB[j];
+    double al[kMaxRhs], be[kMaxRhs];
+    bool live[kMaxRhs];
+    for (int k = 0; k < kMaxRhs; ++k) {
+        al[k] = k < v.nrhs ? v.scal[kScalAlpha + k] : 0.0;
+        be[k] = k < v.nrhs ? v.scal[kScalBeta + k] : 0.0;
+        live[k] = k < v.nrhs && v.scal[kScalDone + k] == 0.0 && al[k] != 0.0;
+    }
+    // one column per thread and trip: systems 0 and 1 as 16-byte vectors, system 2 (stand-alone compute_direction) scalar
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < v.mfree; j += stride) {
+        const size_t o = (size_t)j * 4;
+        const double mj = v.mB[j];
+        if (live[0] || live[1]) {
+            double2 z = *reinterpret_cast<const double2*>(v.zb + o), pp = *reinterpret_cast<const double2*>(v.pb + o);
+            double2 w = *reinterpret_cast<const double2*>(v.ub + o), ss = *reinterpret_cast<const double2*>(v.sb + o);
+            double2 r = *reinterpret_cast<const double2*>(v.rb + o), x = *reinterpret_cast<const double2*>(v.xb + o);
+            if (live[0]) {
+                pp.x = z.x + be[0] * pp.x;
+                ss.x = w.x + be[0] * ss.x;
+                x.x += al[0] * pp.x;
+                r.x = r.x - al[0] * ss.x;
+                z.x = r.x / mj;
+            }
+            if (live[1]) {
+                pp.y = z.y + be[1] * pp.y;
+                ss.y = w.y + be[1] * ss.y;
+                x.y += al[1] * pp.y;
+                r.y = r.y - al[1] * ss.y;
+                z.y = r.y / mj;
+            }
+            *reinterpret_cast<double2*>(v.pb + o) = pp;
+            *reinterpret_cast<double2*>(v.sb + o) = ss;
+            *reinterpret_cast<double2*>(v.xb + o) = x;
+            *reinterpret_cast<double2*>(v.rb + o) = r;
+            *reinterpret_cast<double2*>(v.zb + o) = z;
+        }
+        if (live[2]) {
+            const size_t q = o + 2;
+            const double pn = v.zb[q] + be[2] * v.pb[q], sn = v.ub[q] + be[2] * v.sb[q];
+            const double rn = v.rb[q] - al[2] * sn;
+            v.pb[q] = pn;
+            v.sb[q] = sn;
+            v.xb[q] += al[2] * pn;
+            v.rb[q] = rn;
+            v.zb[q] = rn / mj;
         }
     }
 }
@@ -1469,53 +1543,56 @@ __device__ __forceinline__ double schur_diag_guard(double d2, double s)
     const double x = d2 - s, lo = 1e-10 * d2;
     return x > lo ? x : lo;
 }
-constexpr int kDiagThreads = 1024, kDiagWarps = kDiagThreads / 32;
-constexpr int kDiagLong = 2048;  // columns above this many entries are summed by the whole CTA (column 0 of Omega* is full)
+constexpr int kDiagThreads = 256, kDiagWarps = kDiagThreads / 32;
+constexpr int kDiagLong = 4096;  // columns above this many entries are left to k_schur_diag_long (column 0 of Omega* is full)
+constexpr int kDiagLongThreads = 256;
+__device__ __forceinline__ double schur_diag_term(const int* __restrict__ cscrow, const double* __restrict__ cscval,
+                                                  const double* __restrict__ dA, int e)
+{
+    const double v = __ldg(cscval + e);
+    return v * (v / __ldg(dA + __ldg(cscrow + e)));
+}
+// a warp per column (lanes strided, butterfly: a fixed order); long columns are listed for the kernel below
 __global__ void __launch_bounds__(kDiagThreads) k_schur_diag(int mfree, const int* __restrict__ cscptr, const int* __restrict__ cscrow,
                                                              const double* __restrict__ cscval, const double* __restrict__ dA,
-                                                             const double* __restrict__ dB, double* __restrict__ out, int finalize)
+                                                             const double* __restrict__ dB, double* __restrict__ out, int finalize,
+                                                             int* __restrict__ long_list, int* __restrict__ n_long)
 {
-    __shared__ int long_col[kDiagWarps];
-    __shared__ double wsum[kDiagWarps];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    auto term = [&](int e) {
-        const double v = __ldg(cscval + e);
-        return v * (v / __ldg(dA + __ldg(cscrow + e)));
-    };
-    // a warp per column, 32 columns per CTA and trip; every sum in a fixed order (lanes strided, butterfly, warps in order)
-    for (int base = blockIdx.x * kDiagWarps; base < mfree; base += gridDim.x * kDiagWarps) {
-        const int j = base + warp;
-        int beg = 0, end = 0;
-        if (j < mfree) {
-            beg = __ldg(cscptr + j);
-            end = __ldg(cscptr + j + 1);
+    const int lane = threadIdx.x & 31, nw = (gridDim.x * blockDim.x) >> 5;
+    for (int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < mfree; j += nw) {
+        const int beg = __ldg(cscptr + j), end = __ldg(cscptr + j + 1);
+        if (end - beg > kDiagLong) {
+            if (lane == 0) long_list[atomicAdd(n_long, 1)] = j;  // the order of the list does not matter
+            continue;
         }
-        const bool lng = end - beg > kDiagLong;
-        if (lane == 0) long_col[warp] = lng ? j : -1;
-        if (j < mfree && !lng) {
-            double s = 0.0;
-#pragma unroll 4
-            for (int e = beg + lane; e < end; e += 32) s += term(e);
-            s = warp_sum(s);
-            if (lane == 0) out[j] = finalize ? schur_diag_guard(__ldg(dB + j), s) : s;
-        }
+        double s = 0.0;
+#pragma unroll 8
+        for (int e = beg + lane; e < end; e += 32) s += schur_diag_term(cscrow, cscval, dA, e);
+        s = warp_sum(s);
+        if (lane == 0) out[j] = finalize ? schur_diag_guard(__ldg(dB + j), s) : s;
+    }
+}
+// a CTA per long column: threads strided, butterfly per warp, warps in order
+__global__ void __launch_bounds__(kDiagLongThreads) k_schur_diag_long(const int* __restrict__ cscptr, const int* __restrict__ cscrow,
+                                                                      const double* __restrict__ cscval, const double* __restrict__ dA,
+                                                                      const double* __restrict__ dB, double* __restrict__ out,
+                                                                      int finalize, const int* __restrict__ long_list,
+                                                                      const int* __restrict__ n_long)
+{
+    __shared__ double wsum[kDiagLongThreads / 32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, n = *n_long;
+    for (int q = blockIdx.x; q < n; q += gridDim.x) {
+        const int j = long_list[q], beg = __ldg(cscptr + j), end = __ldg(cscptr + j + 1);
+        double s = 0.0;
+#pragma unroll 8
+        for (int e = beg + tid; e < end; e += kDiagLongThreads) s += schur_diag_term(cscrow, cscval, dA, e);
+        s = warp_sum(s);
+        if (lane == 0) wsum[warp] = s;
         __syncthreads();
-        for (int w = 0; w < kDiagWarps; ++w) {
-            const int jl = long_col[w];
-            if (jl < 0) continue;  // uniform over the CTA
-            const int b2 = __ldg(cscptr + jl), e2 = __ldg(cscptr + jl + 1);
-            double s = 0.0;
-#pragma unroll 4
-            for (int e = b2 + tid; e < e2; e += kDiagThreads) s += term(e);
-            s = warp_sum(s);
-            if (lane == 0) wsum[warp] = s;
-            __syncthreads();
-            if (tid == 0) {
-                double t = 0.0;
-                for (int q = 0; q < kDiagWarps; ++q) t += wsum[q];
-                out[jl] = finalize ? schur_diag_guard(__ldg(dB + jl), t) : t;
-            }
-            __syncthreads();
+        if (tid == 0) {
+            double t = 0.0;
+            for (int w = 0; w < kDiagLongThreads / 32; ++w) t += wsum[w];
+            out[j] = finalize ? schur_diag_guard(__ldg(dB + j), t) : t;
         }
         __syncthreads();
     }
@@ -1533,10 +1610,16 @@ static void compute_schur_diag(regot_ctx* ctx, cudaStream_t st, ncclComm* comm, 
         RG_CUDA(cudaMemcpyAsync(S.dS.p, S.dB.p, sizeof(double) * (size_t)mfree, cudaMemcpyDeviceToDevice, st));
         return;
     }
-    const int grid = (int)std::max<long>(1, std::min<long>(((long)mfree + kDiagWarps - 1) / kDiagWarps, 8L * ctx->sm_count));
-    k_schur_diag<<<grid, kDiagThreads, 0, st>>>(mfree, S.cscptr.p, S.cscrow.p, S.cscval.p, S.dA.p, S.dB.p, S.dS.p, ctx->sharded ? 0 : 1);
+    const int grid = (int)std::max<long>(1, std::min<long>(((long)mfree + kDiagWarps - 1) / kDiagWarps, 64L * ctx->sm_count));
+    S.diag_long.ensure((size_t)mfree + 1);  // entry 0: the count; then the list
+    RG_CUDA(cudaMemsetAsync(S.diag_long.p, 0, sizeof(int), st));
+    const int fin = ctx->sharded ? 0 : 1;
+    k_schur_diag<<<grid, kDiagThreads, 0, st>>>(mfree, S.cscptr.p, S.cscrow.p, S.cscval.p, S.dA.p, S.dB.p, S.dS.p, fin, S.diag_long.p + 1,
+                                               S.diag_long.p);
+    k_schur_diag_long<<<8 * ctx->sm_count, kDiagLongThreads, 0, st>>>(S.cscptr.p, S.cscrow.p, S.cscval.p, S.dA.p, S.dB.p, S.dS.p, fin, S.diag_long.p + 1,
+                                                      S.diag_long.p);
     RG_CUDA(cudaGetLastError());
-    ++ctx->launches;
+    ctx->launches += 2;
     if (ctx->sharded) {
         allreduce_sum(ctx, comm, S.dS.p, (size_t)mfree, st);
         k_schur_diag_fin<<<(mfree + 255) / 256, 256, 0, st>>>(mfree, S.dB.p, S.dS.p);

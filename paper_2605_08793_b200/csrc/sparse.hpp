@@ -115,6 +115,7 @@ struct regot_sparse {
     int n_lines_s = 0, n_lines_m = 0;
     rg::PcgSchedule pcg;  // single-GPU direction solve (k5_pcg.cu)
     unsigned long structure_stamp = 0;         // bumped by finish_structure: derived plans know when they are stale
+    mutable rg::DevBuf<int> diag_long;  // compute_schur_diag: count and list of the columns a whole CTA sums
     mutable rg::DevBuf<double> dS;  // diagonal of the Schur complement D2 - B' D1^-1 B: the Jacobi preconditioner of the PCG (per solve)
     mutable rg::PanelPlan panel_rows, panel_cols;  // kernel-by-kernel direction solve of large / sharded problems
     rg::PcgBlocksPlan blocks;                      // block-resident direction solve (k6_pcg_blocks.cu)

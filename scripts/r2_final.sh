@@ -26,3 +26,7 @@ REPS=2 timeout 900 python scripts/solve_cloud.py E 1 2>&1 | tail -10 > gpurun_ou
 REPS=2 timeout 900 python scripts/solve_cloud.py D 0 2>&1 | tail -10 > gpurun_out/e2e_D.txt
 bash scripts/r2_host.sh > /dev/null 2>&1
 ls -la gpurun_out | head -50
+# preconditioner (diag of the Schur complement against D2), ELL stream of the panel mat-vec (on / off, panel widths)
+bash scripts/r2_precond.sh > /dev/null 2>&1
+{ WIDTHS="12800 10016 8352 7168" bash scripts/r2_ell_width.sh; echo "== pieces read from the CSR / CSC copy (REGOT_B200_PANEL_ELL=0)";
+  REGOT_B200_PANEL_ELL=0 REPS=2 timeout 600 python scripts/solve_cloud.py D 0 2>&1 | grep -E "wall_s|spmv" | cut -c1-120; } > gpurun_out/r2_ell_width.txt 2>&1

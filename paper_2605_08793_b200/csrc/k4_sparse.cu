@@ -1240,7 +1240,7 @@ __global__ void __launch_bounds__(kCgThreads) k_schur_init_b(const CgVecs v, con
             v.pb[o] = 0.0;
             v.sb[o] = 0.0;
             acc[k] += c * z;
-            acc[kMaxRhs + k] += rb * (rb / d);
+            acc[kMaxRhs + k] += rb * (rb / v.mB[j]);  // the stopping rule's norm: the preconditioner's
         }
     __shared__ double out6[2 * kMaxRhs];
     if (!two_stage_sum<2 * kMaxRhs>(acc, scratch, v.partials, v.ticket, out6)) return;
@@ -1536,8 +1536,9 @@ static int pcg_schur_multikernel(regot_ctx* ctx, cudaStream_t st, ncclComm* comm
 // and 165 -> 43 PCG iterations on a 700 x 700 instance, config D 4919 -> see DESIGN.md.  One pass over the CSC copy per
 // solve (the values change between solves); sharded runs add the ranks' partial column sums.  A difference lost to
 // rounding (below 1e-10 D2_j: the pattern carries the whole column) falls back to that floor: any positive diagonal
-// is a valid preconditioner.  The stopping rule keeps its D^-1 norm of the right-hand side (gamma0): with
-// 1 / diag(S) >= 1 / D2 the test gamma <= tol^2 gamma0 is at least as strict as before.
+// is a valid preconditioner.  The stopping rule measures the right-hand side in the same norm as the residual
+// (gamma0 = r_a' D1^-1 r_a + r_b' diag(S)^-1 r_b): keeping D2 there made the test stricter than rtol says and cost one or
+// two iterations per solve at the paper's sizes.
 __device__ __forceinline__ double schur_diag_guard(double d2, double s)
 {
     const double x = d2 - s, lo = 1e-10 * d2;
@@ -1546,11 +1547,29 @@ __device__ __forceinline__ double schur_diag_guard(double d2, double s)
 constexpr int kDiagThreads = 256, kDiagWarps = kDiagThreads / 32;
 constexpr int kDiagLong = 4096;  // columns above this many entries are left to k_schur_diag_long (column 0 of Omega* is full)
 constexpr int kDiagLongThreads = 256;
-__device__ __forceinline__ double schur_diag_term(const int* __restrict__ cscrow, const double* __restrict__ cscval,
-                                                  const double* __restrict__ dA, int e)
+// sum over e = first, first + step, ... < end of cscval[e]^2 / dA[cscrow[e]], eight entries in flight: the indices and values
+// of a batch are loaded first, then the gathered diagonal entries, then the arithmetic (a plain loop waits for every
+// dependent pair of loads in turn: 35 us for the 1,600 entries of a full column on one warp)
+__device__ __forceinline__ double schur_diag_strided(const int* __restrict__ cscrow, const double* __restrict__ cscval,
+                                                     const double* __restrict__ dA, int first, int end, int step)
 {
-    const double v = __ldg(cscval + e);
-    return v * (v / __ldg(dA + __ldg(cscrow + e)));
+    double s = 0.0;
+    for (int e0 = first; e0 < end; e0 += 8 * step) {
+        int r[8];
+        double v[8], d[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int e = e0 + u * step;
+            const bool ok = e < end;
+            r[u] = ok ? __ldg(cscrow + e) : -1;
+            v[u] = ok ? __ldg(cscval + e) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) d[u] = r[u] >= 0 ? __ldg(dA + r[u]) : 1.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) s += v[u] * (v[u] / d[u]);
+    }
+    return s;
 }
 // a warp per column (lanes strided, butterfly: a fixed order); long columns are listed for the kernel below
 __global__ void __launch_bounds__(kDiagThreads) k_schur_diag(int mfree, const int* __restrict__ cscptr, const int* __restrict__ cscrow,
@@ -1565,9 +1584,7 @@ __global__ void __launch_bounds__(kDiagThreads) k_schur_diag(int mfree, const in
             if (lane == 0) long_list[atomicAdd(n_long, 1)] = j;  // the order of the list does not matter
             continue;
         }
-        double s = 0.0;
-#pragma unroll 8
-        for (int e = beg + lane; e < end; e += 32) s += schur_diag_term(cscrow, cscval, dA, e);
+        double s = schur_diag_strided(cscrow, cscval, dA, beg + lane, end, 32);
         s = warp_sum(s);
         if (lane == 0) out[j] = finalize ? schur_diag_guard(__ldg(dB + j), s) : s;
     }
@@ -1583,9 +1600,7 @@ __global__ void __launch_bounds__(kDiagLongThreads) k_schur_diag_long(const int*
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, n = *n_long;
     for (int q = blockIdx.x; q < n; q += gridDim.x) {
         const int j = long_list[q], beg = __ldg(cscptr + j), end = __ldg(cscptr + j + 1);
-        double s = 0.0;
-#pragma unroll 8
-        for (int e = beg + tid; e < end; e += kDiagLongThreads) s += schur_diag_term(cscrow, cscval, dA, e);
+        double s = schur_diag_strided(cscrow, cscval, dA, beg + tid, end, kDiagLongThreads);
         s = warp_sum(s);
         if (lane == 0) wsum[warp] = s;
         __syncthreads();
@@ -1612,14 +1627,18 @@ static void compute_schur_diag(regot_ctx* ctx, cudaStream_t st, ncclComm* comm, 
     }
     const int grid = (int)std::max<long>(1, std::min<long>(((long)mfree + kDiagWarps - 1) / kDiagWarps, 64L * ctx->sm_count));
     S.diag_long.ensure((size_t)mfree + 1);  // entry 0: the count; then the list
-    RG_CUDA(cudaMemsetAsync(S.diag_long.p, 0, sizeof(int), st));
     const int fin = ctx->sharded ? 0 : 1;
+    // a column has at most nloc entries: with nloc <= kDiagLong no column is long, and the list, its reset and the second
+    // kernel are not needed (the paper's sizes: one launch per solve)
+    const bool may_be_long = S.nloc > kDiagLong;
+    if (may_be_long) RG_CUDA(cudaMemsetAsync(S.diag_long.p, 0, sizeof(int), st));
     k_schur_diag<<<grid, kDiagThreads, 0, st>>>(mfree, S.cscptr.p, S.cscrow.p, S.cscval.p, S.dA.p, S.dB.p, S.dS.p, fin, S.diag_long.p + 1,
                                                S.diag_long.p);
-    k_schur_diag_long<<<8 * ctx->sm_count, kDiagLongThreads, 0, st>>>(S.cscptr.p, S.cscrow.p, S.cscval.p, S.dA.p, S.dB.p, S.dS.p, fin, S.diag_long.p + 1,
-                                                      S.diag_long.p);
+    if (may_be_long)
+        k_schur_diag_long<<<8 * ctx->sm_count, kDiagLongThreads, 0, st>>>(S.cscptr.p, S.cscrow.p, S.cscval.p, S.dA.p, S.dB.p, S.dS.p, fin,
+                                                                         S.diag_long.p + 1, S.diag_long.p);
     RG_CUDA(cudaGetLastError());
-    ctx->launches += 2;
+    ctx->launches += may_be_long ? 2 : 1;
     if (ctx->sharded) {
         allreduce_sum(ctx, comm, S.dS.p, (size_t)mfree, st);
         k_schur_diag_fin<<<(mfree + 255) / 256, 256, 0, st>>>(mfree, S.dB.p, S.dS.p);

@@ -466,7 +466,7 @@ __global__ void __launch_bounds__(kSchurThreads, 1) k_pcg_schur(const __grid_con
         *reinterpret_cast<double2*>(P.ta + (size_t)i * 2) = make_double2(t[0], t[1]);
     }
     for (int j = tid; j < mfree; j += nthr) {
-        const double d = P.dB[j];
+        const double d = P.mB[j];  // the stopping rule's norm: the preconditioner's
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
             const double r = (k < nrhs) ? P.rhs_b[k][j] : 0.0;

@@ -947,7 +947,7 @@ __global__ void __launch_bounds__(kB2Threads, 1) k_pcg_blocks(const __grid_const
                 ox[item] = 0.0;
                 op[item] = 0.0;
                 os[item] = 0.0;
-                const double g0 = rb * (rb / d);  // the stopping rule's norm keeps D2
+                const double g0 = rb * (rb * inv);  // the stopping rule's norm: the preconditioner's
                 if (k) {
                     part[1] += r * z;
                     part[3] += d * z * z;

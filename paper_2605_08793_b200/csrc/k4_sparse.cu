@@ -1019,6 +1019,8 @@ static void build_panel_plan(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, cons
         Q.eidx.ensure(Q.ell_cap);
         Q.eval.ensure(Q.ell_cap);
         Q.part.ensure((np + Q.item_cap) * 2 + 2);
+        // the piece slots of cut pieces are never written but are read (and discarded) by the consumers' common-case loads
+        RG_CUDA(cudaMemsetAsync(Q.part.p, 0, sizeof(double) * ((np + Q.item_cap) * 2 + 2), st));
         const int gi = (int)std::max<long>(1, std::min<long>(((long)np + 255) / 256, 8L * ctx->sm_count));
         const int gk = (int)std::max<long>(1, std::min<long>(((long)Q.item_cap + 255) / 256, 8L * ctx->sm_count));
         int cta_bits = 1;
@@ -1030,6 +1032,7 @@ static void build_panel_plan(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, cons
         ws.cub_tmp.ensure(sbytes);
         RG_CUDA(cub::DeviceScan::ExclusiveSum(ws.cub_tmp.p, sbytes, Q.nseg.p, Q.itembase.p, (int)np + 1, st));
         k_ell_fill_u32<<<gk, 256, 0, st>>>((long)Q.item_cap, 1u << (kEllKeyBits + cta_bits), Q.ekey.p);
+        RG_CUDA(cudaMemsetAsync(Q.eid0.p, 0, sizeof(int) * Q.item_cap, st));  // the unused tail is sorted along (to the end)
         k_ell_keys<<<gi, 256, 0, st>>>(Q.nlines, Q.P, Q.Bk, Q.ppt.p, Q.blk.p, Q.itembase.p, Q.ekey.p, Q.eid0.p, Q.item_q.p);
         RG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, sbytes, Q.ekey.p, Q.ekey2.p, Q.eid0.p, Q.eid.p, (int)Q.item_cap, 0, key_bits, st));
         ws.cub_tmp.ensure(sbytes);

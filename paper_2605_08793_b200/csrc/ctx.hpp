@@ -60,8 +60,22 @@ struct DevBuf {
     void ensure(size_t count)
     {
         if (count <= n && p) return;
+        // a buffer that grows again gets a quarter of headroom: candidate and pattern sizes creep up from refresh to refresh,
+        // and every regrowth is a cudaFree + cudaMalloc (synchronising; tens of ms at the GB sizes of config D)
+        const bool regrow = p != nullptr;
         release();
-        cudaError_t e = cudaMalloc((void**)&p, sizeof(T) * (count ? count : 1));
+        cudaError_t e = cudaErrorMemoryAllocation;
+        if (regrow && count > 1024) {
+            const size_t padded = count + count / 4;
+            e = cudaMalloc((void**)&p, sizeof(T) * padded);
+            if (e == cudaSuccess) {
+                n = padded;
+                return;
+            }
+            p = nullptr;
+            cudaGetLastError();
+        }
+        e = cudaMalloc((void**)&p, sizeof(T) * (count ? count : 1));
         if (e != cudaSuccess) {
             p = nullptr;
             cudaGetLastError();

@@ -281,12 +281,17 @@ __global__ void k_iota(int n, int* __restrict__ v)
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) v[t] = t;
 }
 // after the stable sort by column: sorted position q holds CSR entry src[q]
-__global__ void k_build_csc(int nnz, const int* __restrict__ src, const int* __restrict__ row, int* __restrict__ cscrow,
-                            int* __restrict__ slot)
+// (colsorted[q] = column of sorted position q; the gathered cost travels along so that the CSC copy of the values can be
+// computed in place instead of scattered from the CSR copy)
+__global__ void k_build_csc(int nnz, const int* __restrict__ src, const int* __restrict__ row, const int* __restrict__ colsorted,
+                            const double* __restrict__ mval, int* __restrict__ cscrow, int* __restrict__ csccol,
+                            double* __restrict__ cscmval, int* __restrict__ slot)
 {
     for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nnz; q += gridDim.x * blockDim.x) {
         const int t = src[q];
         cscrow[q] = row[t];
+        csccol[q] = colsorted[q];
+        cscmval[q] = mval[t];
         slot[t] = q;
     }
 }
@@ -615,7 +620,10 @@ void finish_structure(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, regot_spars
         ws.cub_tmp.ensure(bytes);
         RG_CUDA(cub::DeviceRadixSort::SortPairs(ws.cub_tmp.p, bytes, S.col.p, ws.sort_k1.p, ws.sort_v0.p, ws.sort_v1.p, nnz,
                                                 0, bits, st));
-        k_build_csc<<<lin_grid(ctx, nnz), 256, 0, st>>>(nnz, ws.sort_v1.p, S.row.p, S.cscrow.p, S.slot.p);
+        S.csccol.ensure((size_t)nnz + 1);
+        S.cscmval.ensure((size_t)nnz + 1);
+        k_build_csc<<<lin_grid(ctx, nnz), 256, 0, st>>>(nnz, ws.sort_v1.p, S.row.p, ws.sort_k1.p, S.mval.p, S.cscrow.p, S.csccol.p, S.cscmval.p,
+                                                        S.slot.p);
         RG_CUDA(cudaGetLastError());
         ctx->launches += 4;
         // the block plan of the resident PCG kernel is built on the device behind the CSC (sort_v1[t] = CSR position of

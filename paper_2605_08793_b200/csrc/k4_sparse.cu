@@ -20,8 +20,8 @@ namespace rg {
 
 // ---- K3 -----------------------------------------------------------------------------------
 __global__ void k_fill_values(int nnz, int nloc, int mm1, double eta, const ExpScale E, double tau, const int* __restrict__ row,
-                              const int* __restrict__ col, const int* __restrict__ slot,
-                              const double* __restrict__ mval, const double* __restrict__ alpha,
+                              const int* __restrict__ col, const int* __restrict__ cscrow, const int* __restrict__ csccol,
+                              const double* __restrict__ mval, const double* __restrict__ cscmval, const double* __restrict__ alpha,
                               const double* __restrict__ beta, const double* __restrict__ row_sums,
                               const double* __restrict__ col_sums, const double* __restrict__ exp_table,
                               double* __restrict__ val, double* __restrict__ cscval, double* __restrict__ dA,
@@ -32,8 +32,11 @@ __global__ void k_fill_values(int nnz, int nloc, int mm1, double eta, const ExpS
         // plan_entry(...) / eta (sparsity.h:216): same T arithmetic as K1, true division by eta
         const double v = __ddiv_rn(plan_entry_dev_g((alpha[row[t]] + beta[col[t]]) - mval[t], E, exp_table), eta);
         val[t] = v;
-        cscval[slot[t]] = v;
     }
+    // the CSC copy: the same arithmetic on the same operands in CSC order (identical bits), written coalesced -- scattering
+    // the CSR values through slot[] was 8-byte writes to random sectors (config D: 0.58 ms per call)
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nnz; q += stride)
+        cscval[q] = __ddiv_rn(plan_entry_dev_g((alpha[cscrow[q]] + beta[csccol[q]]) - cscmval[q], E, exp_table), eta);
     // diagonal: full row / column sums over eta plus tau (sparsity.h:208-212)
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nloc; i += stride)
         dA[i] = __dadd_rn(__ddiv_rn(row_sums[i], eta), tau);
@@ -49,7 +52,7 @@ void sparse_fill_values(regot_ctx* ctx, cudaStream_t st, regot_sparse& S, const 
     const long work = std::max<long>(S.nnz, std::max<long>(S.nloc, S.m));
     const int grid = (int)std::max<long>(1, std::min<long>((work + 255) / 256, 8L * ctx->sm_count));
     k_fill_values<<<grid, 256, 0, st>>>((int)S.nnz, (int)S.nloc, (int)S.m - 1, ctx->prob.eta, make_exp_scale(ctx->prob.eta), tau, S.row.p, S.col.p,
-                                        S.slot.p, S.mval.p, alpha, beta, row_sums, col_sums, ctx->exp_table.p, S.val.p,
+                                        S.cscrow.p, S.csccol.p, S.mval.p, S.cscmval.p, alpha, beta, row_sums, col_sums, ctx->exp_table.p, S.val.p,
                                         S.cscval.p, S.dA.p, S.dB.p);
     RG_CUDA(cudaGetLastError());
     ++ctx->launches;

@@ -285,14 +285,13 @@ __global__ void k_iota(int n, int* __restrict__ v)
 // computed in place instead of scattered from the CSR copy)
 __global__ void k_build_csc(int nnz, const int* __restrict__ src, const int* __restrict__ row, const int* __restrict__ colsorted,
                             const double* __restrict__ mval, int* __restrict__ cscrow, int* __restrict__ csccol,
-                            double* __restrict__ cscmval, int* __restrict__ slot)
+                            double* __restrict__ cscmval)
 {
     for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nnz; q += gridDim.x * blockDim.x) {
         const int t = src[q];
         cscrow[q] = row[t];
         csccol[q] = colsorted[q];
         cscmval[q] = mval[t];
-        slot[t] = q;
     }
 }
 __global__ void k_gather_cost(int nnz, const int* __restrict__ row, const int* __restrict__ col, const CostViewDev cost,
@@ -594,7 +593,6 @@ void finish_structure(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, regot_spars
     S.val.ensure((size_t)nnz + 1);
     S.cscval.ensure((size_t)nnz + 1);
     S.cscrow.ensure((size_t)nnz + 1);
-    S.slot.ensure((size_t)nnz + 1);
     S.cscptr.ensure((size_t)std::max(mm1, 0) + 2);
     S.dA.ensure((size_t)nloc);
     S.dB.ensure((size_t)std::max(mm1, 1));
@@ -622,8 +620,7 @@ void finish_structure(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, regot_spars
                                                 0, bits, st));
         S.csccol.ensure((size_t)nnz + 1);
         S.cscmval.ensure((size_t)nnz + 1);
-        k_build_csc<<<lin_grid(ctx, nnz), 256, 0, st>>>(nnz, ws.sort_v1.p, S.row.p, ws.sort_k1.p, S.mval.p, S.cscrow.p, S.csccol.p, S.cscmval.p,
-                                                        S.slot.p);
+        k_build_csc<<<lin_grid(ctx, nnz), 256, 0, st>>>(nnz, ws.sort_v1.p, S.row.p, ws.sort_k1.p, S.mval.p, S.cscrow.p, S.csccol.p, S.cscmval.p);
         RG_CUDA(cudaGetLastError());
         ctx->launches += 4;
         // the block plan of the resident PCG kernel is built on the device behind the CSC (sort_v1[t] = CSR position of

@@ -98,7 +98,7 @@ struct regot_sparse {
     rg::DevBuf<int> rowptr, col, row;
     rg::DevBuf<double> val, mval;  // values and the gathered costs M_ij (so value refreshes never touch M)
     // CSC of B (columns 0..m-2), rows ascending inside a column
-    rg::DevBuf<int> cscptr, cscrow, slot;  // slot[t] = CSC position of CSR entry t
+    rg::DevBuf<int> cscptr, cscrow;
     rg::DevBuf<int> csccol;                // column of every CSC entry
     rg::DevBuf<double> cscmval;            // gathered costs in CSC order (the CSC values are computed in place)
     rg::DevBuf<double> cscval;

@@ -156,6 +156,7 @@ regot_ctx* ctx_create(int device)
         if (const char* e = std::getenv("REGOT_B200_FUSED_FINALIZE")) ctx->fused_finalize = e[0] != '0';
         if (const char* e = std::getenv("REGOT_B200_EXTENDED_F")) ctx->extended_f = e[0] != '0';
         if (const char* e = std::getenv("REGOT_B200_SCHUR_DIAG")) ctx->schur_diag = std::atoi(e);
+        if (const char* e = std::getenv("REGOT_B200_TOPK_GUESS")) ctx->topk_guess = std::atoi(e);
         if (const char* e = std::getenv("REGOT_B200_PCG_BLOCKS")) ctx->pcg_blocks = std::atoi(e);
         if (const char* e = std::getenv("REGOT_B200_PCG_BLOCKS_CLUSTER")) ctx->pcg_blocks_cluster = std::atoi(e);
         if (const char* e = std::getenv("REGOT_B200_PCG_BLOCKS_ONE_CLUSTER_ENTRIES")) ctx->pcg_blocks_one_cluster_entries = std::atol(e);
@@ -324,6 +325,7 @@ static void finish_problem(regot_ctx* ctx)
     if (ctx->prob.on_the_fly) std::memset(&ctx->prob.tmap, 0, sizeof(ctx->prob.tmap));  // the sweeps compute their tiles
     else build_tensor_map(ctx);
     ctx->prob.loaded = true;
+    ctx->topk_prev_bin = -1;  // a threshold bin of the previous problem says nothing about this one
     make_sweep_plan(ctx);
     ensure_sweep_ws(ctx, ctx->ws_main);
     ensure_sweep_ws(ctx, ctx->ws_side);

@@ -305,6 +305,11 @@ struct regot_ctx {
     bool extended_f = true;
     // block-resident PCG (k6_pcg_blocks.cu): -1 auto (whenever the pattern fits), 0 off (REGOT_B200_PCG_BLOCKS);
     // pcg_blocks_p x pcg_blocks_q > 0 force the block grid (REGOT_B200_PCG_BLOCKS_GRID=PxQ, tests)
+    // top-k refresh: the count sweep starts from the previous refresh's threshold bin and histograms the candidates itself;
+    // the histogram sweep runs only when that guess turns out too high (REGOT_B200_TOPK_GUESS=0: always three sweeps)
+    int topk_guess = 1;
+    int topk_prev_bin = -1;
+    long long topk_prev_take = -1;
     int schur_diag = 1;  // REGOT_B200_SCHUR_DIAG=0: precondition with D2 instead of diag(D2 - B' D1^-1 B)
     int pcg_blocks = -1;
     int pcg_blocks_p = 0, pcg_blocks_q = 0;

@@ -3,7 +3,8 @@
 // Replaces regot::plan + select_topk (dual.h:83-94, sparsity.h:44-91) and the
 // structural half of assemble (sparsity.h:226-289).  The dense plan is never
 // materialised: three TMA sweeps over the cost block recompute T on the fly
-//   1. HIST   4096-bin histogram of the top 12 bits of an order-preserving key
+//   1. HIST   4096-bin histogram of the top 12 bits of an order-preserving key (skipped when the previous refresh's
+//             threshold bin, tried first by the COUNT sweep with its own histogram of the candidates, still holds)
 //   2. COUNT  per (row, panel) count of candidates (coarse bin >= b* or Omega*)
 //   3. WRITE  warp-ballot compaction of the candidates in row-major order
 // then the exact k-th largest key K* inside bin b* is found by a 4 x 13-bit
@@ -48,6 +49,7 @@ struct TopkParams {
     int row_begin;  // global index of local row 0 (Omega* first row lives on rank 0)
     int mm1;        // m - 1: the last column is never a candidate
     unsigned bstar; // coarse threshold bin
+    int count_hist; // COUNT pass: also histogram the entries whose bin is >= bstar (bstar is a guess)
     unsigned long long* hist;  // kCoarseBins
     const int* candptr;        // nloc + 1
     const int* pre;            // n_panels x nloc
@@ -66,7 +68,8 @@ k_topk_sweep(const __grid_constant__ CUtensorMap tmap, const TopkParams p)
     const SweepSmem sm = sweep_prologue(smem, &tmap, p.exp_table, !kCloud);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     unsigned int* shist = reinterpret_cast<unsigned int*>(sm.scratch);
-    if (kPass == kPassHist) {
+    const bool hist_here = kPass == kPassHist || (kPass == kPassCount && p.count_hist);
+    if (hist_here) {
         for (int q = threadIdx.x; q < kCoarseBins; q += blockDim.x) shist[q] = 0u;
         __syncthreads();
     }
@@ -160,6 +163,13 @@ k_topk_sweep(const __grid_constant__ CUtensorMap tmap, const TopkParams p)
                         sel[k] = ((cmask >> k) & 1u) && ((unsigned)(key[k] >> 52) >= p.bstar || first_row || c == 0);
                     }
                     if (kPass == kPassCount) {
+                        if (p.count_hist) {  // by value only (Omega* is no part of the ranking): a few percent of the entries
+#pragma unroll
+                            for (int k = 0; k < kEPL; ++k) {
+                                const unsigned bin = (unsigned)(key[k] >> 52);
+                                if (((cmask >> k) & 1u) && bin >= p.bstar) atomicAdd(&shist[bin], 1u);
+                            }
+                        }
                         int tot = 0;
 #pragma unroll
                         for (int k = 0; k < kEPL; ++k) tot += __popc(__ballot_sync(0xffffffffu, sel[k]));
@@ -206,7 +216,7 @@ k_topk_sweep(const __grid_constant__ CUtensorMap tmap, const TopkParams p)
             ++panel;
         }
     }
-    if (kPass == kPassHist) {
+    if (hist_here) {
         bar_sync(1, kConsumerThreads);
         for (int q = threadIdx.x; q < kCoarseBins; q += kConsumerThreads)
             if (shist[q]) atomicAdd(&p.hist[q], (unsigned long long)shist[q]);
@@ -419,13 +429,50 @@ void topk_build_pattern(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, TopkSourc
     p.row_begin = (int)pr.row_begin;
     p.mm1 = mm1;
 
-    // ---- pass 1: coarse histogram, pick the bin b* that holds the take-th largest key ----
+    const size_t np = (size_t)ctx->plan.n_panels * (size_t)nloc;
     ws.hist.ensure(kFineBins);
+    ws.cnt.ensure(np);
+    ws.pre.ensure(np);
+    ws.rowtot.ensure((size_t)nloc + 1);
+    ws.candptr.ensure((size_t)nloc + 1);
+    p.cnt = ws.cnt.p;
+    p.hist = ws.hist.p;
     unsigned bstar = kCoarseBins;  // take == 0: nothing qualifies by value
     long long need = 0;            // how many keys of bin b* belong to the top-k
-    if (take > 0) {
+    unsigned count_bin = kCoarseBins;  // the bin the COUNT and WRITE sweeps select from (<= b*)
+    bool counted = false;
+
+    // ---- the previous refresh's threshold bin as a guess: COUNT from it, histogramming the candidates on the way.  A bin is
+    // a binade of T; from one refresh to the next the threshold stays in it most of the time (config D: 3041 five times in
+    // a row, config C: 3049 for the last 25 refreshes).  The guess is good when the candidates are at least `take`: b* is
+    // then read off their histogram (b* > guess just means a few candidates too many); a guess that is too high costs the
+    // count sweep it took. ----
+    if (take > 0 && src == kFromDual && ctx->topk_guess && ctx->topk_prev_bin >= 0 && ctx->topk_prev_take == take) {
         RG_CUDA(cudaMemsetAsync(ws.hist.p, 0, sizeof(unsigned long long) * kCoarseBins, st));
-        p.hist = ws.hist.p;
+        p.bstar = (unsigned)ctx->topk_prev_bin;
+        p.count_hist = 1;
+        launch_sweep_src<kPassCount>(ctx, st, src, p);
+        fetch_hist(ctx, st, ws, kCoarseBins);
+        int b = -1;
+        int64_t above = 0;
+        regot_b200_host_pick_bucket((const uint64_t*)ws.h_hist, kCoarseBins, take, &b, &above);
+        // a guess far below the threshold is as useless as one above it: the candidates would be a large part of the block
+        // (second refresh of config D: the threshold moves up by 111 binades, 1.1e9 candidates for 2.5e7 places)
+        long long total = 0;
+        for (int q = ctx->topk_prev_bin; q < kCoarseBins; ++q) total += (long long)ws.h_hist[q];
+        if (b >= ctx->topk_prev_bin && total <= 2 * take + 1024) {
+            bstar = (unsigned)b;
+            need = take - above;
+            count_bin = (unsigned)ctx->topk_prev_bin;
+            counted = true;
+        }
+        rt.tick(counted ? "count sweep from the previous bin (hit)" : "count sweep from the previous bin (miss)");
+    }
+    p.count_hist = 0;
+
+    // ---- pass 1: coarse histogram, pick the bin b* that holds the take-th largest key ----
+    if (take > 0 && !counted) {
+        RG_CUDA(cudaMemsetAsync(ws.hist.p, 0, sizeof(unsigned long long) * kCoarseBins, st));
         launch_sweep_src<kPassHist>(ctx, st, src, p);
         fetch_hist(ctx, st, ws, kCoarseBins);
         int b = -1;
@@ -435,17 +482,19 @@ void topk_build_pattern(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, TopkSourc
         bstar = (unsigned)b;
         need = take - above;
     }
+    if (src == kFromDual) {
+        ctx->topk_prev_bin = take > 0 ? (int)bstar : -1;
+        ctx->topk_prev_take = take;
+    }
 
     rt.tick("hist sweep + pick");
     // ---- pass 2 + 3: count and write the candidates in row-major order ----
-    const size_t np = (size_t)ctx->plan.n_panels * (size_t)nloc;
-    ws.cnt.ensure(np);
-    ws.pre.ensure(np);
-    ws.rowtot.ensure((size_t)nloc + 1);
-    ws.candptr.ensure((size_t)nloc + 1);
-    p.bstar = bstar;
-    p.cnt = ws.cnt.p;
-    launch_sweep_src<kPassCount>(ctx, st, src, p);
+    if (!counted) {
+        count_bin = bstar;
+        p.bstar = count_bin;
+        launch_sweep_src<kPassCount>(ctx, st, src, p);
+    }
+    p.bstar = count_bin;
     k_row_prefix<<<lin_grid(ctx, nloc), 256, 0, st>>>(nloc, ctx->plan.n_panels, ws.cnt.p, ws.pre.p, ws.rowtot.p);
     RG_CUDA(cudaGetLastError());
     ++ctx->launches;
@@ -466,6 +515,7 @@ void topk_build_pattern(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, TopkSourc
     p.cand_row = ws.cand_row.p;
     p.cand_m = ws.cand_m.p;
     rt.tick("count sweep + scan");
+    if (rt.on) rt.line += "bin " + std::to_string(bstar) + " candidates " + std::to_string(nc) + " take " + std::to_string((long long)take) + " | ";
     launch_sweep_src<kPassWrite>(ctx, st, src, p);
     rt.tick("write sweep");
 

@@ -351,3 +351,47 @@ def test_foreign_and_invalid_inputs_rejected(solver, oracle):
         solver.assemble(x, rg.SparsityPattern(8, 5, np.array([[0, 0], [1, 1]], np.int32)), 0.1)  # Omega* missing
     with pytest.raises(rg.ValidationError):
         rg.select_topk(np.ones((3, 3)), -1)
+
+
+@pytest.mark.parametrize("shift_binades", [0.0, 0.4, 3.0, -3.0, -0.6])
+def test_topk_refresh_from_the_previous_threshold_bin_gives_the_same_pattern(oracle, shift_binades):
+    """k2_topk.cu: a refresh starts its count sweep from the previous refresh's threshold bin (a binade of T) and runs the
+    histogram sweep only when that guess is too high.  Same bin, threshold moved up (candidates: a superset) and threshold
+    moved down (guess too high: the three-sweep path) must all give the pattern and values of a context without the
+    guess, bit for bit, and that pattern is the oracle's."""
+    import os
+
+    n, m, k = 203, 157, 2500
+    p = oracle.gen_problem("rand", n, m, 0.05, seed=811)
+    a0, b0 = oracle.rand_dual(n, m, 0.1, 812)
+    a1 = a0 + shift_binades * 0.05 * np.log(2.0) + 0.002 * np.cos(np.arange(n))  # T scaled by 2^shift, slightly reshuffled
+    x0, x1 = rg.DualPoint(a0, b0), rg.DualPoint(a1, b0)
+
+    def pattern_after(env, warm):
+        old = os.environ.get("REGOT_B200_TOPK_GUESS")
+        if env is not None:
+            os.environ["REGOT_B200_TOPK_GUESS"] = env
+        try:
+            s = rg.Solver(0)
+        finally:
+            if env is not None:
+                if old is None:
+                    del os.environ["REGOT_B200_TOPK_GUESS"]
+                else:
+                    os.environ["REGOT_B200_TOPK_GUESS"] = old
+        try:
+            s.set_problem(to_problem(p))
+            if warm:
+                s.assemble_topk(x0, k, 0.1).free()  # leaves its threshold bin behind
+            A = s.assemble_topk(x1, k, 0.1)
+            return A.export_local()
+        finally:
+            s.close()
+
+    guessed = pattern_after(None, True)
+    plain = pattern_after("0", True)
+    cold = pattern_after(None, False)
+    for got in (guessed, cold):
+        assert np.array_equal(got[0], plain[0]) and np.array_equal(got[1], plain[1])
+    ref = oracle.select_topk(oracle.plan(p, a1, b0), k)
+    assert np.array_equal(np.asarray(guessed[0]), np.asarray(ref))

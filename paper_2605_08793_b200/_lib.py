@@ -185,6 +185,8 @@ PROTOTYPES = {
     "regot_b200_host_pick_bucket": (None, [C.POINTER(C.c_uint64), C.c_int, C.c_int64, C.POINTER(C.c_int), c_int64_p]),
     "regot_b200_time_kernel": (C.c_int, [_vp, C.c_int, _vp, _vp, C.c_int, c_float_p]),
     "regot_b200_launch_count": (C.c_int64, [_vp]),
+    "regot_b200_set_pattern_reuse": (C.c_int, [_vp, C.c_double, C.c_int]),
+    "regot_b200_pattern_counts": (None, [_vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "regot_b200_set_profiling": (C.c_int, [_vp, C.c_int]),
     "regot_b200_get_profile": (C.c_int, [_vp, C.c_int, c_int64_p, c_double_p]),
 }

@@ -76,6 +76,22 @@ const char* regot_b200_last_error(const regot_ctx* ctx) { return ctx ? ctx->err.
 
 int64_t regot_b200_launch_count(const regot_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
+regot_status regot_b200_set_pattern_reuse(regot_ctx* ctx, double drift_tol, int max_skips)
+{
+    return guard(ctx, [&] {
+        if (!(drift_tol >= 0.0) || drift_tol >= 1.0 || max_skips < 0)
+            rg::raise(REGOT_E_VALIDATION, "set_pattern_reuse: need 0 <= drift_tol < 1 and max_skips >= 0");
+        ctx->pattern_drift = drift_tol;
+        ctx->pattern_max_skips = max_skips;
+    });
+}
+
+void regot_b200_pattern_counts(const regot_ctx* ctx, int64_t* rebuilds, int64_t* reuses)
+{
+    if (rebuilds) *rebuilds = ctx ? ctx->pattern_rebuilds : 0;
+    if (reuses) *reuses = ctx ? ctx->pattern_reuses : 0;
+}
+
 regot_status regot_b200_set_profiling(regot_ctx* ctx, int enabled)
 {
     return guard(ctx, [&] {

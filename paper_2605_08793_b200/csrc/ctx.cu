@@ -157,6 +157,8 @@ regot_ctx* ctx_create(int device)
         if (const char* e = std::getenv("REGOT_B200_EXTENDED_F")) ctx->extended_f = e[0] != '0';
         if (const char* e = std::getenv("REGOT_B200_SCHUR_DIAG")) ctx->schur_diag = std::atoi(e);
         if (const char* e = std::getenv("REGOT_B200_TOPK_GUESS")) ctx->topk_guess = std::atoi(e);
+        if (const char* e = std::getenv("REGOT_B200_PATTERN_DRIFT")) ctx->pattern_drift = std::max(0.0, std::atof(e));
+        if (const char* e = std::getenv("REGOT_B200_PATTERN_MAX_SKIPS")) ctx->pattern_max_skips = std::max(0, std::atoi(e));
         if (const char* e = std::getenv("REGOT_B200_PCG_BLOCKS")) ctx->pcg_blocks = std::atoi(e);
         if (const char* e = std::getenv("REGOT_B200_PCG_BLOCKS_CLUSTER")) ctx->pcg_blocks_cluster = std::atoi(e);
         if (const char* e = std::getenv("REGOT_B200_PCG_BLOCKS_ONE_CLUSTER_ENTRIES")) ctx->pcg_blocks_one_cluster_entries = std::atol(e);

@@ -310,6 +310,14 @@ struct regot_ctx {
     int topk_guess = 1;
     int topk_prev_bin = -1;
     long long topk_prev_take = -1;
+    // pattern reuse across refreshes (north_star item 2, an extension of the reference's fixed-S rule splr.h:352-364): at
+    // an iteration with k % S == 0 the top-k pattern is rebuilt only if the share of the Hessian block's mass it holds fell
+    // below (1 - pattern_drift) x the share it held when it was built, or after pattern_max_skips refreshes in a row kept it;
+    // otherwise the refresh is a value update and the candidate chain.  0 (default): the reference's rule, always rebuild
+    // (regot_b200_set_pattern_reuse, REGOT_B200_PATTERN_DRIFT / REGOT_B200_PATTERN_MAX_SKIPS)
+    double pattern_drift = 0.0;
+    int pattern_max_skips = 4;
+    int64_t pattern_rebuilds = 0, pattern_reuses = 0;
     int schur_diag = 1;  // REGOT_B200_SCHUR_DIAG=0: precondition with D2 instead of diag(D2 - B' D1^-1 B)
     int pcg_blocks = -1;
     int pcg_blocks_p = 0, pcg_blocks_q = 0;

@@ -58,6 +58,61 @@ void sparse_fill_values(regot_ctx* ctx, cudaStream_t st, regot_sparse& S, const 
     ++ctx->launches;
 }
 
+// ---- captured mass of the frozen pattern (pattern reuse, regot_b200_set_pattern_reuse) ---------------
+// sum of the pattern's values and of the full row sums over eta, in a fixed order: thread-strided partial sums, a fixed
+// shared-memory tree per block, then one block over the per-block partials.  The ratio is the share of the Hessian block's
+// mass the pattern still holds at the current point; the solver compares it with the share at the last rebuild.
+constexpr int kMassBlocks = 296, kMassThreads = 256;
+
+__global__ void k_captured_mass_partials(int nnz, int nloc, double eta, const double* __restrict__ val,
+                                         const double* __restrict__ row_sums, double* __restrict__ partials)
+{
+    __shared__ double sh[2][kMassThreads];
+    const int stride = gridDim.x * blockDim.x;
+    double sv = 0.0, sr = 0.0;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nnz; t += stride) sv = __dadd_rn(sv, val[t]);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nloc; i += stride) sr = __dadd_rn(sr, __ddiv_rn(row_sums[i], eta));
+    sh[0][threadIdx.x] = sv;
+    sh[1][threadIdx.x] = sr;
+    __syncthreads();
+    for (int w = kMassThreads / 2; w > 0; w >>= 1) {
+        if ((int)threadIdx.x < w) {
+            sh[0][threadIdx.x] = __dadd_rn(sh[0][threadIdx.x], sh[0][threadIdx.x + w]);
+            sh[1][threadIdx.x] = __dadd_rn(sh[1][threadIdx.x], sh[1][threadIdx.x + w]);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        partials[2 * blockIdx.x] = sh[0][0];
+        partials[2 * blockIdx.x + 1] = sh[1][0];
+    }
+}
+
+__global__ void k_captured_mass_final(int blocks, const double* __restrict__ partials, double* __restrict__ out)
+{
+    if (threadIdx.x < 2) {
+        double s = 0.0;
+        for (int b = 0; b < blocks; ++b) s = __dadd_rn(s, partials[2 * b + threadIdx.x]);
+        out[threadIdx.x] = s;
+    }
+}
+
+double sparse_captured_mass(regot_ctx* ctx, cudaStream_t st, ncclComm* comm, const regot_sparse& S, DevBuf<double>& scratch,
+                            const double* row_sums)
+{
+    scratch.ensure(2 * kMassBlocks + 2);
+    double* out = scratch.p + 2 * kMassBlocks;
+    k_captured_mass_partials<<<kMassBlocks, kMassThreads, 0, st>>>((int)S.nnz, (int)S.nloc, ctx->prob.eta, S.val.p, row_sums, scratch.p);
+    k_captured_mass_final<<<1, 32, 0, st>>>(kMassBlocks, scratch.p, out);
+    RG_CUDA(cudaGetLastError());
+    ctx->launches += 2;
+    allreduce_sum(ctx, comm, out, 2, st);  // sharded runs: every rank takes the same decision from the same bits
+    double h[2] = {0.0, 0.0};
+    RG_CUDA(cudaMemcpyAsync(h, out, sizeof(h), cudaMemcpyDeviceToHost, st));
+    RG_CUDA(cudaStreamSynchronize(st));
+    return h[1] > 0.0 ? h[0] / h[1] : 0.0;
+}
+
 // ---- K4 -----------------------------------------------------------------------------------
 constexpr int kMaxRhs = 3;
 constexpr int kSpmvThreads = 256;

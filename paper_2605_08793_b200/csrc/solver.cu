@@ -431,6 +431,8 @@ void splr_init_state(regot_ctx* ctx, const double* alpha0, const double* beta0, 
     gradient_sync(ctx, ctx->stream, ctx->ws_main, ctx->comm, S.x, nullptr, S.cur, stats);
     S.has_prev = false;
     S.iter = 0;
+    S.mass_at_build = -1.0;
+    S.pattern_skips = 0;
 }
 
 // ---- splr_step (splr.h:348-478) -------------------------------------------------------------------
@@ -496,23 +498,42 @@ void splr_step_state(regot_ctx* ctx, SplrStateDev& S, const regot_splr_config& c
         // pattern's pointer arrays into line lists and the PCG schedule.  Same kernels, same order of
         // arithmetic, same results.
         bool chain_started = false;
-        if (cfg.J > 0 && !cfg.overlap && !ctx->profiling)
-            W.sparse.after_pointer_download = [&]() {
-                run_chain(ctx->fast_sinkhorn_chain);
-                chain_started = true;
-            };
-        // plan + select_topk + assemble (splr.h:361-364); T is never materialised
-        try {
-            ProfScope prof(ctx, st, 6);  // the whole pattern refresh: sweeps, selection, structure, host work
-            topk_build_pattern(ctx, st, W.sparse, kFromDual, S.x.a.p, S.x.b.p,
-                               regot_b200_topk_budget(pr.n, pr.m, cfg.density), S.A);
-        } catch (...) {
-            W.sparse.after_pointer_download = nullptr;
-            throw;
+        // Pattern reuse (regot_b200_set_pattern_reuse; off by default = the reference's rule): the values of the pattern in
+        // hand are refreshed at the current point first -- the update a non-refresh iteration makes -- and the pattern is
+        // kept while it still holds its share of the Hessian block's mass.  The candidate chain runs either way.
+        bool keep_pattern = false;
+        const bool reuse_on = ctx->pattern_drift > 0.0;
+        if (reuse_on && k > 0 && S.mass_at_build > 0.0 && S.pattern_skips < ctx->pattern_max_skips && S.A.ctx == ctx &&
+            S.A.n == pr.n && S.A.m == pr.m && S.A.nloc == pr.nloc) {
+            sparse_fill_values(ctx, st, S.A, S.x.a.p, S.x.b.p, tau, S.cur.sums.a.p, S.cur.sums.b.p);
+            const double share = sparse_captured_mass(ctx, st, ctx->comm, S.A, S.mass_scratch, S.cur.sums.a.p);
+            keep_pattern = share >= (1.0 - ctx->pattern_drift) * S.mass_at_build;
         }
-        W.sparse.after_pointer_download = nullptr;
-        out.gradient_passes += 3;  // three sweeps over M
-        sparse_fill_values(ctx, st, S.A, S.x.a.p, S.x.b.p, tau, S.cur.sums.a.p, S.cur.sums.b.p);
+        if (keep_pattern) {
+            ++S.pattern_skips;
+            ++ctx->pattern_reuses;
+        } else {
+            if (cfg.J > 0 && !cfg.overlap && !ctx->profiling)
+                W.sparse.after_pointer_download = [&]() {
+                    run_chain(ctx->fast_sinkhorn_chain);
+                    chain_started = true;
+                };
+            // plan + select_topk + assemble (splr.h:361-364); T is never materialised
+            try {
+                ProfScope prof(ctx, st, 6);  // the whole pattern refresh: sweeps, selection, structure, host work
+                topk_build_pattern(ctx, st, W.sparse, kFromDual, S.x.a.p, S.x.b.p,
+                                   regot_b200_topk_budget(pr.n, pr.m, cfg.density), S.A);
+            } catch (...) {
+                W.sparse.after_pointer_download = nullptr;
+                throw;
+            }
+            W.sparse.after_pointer_download = nullptr;
+            out.gradient_passes += 3;  // three sweeps over M
+            sparse_fill_values(ctx, st, S.A, S.x.a.p, S.x.b.p, tau, S.cur.sums.a.p, S.cur.sums.b.p);
+            ++ctx->pattern_rebuilds;
+            S.pattern_skips = 0;
+            if (reuse_on) S.mass_at_build = sparse_captured_mass(ctx, st, ctx->comm, S.A, S.mass_scratch, S.cur.sums.a.p);
+        }
         sect.tick(0);
         if (cfg.J > 0) {
             if (cfg.overlap) {

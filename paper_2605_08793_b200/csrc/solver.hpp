@@ -43,6 +43,10 @@ struct SplrStateDev {
     bool has_prev = false;
     regot_sparse A;  // H_Omega + tau I at the frozen pattern
     long iter = 0;
+    // pattern reuse (regot_b200_set_pattern_reuse): share of the mass the pattern held when it was built, refreshes that kept it
+    double mass_at_build = -1.0;
+    int pattern_skips = 0;
+    DevBuf<double> mass_scratch;
     // per-step scratch
     DVec xs, d, sdiff, ydiff, v, ag, au, av;
     GradOut cand;

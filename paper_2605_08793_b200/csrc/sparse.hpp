@@ -188,6 +188,10 @@ void finish_structure(regot_ctx* ctx, cudaStream_t st, SparseWS& ws, regot_spars
 // k4_sparse.cu -- fill_transport_values (sparsity.h:202-220): K3
 void sparse_fill_values(regot_ctx* ctx, cudaStream_t st, regot_sparse& S, const double* alpha, const double* beta,
                         double tau, const double* row_sums, const double* col_sums);
+// share of the Hessian block's mass (sum of all row sums over eta) held by the pattern's values as they stand; synchronises
+// `st`; summed over the ranks when sharded (pattern reuse, regot_b200_set_pattern_reuse)
+double sparse_captured_mass(regot_ctx* ctx, cudaStream_t st, ncclComm* comm, const regot_sparse& S, DevBuf<double>& scratch,
+                            const double* row_sums);
 // y = A v on free vectors (K4); nrhs systems stored back to back with strides
 void sparse_matvec(regot_ctx* ctx, cudaStream_t st, ncclComm* comm, const regot_sparse& S, int nrhs, const double* va,
                    const double* vb, double* ya, double* yb, int64_t stride_a, int64_t stride_b);

@@ -413,6 +413,18 @@ class Solver:
     def launch_count(self) -> int:
         return int(self._lib.regot_b200_launch_count(self._h))
 
+    def set_pattern_reuse(self, drift_tol: float, max_skips: int = 4) -> None:
+        """north_star item (2): at k % S == 0 rebuild the top-k pattern only when the share of the Hessian block's mass
+        it holds fell below (1 - drift_tol) x its share at the last rebuild (or after max_skips kept refreshes in a row).
+        drift_tol = 0 restores the reference's fixed-S rule (splr.h:352, 359-364)."""
+        self._check(self._lib.regot_b200_set_pattern_reuse(self._h, float(drift_tol), int(max_skips)))
+
+    def pattern_counts(self):
+        """(rebuilds, reuses) of the top-k pattern since this context was created."""
+        a, b = C.c_int64(0), C.c_int64(0)
+        self._lib.regot_b200_pattern_counts(self._h, C.byref(a), C.byref(b))
+        return int(a.value), int(b.value)
+
     # -- multi-GPU ---------------------------------------------------------------
     @staticmethod
     def comm_unique_id() -> bytes:

@@ -57,7 +57,8 @@ print(json.dumps({"wall_s": round(wall, 3), "device_ms": round(res.stats.device_
                   "err": last.marginal_error, "f": last.f, "grad_passes": res.stats.gradient_passes,
                   "lse_passes": res.stats.lse_passes, "ls_evals": sum(x.ls_evals for x in res.steps),
                   "cg_iters": sum(x.cg_iters for x in res.steps), "ls_failed": sum(x.ls_failed for x in res.steps),
-                  "sink_sel": sum(x.sinkhorn_selected for x in res.steps)}), flush=True)
+                  "sink_sel": sum(x.sinkhorn_selected for x in res.steps),
+                  "pattern_rebuilds_reuses": s.pattern_counts()}), flush=True)
 for k, nm in enumerate(["gradient", "row_lse", "col_lse", "topk", "spmv", "pcg"]):
     cnt, tot = s.get_profile(k)
     print(f"  {nm:9s} launches {cnt:6d} total {tot:10.2f} ms avg {tot / max(cnt, 1):.4f} ms")

@@ -65,7 +65,8 @@ for rep in range(2):
                       "launches": res.stats.kernel_launches,
                       "ls_evals": sum(x.ls_evals for x in res.steps), "cg_iters": sum(x.cg_iters for x in res.steps),
                       "ls_failed": sum(x.ls_failed for x in res.steps), "sink_sel": sum(x.sinkhorn_selected for x in res.steps),
-                      "retries": sum(x.factor_retries for x in res.steps)}), flush=True)
+                      "retries": sum(x.factor_retries for x in res.steps),
+                      "pattern_rebuilds_reuses": s.pattern_counts()}), flush=True)
 names = ["gradient", "row_lse", "col_lse", "topk", "spmv", "pcg", "refresh"]
 for k, nm in enumerate(names):
     n, ms = s.get_profile(k)

@@ -229,6 +229,38 @@ def test_sharded_run_splr_config_A(solver, R, overlap):
         assert np.array_equal(q.x.beta, res[0].x.beta) and np.array_equal(q.x.alpha, res[0].x.alpha)
 
 
+def test_sharded_pattern_reuse_takes_the_same_decisions_as_one_gpu():
+    """Pattern reuse (regot_b200_set_pattern_reuse): the captured-mass share is allreduced, so every rank keeps or rebuilds
+    the pattern at the same refreshes as the unsharded solve (shares differ in the last bits only)."""
+    p = problems.gen_synthetic2(256, 192, 0.005)
+    cfg = rg.SplrConfig(tol=1e-8)
+    x0 = rg.DualPoint.zeros(p.n, p.m)
+    one = rg.Solver(0)
+    try:
+        one.set_pattern_reuse(0.05, 3)
+        one.set_problem(p)
+        ref = one.run_splr(x0, cfg)
+        counts0 = one.pattern_counts()
+    finally:
+        one.close()
+    assert counts0[1] >= 1
+
+    def fn(s, r):
+        s.set_pattern_reuse(0.05, 3)
+        q = s.run_splr(x0, cfg)
+        return q, s.pattern_counts()
+
+    res = run_ranks(2, p, fn)
+    last0 = ref.trace.rows[-1]
+    for q, counts in res:
+        last = q.trace.rows[-1]
+        assert last.marginal_error <= 1e-8
+        assert counts == counts0, (counts, counts0)
+        assert abs(last.iter - last0.iter) <= 2
+        assert abs(last.f - last0.f) <= 1e-9 * (1 + abs(last0.f))
+    assert [t.f for t in res[0][0].trace.rows] == [t.f for t in res[1][0].trace.rows]
+
+
 def test_sharded_overlap_is_bitwise_identical_to_serial(oracle):
     """cfg.overlap moves the candidate chain to the side stream and the side communicator; results must not
     change (test_splr.cpp:270-305), also when sharded."""

@@ -279,6 +279,8 @@ public:
         if (m_bound != &p) set_problem(p);
     }
     void validate_problem() { check(regot_b200_validate_problem(m_ctx)); }
+    // north_star item (2): rebuild the top-k pattern at k % S == 0 only when it drifted (0: the reference's fixed rule)
+    void set_pattern_reuse(double drift_tol, int max_skips = 4) { check(regot_b200_set_pattern_reuse(m_ctx, drift_tol, max_skips)); }
 
     // dual.h:106-164
     GradientResult fused_gradient(const DualPoint& x)

@@ -100,7 +100,7 @@ __global__ void k_captured_mass_final(int blocks, const double* __restrict__ par
 double sparse_captured_mass(regot_ctx* ctx, cudaStream_t st, ncclComm* comm, const regot_sparse& S, DevBuf<double>& scratch,
                             const double* row_sums)
 {
-    scratch.ensure(2 * kMassBlocks + 2);
+    scratch.ensure(2 * kMassBlocks + 8);
     double* out = scratch.p + 2 * kMassBlocks;
     k_captured_mass_partials<<<kMassBlocks, kMassThreads, 0, st>>>((int)S.nnz, (int)S.nloc, ctx->prob.eta, S.val.p, row_sums, scratch.p);
     k_captured_mass_final<<<1, 32, 0, st>>>(kMassBlocks, scratch.p, out);
@@ -111,6 +111,50 @@ double sparse_captured_mass(regot_ctx* ctx, cudaStream_t st, ncclComm* comm, con
     RG_CUDA(cudaMemcpyAsync(h, out, sizeof(h), cudaMemcpyDeviceToHost, st));
     RG_CUDA(cudaStreamSynchronize(st));
     return h[1] > 0.0 ? h[0] / h[1] : 0.0;
+}
+
+// oscillation of the dual variables since the pattern was built: out = {max d_alpha, -min d_alpha, max d_beta, -min d_beta}.
+// Every entry of T moved by a factor within exp(+-(osc(d_alpha) + osc(d_beta)) / eta) relative to every other one, so a small
+// oscillation bounds how far the top-k ranking can have moved.  One block (the vectors are n + m long).
+__global__ void k_dual_drift(int nloc, int m, const double* __restrict__ a, const double* __restrict__ a0,
+                             const double* __restrict__ b, const double* __restrict__ b0, double* __restrict__ out)
+{
+    __shared__ double sh[4][32];
+    double v[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+    for (int i = threadIdx.x; i < nloc; i += blockDim.x) {
+        const double d = a[i] - a0[i];
+        v[0] = fmax(v[0], d);
+        v[1] = fmax(v[1], -d);
+    }
+    for (int j = threadIdx.x; j < m; j += blockDim.x) {
+        const double d = b[j] - b0[j];
+        v[2] = fmax(v[2], d);
+        v[3] = fmax(v[3], -d);
+    }
+    for (int q = 0; q < 4; ++q) {
+        for (int o = 16; o > 0; o >>= 1) v[q] = fmax(v[q], __shfl_xor_sync(0xffffffffu, v[q], o));
+        if ((threadIdx.x & 31) == 0) sh[q][threadIdx.x >> 5] = v[q];
+    }
+    __syncthreads();
+    if (threadIdx.x < 4) {
+        double r = -INFINITY;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) r = fmax(r, sh[threadIdx.x][w]);
+        out[threadIdx.x] = r;
+    }
+}
+
+double dual_drift(regot_ctx* ctx, cudaStream_t st, ncclComm* comm, const DVec& x, const DVec& x0, DevBuf<double>& scratch)
+{
+    scratch.ensure(2 * kMassBlocks + 8);
+    double* out = scratch.p + 2 * kMassBlocks + 2;
+    k_dual_drift<<<1, 1024, 0, st>>>((int)ctx->prob.nloc, (int)ctx->prob.m, x.a.p, x0.a.p, x.b.p, x0.b.p, out);
+    RG_CUDA(cudaGetLastError());
+    ++ctx->launches;
+    allreduce_max(ctx, comm, out, 4, st);  // alpha is row-sharded; the replicated beta entries are unchanged by the max
+    double h[4];
+    RG_CUDA(cudaMemcpyAsync(h, out, sizeof(h), cudaMemcpyDeviceToHost, st));
+    RG_CUDA(cudaStreamSynchronize(st));
+    return (h[0] + h[1]) + (h[2] + h[3]);
 }
 
 // ---- K4 -----------------------------------------------------------------------------------

@@ -505,9 +505,15 @@ void splr_step_state(regot_ctx* ctx, SplrStateDev& S, const regot_splr_config& c
         const bool reuse_on = ctx->pattern_drift > 0.0;
         if (reuse_on && k > 0 && S.mass_at_build > 0.0 && S.pattern_skips < ctx->pattern_max_skips && S.A.ctx == ctx &&
             S.A.n == pr.n && S.A.m == pr.m && S.A.nloc == pr.nloc) {
-            sparse_fill_values(ctx, st, S.A, S.x.a.p, S.x.b.p, tau, S.cur.sums.a.p, S.cur.sums.b.p);
-            const double share = sparse_captured_mass(ctx, st, ctx->comm, S.A, S.mass_scratch, S.cur.sums.a.p);
-            keep_pattern = share >= (1.0 - ctx->pattern_drift) * S.mass_at_build;
+            // (i) the duals moved by less than drift_tol x eta in oscillation since the pattern was selected: every T_ij
+            // moved by a factor within exp(+-drift_tol) relative to every other, so only entries that close to the
+            // threshold can have changed sides; (ii) the pattern still holds its share of the mass
+            const double osc = dual_drift(ctx, st, ctx->comm, S.x, S.x_build, S.mass_scratch);
+            if (osc <= ctx->pattern_drift * pr.eta) {
+                sparse_fill_values(ctx, st, S.A, S.x.a.p, S.x.b.p, tau, S.cur.sums.a.p, S.cur.sums.b.p);
+                const double share = sparse_captured_mass(ctx, st, ctx->comm, S.A, S.mass_scratch, S.cur.sums.a.p);
+                keep_pattern = share >= (1.0 - ctx->pattern_drift) * S.mass_at_build;
+            }
         }
         if (keep_pattern) {
             ++S.pattern_skips;
@@ -532,7 +538,10 @@ void splr_step_state(regot_ctx* ctx, SplrStateDev& S, const regot_splr_config& c
             sparse_fill_values(ctx, st, S.A, S.x.a.p, S.x.b.p, tau, S.cur.sums.a.p, S.cur.sums.b.p);
             ++ctx->pattern_rebuilds;
             S.pattern_skips = 0;
-            if (reuse_on) S.mass_at_build = sparse_captured_mass(ctx, st, ctx->comm, S.A, S.mass_scratch, S.cur.sums.a.p);
+            if (reuse_on) {
+                S.mass_at_build = sparse_captured_mass(ctx, st, ctx->comm, S.A, S.mass_scratch, S.cur.sums.a.p);
+                vec_copy(ctx, st, S.x, S.x_build);
+            }
         }
         sect.tick(0);
         if (cfg.J > 0) {

@@ -47,6 +47,7 @@ struct SplrStateDev {
     double mass_at_build = -1.0;
     int pattern_skips = 0;
     DevBuf<double> mass_scratch;
+    DVec x_build;  // the point the pattern was selected at
     // per-step scratch
     DVec xs, d, sdiff, ydiff, v, ag, au, av;
     GradOut cand;

@@ -192,6 +192,8 @@ void sparse_fill_values(regot_ctx* ctx, cudaStream_t st, regot_sparse& S, const 
 // `st`; summed over the ranks when sharded (pattern reuse, regot_b200_set_pattern_reuse)
 double sparse_captured_mass(regot_ctx* ctx, cudaStream_t st, ncclComm* comm, const regot_sparse& S, DevBuf<double>& scratch,
                             const double* row_sums);
+// osc(alpha - alpha0) + osc(beta - beta0) over the whole problem (max over the ranks when sharded); synchronises `st`
+double dual_drift(regot_ctx* ctx, cudaStream_t st, ncclComm* comm, const DVec& x, const DVec& x0, DevBuf<double>& scratch);
 // y = A v on free vectors (K4); nrhs systems stored back to back with strides
 void sparse_matvec(regot_ctx* ctx, cudaStream_t st, ncclComm* comm, const regot_sparse& S, int nrhs, const double* va,
                    const double* vb, double* ya, double* yb, int64_t stride_a, int64_t stride_b);

@@ -237,7 +237,7 @@ def test_sharded_pattern_reuse_takes_the_same_decisions_as_one_gpu():
     x0 = rg.DualPoint.zeros(p.n, p.m)
     one = rg.Solver(0)
     try:
-        one.set_pattern_reuse(0.05, 3)
+        one.set_pattern_reuse(0.5, 3)
         one.set_problem(p)
         ref = one.run_splr(x0, cfg)
         counts0 = one.pattern_counts()
@@ -246,7 +246,7 @@ def test_sharded_pattern_reuse_takes_the_same_decisions_as_one_gpu():
     assert counts0[1] >= 1
 
     def fn(s, r):
-        s.set_pattern_reuse(0.05, 3)
+        s.set_pattern_reuse(0.5, 3)
         q = s.run_splr(x0, cfg)
         return q, s.pattern_counts()
 

@@ -334,10 +334,12 @@ regot_status regot_b200_set_profiling(regot_ctx* ctx, int enabled);
 regot_status regot_b200_get_profile(regot_ctx* ctx, int kind, int64_t* launches, double* total_ms);
 /* Pattern reuse across refreshes -- north_star item (2): "the symbolic structure is reused across iterations and rebuilt
  * only when the pattern drifts".  The reference rebuilds the top-k pattern at every k % S == 0 (splr.h:352, 359-364); with
- * drift_tol > 0 such an iteration first refreshes the values of the pattern it holds (update_values, sparsity.h:305-317),
- * measures the share of the Hessian block's mass (sum of the row sums over eta) they capture, and keeps pattern, pointer
- * arrays and the direction solve's plans when that share is still >= (1 - drift_tol) x the share at the last rebuild and
- * fewer than max_skips refreshes in a row kept it; the Sinkhorn candidate chain (splr.h:366-378) runs either way.
+ * drift_tol > 0 such an iteration keeps pattern, pointer arrays and the direction solve's plans when (i) the duals moved
+ * by at most drift_tol x eta in oscillation since the pattern was selected (osc(d_alpha) + osc(d_beta): every T_ij then
+ * moved by a factor within exp(+-drift_tol) relative to every other), (ii) the values of the pattern refreshed at the
+ * current point (update_values, sparsity.h:305-317) still capture >= (1 - drift_tol) x the share of the Hessian block's
+ * mass (sum of the row sums over eta) they captured when the pattern was built, and (iii) fewer than max_skips refreshes
+ * in a row kept it; the Sinkhorn candidate chain (splr.h:366-378) runs either way.
  * drift_tol = 0 (default) is the reference's rule, bit for bit.  pattern_counts: rebuilds and reuses since creation. */
 regot_status regot_b200_set_pattern_reuse(regot_ctx* ctx, double drift_tol, int max_skips);
 void regot_b200_pattern_counts(const regot_ctx* ctx, int64_t* rebuilds, int64_t* reuses);

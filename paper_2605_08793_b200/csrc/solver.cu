@@ -477,10 +477,12 @@ void splr_step_state(regot_ctx* ctx, SplrStateDev& S, const regot_splr_config& c
             RG_CUDA(cudaMemcpyAsync(S.xs.a.p, S.x.a.p, sizeof(double) * (size_t)pr.nloc, cudaMemcpyDeviceToDevice, cs));
             RG_CUDA(cudaMemcpyAsync(S.xs.b.p, S.x.b.p, sizeof(double) * (size_t)pr.m, cudaMemcpyDeviceToDevice, cs));
             for (long j = 0; j < cfg.J; ++j) {
-                if (fast) launch_sinkhorn_step_fast(ctx, cs, w, ccomm, S.xs.a.p, S.xs.b.p);
+                // S.cur is the gradient pass at the snapshot: its row sums are what the first sweep of the first step
+                // would compute (same partial sums, same panel order: identical bits), so that sweep is skipped
+                if (fast) launch_sinkhorn_step_fast(ctx, cs, w, ccomm, S.xs.a.p, S.xs.b.p, j == 0 ? S.cur.sums.a.p : nullptr);
                 else launch_sinkhorn_step(ctx, cs, w, ccomm, S.xs.a.p, S.xs.b.p);
             }
-            out.lse_passes += 2 * cfg.J;
+            out.lse_passes += 2 * cfg.J - ((fast && cfg.J > 0) ? 1 : 0);
             launch_gradient(ctx, cs, w, ccomm, S.xs.a.p, S.xs.b.p, nullptr, nullptr, S.cand);
             ++out.gradient_passes;
         };

@@ -410,6 +410,9 @@ void launch_sinkhorn_step(regot_ctx* ctx, cudaStream_t st, SweepWS& ws, ncclComm
 // row_sums_here (nullable): row sums of T at (alpha, beta) from a gradient pass made at this very point.
 void launch_sinkhorn_step_fast(regot_ctx* ctx, cudaStream_t st, SweepWS& ws, ncclComm* comm, double* alpha_io,
                                double* beta_io, const double* row_sums_here = nullptr);
+// true when every row sum lies in the fast update's safe range (one small kernel + a host round trip on `st`; summed over
+// the ranks): a chain whose first update would be flagged goes straight to the log-sum-exp kernels
+bool fast_sinkhorn_update_is_safe(regot_ctx* ctx, cudaStream_t st, ncclComm* comm, const double* row_sums, DevBuf<double>& scratch);
 void reset_sinkhorn_flag(regot_ctx* ctx, cudaStream_t st, SweepWS& ws);
 
 // host <-> device helpers (ctx.cu)

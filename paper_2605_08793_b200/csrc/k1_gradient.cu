@@ -261,7 +261,8 @@ __device__ __forceinline__ void split30(double hi, double& h1, double& h2)
     h1 = c - (c - hi);
     h2 = hi - h1;
 }
-constexpr int kNScalPack = 12;  // row-side scalars behind the m column sums of the allreduce payload: 6 plain + 2 x 3 pieces
+constexpr int kNScalPack = 13;  // row-side scalars behind the m column sums of the allreduce payload: 6 plain + 2 x 3 pieces + the
+                                // rank's fast-Sinkhorn flag (summed: every rank must take the same redo decision)
 
 struct Fin1Params {
     int nloc, m, n_panels;
@@ -277,6 +278,7 @@ struct Fin1Params {
     double* partials;  // gridDim.x * kNScal
     unsigned int* ticket;
     int extended;      // also sum r and alpha.a in double-double -> pack[m + 6 .. m + 12) as (30-bit, 23-bit, low) pieces
+    const unsigned int* sk_flag;  // this rank's fast-Sinkhorn flag -> pack[m + 12] (the two-kernel form)
 };
 
 __device__ __forceinline__ bool last_block_done(unsigned int* ticket)
@@ -382,7 +384,10 @@ __global__ void __launch_bounds__(kFinThreads) k_gradient_fin1(const Fin1Params 
                     p.pack[p.m + 8 + 3 * k] = t.lo;
                 }
             }
-            if (threadIdx.x == 0) *p.ticket = 0u;
+            if (threadIdx.x == 0) {
+                p.pack[p.m + 12] = (double)*p.sk_flag;
+                *p.ticket = 0u;
+            }
         }
     }
 }
@@ -461,7 +466,7 @@ __global__ void __launch_bounds__(kFinThreads) k_gradient_fin2(const Fin2Params 
                 o.duality_gap = S[3] + c[2];     // dual.h:225-229
                 o.grad_sqnorm = S[4] + c[3];
                 o.g_dot_d = S[5] + c[4];
-                o.lse_flag = (double)*p.sk_flag;
+                o.lse_flag = p.pack[p.m + 12];  // any rank's flag (summed by the allreduce; this rank's own on one GPU)
                 o.f_lo = 0.0;
                 if (p.extended) {
                     // sum r and alpha.a arrive as (30-bit, 23-bit, low) pieces summed over the ranks
@@ -706,6 +711,7 @@ void launch_gradient(regot_ctx* ctx, cudaStream_t st, SweepWS& ws, ncclComm* com
     f1.partials = ws.partials.p;
     f1.ticket = ws.ticket.p;
     f1.extended = ctx->extended_f ? 1 : 0;
+    f1.sk_flag = ws.sk_flag.p;
     const bool fused = !ctx->sharded && ctx->fused_finalize;
     if (!fused) {
         k_gradient_fin1<<<g1, kFinThreads, 0, st>>>(f1);

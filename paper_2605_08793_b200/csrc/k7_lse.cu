@@ -595,6 +595,35 @@ void launch_sinkhorn_step_fast(regot_ctx* ctx, cudaStream_t st, SweepWS& ws, ncc
     ctx->launches += 4;
 }
 
+// would the first fast update from these row sums stay in its safe range?  (out[0] = rows outside it)
+__global__ void k_rows_outside_safe_range(int nloc, const double* __restrict__ row_sums, double* __restrict__ out)
+{
+    __shared__ int any;
+    if (threadIdx.x == 0) any = 0;
+    __syncthreads();
+    bool bad = false;
+    for (int i = threadIdx.x; i < nloc; i += blockDim.x) {
+        const double r = row_sums[i];
+        bad |= !(r >= kSafeLo && r <= kSafeHi);
+    }
+    if (bad) any = 1;
+    __syncthreads();
+    if (threadIdx.x == 0) out[0] = any ? 1.0 : 0.0;
+}
+
+bool fast_sinkhorn_update_is_safe(regot_ctx* ctx, cudaStream_t st, ncclComm* comm, const double* row_sums, DevBuf<double>& scratch)
+{
+    scratch.ensure(1);
+    k_rows_outside_safe_range<<<1, 1024, 0, st>>>((int)ctx->prob.nloc, row_sums, scratch.p);
+    RG_CUDA(cudaGetLastError());
+    ++ctx->launches;
+    allreduce_sum(ctx, comm, scratch.p, 1, st);  // sharded runs: every rank takes the same form of the chain
+    double h = 0.0;
+    RG_CUDA(cudaMemcpyAsync(&h, scratch.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+    RG_CUDA(cudaStreamSynchronize(st));
+    return h == 0.0;
+}
+
 void reset_sinkhorn_flag(regot_ctx* ctx, cudaStream_t st, SweepWS& ws)
 {
     (void)ctx;

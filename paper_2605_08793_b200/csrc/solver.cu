@@ -500,6 +500,11 @@ void splr_step_state(regot_ctx* ctx, SplrStateDev& S, const regot_splr_config& c
         // pattern's pointer arrays into line lists and the PCG schedule.  Same kernels, same order of
         // arithmetic, same results.
         bool chain_started = false;
+        // The fast form's first update takes the state's row sums: when one of them is outside the safe range the chain
+        // would be flagged and redone with the log-sum-exp kernels (the first refresh of a solve from x0 = 0 at small eta:
+        // 9 wasted sweeps) -- known before it is enqueued, so it starts in the exact form.  Same results either way.
+        const bool chain_fast = ctx->fast_sinkhorn_chain && cfg.J > 0 &&
+                                fast_sinkhorn_update_is_safe(ctx, st, ctx->comm, S.cur.sums.a.p, S.chain_scratch);
         // Pattern reuse (regot_b200_set_pattern_reuse; off by default = the reference's rule): the values of the pattern in
         // hand are refreshed at the current point first -- the update a non-refresh iteration makes -- and the pattern is
         // kept while it still holds its share of the Hessian block's mass.  The candidate chain runs either way.
@@ -523,7 +528,7 @@ void splr_step_state(regot_ctx* ctx, SplrStateDev& S, const regot_splr_config& c
         } else {
             if (cfg.J > 0 && !cfg.overlap && !ctx->profiling)
                 W.sparse.after_pointer_download = [&]() {
-                    run_chain(ctx->fast_sinkhorn_chain);
+                    run_chain(chain_fast);
                     chain_started = true;
                 };
             // plan + select_topk + assemble (splr.h:361-364); T is never materialised
@@ -551,7 +556,7 @@ void splr_step_state(regot_ctx* ctx, SplrStateDev& S, const regot_splr_config& c
                 RG_CUDA(cudaEventRecord(ctx->ev_fork, st));
                 RG_CUDA(cudaStreamWaitEvent(cs, ctx->ev_fork, 0));
             }
-            if (!chain_started) run_chain(ctx->fast_sinkhorn_chain);
+            if (!chain_started) run_chain(chain_fast);
             if (!cfg.overlap) finish_chain();
             else join_chain = finish_chain;
             have_s = true;

@@ -46,7 +46,7 @@ struct SplrStateDev {
     // pattern reuse (regot_b200_set_pattern_reuse): share of the mass the pattern held when it was built, refreshes that kept it
     double mass_at_build = -1.0;
     int pattern_skips = 0;
-    DevBuf<double> mass_scratch;
+    DevBuf<double> mass_scratch, chain_scratch;
     DVec x_build;  // the point the pattern was selected at
     // per-step scratch
     DVec xs, d, sdiff, ydiff, v, ag, au, av;

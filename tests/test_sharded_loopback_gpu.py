@@ -295,3 +295,31 @@ def test_sharded_run_sinkhorn_and_pointcloud(solver, oracle):
             np.testing.assert_allclose(q.x.beta, ref.x.beta, rtol=0, atol=1e-11)
             np.testing.assert_allclose(q.x.alpha, ref.x.alpha, rtol=0, atol=1e-11)
             assert abs(q.trace.rows[-1].marginal_error - ref.trace.rows[-1].marginal_error) <= 1e-11
+
+
+def test_a_fast_update_flagged_on_one_rank_is_redone_by_all_of_them(solver):
+    """The gradient-sweep form of a Sinkhorn update is exact only while every sum lies in [e^-600, e^600]; outside it the
+    update is flagged and redone with the log-sum-exp kernels.  Row sums are rank-local, so the flag travels with the
+    gradient pass's allreduce payload: here only the rows of the LAST rank are out of range at x0 = 0 (costs >= 0.75 at
+    eta = 0.001), and every rank must still take the same kernels (a rank on its own would desynchronise the collectives)."""
+    rng = np.random.default_rng(3)
+    n, m = 192, 160
+    M = rng.random((n, m))
+    M[n // 2:, :] = 0.75 + 0.25 * M[n // 2:, :]
+    p = rg.ProblemInstance(n, m, M, np.full(n, 1.0 / n), np.full(m, 1.0 / m), 0.001)
+    x0 = rg.DualPoint.zeros(n, m)
+    kcfg = rg.SinkhornConfig(max_iter=12, tol=1e-9)
+    scfg = rg.SplrConfig(max_iter=12, tol=1e-8)
+    solver.set_problem(p)
+    ref_k = solver.run_sinkhorn(x0, kcfg)
+    ref_s = solver.run_splr(x0, scfg)
+
+    def fn(s, r):
+        return s.run_sinkhorn(x0, kcfg), s.run_splr(x0, scfg)
+
+    for qk, qs in run_ranks(2, p, fn):
+        for q, ref in ((qk, ref_k), (qs, ref_s)):
+            assert len(q.trace.rows) == len(ref.trace.rows)
+            for u, v in zip(q.trace.rows, ref.trace.rows):
+                assert abs(u.f - v.f) <= 1e-9 * (1 + abs(v.f)), (u.iter, u.f, v.f)
+        np.testing.assert_allclose(qk.x.beta, ref_k.x.beta, rtol=0, atol=1e-9)
